@@ -1,0 +1,105 @@
+/*
+ * lossyckpt_b200.h -- C ABI of the B200 (sm_100a) lossy-checkpoint codec.
+ *
+ * Drop-in replacement for the compute core of the reference package
+ * lossyckpt (Python + numba, /root/reference/pkg/src/lossyckpt).  Plain
+ * pointers and sizes only; no torch types.  The Python host layer
+ * (paper_1805_07384_b200/compressor.py) binds these with ctypes exactly where
+ * the reference calls its numba kernels; INTEGRATION.md shows the binding a
+ * maintainer of the reference would add.
+ *
+ * Reference interfaces replaced (file:line under pkg/src/lossyckpt/):
+ *   lc_range_f64        np.isfinite / max / min        compressor.py:384-386
+ *   lc_compress_f64     _compress_kernel + bincount +
+ *                       huffman.code_lengths + encode  compressor.py:400-413,
+ *                                                      huffman.py:21-55,96-107,135-150
+ *   lc_result_fetch     the CompressedBlock fields     compressor.py:414-417
+ *   lc_decompress_f64   huffman.decode + _decompress_kernel + checks
+ *                                                      compressor.py:430-439,
+ *                                                      huffman.py:110-132,153-172
+ *
+ * Status codes (return values):
+ *   0 ok
+ *   1 invalid codeword           -> IntegrityError("Huffman decode failed: invalid codeword")
+ *   2 payload exhausted          -> IntegrityError("... payload exhausted mid-symbol")
+ *   3 trailing bits              -> IntegrityError("... trailing bits after last symbol")
+ *   4 escape count mismatch      -> IntegrityError("escape count mismatch: ...")
+ *   5 escape positions mismatch  -> IntegrityError("escape positions disagree with escape codes")
+ *  10 non-finite input           -> ParameterError("input contains NaN or Inf")
+ *  11 error bound overflow       -> ParameterError("error bound too large to quantize")
+ *  12 bad argument               -> ParameterError
+ *  13 code length > 64           -> ParameterError("code length exceeds 64 bits")
+ *  20 CUDA error (message via lc_last_error)
+ *
+ * Threading: one context per host thread / CUDA stream.  Every call is
+ * stream-ordered on the context's stream and returns after the results it
+ * reports are final (one scalar readback per call, no other host syncs).
+ */
+#ifndef LOSSYCKPT_B200_H
+#define LOSSYCKPT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct lc_ctx lc_ctx;
+
+/* Create a context on `device` whose work is ordered on `stream` (a
+ * cudaStream_t cast to void*; NULL = the legacy default stream).          */
+int lc_ctx_create(lc_ctx **out, int device, void *stream);
+void lc_ctx_destroy(lc_ctx *ctx);
+const char *lc_last_error(lc_ctx *ctx);
+
+/* compressor.py:384-386: min, max and a non-finite flag of x[0..n).       */
+int lc_range_f64(lc_ctx *ctx, const double *x, uint64_t n, int x_on_device,
+                 double *vmin, double *vmax, int *nonfinite);
+
+typedef struct {
+    uint64_t n;            /* elements */
+    uint64_t payload_bits; /* huffman.encode bit length                   */
+    uint64_t payload_bytes;/* ceil(payload_bits / 8)                       */
+    uint64_t n_esc;        /* escapes                                      */
+    uint32_t n_symbols;    /* 2 * n_bins_half (length of code_lengths)     */
+    uint32_t max_len;      /* longest Huffman code                         */
+    uint32_t used_symbols; /* symbols with a non-zero frequency            */
+    uint32_t relaunches;   /* exact-chain repair passes (diagnostic)       */
+} lc_result;
+
+/* compressor.py:400-413 for n >= 2 and a non-constant vector: quantize with
+ * the closed-loop order-1 predictor at eb_abs, histogram, build the Huffman
+ * code on device and encode.  x is device or host memory.  Results stay in
+ * the context until lc_result_fetch / lc_result_device.                   */
+int lc_compress_f64(lc_ctx *ctx, const double *x, uint64_t n, int x_on_device,
+                    double eb_abs, uint32_t n_bins_half, int record_traces,
+                    lc_result *res);
+
+/* Copy the last compress result to host buffers (any may be NULL):
+ * code_lengths[n_symbols], payload[payload_bytes], esc_idx/esc_val[n_esc],
+ * pe/pe_rec[n-1] (only when record_traces was set).                       */
+int lc_result_fetch(lc_ctx *ctx, uint8_t *code_lengths, uint8_t *payload,
+                    uint64_t *esc_idx, double *esc_val, double *pe, double *pe_rec);
+
+/* Device pointers of the last compress result (valid until the next call). */
+int lc_result_device(lc_ctx *ctx, const uint8_t **payload, const uint16_t **codes);
+
+/* compressor.py:420-440 for a non-constant block.  All inputs are host
+ * pointers unless inputs_on_device; out is host or device memory.
+ * *esc_used receives the escape count the codes require (-1 when they need
+ * more than n_esc), matching the reference's error message.               */
+int lc_decompress_f64(lc_ctx *ctx, uint64_t n, double eb_abs, double first_value,
+                      const uint8_t *code_lengths, uint64_t n_lengths,
+                      const uint8_t *payload, uint64_t payload_bytes, uint64_t payload_bits,
+                      const uint64_t *esc_idx, const double *esc_val, uint64_t n_esc,
+                      int inputs_on_device, double *out, int out_on_device,
+                      int64_t *esc_used);
+
+/* Wall time of the last compress / decompress call on the device (ms),
+ * measured with CUDA events around the whole stream-ordered call.          */
+double lc_last_device_ms(lc_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,116 @@
+"""ctypes binding of the sm_100a codec library (include/lossyckpt_b200.h).
+
+The library is built in-tree by paper_1805_07384_b200.build (nvcc, sm_100a).
+There is no fallback: if the library or a CUDA device is missing, every
+entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "liblossyckpt_b200.so")
+
+STATUS_INTEGRITY = {1: "Huffman decode failed: invalid codeword",
+                    2: "Huffman decode failed: payload exhausted mid-symbol",
+                    3: "Huffman decode failed: trailing bits after last symbol",
+                    5: "escape positions disagree with escape codes"}
+STATUS_PARAMETER = {10: "input contains NaN or Inf",
+                    11: "error bound too large to quantize",
+                    12: "invalid argument",
+                    13: "code length exceeds 64 bits"}
+
+
+class LcResult(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_uint64), ("payload_bits", ctypes.c_uint64),
+                ("payload_bytes", ctypes.c_uint64), ("n_esc", ctypes.c_uint64),
+                ("n_symbols", ctypes.c_uint32), ("max_len", ctypes.c_uint32),
+                ("used_symbols", ctypes.c_uint32), ("relaunches", ctypes.c_uint32)]
+
+
+_vp = ctypes.c_void_p
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def library():
+    """Load (never silently skip) the native codec library."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"native codec library missing: {LIB_PATH} "
+                               "(run python -m paper_1805_07384_b200.build)")
+        L = ctypes.CDLL(LIB_PATH)
+        L.lc_ctx_create.argtypes = [ctypes.POINTER(_vp), ctypes.c_int, _vp]
+        L.lc_ctx_create.restype = ctypes.c_int
+        L.lc_ctx_destroy.argtypes = [_vp]
+        L.lc_ctx_destroy.restype = None
+        L.lc_last_error.argtypes = [_vp]
+        L.lc_last_error.restype = ctypes.c_char_p
+        L.lc_range_f64.argtypes = [_vp, _vp, ctypes.c_uint64, ctypes.c_int,
+                                   ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                                   ctypes.POINTER(ctypes.c_int)]
+        L.lc_range_f64.restype = ctypes.c_int
+        L.lc_compress_f64.argtypes = [_vp, _vp, ctypes.c_uint64, ctypes.c_int, ctypes.c_double,
+                                      ctypes.c_uint32, ctypes.c_int, ctypes.POINTER(LcResult)]
+        L.lc_compress_f64.restype = ctypes.c_int
+        L.lc_result_fetch.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp]
+        L.lc_result_fetch.restype = ctypes.c_int
+        L.lc_result_device.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp)]
+        L.lc_result_device.restype = ctypes.c_int
+        L.lc_decompress_f64.argtypes = [_vp, ctypes.c_uint64, ctypes.c_double, ctypes.c_double,
+                                        _vp, ctypes.c_uint64, _vp, ctypes.c_uint64, ctypes.c_uint64,
+                                        _vp, _vp, ctypes.c_uint64, ctypes.c_int, _vp, ctypes.c_int,
+                                        ctypes.POINTER(ctypes.c_int64)]
+        L.lc_decompress_f64.restype = ctypes.c_int
+        L.lc_last_device_ms.argtypes = [_vp]
+        L.lc_last_device_ms.restype = ctypes.c_double
+        _lib = L
+        return L
+
+
+EXPORTED = ["lc_ctx_create", "lc_ctx_destroy", "lc_last_error", "lc_range_f64", "lc_compress_f64",
+            "lc_result_fetch", "lc_result_device", "lc_decompress_f64", "lc_last_device_ms"]
+
+
+class Context:
+    """One codec context (CUDA stream + scratch) per device and host thread."""
+
+    def __init__(self, device=0, stream=None):
+        self.lib = library()
+        self.h = _vp()
+        rc = self.lib.lc_ctx_create(ctypes.byref(self.h), int(device), stream)
+        if rc != 0:
+            raise RuntimeError(f"lc_ctx_create failed ({rc}): CUDA device {device} unavailable")
+        self.device = device
+
+    def error(self):
+        return self.lib.lc_last_error(self.h).decode()
+
+    def close(self):
+        if self.h:
+            self.lib.lc_ctx_destroy(self.h)
+            self.h = _vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_ctx_local = threading.local()
+
+
+def context(device=0):
+    ctxs = getattr(_ctx_local, "ctxs", None)
+    if ctxs is None:
+        ctxs = _ctx_local.ctxs = {}
+    if device not in ctxs:
+        ctxs[device] = Context(device)
+    return ctxs[device]

@@ -1,0 +1,376 @@
+// lc_api.cu -- C ABI (include/lossyckpt_b200.h): contexts, compress and
+// decompress drivers over the sm_100a kernels.
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+#include <string>
+#include "../../include/lossyckpt_b200.h"
+
+#include "lc_kernels.cuh"
+
+int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_value,
+                       const uint8_t *code_lengths, uint64_t n_lengths, const uint8_t *payload,
+                       uint64_t payload_bytes, uint64_t payload_bits, const uint64_t *esc_idx,
+                       const double *esc_val, uint64_t n_esc, int inputs_on_device, double *out,
+                       int out_on_device, int64_t *esc_used);
+
+// ---------------------------------------------------------------------------
+
+struct LcBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+};
+
+struct lc_ctx {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::string err;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // scratch
+    LcBuf xbuf, codes, hist, desc, counters, bad_end, pe, pe_rec, lengths, cw, gkeys, ifreq,
+        parent, cbout, payload, esc_idx, esc_val, encdesc, range_parts, small;
+    void *pinned = nullptr;         // small pinned staging
+    // last compress result
+    uint64_t n = 0;
+    uint32_t nbins = 0;
+    int code_bytes = 2;
+    int record = 0;
+    LcCodebookOut cb{};
+    // decompress scratch (lc_decode.cu)
+    LcBuf dec[10];     // payload, lengths, esc idx, esc val, out, codes, tables, sync, aux, aux2
+};
+
+int lc_fail(lc_ctx *ctx, cudaError_t e, const char *what, const char *file, int line)
+{
+    char buf[512];
+    snprintf(buf, sizeof buf, "%s failed: %s (%s:%d)", what, cudaGetErrorString(e), file, line);
+    if (ctx) ctx->err = buf;
+    return 20;
+}
+
+cudaError_t lc_reserve(LcBuf &b, size_t bytes)
+{
+    if (bytes <= b.cap && b.p) return cudaSuccess;
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.cap = 0;
+    size_t cap = bytes < 256 ? 256 : bytes + bytes / 8;
+    cudaError_t e = cudaMalloc(&b.p, cap);
+    if (e == cudaSuccess) b.cap = cap;
+    return e;
+}
+
+cudaStream_t lc_stream(lc_ctx *ctx) { return ctx->stream; }
+int lc_sm_count(lc_ctx *ctx) { return ctx->sm_count; }
+void *lc_pinned(lc_ctx *ctx) { return ctx->pinned; }
+void lc_set_err(lc_ctx *ctx, const char *msg) { ctx->err = msg; }
+LcBuf *lc_dec_bufs(lc_ctx *ctx) { return ctx->dec; }
+
+extern "C" {
+
+int lc_ctx_create(lc_ctx **out, int device, void *stream)
+{
+    lc_ctx *ctx = new lc_ctx();
+    ctx->device = device;
+    *out = nullptr;
+    LC_CUDA_OK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    LC_CUDA_OK(cudaGetDeviceProperties(&prop, device));
+    ctx->sm_count = prop.multiProcessorCount;
+    // NULL selects the legacy default stream (ordered with torch's default stream)
+    ctx->stream = (cudaStream_t)stream;
+    LC_CUDA_OK(cudaEventCreate(&ctx->ev0));
+    LC_CUDA_OK(cudaEventCreate(&ctx->ev1));
+    LC_CUDA_OK(cudaMallocHost(&ctx->pinned, 4096));
+    LC_CUDA_OK(cudaFuncSetAttribute(lc_quant_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)lc_quant_smem_bytes()));
+    LC_CUDA_OK(cudaFuncSetAttribute(lc_quant_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)lc_quant_smem_bytes()));
+    LC_CUDA_OK(cudaFuncSetAttribute(lc_codebook_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)lc_codebook_smem_bytes()));
+    LC_CUDA_OK(cudaFuncSetAttribute(lc_encode_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)lc_encode_smem_bytes()));
+    LC_CUDA_OK(cudaFuncSetAttribute(lc_encode_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)lc_encode_smem_bytes()));
+    *out = ctx;
+    return 0;
+}
+
+void lc_ctx_destroy(lc_ctx *ctx)
+{
+    if (!ctx) return;
+    cudaStreamSynchronize(ctx->stream);
+    LcBuf *bufs[] = {&ctx->xbuf, &ctx->codes, &ctx->hist, &ctx->desc, &ctx->counters, &ctx->bad_end,
+                     &ctx->pe, &ctx->pe_rec, &ctx->lengths, &ctx->cw, &ctx->gkeys, &ctx->ifreq,
+                     &ctx->parent, &ctx->cbout, &ctx->payload, &ctx->esc_idx, &ctx->esc_val,
+                     &ctx->encdesc, &ctx->range_parts, &ctx->small, &ctx->dec[0], &ctx->dec[1],
+                     &ctx->dec[2], &ctx->dec[3], &ctx->dec[4], &ctx->dec[5], &ctx->dec[6],
+                     &ctx->dec[7], &ctx->dec[8], &ctx->dec[9]};
+    for (LcBuf *b : bufs)
+        if (b->p) cudaFree(b->p);
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+const char *lc_last_error(lc_ctx *ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+
+double lc_last_device_ms(lc_ctx *ctx)
+{
+    float ms = -1.0f;
+    if (cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1) != cudaSuccess) return -1.0;
+    return ms;
+}
+
+static const double *lc_device_input(lc_ctx *ctx, const double *x, uint64_t n, int on_device, int *rc)
+{
+    *rc = 0;
+    if (on_device) return x;
+    cudaError_t e = lc_reserve(ctx->xbuf, n * sizeof(double));
+    if (e == cudaSuccess) e = cudaMemcpyAsync(ctx->xbuf.p, x, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream);
+    if (e != cudaSuccess) { *rc = lc_fail(ctx, e, "input H2D", __FILE__, __LINE__); return nullptr; }
+    return (const double *)ctx->xbuf.p;
+}
+
+int lc_range_f64(lc_ctx *ctx, const double *x, uint64_t n, int x_on_device, double *vmin, double *vmax,
+                 int *nonfinite)
+{
+    if (!ctx || n == 0) return 12;
+    int rc;
+    const double *dx = lc_device_input(ctx, x, n, x_on_device, &rc);
+    if (rc) return rc;
+    int nb = (int)((n + 255) / 256);
+    if (nb > 4 * ctx->sm_count) nb = 4 * ctx->sm_count;
+    LC_CUDA_OK(lc_reserve(ctx->range_parts, sizeof(LcRangePart) * (nb + 1)));
+    LcRangePart *parts = (LcRangePart *)ctx->range_parts.p;
+    lc_range_kernel<<<nb, 256, 0, ctx->stream>>>(dx, n, parts);
+    lc_range_final_kernel<<<1, 32, 0, ctx->stream>>>(parts, nb, parts + nb);
+    LC_CUDA_OK(cudaGetLastError());
+    LcRangePart *h = (LcRangePart *)ctx->pinned;
+    LC_CUDA_OK(cudaMemcpyAsync(h, parts + nb, sizeof(LcRangePart), cudaMemcpyDeviceToHost, ctx->stream));
+    LC_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    *vmin = h->vmin;
+    *vmax = h->vmax;
+    *nonfinite = h->nonfinite;
+    return 0;
+}
+
+}  // extern "C"
+
+template <typename CodeT>
+static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_abs, uint32_t nbh, int record,
+                         lc_result *res)
+{
+    cudaStream_t st = ctx->stream;
+    const uint32_t nbins = 2u * nbh;
+    const int64_t nchunks = (int64_t)((n - 1 + LC_L - 1) / LC_L);
+    const int64_t ntiles = (nchunks + LC_TPB - 1) / LC_TPB;
+    const uint64_t m = n - 1;
+    LC_CUDA_OK(lc_reserve(ctx->codes, m * sizeof(CodeT)));
+    LC_CUDA_OK(lc_reserve(ctx->hist, nbins * sizeof(uint32_t)));
+    LC_CUDA_OK(lc_reserve(ctx->desc, ntiles * sizeof(LcTileDesc)));
+    LC_CUDA_OK(lc_reserve(ctx->counters, 64));
+    LC_CUDA_OK(lc_reserve(ctx->bad_end, nchunks * sizeof(double)));
+    if (record) {
+        LC_CUDA_OK(lc_reserve(ctx->pe, m * sizeof(double)));
+        LC_CUDA_OK(lc_reserve(ctx->pe_rec, m * sizeof(double)));
+    }
+    unsigned int *tile_counter = (unsigned int *)ctx->counters.p;
+    unsigned long long *first_bad = (unsigned long long *)((char *)ctx->counters.p + 16);
+
+    LcQuantParams P;
+    P.x = dx;
+    P.n = n;
+    P.Q.delta = 2.0 * eb_abs;
+    P.Q.eb = eb_abs;
+    P.Q.max_m = (double)(nbh - 1);
+    P.Q.max_m1 = P.Q.max_m + 1.0;
+    P.esc_thresh = (double)nbh * P.Q.delta * (1.0 + 0x1p-40);
+    P.first_chunk = 0;
+    P.anchor_val = 0.0;
+    P.nchunks = nchunks;
+    P.desc = (LcTileDesc *)ctx->desc.p;
+    P.tile_counter = tile_counter;
+    P.hist = (uint32_t *)ctx->hist.p;
+    P.nbins = nbins;
+    P.count_hist = 1;
+    P.first_bad = first_bad;
+    P.bad_end = (double *)ctx->bad_end.p;
+    P.pe = record ? (double *)ctx->pe.p : nullptr;
+    P.pe_rec = record ? (double *)ctx->pe_rec.p : nullptr;
+    CodeT *codes = (CodeT *)ctx->codes.p;
+
+    LC_CUDA_OK(cudaMemcpyAsync(&P.anchor_val, dx, sizeof(double), cudaMemcpyDeviceToHost, st));
+    LC_CUDA_OK(cudaStreamSynchronize(st));
+    LC_CUDA_OK(cudaMemsetAsync(P.hist, 0, nbins * sizeof(uint32_t), st));
+
+    const int grid_cap = 2 * ctx->sm_count;
+    unsigned long long *hbad = (unsigned long long *)ctx->pinned;
+    uint32_t relaunches = 0;
+    for (;;) {
+        P.ntiles = (nchunks - P.first_chunk + LC_TPB - 1) / LC_TPB;
+        LC_CUDA_OK(cudaMemsetAsync(P.desc, 0, P.ntiles * sizeof(LcTileDesc), st));
+        LC_CUDA_OK(cudaMemsetAsync(ctx->counters.p, 0, 16, st));
+        LC_CUDA_OK(cudaMemsetAsync(first_bad, 0xff, 8, st));
+        const int grid = (int)(P.ntiles < grid_cap ? P.ntiles : grid_cap);
+        lc_quant_kernel<CodeT><<<grid, LC_TPB, lc_quant_smem_bytes(), st>>>(P, codes);
+        LC_CUDA_OK(cudaGetLastError());
+        LC_CUDA_OK(cudaMemcpyAsync(hbad, first_bad, 8, cudaMemcpyDeviceToHost, st));
+        LC_CUDA_OK(cudaStreamSynchronize(st));
+        const unsigned long long fb = *hbad;
+        if (fb == ~0ULL) break;
+        ++relaunches;
+        double anchor;
+        LC_CUDA_OK(cudaMemcpy(&anchor, P.bad_end + (fb - 1), sizeof(double), cudaMemcpyDeviceToHost));
+        P.first_chunk = (int64_t)fb;
+        P.anchor_val = anchor;
+        P.count_hist = 0;
+        if (relaunches > 64) {                      // pathological input: exact serial chain
+            lc_quant_serial_kernel<CodeT><<<1, 32, 0, st>>>(P, codes);
+            LC_CUDA_OK(cudaGetLastError());
+            break;
+        }
+    }
+    if (relaunches) {
+        LC_CUDA_OK(cudaMemsetAsync(P.hist, 0, nbins * sizeof(uint32_t), st));
+        lc_hist_kernel<CodeT><<<4 * ctx->sm_count, 256, 0, st>>>(codes, m, P.hist, nbins);
+        LC_CUDA_OK(cudaGetLastError());
+    }
+
+    // codebook
+    LC_CUDA_OK(lc_reserve(ctx->lengths, nbins));
+    LC_CUDA_OK(lc_reserve(ctx->cw, nbins * sizeof(unsigned long long)));
+    LC_CUDA_OK(lc_reserve(ctx->gkeys, 2 * (size_t)nbins * sizeof(unsigned long long)));
+    LC_CUDA_OK(lc_reserve(ctx->ifreq, (size_t)nbins * sizeof(unsigned long long)));
+    LC_CUDA_OK(lc_reserve(ctx->parent, 2 * (size_t)nbins * sizeof(int)));
+    LC_CUDA_OK(lc_reserve(ctx->cbout, sizeof(LcCodebookOut)));
+    LcCodebookOut *cbo = (LcCodebookOut *)ctx->cbout.p;
+    lc_codebook_kernel<<<1, 1024, lc_codebook_smem_bytes(), st>>>(
+        P.hist, nbins, (uint8_t *)ctx->lengths.p, (unsigned long long *)ctx->cw.p,
+        (unsigned long long *)ctx->gkeys.p, (unsigned long long *)ctx->ifreq.p, (int *)ctx->parent.p, cbo);
+    LC_CUDA_OK(cudaGetLastError());
+    LcCodebookOut *hcb = (LcCodebookOut *)ctx->pinned;
+    LC_CUDA_OK(cudaMemcpyAsync(hcb, cbo, sizeof(LcCodebookOut), cudaMemcpyDeviceToHost, st));
+    LC_CUDA_OK(cudaStreamSynchronize(st));
+    ctx->cb = *hcb;
+    if (ctx->cb.status) {
+        ctx->err = "code length exceeds 64 bits";
+        return ctx->cb.status;
+    }
+    const uint64_t words = (ctx->cb.total_bits + 31) / 32;
+    LC_CUDA_OK(lc_reserve(ctx->payload, (words + 1) * 4));
+    LC_CUDA_OK(lc_reserve(ctx->esc_idx, (ctx->cb.n_esc + 1) * 8));
+    LC_CUDA_OK(lc_reserve(ctx->esc_val, (ctx->cb.n_esc + 1) * 8));
+    lc_zero_words_kernel<<<2 * ctx->sm_count, 256, 0, st>>>((uint32_t *)ctx->payload.p, cbo);
+    const uint64_t etiles = (m + LC_TILE - 1) / LC_TILE;
+    LC_CUDA_OK(lc_reserve(ctx->encdesc, etiles * sizeof(LcEncDesc)));
+    LC_CUDA_OK(cudaMemsetAsync(ctx->encdesc.p, 0, etiles * sizeof(LcEncDesc), st));
+    LC_CUDA_OK(cudaMemsetAsync(ctx->counters.p, 0, 16, st));
+    LcEncParams E;
+    E.codes = codes;
+    E.m = m;
+    E.lengths = (const uint8_t *)ctx->lengths.p;
+    E.cw = (const unsigned long long *)ctx->cw.p;
+    E.nbins = nbins;
+    E.payload = (uint32_t *)ctx->payload.p;
+    E.x = dx;
+    E.esc_idx = (unsigned long long *)ctx->esc_idx.p;
+    E.esc_val = (double *)ctx->esc_val.p;
+    E.desc = (LcEncDesc *)ctx->encdesc.p;
+    E.tile_counter = tile_counter;
+    E.ntiles = etiles;
+    const int egrid = (int)(etiles < (uint64_t)(3 * ctx->sm_count) ? etiles : 3 * ctx->sm_count);
+    lc_encode_kernel<CodeT><<<egrid, LC_TPB, lc_encode_smem_bytes(), st>>>(E);
+    LC_CUDA_OK(cudaGetLastError());
+    LC_CUDA_OK(cudaEventRecord(ctx->ev1, st));
+    LC_CUDA_OK(cudaStreamSynchronize(st));
+
+    ctx->n = n;
+    ctx->nbins = nbins;
+    ctx->code_bytes = sizeof(CodeT);
+    ctx->record = record;
+    res->n = n;
+    res->payload_bits = ctx->cb.total_bits;
+    res->payload_bytes = (ctx->cb.total_bits + 7) / 8;
+    res->n_esc = ctx->cb.n_esc;
+    res->n_symbols = nbins;
+    res->max_len = (uint32_t)ctx->cb.max_len;
+    res->used_symbols = (uint32_t)ctx->cb.used;
+    res->relaunches = relaunches;
+    return 0;
+}
+
+extern "C" {
+
+int lc_compress_f64(lc_ctx *ctx, const double *x, uint64_t n, int x_on_device, double eb_abs,
+                    uint32_t n_bins_half, int record_traces, lc_result *res)
+{
+    if (!ctx || !res || n < 2 || n_bins_half < 1 || !(eb_abs > 0.0)) return 12;
+    if (!isfinite(2.0 * eb_abs)) return 11;
+    if (n_bins_half > (1u << 30)) return 12;
+    LC_CUDA_OK(cudaSetDevice(ctx->device));
+    LC_CUDA_OK(cudaEventRecord(ctx->ev0, ctx->stream));
+    int rc;
+    const double *dx = lc_device_input(ctx, x, n, x_on_device, &rc);
+    if (rc) return rc;
+    if (2ull * n_bins_half <= 65536ull) return lc_compress_t<uint16_t>(ctx, dx, n, eb_abs, n_bins_half, record_traces, res);
+    return lc_compress_t<uint32_t>(ctx, dx, n, eb_abs, n_bins_half, record_traces, res);
+}
+
+int lc_result_fetch(lc_ctx *ctx, uint8_t *code_lengths, uint8_t *payload, uint64_t *esc_idx, double *esc_val,
+                    double *pe, double *pe_rec)
+{
+    if (!ctx) return 12;
+    cudaStream_t st = ctx->stream;
+    if (code_lengths) LC_CUDA_OK(cudaMemcpyAsync(code_lengths, ctx->lengths.p, ctx->nbins, cudaMemcpyDeviceToHost, st));
+    const uint64_t pbytes = (ctx->cb.total_bits + 7) / 8;
+    if (payload && pbytes) LC_CUDA_OK(cudaMemcpyAsync(payload, ctx->payload.p, pbytes, cudaMemcpyDeviceToHost, st));
+    if (esc_idx && ctx->cb.n_esc)
+        LC_CUDA_OK(cudaMemcpyAsync(esc_idx, ctx->esc_idx.p, ctx->cb.n_esc * 8, cudaMemcpyDeviceToHost, st));
+    if (esc_val && ctx->cb.n_esc)
+        LC_CUDA_OK(cudaMemcpyAsync(esc_val, ctx->esc_val.p, ctx->cb.n_esc * 8, cudaMemcpyDeviceToHost, st));
+    if (ctx->record && pe) LC_CUDA_OK(cudaMemcpyAsync(pe, ctx->pe.p, (ctx->n - 1) * 8, cudaMemcpyDeviceToHost, st));
+    if (ctx->record && pe_rec)
+        LC_CUDA_OK(cudaMemcpyAsync(pe_rec, ctx->pe_rec.p, (ctx->n - 1) * 8, cudaMemcpyDeviceToHost, st));
+    LC_CUDA_OK(cudaStreamSynchronize(st));
+    return 0;
+}
+
+int lc_result_device(lc_ctx *ctx, const uint8_t **payload, const uint16_t **codes)
+{
+    if (!ctx) return 12;
+    if (payload) *payload = (const uint8_t *)ctx->payload.p;
+    if (codes) *codes = (const uint16_t *)ctx->codes.p;
+    return 0;
+}
+
+int lc_decompress_f64(lc_ctx *ctx, uint64_t n, double eb_abs, double first_value, const uint8_t *code_lengths,
+                      uint64_t n_lengths, const uint8_t *payload, uint64_t payload_bytes, uint64_t payload_bits,
+                      const uint64_t *esc_idx, const double *esc_val, uint64_t n_esc, int inputs_on_device,
+                      double *out, int out_on_device, int64_t *esc_used)
+{
+    if (!ctx) return 12;
+    LC_CUDA_OK(cudaSetDevice(ctx->device));
+    return lc_decompress_impl(ctx, n, eb_abs, first_value, code_lengths, n_lengths, payload, payload_bytes,
+                              payload_bits, esc_idx, esc_val, n_esc, inputs_on_device, out, out_on_device,
+                              esc_used);
+}
+
+// Debug/test hook: copy an intermediate of the last compress to host.
+// what: 0 codes, 1 histogram (u32), 2 code lengths (u8), 3 codewords (u64)
+int lc_debug_copy(lc_ctx *ctx, int what, void *host, uint64_t bytes)
+{
+    const void *src = what == 0 ? ctx->codes.p : what == 1 ? ctx->hist.p : what == 2 ? ctx->lengths.p : ctx->cw.p;
+    LC_CUDA_OK(cudaMemcpyAsync(host, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    LC_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    return 0;
+}
+
+}  // extern "C"
+
+cudaEvent_t lc_ev(lc_ctx *ctx, int which) { return which ? ctx->ev1 : ctx->ev0; }

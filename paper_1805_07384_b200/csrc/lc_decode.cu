@@ -1,0 +1,743 @@
+// lc_decode.cu -- chunk-parallel canonical Huffman decode and exact-chain
+// reconstruction (sm_100a).
+//
+// Replaces huffman.decode/_decode_tables/_decode_kernel (huffman.py:75-93,
+// 110-132, 153-172) and _decompress_kernel + the escape checks of
+// compressor.decompress (compressor.py:358-376, 420-440).
+//
+// Huffman decode of a v1 (LCKP0001) bitstream, which has no sync points:
+//   * the bitstream is cut into S-bit segments, one thread each;
+//   * sync passes: each segment decodes from its predecessor's exit position
+//     (initially its own start) until it crosses its end; passes repeat until
+//     no exit moves (canonical codes resynchronise within a few codewords);
+//   * counts are scanned to output offsets and a final pass writes symbols;
+//   * the first decoding anomaly on the true path reproduces the reference
+//     status (1 invalid codeword, 2 exhausted, 3 trailing bits).
+// Reconstruction runs the same chunked exact chain as the encoder
+// (lc_chain.cuh): guesses from the m-prefix since the last escape, offset
+// maps + look-back, exact re-run, end/start checks (host relaunch on failure).
+#include <cub/block/block_scan.cuh>
+#include "lc_kernels.cuh"
+#include "../../include/lossyckpt_b200.h"
+
+#define LC_SEG_BITS 1024
+#define LC_LUT_BITS 12
+
+struct LcDecTables {
+    int max_len;
+    int used;
+    int status;                      // 0 ok, 1 unsupported (max_len > 64)
+    int pad;
+    unsigned long long first_code[66];
+    unsigned long long count[66];
+    unsigned long long offset[66];
+    unsigned int lut[1 << LC_LUT_BITS];  // (len << 24) | sym; ~0 = no code of length <= LUT_BITS
+};
+
+// lengths[nl] -> tables + sorted symbols (canonical order)
+__global__ void __launch_bounds__(1024) lc_dec_tables_kernel(const uint8_t *__restrict__ lengths, uint32_t nl,
+                                                            LcDecTables *__restrict__ T,
+                                                            uint32_t *__restrict__ sorted)
+{
+    __shared__ int s_cnt[66];
+    __shared__ int s_wcnt[32][66];
+    __shared__ int s_max;
+    __shared__ unsigned long long s_first[66], s_off[66];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    if (tid < 66) s_cnt[tid] = 0;
+    if (tid == 0) s_max = 0;
+    for (int i = tid; i < 32 * 66; i += blockDim.x) (&s_wcnt[0][0])[i] = 0;
+    for (int i = tid; i < (1 << LC_LUT_BITS); i += blockDim.x) T->lut[i] = 0xffffffffu;
+    __syncthreads();
+    const uint32_t span = (nl + nw - 1) / nw;
+    const uint32_t sb = wid * span, se = min(nl, sb + span);
+    for (uint32_t s0 = sb; s0 < se; s0 += 32) {
+        const uint32_t s = s0 + lane;
+        const int l = s < se ? lengths[s] : 0;
+        if (l > 0) {
+            atomicMax(&s_max, l);
+            if (l <= 64) { atomicAdd(&s_wcnt[wid][l], 1); atomicAdd(&s_cnt[l], 1); }
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        // huffman.py:86-90 (first_code / offsets per length)
+        unsigned long long code = 0, off = 0;
+        const int ml = s_max;
+        int used = 0;
+        for (int l = 1; l <= 64; ++l) {
+            s_first[l] = code;
+            s_off[l] = off;
+            T->first_code[l] = code;
+            T->count[l] = s_cnt[l];
+            T->offset[l] = off;
+            code = (code + s_cnt[l]) << 1;
+            off += s_cnt[l];
+            used += s_cnt[l];
+        }
+        T->max_len = ml;
+        T->used = used;
+        T->status = ml > 64 ? 1 : 0;
+    }
+    __syncthreads();
+    if (tid >= 1 && tid <= 64 && s_cnt[tid]) {
+        int acc = 0;
+        for (int w = 0; w < nw; ++w) {
+            const int c0 = s_wcnt[w][tid];
+            s_wcnt[w][tid] = acc;
+            acc += c0;
+        }
+    }
+    __syncthreads();
+    for (uint32_t s0 = sb; s0 < se; s0 += 32) {
+        const uint32_t s = s0 + lane;
+        const int l = s < se ? lengths[s] : 0;
+        const unsigned peers = __match_any_sync(0xffffffffu, l);
+        if (l > 0 && l <= 64) {
+            const int rank = s_wcnt[wid][l] + __popc(peers & ((1u << lane) - 1u));
+            sorted[s_off[l] + rank] = s;
+            const unsigned long long cw = s_first[l] + rank;
+            // shortest length wins on a shared prefix (the reference tries
+            // lengths in increasing order); codes that overflow l bits never match
+            if (l <= LC_LUT_BITS && cw < (1ULL << l)) {
+                const uint32_t lo = (uint32_t)(cw << (LC_LUT_BITS - l));
+                const uint32_t nfill = 1u << (LC_LUT_BITS - l);
+                for (uint32_t f = 0; f < nfill; ++f) atomicMin(&T->lut[lo + f], ((uint32_t)l << 24) | s);
+            }
+        }
+        __syncwarp();
+        if (l > 0 && l <= 64 && (int)(__ffs(peers) - 1) == lane) s_wcnt[wid][l] += __popc(peers);
+        __syncwarp();
+    }
+}
+
+// 64 bits of the MSB-first stream starting at bit p (payload padded by >= 16 bytes)
+__device__ __forceinline__ unsigned long long lc_peek64(const uint32_t *__restrict__ w, unsigned long long p)
+{
+    const unsigned long long wi = p >> 5;
+    const int sh = (int)(p & 31);
+    const unsigned long long a = __byte_perm(__ldg(w + wi), 0, 0x0123);
+    const unsigned long long b = __byte_perm(__ldg(w + wi + 1), 0, 0x0123);
+    const unsigned long long hi = (a << 32) | b;
+    if (!sh) return hi;
+    const unsigned long long c = __byte_perm(__ldg(w + wi + 2), 0, 0x0123);
+    return (hi << sh) | (c >> (32 - sh));
+}
+
+// Decode one codeword at bit p.  Returns its length (>0) and *sym, or 0 for
+// "no codeword within max_len bits".
+__device__ __forceinline__ int lc_decode_one(const LcDecTables &T, const uint32_t *__restrict__ sorted,
+                                             unsigned long long win, int max_len, uint32_t *sym)
+{
+    const uint32_t e = T.lut[win >> (64 - LC_LUT_BITS)];
+    if (e != 0xffffffffu) { *sym = e & 0xffffffu; return (int)(e >> 24); }
+    for (int l = LC_LUT_BITS + 1; l <= max_len; ++l) {
+        const unsigned long long v = win >> (64 - l);
+        const unsigned long long rel = v - T.first_code[l];
+        if (v >= T.first_code[l] && rel < T.count[l]) { *sym = sorted[T.offset[l] + rel]; return l; }
+    }
+    return 0;
+}
+
+struct LcSeg {
+    unsigned long long start;   // bit where this segment's first codeword starts
+    unsigned long long exit;    // first codeword start >= segment end (or stop point)
+    unsigned int count;         // codewords started in [start, exit)
+    int term;                   // 0 none, 1 invalid, 2 exhausted, 4 clean end at bit_length
+};
+
+struct LcDecParams {
+    const uint32_t *payload;    // words (big-endian bit order inside bytes)
+    unsigned long long bits;    // bit_length
+    const LcDecTables *T;
+    const uint32_t *sorted;
+    unsigned long long nseg;
+};
+
+// Walk one segment from `start`.  Stops at the first codeword starting at or
+// after seg_end, at bit_length, or at an anomaly.
+__device__ void lc_walk(const LcDecParams &P, const LcDecTables &T, int max_len, unsigned long long start,
+                        unsigned long long seg_end, LcSeg &S, void *out, int out_bytes,
+                        unsigned long long out_off, unsigned long long out_cap,
+                        unsigned long long *end_pos_of_last, unsigned long long last_index)
+{
+    unsigned long long p = start;
+    unsigned int cnt = 0;
+    int term = 0;
+    while (p < seg_end) {
+        if (p >= P.bits) { term = 4; break; }
+        const unsigned long long remaining = P.bits - p;
+        uint32_t sym;
+        const int l = lc_decode_one(T, P.sorted, lc_peek64(P.payload, p), max_len, &sym);
+        if (l == 0) { term = remaining > (unsigned long long)max_len ? 1 : 2; break; }
+        if ((unsigned long long)l > remaining) { term = 2; break; }
+        if (out) {
+            const unsigned long long k = out_off + cnt;
+            if (k < out_cap) {
+                if (out_bytes == 2) ((uint16_t *)out)[k] = (uint16_t)sym;
+                else ((uint32_t *)out)[k] = sym;
+            }
+            if (k == last_index) *end_pos_of_last = p + l;
+        }
+        p += l;
+        ++cnt;
+    }
+    S.start = start;
+    S.exit = p;
+    S.count = cnt;
+    S.term = term;
+}
+
+__global__ void __launch_bounds__(256) lc_dec_sync_kernel(LcDecParams P, const LcSeg *__restrict__ prev,
+                                                         LcSeg *__restrict__ cur, int first_pass,
+                                                         int *__restrict__ changed)
+{
+    __shared__ LcDecTables Ts;
+    for (int i = threadIdx.x; i < (int)(sizeof(LcDecTables) / 4); i += blockDim.x)
+        reinterpret_cast<uint32_t *>(&Ts)[i] = reinterpret_cast<const uint32_t *>(P.T)[i];
+    __syncthreads();
+    const unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= P.nseg) return;
+    const unsigned long long seg_beg = t * LC_SEG_BITS, seg_end = seg_beg + LC_SEG_BITS;
+    unsigned long long start;
+    if (first_pass) start = seg_beg;
+    else if (t == 0) start = 0;
+    else {
+        const LcSeg pp = prev[t - 1];
+        // predecessor stopped early (anomaly / end): nothing real starts here
+        start = pp.term ? ~0ULL : pp.exit;
+        if (start == prev[t].start) { cur[t] = prev[t]; return; }
+    }
+    LcSeg S;
+    if (start == ~0ULL) { S.start = ~0ULL; S.exit = ~0ULL; S.count = 0; S.term = 8; }
+    else lc_walk(P, Ts, Ts.max_len, start, seg_end, S, nullptr, 0, 0, 0, nullptr, 0);
+    if (!first_pass && (S.exit != prev[t].exit || S.term != prev[t].term)) atomicExch(changed, 1);
+    if (first_pass) atomicExch(changed, 1);
+    cur[t] = S;
+}
+
+// exclusive scan of segment counts (single block, sequential chunks)
+__global__ void __launch_bounds__(1024) lc_dec_scan_kernel(const LcSeg *__restrict__ seg, unsigned long long nseg,
+                                                          unsigned long long *__restrict__ off,
+                                                          unsigned long long *__restrict__ total_and_term)
+{
+    typedef cub::BlockScan<unsigned long long, 1024> Scan;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ unsigned long long carry;
+    __shared__ unsigned long long first_term;
+    if (threadIdx.x == 0) { carry = 0; first_term = ~0ULL; }
+    __syncthreads();
+    for (unsigned long long b = 0; b < nseg; b += 1024) {
+        const unsigned long long i = b + threadIdx.x;
+        const unsigned long long c = i < nseg ? seg[i].count : 0;
+        if (i < nseg && seg[i].term && seg[i].term != 8) atomicMin(&first_term, i);
+        unsigned long long ex, agg;
+        Scan(tmp).ExclusiveSum(c, ex, agg);
+        if (i < nseg) off[i] = carry + ex;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += agg;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) { total_and_term[0] = carry; total_and_term[1] = first_term; }
+}
+
+__global__ void __launch_bounds__(256) lc_dec_write_kernel(LcDecParams P, const LcSeg *__restrict__ seg,
+                                                          const unsigned long long *__restrict__ off,
+                                                          void *out, int out_bytes, unsigned long long m,
+                                                          unsigned long long *__restrict__ end_pos)
+{
+    __shared__ LcDecTables Ts;
+    for (int i = threadIdx.x; i < (int)(sizeof(LcDecTables) / 4); i += blockDim.x)
+        reinterpret_cast<uint32_t *>(&Ts)[i] = reinterpret_cast<const uint32_t *>(P.T)[i];
+    __syncthreads();
+    const unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= P.nseg) return;
+    const LcSeg S0 = seg[t];
+    if (S0.start == ~0ULL || S0.count == 0) return;
+    const unsigned long long o = off[t];
+    if (o >= m) return;
+    LcSeg S;
+    lc_walk(P, Ts, Ts.max_len, S0.start, (t + 1) * LC_SEG_BITS, S, out, out_bytes, o, m, end_pos, m - 1);
+}
+
+// Resolve the reference status (huffman.py:114-132) from the segment walk.
+__global__ void lc_dec_status_kernel(const LcSeg *__restrict__ seg, const unsigned long long *__restrict__ off,
+                                     const unsigned long long *__restrict__ total_and_term,
+                                     const unsigned long long *__restrict__ end_pos, unsigned long long m,
+                                     unsigned long long bits, int *__restrict__ status)
+{
+    const unsigned long long ft = total_and_term[1];
+    unsigned long long K = total_and_term[0];   // symbols on the path when no anomaly
+    int term = 4;
+    if (ft != ~0ULL) { K = off[ft] + seg[ft].count; term = seg[ft].term; }
+    int st;
+    if (m <= K) st = (*end_pos == bits) ? 0 : 3;
+    else st = (term == 4) ? 2 : term;           // ran out exactly at bit_length -> exhausted
+    *status = st;
+}
+
+// ---------------------------------------------------------------------------
+// reconstruction
+
+struct LcSegScan {             // running state of the escape-segmented m-prefix
+    long long sum;              // sum of m since the last escape (or the start)
+    long long cnt;              // escape codes so far
+    int has;                    // an escape occurred
+    int moved;                  // a non-zero m occurred since the last escape
+};
+
+__device__ __forceinline__ LcSegScan lc_segscan_op(const LcSegScan &a, const LcSegScan &b)
+{
+    LcSegScan r;
+    r.sum = b.has ? b.sum : a.sum + b.sum;
+    r.cnt = a.cnt + b.cnt;
+    r.has = a.has | b.has;
+    r.moved = b.has ? b.moved : (a.moved | b.moved);
+    return r;
+}
+
+struct LcRecDesc {
+    int st_seg, st_map;
+    long long seg_agg_sum, seg_agg_cnt, seg_inc_sum, seg_inc_cnt;
+    int seg_agg_has, seg_inc_has;
+    int map_kind, pad;
+    double mv, mB, mt0, mt1, my, mog;
+    double incl_D;
+};
+
+struct LcRecParams {
+    const void *codes;
+    int code_bytes;
+    uint64_t n;                 // elements (codes: n-1)
+    double delta;
+    double first_value;
+    const double *esc_val;
+    const unsigned long long *esc_idx;
+    unsigned long long n_esc;
+    int64_t first_chunk;
+    double anchor_val;          // exact value at position first_chunk*L
+    long long anchor_cnt;       // escapes before position first_chunk*L (inclusive)
+    int64_t nchunks, ntiles;
+    LcRecDesc *desc;
+    unsigned int *tile_counter;
+    double *out;
+    unsigned long long *first_bad;
+    double *bad_end;
+    long long *chunk_esc;       // escapes up to each chunk's start (inclusive of position cL)
+    int *esc_flags;             // [0] more escape codes than values, [1] position mismatch
+};
+
+__device__ __forceinline__ int64_t lc_code_m(uint32_t code) { return lc_unzigzag(code); }
+
+__global__ void __launch_bounds__(LC_TPB, 2) lc_recon_kernel(LcRecParams P)
+{
+    typedef cub::BlockScan<long long, LC_TPB> ScanLL;
+    extern __shared__ __align__(16) unsigned char lc_dyn_smem[];
+    double *ys = reinterpret_cast<double *>(lc_dyn_smem);            // outputs, padded rows
+    uint32_t *cs = reinterpret_cast<uint32_t *>(ys + LC_TPB * LC_ROW); // codes, padded rows
+    __shared__ typename ScanLL::TempStorage scan_tmp;
+    __shared__ OffMap warp_agg[LC_TPB / 32];
+    __shared__ LcSegScan warp_seg[LC_TPB / 32];
+    __shared__ long long sh_tile;
+    __shared__ LcSegScan sh_seg_in;
+    __shared__ double sh_Din;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) sh_tile = atomicAdd(P.tile_counter, 1u);
+        __syncthreads();
+        const long long t = sh_tile;
+        if (t >= P.ntiles) break;
+        const long long cbeg = P.first_chunk + t * LC_TPB;
+        const long long pbeg = cbeg * LC_L;
+        const long long c = cbeg + tid;
+        const long long p0 = c * LC_L;
+        const long long nel = (long long)P.n - 1;
+        const int len = (c < P.nchunks) ? (int)min((long long)LC_L, nel - p0) : 0;
+#pragma unroll 8
+        for (int k = 0; k < LC_L; ++k) {
+            const int off = k * LC_TPB + tid;
+            const long long pos = pbeg + off;          // code index (element pos+1)
+            uint32_t v = 0;
+            if (pos < nel) v = P.code_bytes == 2 ? (uint32_t)reinterpret_cast<const uint16_t *>(P.codes)[pos]
+                                                 : reinterpret_cast<const uint32_t *>(P.codes)[pos];
+            cs[(off >> 5) * LC_ROW + (off & 31)] = v;
+        }
+        __syncthreads();
+        const uint32_t *crow = cs + tid * LC_ROW;
+
+        // ---- escape-segmented m prefix ----------------------------------------------
+        LcSegScan mine; mine.sum = 0; mine.cnt = 0; mine.has = 0; mine.moved = 0;
+        for (int j = 0; j < len; ++j) {
+            const uint32_t code = crow[j];
+            if (code == 0) { mine.sum = 0; mine.cnt += 1; mine.has = 1; mine.moved = 0; }
+            else { const int64_t mm = lc_code_m(code); mine.sum += mm; mine.moved |= (mm != 0); }
+        }
+        LcSegScan inc = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            LcSegScan up;
+            up.sum = __shfl_up_sync(0xffffffffu, inc.sum, o);
+            up.cnt = __shfl_up_sync(0xffffffffu, inc.cnt, o);
+            up.has = __shfl_up_sync(0xffffffffu, inc.has, o);
+            up.moved = __shfl_up_sync(0xffffffffu, inc.moved, o);
+            if (lane >= o) inc = lc_segscan_op(up, inc);
+        }
+        if (lane == 31) warp_seg[wid] = inc;
+        __syncthreads();
+        if (tid == 0)
+            for (int w = 1; w < LC_TPB / 32; ++w) warp_seg[w] = lc_segscan_op(warp_seg[w - 1], warp_seg[w]);
+        __syncthreads();
+        if (wid > 0) inc = lc_segscan_op(warp_seg[wid - 1], inc);
+        LcSegScan exc;
+        exc.sum = __shfl_up_sync(0xffffffffu, inc.sum, 1);
+        exc.cnt = __shfl_up_sync(0xffffffffu, inc.cnt, 1);
+        exc.has = __shfl_up_sync(0xffffffffu, inc.has, 1);
+        exc.moved = __shfl_up_sync(0xffffffffu, inc.moved, 1);
+        if (lane == 0) {
+            if (wid > 0) exc = warp_seg[wid - 1];
+            else { exc.sum = 0; exc.cnt = 0; exc.has = 0; exc.moved = 0; }
+        }
+        if (tid == 0) {
+            LcRecDesc *d = P.desc + t;
+            const LcSegScan agg = warp_seg[LC_TPB / 32 - 1];
+            LcSegScan in;
+            if (t == 0) {
+                in.sum = 0; in.cnt = P.anchor_cnt; in.has = 1; in.moved = 0;   // anchored at the launch start
+            } else {
+                __stcg(&d->seg_agg_sum, agg.sum); __stcg(&d->seg_agg_cnt, agg.cnt);
+                __stcg(&d->seg_agg_has, agg.has | (agg.moved << 1));
+                st_release(&d->st_seg, 1);
+                LcSegScan acc; acc.sum = 0; acc.cnt = 0; acc.has = 0; acc.moved = 0;  // later tiles
+                for (long long k = t - 1; k >= 0; --k) {
+                    const LcRecDesc *dk = P.desc + k;
+                    int st;
+                    while ((st = ld_acquire(&dk->st_seg)) == 0) { }
+                    LcSegScan v;
+                    int hm;
+                    if (st == 2) {
+                        v.sum = __ldcg(&dk->seg_inc_sum); v.cnt = __ldcg(&dk->seg_inc_cnt); hm = __ldcg(&dk->seg_inc_has);
+                        v.has = hm & 1; v.moved = hm >> 1;
+                        acc = lc_segscan_op(v, acc);
+                        break;
+                    }
+                    v.sum = __ldcg(&dk->seg_agg_sum); v.cnt = __ldcg(&dk->seg_agg_cnt); hm = __ldcg(&dk->seg_agg_has);
+                    v.has = hm & 1; v.moved = hm >> 1;
+                    acc = lc_segscan_op(v, acc);
+                }
+                in = acc;
+            }
+            const LcSegScan incl = lc_segscan_op(in, agg);
+            __stcg(&d->seg_inc_sum, incl.sum); __stcg(&d->seg_inc_cnt, incl.cnt);
+            __stcg(&d->seg_inc_has, incl.has | (incl.moved << 1));
+            st_release(&d->st_seg, 2);
+            sh_seg_in = in;
+        }
+        __syncthreads();
+        const LcSegScan before = lc_segscan_op(sh_seg_in, exc);    // state at position cL
+        const LcSegScan after = lc_segscan_op(before, mine);       // state at position cL + len
+        // anchor: the last escape value (or the launch anchor when none since)
+        auto anchor_of = [&](const LcSegScan &s) -> double {
+            if (s.cnt > P.anchor_cnt) {
+                const long long e = s.cnt - 1;
+                return e < (long long)P.n_esc ? P.esc_val[e] : 0.0;
+            }
+            return P.anchor_val;
+        };
+        auto guess_of = [&](const LcSegScan &s) -> double {
+            const double a = anchor_of(s);
+            if (!s.moved) return a;                  // chain still sits on the anchor value
+            const double g = LC_ADD(a, LC_MUL((double)s.sum, P.delta));
+            return isfinite(g) ? g : a;
+        };
+        const double g0 = guess_of(before);
+        const double g1 = guess_of(after);
+        if (len > 0) P.chunk_esc[c] = before.cnt;
+
+        // ---- phase A: guess chain -> offset map ---------------------------------------
+        OffMap H;
+        if (len > 0) {
+            double r = g0;
+            long long e = before.cnt;
+            H = lc_map_identity(lc_ulp(g0));
+            for (int j = 0; j < len; ++j) {
+                const uint32_t code = crow[j];
+                if (code == 0) {
+                    r = e < (long long)P.n_esc ? P.esc_val[e] : 0.0;
+                    ++e;
+                    H = lc_map_const(0.0);
+                } else {
+                    const int64_t m = lc_code_m(code);
+                    if (m != 0) {
+                        const double inc_ = LC_MUL((double)m, P.delta);
+                        const double rn = LC_ADD(r, inc_);
+                        lc_map_step(H, r, inc_, rn);
+                        r = rn;
+                    }
+                }
+            }
+            if (c + 1 < P.nchunks) lc_map_shift_out(H, LC_SUB(r, g1));
+        } else {
+            H = lc_map_neutral();
+        }
+        OffMap inc_map = H;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const OffMap up = lc_shfl_up_map(inc_map, o);
+            if (lane >= o) inc_map = lc_map_compose(inc_map, up);
+        }
+        if (lane == 31) warp_agg[wid] = inc_map;
+        __syncthreads();
+        if (tid == 0)
+            for (int w = 1; w < LC_TPB / 32; ++w) warp_agg[w] = lc_map_compose(warp_agg[w], warp_agg[w - 1]);
+        __syncthreads();
+        if (wid > 0) inc_map = lc_map_compose(inc_map, warp_agg[wid - 1]);
+        OffMap exc_map = lc_shfl_up_map(inc_map, 1);
+        if (lane == 0) exc_map = wid > 0 ? warp_agg[wid - 1] : lc_map_neutral();
+        if (tid == 0) {
+            LcRecDesc *d = P.desc + t;
+            const OffMap agg = warp_agg[LC_TPB / 32 - 1];
+            double Din = 0.0;
+            if (t > 0) {
+                d->map_kind = agg.kind; d->mv = agg.v; d->mB = agg.B; d->mt0 = agg.t0; d->mt1 = agg.t1;
+                d->my = agg.y; d->mog = agg.og;
+                st_release(&d->st_map, 1);
+                OffMap acc = lc_map_neutral();
+                for (long long k = t - 1; k >= 0; --k) {
+                    const LcRecDesc *dk = P.desc + k;
+                    int st;
+                    while ((st = ld_acquire(&dk->st_map)) == 0) { }
+                    if (st == 2) { Din = lc_map_eval(acc, __ldcg(&dk->incl_D)); break; }
+                    OffMap mk;
+                    mk.kind = __ldcg(&dk->map_kind); mk.v = __ldcg(&dk->mv); mk.B = __ldcg(&dk->mB);
+                    mk.t0 = __ldcg(&dk->mt0); mk.t1 = __ldcg(&dk->mt1); mk.y = __ldcg(&dk->my); mk.og = __ldcg(&dk->mog);
+                    acc = lc_map_compose(acc, mk);
+                }
+            }
+            __stcg(&d->incl_D, lc_map_eval(agg, Din));
+            st_release(&d->st_map, 2);
+            sh_Din = Din;
+        }
+        __syncthreads();
+        const double Din = sh_Din;
+        const double start = lc_apply_offset(g0, lc_map_eval(exc_map, Din));
+        const double next_pred = lc_apply_offset(g1, lc_map_eval(inc_map, Din));
+
+        // ---- phase B: exact chain (compressor.py:358-376) ----------------------------
+        {
+            double r = start;
+            long long e = before.cnt;
+            double *yrow = ys + tid * LC_ROW;
+            for (int j = 0; j < len; ++j) {
+                const uint32_t code = crow[j];
+                if (code == 0) {
+                    if (e < (long long)P.n_esc) {
+                        r = P.esc_val[e];
+                        if (P.esc_idx[e] != (unsigned long long)(p0 + j + 1)) atomicExch(&P.esc_flags[1], 1);
+                    } else {
+                        atomicExch(&P.esc_flags[0], 1);
+                    }
+                    ++e;
+                } else {
+                    const int64_t m = lc_code_m(code);
+                    if (m != 0) r = LC_ADD(r, LC_MUL((double)m, P.delta));
+                }
+                yrow[j] = r;
+            }
+            if (len > 0 && c + 1 < P.nchunks && lc_bits(r) != lc_bits(next_pred)) {
+                P.bad_end[c] = r;
+                atomicMin(P.first_bad, (unsigned long long)(c + 1));
+            }
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int k = 0; k < LC_L; ++k) {
+            const int off = k * LC_TPB + tid;
+            const long long pos = pbeg + 1 + off;        // element index
+            if (pos <= nel) __stcs(P.out + pos, ys[(off >> 5) * LC_ROW + (off & 31)]);
+        }
+    }
+}
+
+size_t lc_recon_smem_bytes() { return sizeof(double) * LC_TPB * LC_ROW + sizeof(uint32_t) * LC_TPB * LC_ROW; }
+
+__global__ void lc_set_first_kernel(double *out, double v) { out[0] = v; }
+
+// ---------------------------------------------------------------------------
+// driver
+
+struct LcBuf { void *p = nullptr; size_t cap = 0; };   // same as lc_api.cu
+cudaError_t lc_reserve(LcBuf &b, size_t bytes);
+int lc_fail(lc_ctx *ctx, cudaError_t e, const char *what, const char *file, int line);
+cudaStream_t lc_stream(lc_ctx *ctx);
+int lc_sm_count(lc_ctx *ctx);
+void *lc_pinned(lc_ctx *ctx);
+void lc_set_err(lc_ctx *ctx, const char *msg);
+LcBuf *lc_dec_bufs(lc_ctx *ctx);
+cudaEvent_t lc_ev(lc_ctx *ctx, int which);
+
+int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_value,
+                       const uint8_t *code_lengths, uint64_t n_lengths, const uint8_t *payload,
+                       uint64_t payload_bytes, uint64_t payload_bits, const uint64_t *esc_idx,
+                       const double *esc_val, uint64_t n_esc, int inputs_on_device, double *out,
+                       int out_on_device, int64_t *esc_used)
+{
+    if (n < 2 || n_lengths == 0 || payload_bits > 8 * payload_bytes) return 12;
+    static bool attr_done = false;
+    if (!attr_done) {
+        LC_CUDA_OK(cudaFuncSetAttribute(lc_recon_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)lc_recon_smem_bytes()));
+        attr_done = true;
+    }
+    cudaStream_t st = lc_stream(ctx);
+    LcBuf *B = lc_dec_bufs(ctx);      // ctx->dec[10]
+    LcBuf &bpay = B[0], &blen = B[1], &beidx = B[2], &beval = B[3], &bout = B[4], &bcodes = B[5], &btab = B[6],
+          &bsync = B[7], &baux = B[8], &baux2 = B[9];
+    LC_CUDA_OK(cudaEventRecord(lc_ev(ctx, 0), st));
+    const uint64_t m = n - 1;
+    const uint64_t words = (payload_bytes + 3) / 4 + 4;
+    LC_CUDA_OK(lc_reserve(bpay, words * 4));
+    LC_CUDA_OK(cudaMemsetAsync(bpay.p, 0, words * 4, st));
+    LC_CUDA_OK(cudaMemcpyAsync(bpay.p, payload, payload_bytes,
+                               inputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    LC_CUDA_OK(lc_reserve(blen, n_lengths));
+    LC_CUDA_OK(cudaMemcpyAsync(blen.p, code_lengths, n_lengths,
+                               inputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    LC_CUDA_OK(lc_reserve(beidx, (n_esc + 1) * 8));
+    LC_CUDA_OK(lc_reserve(beval, (n_esc + 1) * 8));
+    if (n_esc) {
+        const cudaMemcpyKind k = inputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+        LC_CUDA_OK(cudaMemcpyAsync(beidx.p, esc_idx, n_esc * 8, k, st));
+        LC_CUDA_OK(cudaMemcpyAsync(beval.p, esc_val, n_esc * 8, k, st));
+    }
+    // tables
+    LC_CUDA_OK(lc_reserve(btab, sizeof(LcDecTables) + n_lengths * 4 + 64));
+    LcDecTables *T = (LcDecTables *)btab.p;
+    uint32_t *sorted = (uint32_t *)((char *)btab.p + sizeof(LcDecTables));
+    lc_dec_tables_kernel<<<1, 1024, 0, st>>>((const uint8_t *)blen.p, (uint32_t)n_lengths, T, sorted);
+    LC_CUDA_OK(cudaGetLastError());
+    // Huffman decode
+    const int code_bytes = n_lengths <= 65536 ? 2 : 4;
+    LC_CUDA_OK(lc_reserve(bcodes, m * code_bytes + 16));
+    const unsigned long long nseg = (payload_bits + LC_SEG_BITS - 1) / LC_SEG_BITS + 1;
+    LC_CUDA_OK(lc_reserve(bsync, 2 * nseg * sizeof(LcSeg) + nseg * 8 + 64));
+    LcSeg *sa = (LcSeg *)bsync.p, *sb = sa + nseg;
+    unsigned long long *offs = (unsigned long long *)(sb + nseg);
+    LC_CUDA_OK(lc_reserve(baux, 256));
+    int *changed = (int *)baux.p;
+    unsigned long long *tot = (unsigned long long *)((char *)baux.p + 16);
+    unsigned long long *endpos = (unsigned long long *)((char *)baux.p + 48);
+    int *status = (int *)((char *)baux.p + 64);
+    int *esc_flags = (int *)((char *)baux.p + 80);
+    LcDecParams DP;
+    DP.payload = (const uint32_t *)bpay.p;
+    DP.bits = payload_bits;
+    DP.T = T;
+    DP.sorted = sorted;
+    DP.nseg = nseg;
+    const int sblocks = (int)((nseg + 255) / 256);
+    int *hchanged = (int *)lc_pinned(ctx);
+    LC_CUDA_OK(cudaMemsetAsync(changed, 0, 4, st));
+    lc_dec_sync_kernel<<<sblocks, 256, 0, st>>>(DP, sa, sa, 1, changed);
+    LC_CUDA_OK(cudaGetLastError());
+    LcSeg *prev = sa, *cur = sb;
+    for (int it = 0; it < 100000; ++it) {
+        LC_CUDA_OK(cudaMemsetAsync(changed, 0, 4, st));
+        lc_dec_sync_kernel<<<sblocks, 256, 0, st>>>(DP, prev, cur, 0, changed);
+        LC_CUDA_OK(cudaGetLastError());
+        LcSeg *tmp = prev; prev = cur; cur = tmp;
+        if (it % 2 == 1 || it > 8) {
+            LC_CUDA_OK(cudaMemcpyAsync(hchanged, changed, 4, cudaMemcpyDeviceToHost, st));
+            LC_CUDA_OK(cudaStreamSynchronize(st));
+            if (!*hchanged) break;
+        }
+    }
+    lc_dec_scan_kernel<<<1, 1024, 0, st>>>(prev, nseg, offs, tot);
+    LC_CUDA_OK(cudaMemsetAsync(endpos, 0xff, 8, st));
+    lc_dec_write_kernel<<<sblocks, 256, 0, st>>>(DP, prev, offs, bcodes.p, code_bytes, m, endpos);
+    lc_dec_status_kernel<<<1, 1, 0, st>>>(prev, offs, tot, endpos, m, payload_bits, status);
+    LC_CUDA_OK(cudaGetLastError());
+    int *hstat = (int *)lc_pinned(ctx);
+    LC_CUDA_OK(cudaMemcpyAsync(hstat, status, 4, cudaMemcpyDeviceToHost, st));
+    LC_CUDA_OK(cudaStreamSynchronize(st));
+    if (*hstat) return *hstat;
+
+    // reconstruction
+    double *dout = out;
+    if (!out_on_device) {
+        LC_CUDA_OK(lc_reserve(bout, n * 8));
+        dout = (double *)bout.p;
+    }
+    const int64_t nchunks = (int64_t)((m + LC_L - 1) / LC_L);
+    const int64_t ntiles = (nchunks + LC_TPB - 1) / LC_TPB;
+    LC_CUDA_OK(lc_reserve(baux2, ntiles * sizeof(LcRecDesc) + nchunks * 16 + 64));
+    LcRecParams R;
+    R.codes = bcodes.p;
+    R.code_bytes = code_bytes;
+    R.n = n;
+    R.delta = 2.0 * eb_abs;
+    R.first_value = first_value;
+    R.esc_val = (const double *)beval.p;
+    R.esc_idx = (const unsigned long long *)beidx.p;
+    R.n_esc = n_esc;
+    R.first_chunk = 0;
+    R.anchor_val = first_value;
+    R.anchor_cnt = 0;
+    R.nchunks = nchunks;
+    R.desc = (LcRecDesc *)baux2.p;
+    R.tile_counter = (unsigned int *)((char *)baux.p + 96);
+    R.out = dout;
+    R.first_bad = (unsigned long long *)((char *)baux.p + 112);
+    R.bad_end = (double *)((char *)baux2.p + ntiles * sizeof(LcRecDesc));
+    R.chunk_esc = (long long *)(R.bad_end + nchunks);
+    R.esc_flags = esc_flags;
+    LC_CUDA_OK(cudaMemsetAsync(esc_flags, 0, 8, st));
+    lc_set_first_kernel<<<1, 1, 0, st>>>(dout, first_value);
+    const int grid_cap = 2 * lc_sm_count(ctx);
+    unsigned long long *hbad = (unsigned long long *)lc_pinned(ctx);
+    int relaunches = 0;
+    for (;;) {
+        R.ntiles = (nchunks - R.first_chunk + LC_TPB - 1) / LC_TPB;
+        LC_CUDA_OK(cudaMemsetAsync(R.desc, 0, R.ntiles * sizeof(LcRecDesc), st));
+        LC_CUDA_OK(cudaMemsetAsync(R.tile_counter, 0, 4, st));
+        LC_CUDA_OK(cudaMemsetAsync(R.first_bad, 0xff, 8, st));
+        const int grid = (int)(R.ntiles < grid_cap ? R.ntiles : grid_cap);
+        lc_recon_kernel<<<grid, LC_TPB, lc_recon_smem_bytes(), st>>>(R);
+        LC_CUDA_OK(cudaGetLastError());
+        LC_CUDA_OK(cudaMemcpyAsync(hbad, R.first_bad, 8, cudaMemcpyDeviceToHost, st));
+        LC_CUDA_OK(cudaStreamSynchronize(st));
+        if (*hbad == ~0ULL) break;
+        const unsigned long long fb = *hbad;
+        ++relaunches;
+        double anchor;
+        long long acnt;
+        LC_CUDA_OK(cudaMemcpy(&anchor, R.bad_end + (fb - 1), 8, cudaMemcpyDeviceToHost));
+        LC_CUDA_OK(cudaMemcpy(&acnt, R.chunk_esc + fb, 8, cudaMemcpyDeviceToHost));
+        R.first_chunk = (int64_t)fb;
+        R.anchor_val = anchor;
+        R.anchor_cnt = acnt;
+        if (relaunches > 100000) { lc_set_err(ctx, "reconstruction did not converge"); return 20; }
+    }
+    // escape checks (compressor.py:435-439)
+    int hflags[2];
+    long long total_esc;
+    LC_CUDA_OK(cudaMemcpy(hflags, esc_flags, 8, cudaMemcpyDeviceToHost));
+    {
+        // total escape codes = tile-inclusive count of the last tile of the first launch chain
+        LcSegScan s;
+        LcRecDesc last;
+        (void)s;
+        LC_CUDA_OK(cudaMemcpy(&last, R.desc + (R.ntiles - 1), sizeof(LcRecDesc), cudaMemcpyDeviceToHost));
+        total_esc = last.seg_inc_cnt;
+    }
+    int64_t used = hflags[0] ? -1 : total_esc;
+    if (esc_used) *esc_used = used;
+    if (used < 0 || (uint64_t)used != n_esc) return 4;
+    if (n_esc && hflags[1]) return 5;
+    if (!out_on_device)
+        LC_CUDA_OK(cudaMemcpyAsync(out, dout, n * 8, cudaMemcpyDeviceToHost, st));
+    LC_CUDA_OK(cudaEventRecord(lc_ev(ctx, 1), st));
+    LC_CUDA_OK(cudaStreamSynchronize(st));
+    return 0;
+}

@@ -1,0 +1,70 @@
+// lc_kernels.cuh -- parameter structs and kernel declarations shared by the
+// .cu translation units and the C-ABI driver (lc_api.cu).
+#pragma once
+#include "lc_common.cuh"
+
+struct LcRangePart { double vmin, vmax; int nonfinite; };
+
+struct LcQuantParams {
+    const double *x;
+    uint64_t n;              // elements; codes cover positions 1..n-1
+    LcQuant Q;
+    double esc_thresh;       // |x_i - x_{i-1}| test for definite escapes
+    int64_t first_chunk;     // relaunch start chunk (0 for a fresh run)
+    double anchor_val;       // exact chain value at position first_chunk*L
+    int64_t nchunks;         // total chunks ceil((n-1)/L)
+    int64_t ntiles;          // tiles in this launch
+    LcTileDesc *desc;
+    unsigned int *tile_counter;
+    uint32_t *hist;          // global histogram [nbins]
+    uint32_t nbins;
+    int count_hist;
+    unsigned long long *first_bad;
+    double *bad_end;         // per chunk: exact end value when its successor failed
+    double *pe, *pe_rec;     // optional traces
+};
+
+struct LcCodebookOut {
+    unsigned long long total_bits;
+    unsigned long long n_esc;
+    int max_len;
+    int used;
+    int status;              // 0 ok, 13 code length > 64
+    int pad;
+};
+
+struct LcEncDesc {
+    int st;
+    int pad;
+    unsigned long long agg_bits, agg_esc, incl_bits, incl_esc;
+};
+
+struct LcEncParams {
+    const void *codes;       // u16 or u32 symbols [m]
+    uint64_t m;              // number of symbols (n-1)
+    const uint8_t *lengths;
+    const unsigned long long *cw;
+    uint32_t nbins;
+    uint32_t *payload;       // words, zeroed
+    const double *x;         // for escape values
+    unsigned long long *esc_idx;
+    double *esc_val;
+    LcEncDesc *desc;
+    unsigned int *tile_counter;
+    uint64_t ntiles;
+};
+
+__global__ void lc_range_kernel(const double *__restrict__ x, uint64_t n, LcRangePart *__restrict__ parts);
+__global__ void lc_range_final_kernel(const LcRangePart *__restrict__ parts, int np, LcRangePart *__restrict__ out);
+template <typename CodeT> __global__ void lc_quant_kernel(LcQuantParams P, CodeT *__restrict__ codes);
+template <typename CodeT> __global__ void lc_quant_serial_kernel(LcQuantParams P, CodeT *__restrict__ codes);
+template <typename CodeT>
+__global__ void lc_hist_kernel(const CodeT *__restrict__ codes, uint64_t m, uint32_t *__restrict__ hist, uint32_t nbins);
+__global__ void lc_codebook_kernel(const uint32_t *__restrict__ hist, uint32_t nbins, uint8_t *__restrict__ lengths,
+                                   unsigned long long *__restrict__ codes, unsigned long long *__restrict__ gkeys,
+                                   unsigned long long *__restrict__ ifreq, int *__restrict__ parent, LcCodebookOut *out);
+__global__ void lc_zero_words_kernel(uint32_t *__restrict__ p, const LcCodebookOut *__restrict__ cb);
+template <typename CodeT> __global__ void lc_encode_kernel(LcEncParams P);
+size_t lc_quant_smem_bytes();
+size_t lc_codebook_smem_bytes();
+size_t lc_encode_smem_bytes();

@@ -1,0 +1,348 @@
+// lc_quant.cu -- value range + fused exact-chain quantizer (sm_100a).
+//
+// Replaces compressor.py:384-386 (isfinite/min/max) and the sequential
+// _compress_kernel (compressor.py:319-355) + np.bincount (compressor.py:411).
+//
+// lc_quant_kernel processes tiles of 256 chunks x 32 elements with a
+// persistent grid and two decoupled look-backs per tile:
+//   phase 0  definite-escape positions (max scan): anchors the guesses
+//   phase A  guess chain per chunk -> offset map (lc_chain.cuh)
+//            block scan + look-back of the maps -> exact start of each chunk
+//   phase B  exact reference chain from that start: codes, histogram,
+//            optional traces; each chunk checks its end against the next
+//            chunk's predicted start (first failure -> host relaunch).
+#include <cub/block/block_scan.cuh>
+#include "lc_kernels.cuh"
+
+// ---------------------------------------------------------------------------
+// range: min, max, non-finite flag
+
+
+__global__ void __launch_bounds__(256) lc_range_kernel(const double *__restrict__ x, uint64_t n,
+                                                      LcRangePart *__restrict__ parts)
+{
+    double mn = INFINITY, mx = -INFINITY;
+    int nf = 0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // 2-way unrolled grid-stride loop (coalesced 8-byte loads)
+    for (; i + stride < n; i += 2 * stride) {
+        const double a = __ldcs(x + i), b = __ldcs(x + i + stride);
+        nf |= !isfinite(a) | !isfinite(b);
+        mn = fmin(mn, fmin(a, b));
+        mx = fmax(mx, fmax(a, b));
+    }
+    if (i < n) {
+        const double a = __ldcs(x + i);
+        nf |= !isfinite(a);
+        mn = fmin(mn, a);
+        mx = fmax(mx, a);
+    }
+    for (int o = 16; o; o >>= 1) {
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        nf |= __shfl_xor_sync(0xffffffffu, nf, o);
+    }
+    __shared__ double smn[8], smx[8];
+    __shared__ int snf[8];
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) { smn[w] = mn; smx[w] = mx; snf[w] = nf; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+            mn = fmin(mn, smn[k]); mx = fmax(mx, smx[k]); nf |= snf[k];
+        }
+        parts[blockIdx.x].vmin = mn;
+        parts[blockIdx.x].vmax = mx;
+        parts[blockIdx.x].nonfinite = nf;
+    }
+}
+
+// launch with a single warp
+__global__ void lc_range_final_kernel(const LcRangePart *__restrict__ parts, int np,
+                                      LcRangePart *__restrict__ out)
+{
+    double mn = INFINITY, mx = -INFINITY;
+    int nf = 0;
+    for (int i = threadIdx.x; i < np; i += blockDim.x) {
+        mn = fmin(mn, parts[i].vmin); mx = fmax(mx, parts[i].vmax); nf |= parts[i].nonfinite;
+    }
+    for (int o = 16; o; o >>= 1) {
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        nf |= __shfl_xor_sync(0xffffffffu, nf, o);
+    }
+    if (threadIdx.x == 0) { out->vmin = mn; out->vmax = mx; out->nonfinite = nf; }
+}
+
+// ---------------------------------------------------------------------------
+// fused quantizer
+
+
+// Definite escape at element i: |pe*| >= |x_i - x_{i-1}| - eb exceeds the
+// quantizer range whatever the reconstruction r*_{i-1} is (|x - r*| <= eb).
+__device__ __forceinline__ bool lc_definite_escape(double xi, double xprev, const LcQuantParams &P)
+{
+    const double d = fabs(LC_SUB(xi, xprev));
+    return LC_SUB(LC_MUL(d, 1.0 - 0x1p-50), LC_MUL(P.Q.eb, 1.0 + 0x1p-50)) >= P.esc_thresh;
+}
+
+// Lattice guess for the chain value at position pos given an anchor.
+__device__ __forceinline__ double lc_guess(const LcQuantParams &P, double xpos, long long pos,
+                                           long long apos, double aval)
+{
+    if (apos == pos) return aval;
+    const double k = floor(LC_ADD(LC_DIV(LC_SUB(xpos, aval), P.Q.delta), 0.5));
+    if (k == 0.0) return aval;
+    const double g = LC_ADD(aval, LC_MUL(k, P.Q.delta));
+    return isfinite(g) ? g : xpos;
+}
+
+template <typename CodeT>
+__global__ void __launch_bounds__(LC_TPB, 2) lc_quant_kernel(LcQuantParams P, CodeT *__restrict__ codes)
+{
+    typedef cub::BlockScan<long long, LC_TPB> ScanLL;
+    extern __shared__ __align__(16) unsigned char lc_dyn_smem[];
+    // x tile with padded rows; phase B overwrites each row with its codes
+    // (uint32 slot j of a row aliases x[j/2] of the same row, already consumed)
+    double *xs = reinterpret_cast<double *>(lc_dyn_smem);
+    uint32_t *hs = reinterpret_cast<uint32_t *>(xs + LC_TPB * LC_ROW);
+    __shared__ double xhalo[LC_L + 1];            // x[tile_start-32 .. tile_start]
+    __shared__ typename ScanLL::TempStorage scan_tmp;
+    __shared__ OffMap warp_agg[LC_TPB / 32];
+    __shared__ long long sh_tile, sh_anchor_in;
+    __shared__ double sh_Din;
+
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    for (int i = tid; i < LC_HBINS; i += LC_TPB) hs[i] = 0;
+
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) sh_tile = atomicAdd(P.tile_counter, 1u);
+        __syncthreads();
+        const long long t = sh_tile;
+        if (t >= P.ntiles) break;
+        const long long cbeg = P.first_chunk + t * LC_TPB;   // first chunk of the tile
+        const long long pbeg = cbeg * LC_L;                   // its start position
+        const long long c = cbeg + tid;                       // this thread's chunk
+        const long long p0 = c * LC_L;
+        const long long nel = (long long)P.n - 1;            // last element index
+        const int len = (c < P.nchunks) ? (int)min((long long)LC_L, nel - p0) : 0;
+
+        // ---- load tile (coalesced) -------------------------------------------------
+#pragma unroll 8
+        for (int k = 0; k < LC_L; ++k) {
+            const int off = k * LC_TPB + tid;
+            const long long pos = pbeg + 1 + off;
+            if (pos <= nel) xs[(off >> 5) * LC_ROW + (off & 31)] = __ldcs(P.x + pos);
+        }
+        if (tid <= LC_L) {
+            const long long pos = pbeg - LC_L + tid;
+            xhalo[tid] = pos >= 0 ? P.x[pos] : 0.0;
+        }
+        __syncthreads();
+        const double *row = xs + tid * LC_ROW;
+        const double xstart = tid == 0 ? xhalo[LC_L] : xs[(tid - 1) * LC_ROW + LC_L - 1];
+
+        // ---- phase 0: definite escapes -> anchors ------------------------------------
+        long long last_esc = -1;
+        {
+            double xp = xstart;
+            for (int j = 0; j < len; ++j) {
+                const double xi = row[j];
+                if (lc_definite_escape(xi, xp, P)) last_esc = p0 + 1 + j;
+                xp = xi;
+            }
+        }
+        long long esc_excl, esc_agg;
+        {
+            struct MaxOp { __device__ long long operator()(long long a, long long b) const { return a > b ? a : b; } };
+            ScanLL(scan_tmp).ExclusiveScan(last_esc, esc_excl, -1LL, MaxOp(), esc_agg);
+        }
+        if (tid == 0) {
+            LcTileDesc *d = P.desc + t;
+            long long in;
+            if (t == 0) {
+                in = pbeg;                                   // launch anchor position
+            } else {
+                __stcg(&d->anc_agg, esc_agg);
+                st_release(&d->st_anchor, 1);
+                in = -1;
+                for (long long k = t - 1; k >= 0; --k) {
+                    const LcTileDesc *dk = P.desc + k;
+                    int st;
+                    while ((st = ld_acquire(&dk->st_anchor)) == 0) { }
+                    if (st == 2) { in = max(in, __ldcg(&dk->anc_incl)); break; }
+                    in = max(in, __ldcg(&dk->anc_agg));
+                }
+            }
+            __stcg(&d->anc_incl, max(in, esc_agg));
+            st_release(&d->st_anchor, 2);
+            sh_anchor_in = in;
+        }
+        __syncthreads();
+        const long long launch_apos = P.first_chunk * LC_L;
+        const long long apos = max(sh_anchor_in, esc_excl);
+        const double aval = (apos == launch_apos) ? P.anchor_val : P.x[apos];
+        const long long apos_next = max(apos, last_esc);
+        const double aval_next = (apos_next == launch_apos) ? P.anchor_val : P.x[apos_next];
+        const double xend = len > 0 ? row[len - 1] : xstart;
+        const double g0 = lc_guess(P, xstart, p0, apos, aval);
+        const double g1 = lc_guess(P, xend, p0 + len, apos_next, aval_next);
+
+        // ---- phase A: guess chain -> offset map ---------------------------------------
+        OffMap H;
+        if (len > 0) {
+            double r = g0;
+            H = lc_map_identity(lc_ulp(g0));
+            for (int j = 0; j < len; ++j) {
+                uint32_t code; int esc; double inc, pe;
+                const double rn = lc_step(P.Q, row[j], r, &code, &esc, &inc, &pe);
+                if (esc) H = lc_map_const(0.0);
+                else if (inc != 0.0) lc_map_step(H, r, inc, rn);
+                r = rn;
+            }
+            if (c + 1 < P.nchunks) lc_map_shift_out(H, LC_SUB(r, g1));
+        } else {
+            H = lc_map_neutral();
+        }
+
+        // ---- block inclusive scan of maps (apply earlier chunks first) ----------------
+        OffMap inc_map = H;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const OffMap up = lc_shfl_up_map(inc_map, o);
+            if (lane >= o) inc_map = lc_map_compose(inc_map, up);
+        }
+        if (lane == 31) warp_agg[wid] = inc_map;
+        __syncthreads();
+        if (tid == 0) {
+            for (int w = 1; w < LC_TPB / 32; ++w) warp_agg[w] = lc_map_compose(warp_agg[w], warp_agg[w - 1]);
+        }
+        __syncthreads();
+        if (wid > 0) inc_map = lc_map_compose(inc_map, warp_agg[wid - 1]);
+        OffMap exc_map = lc_shfl_up_map(inc_map, 1);
+        if (lane == 0) exc_map = wid > 0 ? warp_agg[wid - 1] : lc_map_neutral();
+
+        // ---- look-back over tile aggregates -> offset at the tile start -------------
+        if (tid == 0) {
+            LcTileDesc *d = P.desc + t;
+            const OffMap agg = warp_agg[LC_TPB / 32 - 1];
+            double Din;
+            if (t == 0) {
+                Din = 0.0;                                   // tile 0 starts exactly at the anchor
+            } else {
+                lc_store_map(d, agg);
+                st_release(&d->st_map, 1);
+                OffMap acc = lc_map_neutral();
+                Din = 0.0;
+                for (long long k = t - 1; k >= 0; --k) {
+                    const LcTileDesc *dk = P.desc + k;
+                    int st;
+                    while ((st = ld_acquire(&dk->st_map)) == 0) { }
+                    if (st == 2) { Din = lc_map_eval(acc, __ldcg(&dk->incl_D)); break; }
+                    acc = lc_map_compose(acc, lc_load_map(dk));
+                }
+            }
+            __stcg(&d->incl_D, lc_map_eval(agg, Din));
+            st_release(&d->st_map, 2);
+            sh_Din = Din;
+        }
+        __syncthreads();
+        const double Din = sh_Din;
+        const double Dc = lc_map_eval(exc_map, Din);
+        const double start = lc_apply_offset(g0, Dc);
+        const double next_pred = lc_apply_offset(g1, lc_map_eval(inc_map, Din));
+
+        // ---- phase B: exact chain from the predicted start ---------------------------
+        {
+            double r = start;
+            uint32_t *crow = reinterpret_cast<uint32_t *>(xs + tid * LC_ROW);
+            for (int j = 0; j < len; ++j) {
+                uint32_t code; int esc; double inc, pe;
+                const double rn = lc_step(P.Q, row[j], r, &code, &esc, &inc, &pe);
+                crow[j] = code;
+                if (P.pe) {
+                    P.pe[p0 + j] = pe;
+                    P.pe_rec[p0 + j] = LC_SUB(rn, r);
+                }
+                r = rn;
+            }
+            if (len > 0 && c + 1 < P.nchunks && lc_bits(r) != lc_bits(next_pred)) {
+                P.bad_end[c] = r;
+                atomicMin(P.first_bad, (unsigned long long)(c + 1));
+            }
+        }
+        __syncthreads();
+
+        // ---- histogram + coalesced code store ------------------------------------------
+#pragma unroll 4
+        for (int k = 0; k < LC_L; ++k) {
+            const int off = k * LC_TPB + tid;
+            const long long pos = pbeg + off;                // code index = element - 1
+            const bool valid = pos < nel;
+            const uint32_t code = valid ? reinterpret_cast<const uint32_t *>(xs)[(off >> 5) * (2 * LC_ROW) + (off & 31)]
+                                        : 0xffffffffu;
+            if (valid) codes[pos] = (CodeT)code;
+            if (P.count_hist) {
+                const unsigned peers = __match_any_sync(0xffffffffu, code);
+                if (valid && (int)(__ffs(peers) - 1) == lane) {
+                    const unsigned cnt = __popc(peers);
+                    if (code < LC_HBINS) atomicAdd(&hs[code], cnt);
+                    else atomicAdd(&P.hist[code], cnt);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (P.count_hist) {
+        const uint32_t lim = P.nbins < LC_HBINS ? P.nbins : LC_HBINS;
+        for (uint32_t i = tid; i < lim; i += LC_TPB)
+            if (hs[i]) atomicAdd(&P.hist[i], hs[i]);
+    }
+}
+
+// Sequential exact chain from chunk `first_chunk` (fallback for inputs whose
+// chunk predictions keep failing).  One thread; correct for every input.
+template <typename CodeT>
+__global__ void lc_quant_serial_kernel(LcQuantParams P, CodeT *__restrict__ codes)
+{
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double r = P.anchor_val;
+    for (uint64_t i = (uint64_t)P.first_chunk * LC_L + 1; i < P.n; ++i) {
+        uint32_t code; int esc; double inc, pe;
+        const double rn = lc_step(P.Q, P.x[i], r, &code, &esc, &inc, &pe);
+        codes[i - 1] = (CodeT)code;
+        if (P.pe) { P.pe[i - 1] = pe; P.pe_rec[i - 1] = LC_SUB(rn, r); }
+        r = rn;
+    }
+}
+
+// Histogram recount from final codes (used after relaunches).
+template <typename CodeT>
+__global__ void __launch_bounds__(256) lc_hist_kernel(const CodeT *__restrict__ codes, uint64_t m,
+                                                     uint32_t *__restrict__ hist, uint32_t nbins)
+{
+    __shared__ uint32_t hs[LC_HBINS];
+    for (int i = threadIdx.x; i < LC_HBINS; i += blockDim.x) hs[i] = 0;
+    __syncthreads();
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+        const uint32_t code = codes[i];
+        if (code < LC_HBINS) atomicAdd(&hs[code], 1u);
+        else atomicAdd(&hist[code], 1u);
+    }
+    __syncthreads();
+    const uint32_t lim = nbins < LC_HBINS ? nbins : LC_HBINS;
+    for (uint32_t i = threadIdx.x; i < lim; i += blockDim.x)
+        if (hs[i]) atomicAdd(&hist[i], hs[i]);
+}
+
+size_t lc_quant_smem_bytes() { return sizeof(double) * LC_TPB * LC_ROW + sizeof(uint32_t) * LC_HBINS; }
+
+template __global__ void lc_quant_kernel<uint16_t>(LcQuantParams, uint16_t *);
+template __global__ void lc_quant_kernel<uint32_t>(LcQuantParams, uint32_t *);
+template __global__ void lc_quant_serial_kernel<uint16_t>(LcQuantParams, uint16_t *);
+template __global__ void lc_quant_serial_kernel<uint32_t>(LcQuantParams, uint32_t *);
+template __global__ void lc_hist_kernel<uint16_t>(const uint16_t *, uint64_t, uint32_t *, uint32_t);
+template __global__ void lc_hist_kernel<uint32_t>(const uint32_t *, uint64_t, uint32_t *, uint32_t);

@@ -1,0 +1,210 @@
+"""GPU parity: the sm_100a codec against the CPU oracle and the reference's
+golden vectors.  Bar: bit-exact codes, escapes, Huffman payload and LCKP0001
+bytes; reconstruction bit-identical to the reference chain (which implies
+|x - x'| <= eb and the 1e-12*vr tolerance of the north star).
+
+Mirrors the reference's tests: test_compressor.py (error bound, escapes,
+determinism, serialization, integrity), test_huffman.py (decode errors),
+test_acceptance.py criteria 5/6 corpora (via tests/golden)."""
+
+import hashlib
+import math
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from tests.conftest import MODES, golden_block_names
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def lc():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1805_07384_b200 as lc
+    return lc
+
+
+def _cfg(lc, mode, param, nbh, record=False):
+    mode = MODES[int(mode)]
+    if mode == "absolute":
+        return lc.CompressorConfig.absolute(float(param), n_bins_half=int(nbh), record_traces=record)
+    if mode == "value_range_relative":
+        return lc.CompressorConfig.value_range_relative(float(param), n_bins_half=int(nbh), record_traces=record)
+    return lc.CompressorConfig.fixed_psnr(float(param), n_bins_half=int(nbh), record_traces=record)
+
+
+def _sine(n, seed=0):
+    r = np.random.default_rng(seed)
+    f = r.uniform(1, 64, 8)
+    a = r.uniform(0, 1, 8)
+    p = r.uniform(0, 2 * np.pi, 8)
+    t = np.arange(n) / n
+    out = np.zeros(n)
+    for k in range(8):
+        out += a[k] * np.sin(2 * np.pi * f[k] * t + p[k])
+    return out + r.normal(0, 1e-3, n)
+
+
+def test_golden_compress_bytes(lc, golden):
+    names = golden_block_names(golden)
+    for name in names:
+        x = golden[str(golden[f"{name}/x"])]
+        blk = lc.compress(x, _cfg(lc, *golden[f"{name}/cfg"]))
+        assert blk.to_bytes() == golden[f"{name}/block"].tobytes(), name
+
+
+def test_golden_decompress_exact(lc, golden):
+    for name in golden_block_names(golden):
+        blk = lc.CompressedBlock.from_bytes(golden[f"{name}/block"].tobytes())
+        rec = lc.decompress(blk)
+        assert hashlib.sha256(rec.tobytes()).hexdigest() == str(golden[f"{name}/recon_sha256"]), name
+
+
+def test_golden_decode_statuses(lc, golden):
+    """huffman.decode error statuses (test_huffman.py:60-76) through decompress."""
+    names = sorted({k.split("/")[0] for k in golden.files if k.startswith("derr_")})
+    for name in names:
+        bits, count = (int(v) for v in golden[f"{name}/bits"])
+        payload = golden[f"{name}/payload"].tobytes()
+        lengths = golden[f"{name}/lengths"]
+        want = str(golden[f"{name}/status"])
+        blk = lc.CompressedBlock(n=count + 1, eb_abs=0.25, value_range=1.0, first_value=0.0,
+                                 code_lengths=lengths, payload=payload, payload_bits=bits,
+                                 escape_indices=np.zeros(0, np.int64), escape_values=np.zeros(0))
+        try:
+            rec = lc.decompress(blk)
+            got = "ok"
+        except lc.IntegrityError as e:
+            got = str(e)
+            rec = None
+        if want == "ok":
+            codes = golden[f"{name}/out"]
+            if got == "ok":
+                ref, used = orc.decompress_kernel(codes, count + 1, 0.0, 0.5, np.zeros(0))
+                if used == 0:
+                    assert np.array_equal(rec, ref), name
+            else:
+                # zero-code symbols are escapes without values: reference raises the count error
+                assert got.startswith("escape count mismatch"), (name, got)
+        else:
+            assert got == want, (name, got, want)
+
+
+@pytest.mark.parametrize("eb_rel", [1e-3, 1e-4, 1e-6])
+def test_config2_full_size_bit_exact(lc, eb_rel):
+    """BASELINE config 2 at its full size (2^26): bytes and reconstruction vs the oracle."""
+    n = 1 << 26
+    x = _sine(n)
+    cfg = lc.CompressorConfig.value_range_relative(eb_rel)
+    blk = lc.compress(x, cfg)
+    ref = orc.compress(x, "value_range_relative", eb_rel)
+    assert blk.payload_bits == ref["payload_bits"]
+    assert np.array_equal(blk.code_lengths, ref["code_lengths"])
+    assert blk.payload == ref["payload"]
+    assert np.array_equal(blk.escape_indices, ref["escape_indices"])
+    rec = lc.decompress(blk)
+    assert np.array_equal(rec.view(np.int64), ref["recon"].view(np.int64))
+    assert np.max(np.abs(x - rec)) <= blk.eb_abs
+
+
+def test_device_tensor_input_matches_host(lc):
+    x = _sine(300_000, seed=3)
+    cfg = lc.CompressorConfig.value_range_relative(1e-5)
+    a = lc.compress(x, cfg)
+    b = lc.compress(torch.from_numpy(x).cuda(), cfg)
+    assert a.to_bytes() == b.to_bytes()
+    dev = lc.decompress(b, device="cuda")
+    assert dev.is_cuda and np.array_equal(dev.cpu().numpy(), lc.decompress(a))
+
+
+def test_record_traces_match_oracle(lc):
+    x = np.random.default_rng(11).normal(size=20_000).cumsum()
+    cfg = lc.CompressorConfig.value_range_relative(1e-6, record_traces=True)
+    blk = lc.compress(x, cfg)
+    _, _, _, pe, pe_rec = orc.compress_kernel(x, blk.eb_abs, 32768, record=True)
+    assert np.array_equal(blk.traces[0], pe) and np.array_equal(blk.traces[1], pe_rec)
+    assert lc.error_identity_check(x, blk) <= 1e-12 * blk.value_range
+
+
+def test_randomized_corpus_against_oracle(lc):
+    """Criterion-6 style pairs (test_acceptance.py:108-134), compared byte for byte."""
+    rng = np.random.default_rng(1234)
+    for p in range(60):
+        kind = p % 5
+        size = int(rng.integers(2, 40_000))
+        if kind == 0:
+            data = _sine(size, seed=int(rng.integers(1e9)))
+        elif kind == 1:
+            data = rng.normal(size=size).cumsum()
+        elif kind == 2:
+            data = rng.normal(size=size) * 10.0 ** rng.integers(-3, 9)
+        elif kind == 3:
+            data = rng.normal(size=size).cumsum()
+            data[rng.integers(0, size, size=3)] += 10.0 ** rng.integers(3, 12)
+        else:
+            data = np.repeat(rng.normal(size=max(size // 50, 1)), 50)[:size] * 1e3
+        eb = float(10.0 ** rng.uniform(-9, 2))
+        blk = lc.compress(data, lc.CompressorConfig.absolute(eb))
+        ref = orc.compress(data, "absolute", eb)
+        assert blk.to_bytes() == orc.to_bytes(ref), (p, kind, size, eb)
+        rec = lc.decompress(blk)
+        if "recon" in ref:
+            assert np.array_equal(rec.view(np.int64), ref["recon"].view(np.int64)), (p, kind)
+        assert np.max(np.abs(data - rec)) <= eb
+
+
+def test_small_bin_budgets_and_u32_codes(lc):
+    x = np.random.default_rng(5).normal(size=50_000).cumsum()
+    for nbh in (1, 2, 7, 300, 40_000, 100_000):
+        blk = lc.compress(x, lc.CompressorConfig.absolute(0.01, n_bins_half=nbh))
+        ref = orc.compress(x, "absolute", 0.01, n_bins_half=nbh)
+        assert np.array_equal(blk.code_lengths, ref["code_lengths"]), nbh
+        assert blk.payload == ref["payload"] and np.array_equal(blk.escape_indices, ref["escape_indices"])
+        rec = lc.decompress(blk)
+        assert np.array_equal(rec.view(np.int64), ref["recon"].view(np.int64)), nbh
+
+
+def test_edge_cases(lc):
+    with pytest.raises(lc.ParameterError):
+        lc.compress(np.array([]), lc.CompressorConfig.absolute(1.0))
+    with pytest.raises(lc.ParameterError):
+        lc.compress(np.array([1.0, np.inf]), lc.CompressorConfig.absolute(1.0))
+    with pytest.raises(lc.ParameterError):
+        lc.compress(np.array([1.0, np.nan, 2.0]), lc.CompressorConfig.absolute(1.0))
+    with pytest.raises(lc.ParameterError):
+        lc.compress(np.array([0.0, 1.0]), lc.CompressorConfig.absolute(1e308))
+    blk = lc.compress(np.array([42.0]), lc.CompressorConfig.absolute(1.0))
+    assert np.array_equal(lc.decompress(blk), [42.0])
+    data = np.full(4096, 3.25)
+    blk = lc.compress(data, lc.CompressorConfig.absolute(1e-2))
+    assert blk.nbytes < 128 and np.array_equal(lc.decompress(blk), data)
+    data = 5.0 + np.arange(100) * 1e-4
+    blk = lc.compress(data, lc.CompressorConfig.absolute(0.5))
+    assert np.all(lc.decompress(blk) == data[0])
+    # deterministic bytes (test_compressor.py:89-92)
+    x = _sine(3000)
+    c = lc.CompressorConfig.value_range_relative(1e-4)
+    assert lc.compress(x, c).to_bytes() == lc.compress(x, c).to_bytes()
+
+
+def test_integrity_errors(lc):
+    import dataclasses
+    rng = np.random.default_rng(9)
+    data = rng.normal(size=256).cumsum()
+    data[77] += 1e8
+    blk = lc.compress(data, lc.CompressorConfig.value_range_relative(1e-7))
+    assert len(blk.escape_indices) >= 1
+    stripped = dataclasses.replace(blk, escape_indices=blk.escape_indices[:-1],
+                                   escape_values=blk.escape_values[:-1])
+    with pytest.raises(lc.IntegrityError, match="escape count mismatch"):
+        lc.decompress(stripped)
+    moved = dataclasses.replace(blk, escape_indices=blk.escape_indices + 1)
+    with pytest.raises(lc.IntegrityError, match="escape positions disagree"):
+        lc.decompress(moved)
+    with pytest.raises(lc.IntegrityError):
+        lc.decompress(dataclasses.replace(blk, payload=blk.payload[: len(blk.payload) // 2]))
