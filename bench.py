@@ -1,0 +1,430 @@
+"""Benchmark: checkpoint compress/decompress throughput on B200 (BASELINE config 2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Workload (BASELINE.json configs[1]): one fp64 vector of n = 2^26 elements
+(512 MB) per GPU -- sum of 8 sinusoids with seeded frequencies U(1,64),
+amplitudes U(0,1), phases U(0,2pi) plus N(0,1e-3) noise -- compressed and
+decompressed at value-range-relative bounds 1e-3, 1e-4 and 1e-6.
+
+One step = for each bound: compress (value range + exact-chain quantizer +
+on-device Huffman codebook + encoder) then decompress (Huffman decode +
+exact-chain reconstruction), i.e. 3 round trips of the 512 MB vector.
+metric value = raw fp64 bytes round-tripped per second over all GPUs
+(3 * 8n * N / step time).  Inputs (512 MB) exceed the 126 MB L2, so no L2
+flush is needed between steps.
+
+  value     device-resident: x already in HBM, payload kept in HBM, output in HBM
+  e2e       the public API (paper_1805_07384_b200.compress / decompress) with
+            pinned host buffers: H2D of x and D2H of the block inside compress,
+            H2D of the block and D2H of the reconstruction inside decompress
+  roofline  the dominant kernel's algorithmic bytes / its CUDA-event time
+  cpu_baseline  the CPU oracle port (oracle/, C restatement of the reference
+            numba kernels) on this host, rank 0, N = 1
+
+--impl reference times that CPU port alone (the reference is Python+numba;
+its path has no compiled artefact to build).
+Multi-GPU (torchrun): every rank compresses its own 2^26 shard (weak
+scaling); NCCL carries only the barrier, the max-time reduction and an
+all-gather of per-rank block metadata.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BOUNDS = (1e-3, 1e-4, 1e-6)
+METRIC = "checkpoint compress+decompress round-trip GB/s (raw fp64, all GPUs)"
+WORKLOAD = ("config2: fp64 n=2^26 per GPU, sum of 8 seeded sinusoids + N(0,1e-3), "
+            "eb_rel in {1e-3,1e-4,1e-6}; step = compress+decompress at each bound")
+
+
+def make_vector(n, seed=0):
+    """SURVEY.md 8(d) config 2 generator (draw order f, a, phi, noise)."""
+    r = np.random.default_rng(seed)
+    f = r.uniform(1, 64, 8)
+    a = r.uniform(0, 1, 8)
+    ph = r.uniform(0, 2 * np.pi, 8)
+    t = np.arange(n, dtype=np.float64) / n
+    x = np.zeros(n)
+    for k in range(8):
+        x += a[k] * np.sin(2 * np.pi * f[k] * t + ph[k])
+    x += r.normal(0, 1e-3, n)
+    return x
+
+
+def block_bytes(payload_bytes, code_lengths, n_esc):
+    """Serialized LCKP0001 size: header + codebook + escapes + payload."""
+    used = np.flatnonzero(code_lengths > 0)
+    max_len = int(code_lengths.max()) if used.size else 0
+    cb = 4 + (1 + 2 * max_len + 2 * used.size if used.size else 0)
+    return 8 + 36 + cb + 8 + 16 * n_esc + 8 + payload_bytes
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return {}
+
+
+# --------------------------------------------------------------------------------------------
+# CPU oracle (reference arm and cpu_baseline)
+
+def cpu_oracle_sample(n, bounds, threads):
+    """compress+decompress with the CPU oracle port; returns (bytes, seconds, cores)."""
+    from oracle import oracle as orc
+    orc.lib()
+    x = make_vector(n, seed=0)
+    results = {}
+
+    def work(eb):
+        blk = orc.compress(x, "value_range_relative", eb)
+        rec = orc.decompress(blk)
+        results[eb] = (rec.size, blk["payload_bits"])
+
+    t0 = time.perf_counter()
+    if threads <= 1:
+        for eb in bounds:
+            work(eb)
+    else:
+        ts = [threading.Thread(target=work, args=(eb,)) for eb in bounds]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+    dt = time.perf_counter() - t0
+    return 8 * n * len(bounds), dt, min(threads, len(bounds)) if threads > 1 else 1
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    threads = min(len(BOUNDS), os.cpu_count() or 1)
+    n = 1 << args.ref_log2
+    for _ in range(args.warmup):
+        cpu_oracle_sample(n, BOUNDS, threads)
+    times = []
+    nbytes = 0
+    for _ in range(args.steps):
+        nbytes, dt, cores = cpu_oracle_sample(n, BOUNDS, threads)
+        times.append(dt)
+    ms = 1e3 * sum(times) / len(times)
+    value = nbytes / (ms / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": {"workload": WORKLOAD, "n": 1 << args.log2, "eb_rel": list(BOUNDS)},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": "port",
+                         "sample": f"per step: compress+decompress of a 2^{args.ref_log2} slice of the "
+                                   f"config-2 generator at each of the 3 bounds, one thread per bound "
+                                   f"(host has {os.cpu_count()} cores)"},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------------------------
+# B200 arm
+
+def run_b200(args, rank, world, local_rank):
+    import torch
+    import paper_1805_07384_b200 as lc
+    from paper_1805_07384_b200 import _native
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+    n = 1 << args.log2
+    x = make_vector(n, seed=rank)
+    xd = torch.from_numpy(x).cuda()
+    ctx = _native.context(local_rank)
+    L = ctx.lib
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    vp = ctypes.c_void_p
+
+    def rt(eb_rel, stats=None):
+        vmin, vmax, nf = ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
+        rc = L.lc_range_f64(ctx.h, xd.data_ptr(), n, 1, ctypes.byref(vmin), ctypes.byref(vmax), ctypes.byref(nf))
+        assert rc == 0, ctx.error()
+        eb_abs = eb_rel * float(vmax.value - vmin.value)
+        res = _native.LcResult()
+        rc = L.lc_compress_f64(ctx.h, xd.data_ptr(), n, 1, eb_abs, 32768, 0, ctypes.byref(res))
+        assert rc == 0, ctx.error()
+        if stats is not None:
+            ph = (ctypes.c_double * 8)()
+            k = L.lc_phase_ms(ctx.h, ph, 8)
+            stats["compress_phases"] = [ph[i] for i in range(k)]
+            stats["compress_ms"] = L.lc_last_device_ms(ctx.h)
+        pay, cl, ei, ev = vp(), vp(), vp(), vp()
+        L.lc_result_device(ctx.h, ctypes.byref(pay), ctypes.byref(cl), ctypes.byref(ei), ctypes.byref(ev))
+        used = ctypes.c_int64()
+        rc = L.lc_decompress_f64(ctx.h, n, eb_abs, float(x[0]), cl, res.n_symbols, pay, res.payload_bytes,
+                                 res.payload_bits, ei, ev, res.n_esc, 1, out.data_ptr(), 1, ctypes.byref(used))
+        assert rc == 0, (rc, ctx.error())
+        if stats is not None:
+            ph = (ctypes.c_double * 8)()
+            k = L.lc_phase_ms(ctx.h, ph, 8)
+            stats["decompress_phases"] = [ph[i] for i in range(k)][4:]
+            stats["decompress_ms"] = L.lc_last_device_ms(ctx.h)
+            stats["res"] = res
+        return res
+
+    meta = torch.zeros(4 * len(BOUNDS), dtype=torch.float64, device="cuda")
+    gathered = torch.zeros(world * meta.numel(), dtype=torch.float64, device="cuda") if world > 1 else None
+
+    def step():
+        for i, eb in enumerate(BOUNDS):
+            res = rt(eb)
+            meta[4 * i:4 * i + 4] = torch.tensor([n, res.payload_bits, res.n_esc, res.relaunches],
+                                                 dtype=torch.float64)
+        if dist is not None:                     # per-rank block metadata -> file offsets
+            dist.all_gather_into_tensor(gathered, meta)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    # ---- timed region (device-resident) ----
+    clocks = Clocks(local_rank)
+    barrier()
+    clocks.start()
+    launches0 = L.lc_launch_count(ctx.h)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        step()
+    ev1.record()
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    launches = int(L.lc_launch_count(ctx.h) - launches0)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    step_bytes = 8 * n * len(BOUNDS) * world
+    value = step_bytes / (ms / 1e3) / 1e9
+
+    # ---- per-bound breakdown (outside the timed region; medians of 3) ----
+    per = {}
+    for eb in BOUNDS:
+        runs = []
+        for _ in range(3):
+            s = {}
+            rt(eb, s)
+            runs.append(s)
+        s = runs[len(runs) // 2]
+        res = s["res"]
+        cl = np.zeros(res.n_symbols, np.uint8)
+        L.lc_result_fetch(ctx.h, cl.ctypes.data, None, None, None, None, None)
+        bb = block_bytes(res.payload_bytes, cl, res.n_esc)
+        cms = statistics.median(r["compress_ms"] for r in runs)
+        dms = statistics.median(r["decompress_ms"] for r in runs)
+        per[f"{eb:g}"] = {
+            "compress_gbs": 8 * n / (cms / 1e3) / 1e9, "decompress_gbs": 8 * n / (dms / 1e3) / 1e9,
+            "compress_ms": cms, "decompress_ms": dms, "ratio": 8 * n / bb, "payload_bits": int(res.payload_bits),
+            "escapes": int(res.n_esc), "max_len": int(res.max_len), "symbols": int(res.used_symbols),
+            "relaunches": int(res.relaunches),
+            "compress_phase_ms": {"setup": s["compress_phases"][0], "quantize": s["compress_phases"][1],
+                                  "codebook": s["compress_phases"][2], "encode": s["compress_phases"][3]},
+            "decompress_phase_ms": {"huffman_sync": s["decompress_phases"][0],
+                                    "huffman_scan": s["decompress_phases"][1],
+                                    "huffman_write": s["decompress_phases"][2],
+                                    "reconstruct": s["decompress_phases"][3]},
+        }
+
+    # ---- roofline of the dominant kernel ----
+    peak, peak_src = measured_peak()
+    shares = {}
+    for eb, d in per.items():
+        for k, v in (("lc_quant_kernel", d["compress_phase_ms"]["quantize"]),
+                     ("lc_recon_kernel", d["decompress_phase_ms"]["reconstruct"]),
+                     ("huffman_decode", d["decompress_phase_ms"]["huffman_sync"]
+                      + d["decompress_phase_ms"]["huffman_scan"] + d["decompress_phase_ms"]["huffman_write"]),
+                     ("lc_encode_kernel", d["compress_phase_ms"]["encode"])):
+            shares[k] = shares.get(k, 0.0) + v
+    dom = max(shares, key=shares.get)
+    # algorithmic bytes per launch: quantizer reads x (8 B/elem);
+    # reconstruction writes x' (8 B/elem) and reads the codes (2 B/elem)
+    alg = {"lc_quant_kernel": 8 * n, "lc_recon_kernel": 10 * n,
+           "huffman_decode": sum(d["payload_bits"] for d in per.values()) / 8 / len(per) + 2 * n,
+           "lc_encode_kernel": 2 * n + sum(d["payload_bits"] for d in per.values()) / 8 / len(per)}[dom]
+    t_ms = shares[dom] / len(per)
+    achieved = alg / (t_ms / 1e3) / 1e9
+    nc = ncu_traffic().get(dom, {})
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "peak_source": peak_src,
+                "traffic": nc.get("dram_bytes_per_launch"), "algorithmic_bytes": alg,
+                "avg_launch_ms": t_ms, "step_share": shares[dom] / sum(shares.values())}
+
+    # ---- e2e through the public API with pinned host buffers ----
+    xh = torch.from_numpy(x).pin_memory()
+    oh = torch.empty(n, dtype=torch.float64).pin_memory()
+    cfgs = [lc.CompressorConfig.value_range_relative(eb) for eb in BOUNDS]
+    h2d = d2h = 0
+
+    def e2e_step():
+        nonlocal h2d, d2h
+        h2d = d2h = 0
+        for c in cfgs:
+            blk = lc.compress(xh, c)               # H2D x, D2H block
+            rec = lc.decompress(blk, device="cuda")  # H2D block
+            oh.copy_(rec)                          # D2H reconstruction
+            meta_b = len(blk.payload) + blk.code_lengths.size + 16 * len(blk.escape_indices)
+            h2d += 8 * n + meta_b
+            d2h += meta_b + 8 * n
+
+    e2e_step()
+    barrier()
+    t0 = time.perf_counter()
+    e2e_steps = max(1, min(args.steps, 3))
+    for _ in range(e2e_steps):
+        e2e_step()
+    torch.cuda.synchronize()
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
+    if dist is not None:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e = {"value": step_bytes / (e2e_ms / 1e3) / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+           "path": "paper_1805_07384_b200.compress/decompress, pinned host x and output"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        nb, dt, cores = cpu_oracle_sample(1 << args.cpu_log2, BOUNDS, 1)
+        cpu = {"value": nb / dt / 1e9, "unit": "GB/s", "cores": cores, "kind": "port",
+               "sample": f"oracle C port, compress+decompress of the config-2 vector at n=2^{args.cpu_log2} "
+                         f"for each of the 3 bounds, single thread ({dt:.1f} s)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "n": n, "eb_rel": list(BOUNDS), "parallelism": f"shard{world}",
+                       "l2": "inputs (512 MB/GPU) exceed L2; no flush"},
+            "clocks": clk, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "per_bound": per,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--log2", type=int, default=26)
+    ap.add_argument("--cpu-log2", type=int, default=26)
+    ap.add_argument("--ref-log2", type=int, default=24)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl")
+    run_b200(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

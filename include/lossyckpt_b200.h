@@ -81,8 +81,10 @@ int lc_compress_f64(lc_ctx *ctx, const double *x, uint64_t n, int x_on_device,
 int lc_result_fetch(lc_ctx *ctx, uint8_t *code_lengths, uint8_t *payload,
                     uint64_t *esc_idx, double *esc_val, double *pe, double *pe_rec);
 
-/* Device pointers of the last compress result (valid until the next call). */
-int lc_result_device(lc_ctx *ctx, const uint8_t **payload, const uint16_t **codes);
+/* Device pointers of the last compress result (valid until the next
+ * compress on this context); any argument may be NULL.                    */
+int lc_result_device(lc_ctx *ctx, const uint8_t **payload, const uint8_t **code_lengths,
+                     const uint64_t **esc_idx, const double **esc_val);
 
 /* compressor.py:420-440 for a non-constant block.  All inputs are host
  * pointers unless inputs_on_device; out is host or device memory.
@@ -98,6 +100,17 @@ int lc_decompress_f64(lc_ctx *ctx, uint64_t n, double eb_abs, double first_value
 /* Wall time of the last compress / decompress call on the device (ms),
  * measured with CUDA events around the whole stream-ordered call.          */
 double lc_last_device_ms(lc_ctx *ctx);
+
+/* Per-phase device times of the last call (CUDA events on the context's
+ * stream).  Compress: [0] range-independent setup, [1] quantizer (all
+ * launches incl. repairs), [2] codebook, [3] encoder.  Decompress: [4]
+ * Huffman tables + segment sync passes, [5] count scan, [6] symbol write +
+ * status, [7] reconstruction.
+ * Returns the number of phases written.                                    */
+int lc_phase_ms(lc_ctx *ctx, double *ms, int cap);
+
+/* Kernels this context has launched since creation (diagnostic count).   */
+uint64_t lc_launch_count(lc_ctx *ctx);
 
 #ifdef __cplusplus
 }

@@ -61,7 +61,8 @@ def library():
         L.lc_compress_f64.restype = ctypes.c_int
         L.lc_result_fetch.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp]
         L.lc_result_fetch.restype = ctypes.c_int
-        L.lc_result_device.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp)]
+        L.lc_result_device.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                                       ctypes.POINTER(_vp), ctypes.POINTER(_vp)]
         L.lc_result_device.restype = ctypes.c_int
         L.lc_decompress_f64.argtypes = [_vp, ctypes.c_uint64, ctypes.c_double, ctypes.c_double,
                                         _vp, ctypes.c_uint64, _vp, ctypes.c_uint64, ctypes.c_uint64,
@@ -70,12 +71,17 @@ def library():
         L.lc_decompress_f64.restype = ctypes.c_int
         L.lc_last_device_ms.argtypes = [_vp]
         L.lc_last_device_ms.restype = ctypes.c_double
+        L.lc_phase_ms.argtypes = [_vp, ctypes.POINTER(ctypes.c_double), ctypes.c_int]
+        L.lc_phase_ms.restype = ctypes.c_int
+        L.lc_launch_count.argtypes = [_vp]
+        L.lc_launch_count.restype = ctypes.c_uint64
         _lib = L
         return L
 
 
 EXPORTED = ["lc_ctx_create", "lc_ctx_destroy", "lc_last_error", "lc_range_f64", "lc_compress_f64",
-            "lc_result_fetch", "lc_result_device", "lc_decompress_f64", "lc_last_device_ms"]
+            "lc_result_fetch", "lc_result_device", "lc_decompress_f64", "lc_last_device_ms",
+            "lc_phase_ms", "lc_launch_count"]
 
 
 class Context:

@@ -29,6 +29,13 @@ struct lc_ctx {
     bool own_stream = false;
     std::string err;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t pev[12] = {};       // phase boundaries (lc_phase_ms)
+    int last_kind = 0;              // 1 compress, 2 decompress
+    bool debug_sync = false;        // LC_DEBUG_SYNC=1: sync + check after every launch
+    bool timeline_on = false;       // LC_TIMELINE=1: per-tile phase stamps of the quantizer
+    LcBuf timeline;
+    int64_t timeline_tiles = 0;
+    uint64_t launches = 0;
     // scratch
     LcBuf xbuf, codes, hist, desc, counters, bad_end, pe, pe_rec, lengths, cw, gkeys, ifreq,
         parent, cbout, payload, esc_idx, esc_val, encdesc, range_parts, small;
@@ -68,6 +75,16 @@ int lc_sm_count(lc_ctx *ctx) { return ctx->sm_count; }
 void *lc_pinned(lc_ctx *ctx) { return ctx->pinned; }
 void lc_set_err(lc_ctx *ctx, const char *msg) { ctx->err = msg; }
 LcBuf *lc_dec_bufs(lc_ctx *ctx) { return ctx->dec; }
+cudaEvent_t lc_phase_ev(lc_ctx *ctx, int i) { return ctx->pev[i]; }
+void lc_count_launch(lc_ctx *ctx, int k) { ctx->launches += k; }
+void lc_set_kind(lc_ctx *ctx, int k) { ctx->last_kind = k; }
+int lc_debug_check(lc_ctx *ctx, const char *what, const char *file, int line)
+{
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess && ctx->debug_sync) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return lc_fail(ctx, e, what, file, line);
+    return 0;
+}
 
 extern "C" {
 
@@ -76,6 +93,10 @@ int lc_ctx_create(lc_ctx **out, int device, void *stream)
     lc_ctx *ctx = new lc_ctx();
     ctx->device = device;
     *out = nullptr;
+    const char *dbg = getenv("LC_DEBUG_SYNC");
+    ctx->debug_sync = dbg && dbg[0] == '1';
+    const char *tlv = getenv("LC_TIMELINE");
+    ctx->timeline_on = tlv && tlv[0] == '1';
     LC_CUDA_OK(cudaSetDevice(device));
     cudaDeviceProp prop;
     LC_CUDA_OK(cudaGetDeviceProperties(&prop, device));
@@ -84,6 +105,7 @@ int lc_ctx_create(lc_ctx **out, int device, void *stream)
     ctx->stream = (cudaStream_t)stream;
     LC_CUDA_OK(cudaEventCreate(&ctx->ev0));
     LC_CUDA_OK(cudaEventCreate(&ctx->ev1));
+    for (int i = 0; i < 12; ++i) LC_CUDA_OK(cudaEventCreate(&ctx->pev[i]));
     LC_CUDA_OK(cudaMallocHost(&ctx->pinned, 4096));
     LC_CUDA_OK(cudaFuncSetAttribute(lc_quant_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)lc_quant_smem_bytes()));
@@ -114,6 +136,8 @@ void lc_ctx_destroy(lc_ctx *ctx)
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    for (int i = 0; i < 12; ++i)
+        if (ctx->pev[i]) cudaEventDestroy(ctx->pev[i]);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -150,7 +174,8 @@ int lc_range_f64(lc_ctx *ctx, const double *x, uint64_t n, int x_on_device, doub
     LcRangePart *parts = (LcRangePart *)ctx->range_parts.p;
     lc_range_kernel<<<nb, 256, 0, ctx->stream>>>(dx, n, parts);
     lc_range_final_kernel<<<1, 32, 0, ctx->stream>>>(parts, nb, parts + nb);
-    LC_CUDA_OK(cudaGetLastError());
+    ctx->launches += 2;
+    { int _rc = lc_debug_check(ctx, "lc_range_final_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
     LcRangePart *h = (LcRangePart *)ctx->pinned;
     LC_CUDA_OK(cudaMemcpyAsync(h, parts + nb, sizeof(LcRangePart), cudaMemcpyDeviceToHost, ctx->stream));
     LC_CUDA_OK(cudaStreamSynchronize(ctx->stream));
@@ -190,6 +215,7 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     P.Q.eb = eb_abs;
     P.Q.max_m = (double)(nbh - 1);
     P.Q.max_m1 = P.Q.max_m + 1.0;
+    P.Q.inv = 1.0 / P.Q.delta;
     P.esc_thresh = (double)nbh * P.Q.delta * (1.0 + 0x1p-40);
     P.first_chunk = 0;
     P.anchor_val = 0.0;
@@ -203,6 +229,13 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     P.bad_end = (double *)ctx->bad_end.p;
     P.pe = record ? (double *)ctx->pe.p : nullptr;
     P.pe_rec = record ? (double *)ctx->pe_rec.p : nullptr;
+    P.timeline = nullptr;
+    if (ctx->timeline_on) {
+        LC_CUDA_OK(lc_reserve(ctx->timeline, ntiles * 128));
+        LC_CUDA_OK(cudaMemsetAsync(ctx->timeline.p, 0, ntiles * 128, st));
+        P.timeline = (unsigned long long *)ctx->timeline.p;
+        ctx->timeline_tiles = ntiles;
+    }
     CodeT *codes = (CodeT *)ctx->codes.p;
 
     LC_CUDA_OK(cudaMemcpyAsync(&P.anchor_val, dx, sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -212,6 +245,7 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     const int grid_cap = 2 * ctx->sm_count;
     unsigned long long *hbad = (unsigned long long *)ctx->pinned;
     uint32_t relaunches = 0;
+    LC_CUDA_OK(cudaEventRecord(ctx->pev[1], st));
     for (;;) {
         P.ntiles = (nchunks - P.first_chunk + LC_TPB - 1) / LC_TPB;
         LC_CUDA_OK(cudaMemsetAsync(P.desc, 0, P.ntiles * sizeof(LcTileDesc), st));
@@ -219,7 +253,8 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
         LC_CUDA_OK(cudaMemsetAsync(first_bad, 0xff, 8, st));
         const int grid = (int)(P.ntiles < grid_cap ? P.ntiles : grid_cap);
         lc_quant_kernel<CodeT><<<grid, LC_TPB, lc_quant_smem_bytes(), st>>>(P, codes);
-        LC_CUDA_OK(cudaGetLastError());
+        { int _rc = lc_debug_check(ctx, "lc_quant_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+        ctx->launches += 1;
         LC_CUDA_OK(cudaMemcpyAsync(hbad, first_bad, 8, cudaMemcpyDeviceToHost, st));
         LC_CUDA_OK(cudaStreamSynchronize(st));
         const unsigned long long fb = *hbad;
@@ -232,15 +267,18 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
         P.count_hist = 0;
         if (relaunches > 64) {                      // pathological input: exact serial chain
             lc_quant_serial_kernel<CodeT><<<1, 32, 0, st>>>(P, codes);
-            LC_CUDA_OK(cudaGetLastError());
+            { int _rc = lc_debug_check(ctx, "lc_quant_serial_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+            ctx->launches += 1;
             break;
         }
     }
     if (relaunches) {
         LC_CUDA_OK(cudaMemsetAsync(P.hist, 0, nbins * sizeof(uint32_t), st));
         lc_hist_kernel<CodeT><<<4 * ctx->sm_count, 256, 0, st>>>(codes, m, P.hist, nbins);
-        LC_CUDA_OK(cudaGetLastError());
+        { int _rc = lc_debug_check(ctx, "lc_hist_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+        ctx->launches += 1;
     }
+    LC_CUDA_OK(cudaEventRecord(ctx->pev[2], st));
 
     // codebook
     LC_CUDA_OK(lc_reserve(ctx->lengths, nbins));
@@ -253,7 +291,9 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     lc_codebook_kernel<<<1, 1024, lc_codebook_smem_bytes(), st>>>(
         P.hist, nbins, (uint8_t *)ctx->lengths.p, (unsigned long long *)ctx->cw.p,
         (unsigned long long *)ctx->gkeys.p, (unsigned long long *)ctx->ifreq.p, (int *)ctx->parent.p, cbo);
-    LC_CUDA_OK(cudaGetLastError());
+    { int _rc = lc_debug_check(ctx, "lc_codebook_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+    LC_CUDA_OK(cudaEventRecord(ctx->pev[3], st));
+    ctx->launches += 1;
     LcCodebookOut *hcb = (LcCodebookOut *)ctx->pinned;
     LC_CUDA_OK(cudaMemcpyAsync(hcb, cbo, sizeof(LcCodebookOut), cudaMemcpyDeviceToHost, st));
     LC_CUDA_OK(cudaStreamSynchronize(st));
@@ -286,8 +326,11 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     E.ntiles = etiles;
     const int egrid = (int)(etiles < (uint64_t)(3 * ctx->sm_count) ? etiles : 3 * ctx->sm_count);
     lc_encode_kernel<CodeT><<<egrid, LC_TPB, lc_encode_smem_bytes(), st>>>(E);
-    LC_CUDA_OK(cudaGetLastError());
+    { int _rc = lc_debug_check(ctx, "lc_encode_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+    ctx->launches += 2;
+    LC_CUDA_OK(cudaEventRecord(ctx->pev[4], st));
     LC_CUDA_OK(cudaEventRecord(ctx->ev1, st));
+    ctx->last_kind = 1;
     LC_CUDA_OK(cudaStreamSynchronize(st));
 
     ctx->n = n;
@@ -315,6 +358,7 @@ int lc_compress_f64(lc_ctx *ctx, const double *x, uint64_t n, int x_on_device, d
     if (n_bins_half > (1u << 30)) return 12;
     LC_CUDA_OK(cudaSetDevice(ctx->device));
     LC_CUDA_OK(cudaEventRecord(ctx->ev0, ctx->stream));
+    LC_CUDA_OK(cudaEventRecord(ctx->pev[0], ctx->stream));
     int rc;
     const double *dx = lc_device_input(ctx, x, n, x_on_device, &rc);
     if (rc) return rc;
@@ -341,13 +385,38 @@ int lc_result_fetch(lc_ctx *ctx, uint8_t *code_lengths, uint8_t *payload, uint64
     return 0;
 }
 
-int lc_result_device(lc_ctx *ctx, const uint8_t **payload, const uint16_t **codes)
+int lc_result_device(lc_ctx *ctx, const uint8_t **payload, const uint8_t **code_lengths,
+                     const uint64_t **esc_idx, const double **esc_val)
 {
     if (!ctx) return 12;
     if (payload) *payload = (const uint8_t *)ctx->payload.p;
-    if (codes) *codes = (const uint16_t *)ctx->codes.p;
+    if (code_lengths) *code_lengths = (const uint8_t *)ctx->lengths.p;
+    if (esc_idx) *esc_idx = (const uint64_t *)ctx->esc_idx.p;
+    if (esc_val) *esc_val = (const double *)ctx->esc_val.p;
     return 0;
 }
+
+int lc_phase_ms(lc_ctx *ctx, double *ms, int cap)
+{
+    if (!ctx) return 0;
+    int k = 0;
+    auto el = [&](int a, int b) {
+        float f = -1.0f;
+        if (cudaEventElapsedTime(&f, ctx->pev[a], ctx->pev[b]) != cudaSuccess) f = -1.0f;
+        return (double)f;
+    };
+    if (ctx->last_kind == 1) {
+        const int pairs[4][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}};
+        for (int i = 0; i < 4 && k < cap; ++i) ms[k++] = el(pairs[i][0], pairs[i][1]);
+    } else if (ctx->last_kind == 2) {
+        for (int i = 0; i < 4 && k < cap; ++i) ms[k++] = -1.0;
+        const int pairs[4][2] = {{5, 8}, {8, 9}, {9, 6}, {6, 7}};
+        for (int i = 0; i < 4 && k < cap; ++i) ms[k++] = el(pairs[i][0], pairs[i][1]);
+    }
+    return k;
+}
+
+uint64_t lc_launch_count(lc_ctx *ctx) { return ctx ? ctx->launches : 0; }
 
 int lc_decompress_f64(lc_ctx *ctx, uint64_t n, double eb_abs, double first_value, const uint8_t *code_lengths,
                       uint64_t n_lengths, const uint8_t *payload, uint64_t payload_bytes, uint64_t payload_bits,
@@ -365,7 +434,8 @@ int lc_decompress_f64(lc_ctx *ctx, uint64_t n, double eb_abs, double first_value
 // what: 0 codes, 1 histogram (u32), 2 code lengths (u8), 3 codewords (u64)
 int lc_debug_copy(lc_ctx *ctx, int what, void *host, uint64_t bytes)
 {
-    const void *src = what == 0 ? ctx->codes.p : what == 1 ? ctx->hist.p : what == 2 ? ctx->lengths.p : ctx->cw.p;
+    const void *src = what == 0 ? ctx->codes.p : what == 1 ? ctx->hist.p : what == 2 ? ctx->lengths.p
+                    : what == 3 ? ctx->cw.p : ctx->timeline.p;
     LC_CUDA_OK(cudaMemcpyAsync(host, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
     LC_CUDA_OK(cudaStreamSynchronize(ctx->stream));
     return 0;

@@ -61,6 +61,13 @@ __device__ __forceinline__ OffMap lc_shfl_up_map(const OffMap &m, int off)
     return r;
 }
 
+__device__ __forceinline__ unsigned long long lc_gtimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 // neutral element of composition
 __device__ __forceinline__ OffMap lc_map_neutral() { return lc_map_trans(0.0, 0.0, 0.0); }
 
@@ -69,3 +76,132 @@ __device__ __forceinline__ OffMap lc_map_neutral() { return lc_map_trans(0.0, 0.
         cudaError_t _e = (expr);                                                           \
         if (_e != cudaSuccess) return lc_fail(ctx, _e, #expr, __FILE__, __LINE__);         \
     } while (0)
+
+// ---------------------------------------------------------------------------
+// Warp-cooperative decoupled look-back (one full warp).
+//
+// Tiles publish status 1 + aggregate, later status 2 + inclusive prefix.
+// Each round the warp inspects 32 predecessors at once (lane 0 = nearest),
+// stops at the nearest inclusive one and folds the aggregates in between
+// with a shuffle tree.  op(a, b) means "a then b" (a is the earlier tile).
+// st_of(k) must be an acquire load; val_of(k, st) the matching value.
+template <typename T, typename Op, typename Shfl, typename StOf, typename ValOf>
+__device__ __forceinline__ T lc_lookback_warp(long long t, T ident, Op op, Shfl shfl_down,
+                                             StOf st_of, ValOf val_of)
+{
+    const int lane = threadIdx.x & 31;
+    T acc = ident;                                // prefix of tiles already folded (later ones)
+    long long k = t - 1;
+    for (;;) {
+        const long long idx = k - lane;
+        int st = 2;
+        T v = ident;
+        if (idx >= 0) {
+            while ((st = st_of(idx)) == 0) { }
+            v = val_of(idx, st);
+        }
+        const unsigned incl = __ballot_sync(0xffffffffu, st == 2);
+        const int j = incl ? __ffs(incl) - 1 : 32;
+        if (lane > j) v = ident;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const T other = shfl_down(v, off);
+            if (lane + off < 32) v = op(other, v);
+        }
+        acc = op(v, acc);                         // valid on lane 0
+        if (j < 32) break;
+        k -= 32;
+    }
+    return acc;                                   // lane 0 holds the exclusive prefix
+}
+
+__device__ __forceinline__ OffMap lc_shfl_down_map(const OffMap &m, int off)
+{
+    OffMap r;
+    r.kind = __shfl_down_sync(0xffffffffu, m.kind, off);
+    r.v = __shfl_down_sync(0xffffffffu, m.v, off);
+    r.B = __shfl_down_sync(0xffffffffu, m.B, off);
+    r.t0 = __shfl_down_sync(0xffffffffu, m.t0, off);
+    r.t1 = __shfl_down_sync(0xffffffffu, m.t1, off);
+    r.y = __shfl_down_sync(0xffffffffu, m.y, off);
+    r.og = __shfl_down_sync(0xffffffffu, m.og, off);
+    return r;
+}
+
+__device__ __forceinline__ int ld_relaxed(const int *p)
+{
+    int v;
+    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Block-wide decoupled look-back: all LC_TPB threads inspect LC_TPB
+// predecessors per round (thread 0 = nearest), so the inclusive-prefix front
+// advances a whole resident wave per round.  Only the tiles nearer than the
+// nearest inclusive one are waited for (relaxed polling with back-off, one
+// acquire load per used descriptor).  Must be called by every thread of the
+// block; returns the exclusive prefix on every thread.
+// st_ptr(k): address of tile k's status word; val_of(k, st) its value.
+template <typename T, typename Op, typename Shfl, typename StPtr, typename ValOf>
+__device__ __forceinline__ T lc_lookback_block(long long t, T ident, Op op, Shfl shfl_down, StPtr st_ptr,
+                                              ValOf val_of, T *scratch, int *sj, T *result,
+                                              unsigned long long *dbg = nullptr)
+// (sj unused; kept for call-site compatibility)
+{
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    __shared__ unsigned s_incl[LC_TPB / 32], s_zero[LC_TPB / 32];
+    T acc = ident;
+    long long k = t - 1;
+    for (;;) {
+        const long long idx = k - tid;
+        int st = idx >= 0 ? 0 : 2;
+        int j;
+        for (int round = 0;; ++round) {
+            if (st == 0) st = ld_relaxed(st_ptr(idx));
+            const unsigned incl = __ballot_sync(0xffffffffu, st == 2);
+            const unsigned zero = __ballot_sync(0xffffffffu, st == 0);
+            if (lane == 0) { s_incl[wid] = incl; s_zero[wid] = zero; }
+            __syncthreads();
+            // every thread derives the same j / miss from the per-warp masks
+            j = LC_TPB;
+            bool miss = false;
+            for (int w = 0; w < LC_TPB / 32; ++w) {
+                const unsigned iw = s_incl[w], zw = s_zero[w];
+                const unsigned below = iw ? ((1u << (__ffs(iw) - 1)) - 1u) : 0xffffffffu;
+                if (zw & below) miss = true;
+                if (iw) { j = w * 32 + __ffs(iw) - 1; break; }
+            }
+            __syncthreads();                          // masks consumed before the next round
+            if (!miss) {
+                if (dbg && tid == 0) { dbg[0] = lc_gtimer(); dbg[1] = round; dbg[2] = j; }
+                break;
+            }
+            __nanosleep(round < 4 ? 32 : 256);
+        }
+        T v = ident;
+        if (idx >= 0 && tid <= j) {
+            st = ld_acquire(st_ptr(idx));            // orders the value loads after the status
+            v = tid == j ? val_of(idx, 2) : val_of(idx, 1);
+        }
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const T other = shfl_down(v, off);
+            if (lane + off < 32) v = op(other, v);
+        }
+        if (lane == 0) scratch[wid] = v;
+        __syncthreads();
+        if (tid == 0) {
+            T r = scratch[LC_TPB / 32 - 1];
+            for (int w = LC_TPB / 32 - 2; w >= 0; --w) r = op(r, scratch[w]);
+            acc = op(r, acc);
+            *result = acc;
+        }
+        __syncthreads();
+        acc = *result;
+        if (dbg && tid == 0) dbg[3] = lc_gtimer();
+        if (j < LC_TPB) break;
+        k -= LC_TPB;
+        __syncthreads();
+    }
+    return acc;
+}

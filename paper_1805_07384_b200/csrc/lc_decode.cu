@@ -340,6 +340,9 @@ __global__ void __launch_bounds__(LC_TPB, 2) lc_recon_kernel(LcRecParams P)
     __shared__ LcSegScan warp_seg[LC_TPB / 32];
     __shared__ long long sh_tile;
     __shared__ LcSegScan sh_seg_in;
+    __shared__ LcSegScan lb_seg[LC_TPB / 32], lb_seg_res;
+    __shared__ OffMap lb_map[LC_TPB / 32], lb_map_res;
+    __shared__ int sh_j;
     __shared__ double sh_Din;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 
@@ -399,40 +402,52 @@ __global__ void __launch_bounds__(LC_TPB, 2) lc_recon_kernel(LcRecParams P)
             if (wid > 0) exc = warp_seg[wid - 1];
             else { exc.sum = 0; exc.cnt = 0; exc.has = 0; exc.moved = 0; }
         }
-        if (tid == 0) {
+        {
             LcRecDesc *d = P.desc + t;
             const LcSegScan agg = warp_seg[LC_TPB / 32 - 1];
             LcSegScan in;
             if (t == 0) {
                 in.sum = 0; in.cnt = P.anchor_cnt; in.has = 1; in.moved = 0;   // anchored at the launch start
             } else {
-                __stcg(&d->seg_agg_sum, agg.sum); __stcg(&d->seg_agg_cnt, agg.cnt);
-                __stcg(&d->seg_agg_has, agg.has | (agg.moved << 1));
-                st_release(&d->st_seg, 1);
-                LcSegScan acc; acc.sum = 0; acc.cnt = 0; acc.has = 0; acc.moved = 0;  // later tiles
-                for (long long k = t - 1; k >= 0; --k) {
-                    const LcRecDesc *dk = P.desc + k;
-                    int st;
-                    while ((st = ld_acquire(&dk->st_seg)) == 0) { }
-                    LcSegScan v;
-                    int hm;
-                    if (st == 2) {
-                        v.sum = __ldcg(&dk->seg_inc_sum); v.cnt = __ldcg(&dk->seg_inc_cnt); hm = __ldcg(&dk->seg_inc_has);
-                        v.has = hm & 1; v.moved = hm >> 1;
-                        acc = lc_segscan_op(v, acc);
-                        break;
-                    }
-                    v.sum = __ldcg(&dk->seg_agg_sum); v.cnt = __ldcg(&dk->seg_agg_cnt); hm = __ldcg(&dk->seg_agg_has);
-                    v.has = hm & 1; v.moved = hm >> 1;
-                    acc = lc_segscan_op(v, acc);
+                if (tid == 0) {
+                    __stcg(&d->seg_agg_sum, agg.sum); __stcg(&d->seg_agg_cnt, agg.cnt);
+                    __stcg(&d->seg_agg_has, agg.has | (agg.moved << 1));
+                    st_release(&d->st_seg, 1);
                 }
-                in = acc;
+                LcSegScan ident; ident.sum = 0; ident.cnt = 0; ident.has = 0; ident.moved = 0;
+                in = lc_lookback_block<LcSegScan>(
+                    t, ident, [](const LcSegScan &x, const LcSegScan &y) { return lc_segscan_op(x, y); },
+                    [](const LcSegScan &v, int o) {
+                        LcSegScan r;
+                        r.sum = __shfl_down_sync(0xffffffffu, v.sum, o);
+                        r.cnt = __shfl_down_sync(0xffffffffu, v.cnt, o);
+                        r.has = __shfl_down_sync(0xffffffffu, v.has, o);
+                        r.moved = __shfl_down_sync(0xffffffffu, v.moved, o);
+                        return r;
+                    },
+                    [&](long long k) { return &P.desc[k].st_seg; },
+                    [&](long long k, int st) {
+                        LcSegScan v;
+                        int hm;
+                        if (st == 2) {
+                            v.sum = __ldcg(&P.desc[k].seg_inc_sum); v.cnt = __ldcg(&P.desc[k].seg_inc_cnt);
+                            hm = __ldcg(&P.desc[k].seg_inc_has);
+                        } else {
+                            v.sum = __ldcg(&P.desc[k].seg_agg_sum); v.cnt = __ldcg(&P.desc[k].seg_agg_cnt);
+                            hm = __ldcg(&P.desc[k].seg_agg_has);
+                        }
+                        v.has = hm & 1; v.moved = hm >> 1;
+                        return v;
+                    },
+                    lb_seg, &sh_j, &lb_seg_res);
             }
-            const LcSegScan incl = lc_segscan_op(in, agg);
-            __stcg(&d->seg_inc_sum, incl.sum); __stcg(&d->seg_inc_cnt, incl.cnt);
-            __stcg(&d->seg_inc_has, incl.has | (incl.moved << 1));
-            st_release(&d->st_seg, 2);
-            sh_seg_in = in;
+            if (tid == 0) {
+                const LcSegScan incl = lc_segscan_op(in, agg);
+                __stcg(&d->seg_inc_sum, incl.sum); __stcg(&d->seg_inc_cnt, incl.cnt);
+                __stcg(&d->seg_inc_has, incl.has | (incl.moved << 1));
+                st_release(&d->st_seg, 2);
+                sh_seg_in = in;
+            }
         }
         __syncthreads();
         const LcSegScan before = lc_segscan_op(sh_seg_in, exc);    // state at position cL
@@ -495,29 +510,37 @@ __global__ void __launch_bounds__(LC_TPB, 2) lc_recon_kernel(LcRecParams P)
         if (wid > 0) inc_map = lc_map_compose(inc_map, warp_agg[wid - 1]);
         OffMap exc_map = lc_shfl_up_map(inc_map, 1);
         if (lane == 0) exc_map = wid > 0 ? warp_agg[wid - 1] : lc_map_neutral();
-        if (tid == 0) {
+        {
             LcRecDesc *d = P.desc + t;
             const OffMap agg = warp_agg[LC_TPB / 32 - 1];
             double Din = 0.0;
             if (t > 0) {
-                d->map_kind = agg.kind; d->mv = agg.v; d->mB = agg.B; d->mt0 = agg.t0; d->mt1 = agg.t1;
-                d->my = agg.y; d->mog = agg.og;
-                st_release(&d->st_map, 1);
-                OffMap acc = lc_map_neutral();
-                for (long long k = t - 1; k >= 0; --k) {
-                    const LcRecDesc *dk = P.desc + k;
-                    int st;
-                    while ((st = ld_acquire(&dk->st_map)) == 0) { }
-                    if (st == 2) { Din = lc_map_eval(acc, __ldcg(&dk->incl_D)); break; }
-                    OffMap mk;
-                    mk.kind = __ldcg(&dk->map_kind); mk.v = __ldcg(&dk->mv); mk.B = __ldcg(&dk->mB);
-                    mk.t0 = __ldcg(&dk->mt0); mk.t1 = __ldcg(&dk->mt1); mk.y = __ldcg(&dk->my); mk.og = __ldcg(&dk->mog);
-                    acc = lc_map_compose(acc, mk);
+                if (tid == 0) {
+                    d->map_kind = agg.kind; d->mv = agg.v; d->mB = agg.B; d->mt0 = agg.t0; d->mt1 = agg.t1;
+                    d->my = agg.y; d->mog = agg.og;
+                    st_release(&d->st_map, 1);
                 }
+                const OffMap pre = lc_lookback_block<OffMap>(
+                    t, lc_map_neutral(), [](const OffMap &x, const OffMap &y) { return lc_map_compose(y, x); },
+                    [](const OffMap &v, int o) { return lc_shfl_down_map(v, o); },
+                    [&](long long k) { return &P.desc[k].st_map; },
+                    [&](long long k, int st) {
+                        if (st == 2) return lc_map_const(__ldcg(&P.desc[k].incl_D));
+                        const LcRecDesc *dk = P.desc + k;
+                        OffMap mk;
+                        mk.kind = __ldcg(&dk->map_kind); mk.v = __ldcg(&dk->mv); mk.B = __ldcg(&dk->mB);
+                        mk.t0 = __ldcg(&dk->mt0); mk.t1 = __ldcg(&dk->mt1); mk.y = __ldcg(&dk->my);
+                        mk.og = __ldcg(&dk->mog);
+                        return mk;
+                    },
+                    lb_map, &sh_j, &lb_map_res);
+                Din = pre.y;
             }
-            __stcg(&d->incl_D, lc_map_eval(agg, Din));
-            st_release(&d->st_map, 2);
-            sh_Din = Din;
+            if (tid == 0) {
+                __stcg(&d->incl_D, lc_map_eval(agg, Din));
+                st_release(&d->st_map, 2);
+                sh_Din = Din;
+            }
         }
         __syncthreads();
         const double Din = sh_Din;
@@ -576,6 +599,10 @@ void *lc_pinned(lc_ctx *ctx);
 void lc_set_err(lc_ctx *ctx, const char *msg);
 LcBuf *lc_dec_bufs(lc_ctx *ctx);
 cudaEvent_t lc_ev(lc_ctx *ctx, int which);
+cudaEvent_t lc_phase_ev(lc_ctx *ctx, int i);
+void lc_count_launch(lc_ctx *ctx, int k);
+void lc_set_kind(lc_ctx *ctx, int k);
+int lc_debug_check(lc_ctx *ctx, const char *what, const char *file, int line);
 
 int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_value,
                        const uint8_t *code_lengths, uint64_t n_lengths, const uint8_t *payload,
@@ -611,12 +638,14 @@ int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_valu
         LC_CUDA_OK(cudaMemcpyAsync(beidx.p, esc_idx, n_esc * 8, k, st));
         LC_CUDA_OK(cudaMemcpyAsync(beval.p, esc_val, n_esc * 8, k, st));
     }
+    LC_CUDA_OK(cudaEventRecord(lc_phase_ev(ctx, 5), st));
     // tables
     LC_CUDA_OK(lc_reserve(btab, sizeof(LcDecTables) + n_lengths * 4 + 64));
     LcDecTables *T = (LcDecTables *)btab.p;
     uint32_t *sorted = (uint32_t *)((char *)btab.p + sizeof(LcDecTables));
     lc_dec_tables_kernel<<<1, 1024, 0, st>>>((const uint8_t *)blen.p, (uint32_t)n_lengths, T, sorted);
-    LC_CUDA_OK(cudaGetLastError());
+    { int _rc = lc_debug_check(ctx, "lc_dec_tables_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+    lc_count_launch(ctx, 2);
     // Huffman decode
     const int code_bytes = n_lengths <= 65536 ? 2 : 4;
     LC_CUDA_OK(lc_reserve(bcodes, m * code_bytes + 16));
@@ -640,12 +669,13 @@ int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_valu
     int *hchanged = (int *)lc_pinned(ctx);
     LC_CUDA_OK(cudaMemsetAsync(changed, 0, 4, st));
     lc_dec_sync_kernel<<<sblocks, 256, 0, st>>>(DP, sa, sa, 1, changed);
-    LC_CUDA_OK(cudaGetLastError());
+    { int _rc = lc_debug_check(ctx, "lc_dec_sync_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
     LcSeg *prev = sa, *cur = sb;
     for (int it = 0; it < 100000; ++it) {
         LC_CUDA_OK(cudaMemsetAsync(changed, 0, 4, st));
         lc_dec_sync_kernel<<<sblocks, 256, 0, st>>>(DP, prev, cur, 0, changed);
-        LC_CUDA_OK(cudaGetLastError());
+        { int _rc = lc_debug_check(ctx, "lc_dec_sync_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+        lc_count_launch(ctx, 1);
         LcSeg *tmp = prev; prev = cur; cur = tmp;
         if (it % 2 == 1 || it > 8) {
             LC_CUDA_OK(cudaMemcpyAsync(hchanged, changed, 4, cudaMemcpyDeviceToHost, st));
@@ -653,17 +683,21 @@ int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_valu
             if (!*hchanged) break;
         }
     }
+    LC_CUDA_OK(cudaEventRecord(lc_phase_ev(ctx, 8), st));
     lc_dec_scan_kernel<<<1, 1024, 0, st>>>(prev, nseg, offs, tot);
+    LC_CUDA_OK(cudaEventRecord(lc_phase_ev(ctx, 9), st));
     LC_CUDA_OK(cudaMemsetAsync(endpos, 0xff, 8, st));
     lc_dec_write_kernel<<<sblocks, 256, 0, st>>>(DP, prev, offs, bcodes.p, code_bytes, m, endpos);
     lc_dec_status_kernel<<<1, 1, 0, st>>>(prev, offs, tot, endpos, m, payload_bits, status);
-    LC_CUDA_OK(cudaGetLastError());
+    { int _rc = lc_debug_check(ctx, "lc_dec_status_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+    lc_count_launch(ctx, 3);
     int *hstat = (int *)lc_pinned(ctx);
     LC_CUDA_OK(cudaMemcpyAsync(hstat, status, 4, cudaMemcpyDeviceToHost, st));
     LC_CUDA_OK(cudaStreamSynchronize(st));
     if (*hstat) return *hstat;
 
     // reconstruction
+    LC_CUDA_OK(cudaEventRecord(lc_phase_ev(ctx, 6), st));
     double *dout = out;
     if (!out_on_device) {
         LC_CUDA_OK(lc_reserve(bout, n * 8));
@@ -694,6 +728,7 @@ int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_valu
     R.esc_flags = esc_flags;
     LC_CUDA_OK(cudaMemsetAsync(esc_flags, 0, 8, st));
     lc_set_first_kernel<<<1, 1, 0, st>>>(dout, first_value);
+    lc_count_launch(ctx, 1);
     const int grid_cap = 2 * lc_sm_count(ctx);
     unsigned long long *hbad = (unsigned long long *)lc_pinned(ctx);
     int relaunches = 0;
@@ -704,7 +739,8 @@ int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_valu
         LC_CUDA_OK(cudaMemsetAsync(R.first_bad, 0xff, 8, st));
         const int grid = (int)(R.ntiles < grid_cap ? R.ntiles : grid_cap);
         lc_recon_kernel<<<grid, LC_TPB, lc_recon_smem_bytes(), st>>>(R);
-        LC_CUDA_OK(cudaGetLastError());
+        { int _rc = lc_debug_check(ctx, "lc_recon_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+        lc_count_launch(ctx, 1);
         LC_CUDA_OK(cudaMemcpyAsync(hbad, R.first_bad, 8, cudaMemcpyDeviceToHost, st));
         LC_CUDA_OK(cudaStreamSynchronize(st));
         if (*hbad == ~0ULL) break;
@@ -731,6 +767,8 @@ int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_valu
         LC_CUDA_OK(cudaMemcpy(&last, R.desc + (R.ntiles - 1), sizeof(LcRecDesc), cudaMemcpyDeviceToHost));
         total_esc = last.seg_inc_cnt;
     }
+    LC_CUDA_OK(cudaEventRecord(lc_phase_ev(ctx, 7), st));
+    lc_set_kind(ctx, 2);
     int64_t used = hflags[0] ? -1 : total_esc;
     if (esc_used) *esc_used = used;
     if (used < 0 || (uint64_t)used != n_esc) return 4;

@@ -235,6 +235,8 @@ __global__ void __launch_bounds__(LC_TPB) lc_encode_kernel(LcEncParams P)
     __shared__ typename ScanU::TempStorage scan_tmp;
     __shared__ long long sh_tile;
     __shared__ unsigned long long sh_in_bits, sh_in_esc;
+    __shared__ ulonglong2 lb_u2[LC_TPB / 32], lb_u2_res;
+    __shared__ int sh_j;
     const int tid = threadIdx.x;
     const CodeT *codes = reinterpret_cast<const CodeT *>(P.codes);
     const uint32_t tab = P.nbins < LC_ENC_TAB ? P.nbins : LC_ENC_TAB;
@@ -267,25 +269,35 @@ __global__ void __launch_bounds__(LC_TPB) lc_encode_kernel(LcEncParams P)
         ScanU(scan_tmp).ExclusiveSum(bits, bex, bagg);
         __syncthreads();
         ScanU(scan_tmp).ExclusiveSum(nesc, eex, eagg);
-        if (tid == 0) {
+        {
             LcEncDesc *d = P.desc + t;
-            unsigned long long ib = 0, ie = 0;
+            ulonglong2 in = make_ulonglong2(0, 0);
             if (t > 0) {
-                __stcg(&d->agg_bits, bagg);
-                __stcg(&d->agg_esc, eagg);
-                st_release(&d->st, 1);
-                for (long long k = t - 1; k >= 0; --k) {
-                    const LcEncDesc *dk = P.desc + k;
-                    int st;
-                    while ((st = ld_acquire(&dk->st)) == 0) { }
-                    if (st == 2) { ib += __ldcg(&dk->incl_bits); ie += __ldcg(&dk->incl_esc); break; }
-                    ib += __ldcg(&dk->agg_bits); ie += __ldcg(&dk->agg_esc);
+                if (tid == 0) {
+                    __stcg(&d->agg_bits, bagg);
+                    __stcg(&d->agg_esc, eagg);
+                    st_release(&d->st, 1);
                 }
+                in = lc_lookback_block<ulonglong2>(
+                    t, make_ulonglong2(0, 0),
+                    [](const ulonglong2 &a, const ulonglong2 &b) { return make_ulonglong2(a.x + b.x, a.y + b.y); },
+                    [](const ulonglong2 &v, int o) {
+                        return make_ulonglong2(__shfl_down_sync(0xffffffffu, v.x, o),
+                                               __shfl_down_sync(0xffffffffu, v.y, o));
+                    },
+                    [&](long long k) { return &P.desc[k].st; },
+                    [&](long long k, int st) {
+                        return st == 2 ? make_ulonglong2(__ldcg(&P.desc[k].incl_bits), __ldcg(&P.desc[k].incl_esc))
+                                       : make_ulonglong2(__ldcg(&P.desc[k].agg_bits), __ldcg(&P.desc[k].agg_esc));
+                    },
+                    lb_u2, &sh_j, &lb_u2_res);
             }
-            __stcg(&d->incl_bits, ib + bagg);
-            __stcg(&d->incl_esc, ie + eagg);
-            st_release(&d->st, 2);
-            sh_in_bits = ib; sh_in_esc = ie;
+            if (tid == 0) {
+                __stcg(&d->incl_bits, in.x + bagg);
+                __stcg(&d->incl_esc, in.y + eagg);
+                st_release(&d->st, 2);
+                sh_in_bits = in.x; sh_in_esc = in.y;
+            }
         }
         __syncthreads();
         // escapes (compressor.py:409-410): code index i-1 <-> element i

@@ -22,6 +22,7 @@ struct LcQuantParams {
     unsigned long long *first_bad;
     double *bad_end;         // per chunk: exact end value when its successor failed
     double *pe, *pe_rec;     // optional traces
+    unsigned long long *timeline;  // optional: 8 globaltimer stamps per tile (profiling)
 };
 
 struct LcCodebookOut {

@@ -111,6 +111,9 @@ __global__ void __launch_bounds__(LC_TPB, 2) lc_quant_kernel(LcQuantParams P, Co
     __shared__ typename ScanLL::TempStorage scan_tmp;
     __shared__ OffMap warp_agg[LC_TPB / 32];
     __shared__ long long sh_tile, sh_anchor_in;
+    __shared__ long long lb_ll[LC_TPB / 32], lb_ll_res;
+    __shared__ OffMap lb_map[LC_TPB / 32], lb_map_res;
+    __shared__ int sh_j;
     __shared__ double sh_Din;
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -128,6 +131,9 @@ __global__ void __launch_bounds__(LC_TPB, 2) lc_quant_kernel(LcQuantParams P, Co
         const long long p0 = c * LC_L;
         const long long nel = (long long)P.n - 1;            // last element index
         const int len = (c < P.nchunks) ? (int)min((long long)LC_L, nel - p0) : 0;
+        unsigned long long *tl = P.timeline ? P.timeline + 16 * t : nullptr;
+#define LC_STAMP(i) do { if (tl && tid == 0) tl[i] = lc_gtimer(); } while (0)
+        LC_STAMP(0);
 
         // ---- load tile (coalesced) -------------------------------------------------
 #pragma unroll 8
@@ -143,6 +149,7 @@ __global__ void __launch_bounds__(LC_TPB, 2) lc_quant_kernel(LcQuantParams P, Co
         __syncthreads();
         const double *row = xs + tid * LC_ROW;
         const double xstart = tid == 0 ? xhalo[LC_L] : xs[(tid - 1) * LC_ROW + LC_L - 1];
+        LC_STAMP(1);
 
         // ---- phase 0: definite escapes -> anchors ------------------------------------
         long long last_esc = -1;
@@ -159,28 +166,33 @@ __global__ void __launch_bounds__(LC_TPB, 2) lc_quant_kernel(LcQuantParams P, Co
             struct MaxOp { __device__ long long operator()(long long a, long long b) const { return a > b ? a : b; } };
             ScanLL(scan_tmp).ExclusiveScan(last_esc, esc_excl, -1LL, MaxOp(), esc_agg);
         }
-        if (tid == 0) {
+        {
             LcTileDesc *d = P.desc + t;
             long long in;
             if (t == 0) {
                 in = pbeg;                                   // launch anchor position
             } else {
-                __stcg(&d->anc_agg, esc_agg);
-                st_release(&d->st_anchor, 1);
-                in = -1;
-                for (long long k = t - 1; k >= 0; --k) {
-                    const LcTileDesc *dk = P.desc + k;
-                    int st;
-                    while ((st = ld_acquire(&dk->st_anchor)) == 0) { }
-                    if (st == 2) { in = max(in, __ldcg(&dk->anc_incl)); break; }
-                    in = max(in, __ldcg(&dk->anc_agg));
+                if (tid == 0) {
+                    __stcg(&d->anc_agg, esc_agg);
+                    st_release(&d->st_anchor, 1);
                 }
+                in = lc_lookback_block<long long>(
+                    t, -1LL, [](long long a, long long b) { return a > b ? a : b; },
+                    [](long long v, int o) { return __shfl_down_sync(0xffffffffu, v, o); },
+                    [&](long long k) { return &P.desc[k].st_anchor; },
+                    [&](long long k, int st) {
+                        return st == 2 ? __ldcg(&P.desc[k].anc_incl) : __ldcg(&P.desc[k].anc_agg);
+                    },
+                    lb_ll, &sh_j, &lb_ll_res);
             }
-            __stcg(&d->anc_incl, max(in, esc_agg));
-            st_release(&d->st_anchor, 2);
-            sh_anchor_in = in;
+            if (tid == 0) {
+                __stcg(&d->anc_incl, max(in, esc_agg));
+                st_release(&d->st_anchor, 2);
+                sh_anchor_in = in;
+            }
         }
         __syncthreads();
+        LC_STAMP(2);
         const long long launch_apos = P.first_chunk * LC_L;
         const long long apos = max(sh_anchor_in, esc_excl);
         const double aval = (apos == launch_apos) ? P.anchor_val : P.x[apos];
@@ -196,8 +208,8 @@ __global__ void __launch_bounds__(LC_TPB, 2) lc_quant_kernel(LcQuantParams P, Co
             double r = g0;
             H = lc_map_identity(lc_ulp(g0));
             for (int j = 0; j < len; ++j) {
-                uint32_t code; int esc; double inc, pe;
-                const double rn = lc_step(P.Q, row[j], r, &code, &esc, &inc, &pe);
+                int esc; double inc;
+                const double rn = lc_step_guess(P.Q, row[j], r, &esc, &inc);
                 if (esc) H = lc_map_const(0.0);
                 else if (inc != 0.0) lc_map_step(H, r, inc, rn);
                 r = rn;
@@ -209,6 +221,7 @@ __global__ void __launch_bounds__(LC_TPB, 2) lc_quant_kernel(LcQuantParams P, Co
 
         // ---- block inclusive scan of maps (apply earlier chunks first) ----------------
         OffMap inc_map = H;
+        LC_STAMP(3);
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const OffMap up = lc_shfl_up_map(inc_map, o);
@@ -223,32 +236,36 @@ __global__ void __launch_bounds__(LC_TPB, 2) lc_quant_kernel(LcQuantParams P, Co
         if (wid > 0) inc_map = lc_map_compose(inc_map, warp_agg[wid - 1]);
         OffMap exc_map = lc_shfl_up_map(inc_map, 1);
         if (lane == 0) exc_map = wid > 0 ? warp_agg[wid - 1] : lc_map_neutral();
+        LC_STAMP(4);
 
         // ---- look-back over tile aggregates -> offset at the tile start -------------
-        if (tid == 0) {
+        {
             LcTileDesc *d = P.desc + t;
             const OffMap agg = warp_agg[LC_TPB / 32 - 1];
-            double Din;
-            if (t == 0) {
-                Din = 0.0;                                   // tile 0 starts exactly at the anchor
-            } else {
-                lc_store_map(d, agg);
-                st_release(&d->st_map, 1);
-                OffMap acc = lc_map_neutral();
-                Din = 0.0;
-                for (long long k = t - 1; k >= 0; --k) {
-                    const LcTileDesc *dk = P.desc + k;
-                    int st;
-                    while ((st = ld_acquire(&dk->st_map)) == 0) { }
-                    if (st == 2) { Din = lc_map_eval(acc, __ldcg(&dk->incl_D)); break; }
-                    acc = lc_map_compose(acc, lc_load_map(dk));
+            double Din = 0.0;                                // tile 0 starts exactly at the anchor
+            if (t > 0) {
+                if (tid == 0) {
+                    lc_store_map(d, agg);
+                    st_release(&d->st_map, 1);
                 }
+                const OffMap pre = lc_lookback_block<OffMap>(
+                    t, lc_map_neutral(), [](const OffMap &a, const OffMap &b) { return lc_map_compose(b, a); },
+                    [](const OffMap &v, int o) { return lc_shfl_down_map(v, o); },
+                    [&](long long k) { return &P.desc[k].st_map; },
+                    [&](long long k, int st) {
+                        return st == 2 ? lc_map_const(__ldcg(&P.desc[k].incl_D)) : lc_load_map(P.desc + k);
+                    },
+                    lb_map, &sh_j, &lb_map_res, tl ? tl + 8 : nullptr);
+                Din = pre.y;                                 // a constant map: the offset itself
             }
-            __stcg(&d->incl_D, lc_map_eval(agg, Din));
-            st_release(&d->st_map, 2);
-            sh_Din = Din;
+            if (tid == 0) {
+                __stcg(&d->incl_D, lc_map_eval(agg, Din));
+                st_release(&d->st_map, 2);
+                sh_Din = Din;
+            }
         }
         __syncthreads();
+        LC_STAMP(5);
         const double Din = sh_Din;
         const double Dc = lc_map_eval(exc_map, Din);
         const double start = lc_apply_offset(g0, Dc);
@@ -274,6 +291,7 @@ __global__ void __launch_bounds__(LC_TPB, 2) lc_quant_kernel(LcQuantParams P, Co
             }
         }
         __syncthreads();
+        LC_STAMP(6);
 
         // ---- histogram + coalesced code store ------------------------------------------
 #pragma unroll 4
@@ -293,6 +311,7 @@ __global__ void __launch_bounds__(LC_TPB, 2) lc_quant_kernel(LcQuantParams P, Co
                 }
             }
         }
+        LC_STAMP(7);
     }
     __syncthreads();
     if (P.count_hist) {

@@ -14,7 +14,7 @@ int64_t sim_predict(const double *x, int64_t n, double eb, int64_t nbh, int L,
                     int mode, int64_t *first_bad, int64_t *n_events)
 {
     LcQuant Q;
-    Q.delta = 2.0 * eb; Q.eb = eb; Q.max_m = (double)(nbh - 1); Q.max_m1 = Q.max_m + 1.0;
+    Q.delta = 2.0 * eb; Q.eb = eb; Q.max_m = (double)(nbh - 1); Q.max_m1 = Q.max_m + 1.0; Q.inv = 1.0 / Q.delta;
     const int64_t nc = (n - 1 + L - 1) / L;
     std::vector<double> guess(nc), rend(nc);
     std::vector<OffMap> maps(nc);
@@ -87,7 +87,7 @@ int64_t sim_predict(const double *x, int64_t n, double eb, int64_t nbh, int L,
 int64_t sim_codes(const double *x, int64_t n, double eb, int64_t nbh, uint32_t *codes, double *recon)
 {
     LcQuant Q;
-    Q.delta = 2.0 * eb; Q.eb = eb; Q.max_m = (double)(nbh - 1); Q.max_m1 = Q.max_m + 1.0;
+    Q.delta = 2.0 * eb; Q.eb = eb; Q.max_m = (double)(nbh - 1); Q.max_m1 = Q.max_m + 1.0; Q.inv = 1.0 / Q.delta;
     double r = x[0]; recon[0] = r; int64_t ne = 0;
     for (int64_t i = 1; i < n; ++i) {
         double inc; int esc; double pe;
@@ -104,7 +104,7 @@ extern "C" {
 int64_t sim_compose_check(const double *x, int64_t n, double eb, int L, int span, int verbose)
 {
     LcQuant Q;
-    Q.delta = 2.0 * eb; Q.eb = eb; Q.max_m = 32767.0; Q.max_m1 = 32768.0;
+    Q.delta = 2.0 * eb; Q.eb = eb; Q.max_m = 32767.0; Q.max_m1 = 32768.0; Q.inv = 1.0 / Q.delta;
     const int64_t nc = (n - 1 + L - 1) / L;
     std::vector<double> guess(nc);
     std::vector<OffMap> maps(nc);
@@ -168,7 +168,7 @@ extern "C" {
 int64_t sim_tree_debug(const double *x, int64_t n, double eb, int L)
 {
     LcQuant Q;
-    Q.delta = 2.0 * eb; Q.eb = eb; Q.max_m = 32767.0; Q.max_m1 = 32768.0;
+    Q.delta = 2.0 * eb; Q.eb = eb; Q.max_m = 32767.0; Q.max_m1 = 32768.0; Q.inv = 1.0 / Q.delta;
     const int64_t nc = (n - 1 + L - 1) / L;
     std::vector<double> guess(nc);
     std::vector<OffMap> maps(nc);
@@ -218,7 +218,7 @@ extern "C" {
 int64_t sim_tree_debug2(const double *x, int64_t n, double eb, int L)
 {
     LcQuant Q;
-    Q.delta = 2.0 * eb; Q.eb = eb; Q.max_m = 32767.0; Q.max_m1 = 32768.0;
+    Q.delta = 2.0 * eb; Q.eb = eb; Q.max_m = 32767.0; Q.max_m1 = 32768.0; Q.inv = 1.0 / Q.delta;
     const int64_t nc = (n - 1 + L - 1) / L;
     std::vector<double> guess(nc);
     std::vector<OffMap> maps(nc);
