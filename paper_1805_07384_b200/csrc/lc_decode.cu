@@ -139,53 +139,136 @@ __device__ __forceinline__ int lc_decode_one(const LcDecTables &T, const uint32_
     return 0;
 }
 
-struct LcSeg {
-    unsigned long long start;   // bit where this segment's first codeword starts
+#define LC_SYNC_K 16
+
+// Per-segment decode state.  bnd[] holds the first codeword starts (bit
+// offsets from the segment base) of the last full decode: a later re-decode
+// from a different start that lands on one of them is synchronised.
+struct __align__(16) LcSeg {
+    unsigned long long start;   // bit where this segment's first codeword starts (~0: dead)
     unsigned long long exit;    // first codeword start >= segment end (or stop point)
     unsigned int count;         // codewords started in [start, exit)
-    int term;                   // 0 none, 1 invalid, 2 exhausted, 4 clean end at bit_length
+    int term;                   // 0 none, 1 invalid, 2 exhausted, 4 clean end at bit_length, 8 dead
+    unsigned short bnd[LC_SYNC_K];
+    int nbnd;
+    unsigned int full_count;    // codewords of the full decode that recorded bnd[] (from bnd[0])
 };
 
 struct LcDecParams {
-    const uint32_t *payload;    // words (big-endian bit order inside bytes)
+    const uint32_t *payload;    // words (big-endian bit order inside bytes), padded
     unsigned long long bits;    // bit_length
     const LcDecTables *T;
     const uint32_t *sorted;
     unsigned long long nseg;
 };
 
-// Walk one segment from `start`.  Stops at the first codeword starting at or
-// after seg_end, at bit_length, or at an anomaly.
-__device__ void lc_walk(const LcDecParams &P, const LcDecTables &T, int max_len, unsigned long long start,
-                        unsigned long long seg_end, LcSeg &S, void *out, int out_bytes,
-                        unsigned long long out_off, unsigned long long out_cap,
-                        unsigned long long *end_pos_of_last, unsigned long long last_index)
+// MSB-first bit reader: the top nb bits of buf are valid (nb in (32, 64] after refill).
+struct LcBitReader {
+    const uint32_t *w;
+    unsigned long long buf, pos, next;
+    int nb;
+    __device__ __forceinline__ void init(const uint32_t *words, unsigned long long p)
+    {
+        w = words;
+        pos = p;
+        const unsigned long long wi = p >> 5;
+        const int sh = (int)(p & 31);
+        const unsigned long long a = __byte_perm(__ldg(w + wi), 0, 0x0123);
+        const unsigned long long b = __byte_perm(__ldg(w + wi + 1), 0, 0x0123);
+        buf = ((a << 32) | b) << sh;
+        nb = 64 - sh;
+        next = wi + 2;
+        if (nb <= 32) refill();
+    }
+    __device__ __forceinline__ void refill()
+    {
+        buf |= (unsigned long long)__byte_perm(__ldg(w + next), 0, 0x0123) << (32 - nb);
+        ++next;
+        nb += 32;
+    }
+    __device__ __forceinline__ void consume(int l)
+    {
+        if (l >= nb) { init(w, pos + l); return; }   // only for codes longer than the buffer
+        buf <<= l;
+        nb -= l;
+        pos += l;
+        if (nb <= 32) refill();
+    }
+    __device__ __forceinline__ unsigned long long window(int max_len) const
+    {
+        return max_len > nb ? lc_peek64(w, pos) : buf;
+    }
+};
+
+// One codeword at the reader; returns its length, 0 for "no codeword within
+// max_len bits"; sets *term for anomalies exactly like huffman.py:114-129.
+__device__ __forceinline__ int lc_next_symbol(const LcDecParams &P, const LcDecTables &T, int max_len,
+                                              const LcBitReader &br, uint32_t *sym, int *term)
 {
-    unsigned long long p = start;
+    if (br.pos >= P.bits) { *term = 4; return 0; }
+    const unsigned long long remaining = P.bits - br.pos;
+    const int l = lc_decode_one(T, P.sorted, br.window(max_len), max_len, sym);
+    if (l == 0) { *term = remaining > (unsigned long long)max_len ? 1 : 2; return 0; }
+    if ((unsigned long long)l > remaining) { *term = 2; return 0; }
+    return l;
+}
+
+// Full decode of [start, seg_end): records boundaries, count, exit, anomaly.
+__device__ void lc_walk_full(const LcDecParams &P, const LcDecTables &T, int max_len, unsigned long long start,
+                             unsigned long long seg_base, unsigned long long seg_end, LcSeg &S)
+{
+    LcBitReader br;
+    br.init(P.payload, start);
     unsigned int cnt = 0;
-    int term = 0;
-    while (p < seg_end) {
-        if (p >= P.bits) { term = 4; break; }
-        const unsigned long long remaining = P.bits - p;
+    int term = 0, nb = 0;
+    while (br.pos < seg_end) {
         uint32_t sym;
-        const int l = lc_decode_one(T, P.sorted, lc_peek64(P.payload, p), max_len, &sym);
-        if (l == 0) { term = remaining > (unsigned long long)max_len ? 1 : 2; break; }
-        if ((unsigned long long)l > remaining) { term = 2; break; }
-        if (out) {
-            const unsigned long long k = out_off + cnt;
-            if (k < out_cap) {
-                if (out_bytes == 2) ((uint16_t *)out)[k] = (uint16_t)sym;
-                else ((uint32_t *)out)[k] = sym;
-            }
-            if (k == last_index) *end_pos_of_last = p + l;
-        }
-        p += l;
+        const int l = lc_next_symbol(P, T, max_len, br, &sym, &term);
+        if (!l) break;
+        if (nb < LC_SYNC_K) S.bnd[nb++] = (unsigned short)(br.pos - seg_base);
+        br.consume(l);
         ++cnt;
     }
     S.start = start;
-    S.exit = p;
+    S.exit = br.pos;
     S.count = cnt;
+    S.full_count = cnt;
     S.term = term;
+    S.nbnd = nb;
+}
+
+// Re-decode from a new start; stops as soon as it lands on a boundary of the
+// previous full decode (the remainder is then identical).
+__device__ void lc_walk_resync(const LcDecParams &P, const LcDecTables &T, int max_len, unsigned long long start,
+                               unsigned long long seg_base, unsigned long long seg_end, LcSeg &S)
+{
+    LcBitReader br;
+    br.init(P.payload, start);
+    unsigned int n_new = 0;
+    int j = 0;
+    while (br.pos < seg_end) {
+        while (j < S.nbnd && seg_base + S.bnd[j] < br.pos) ++j;
+        if (j < S.nbnd && seg_base + S.bnd[j] == br.pos) {      // synchronised
+            S.count = n_new + (S.full_count - (unsigned int)j);
+            S.start = start;
+            return;
+        }
+        if (j >= S.nbnd && S.nbnd < LC_SYNC_K) break;            // old decode ended before here
+        uint32_t sym;
+        int term = 0;
+        const int l = lc_next_symbol(P, T, max_len, br, &sym, &term);
+        if (!l) { S.start = start; S.exit = br.pos; S.count = n_new; S.term = term; S.nbnd = 0; return; }
+        br.consume(l);
+        ++n_new;
+    }
+    lc_walk_full(P, T, max_len, start, seg_base, seg_end, S);    // no sync: decode afresh
+}
+
+__device__ __forceinline__ void lc_load_tables(LcDecTables &Ts, const LcDecTables *T)
+{
+    for (int i = threadIdx.x; i < (int)(sizeof(LcDecTables) / 4); i += blockDim.x)
+        reinterpret_cast<uint32_t *>(&Ts)[i] = reinterpret_cast<const uint32_t *>(T)[i];
+    __syncthreads();
 }
 
 __global__ void __launch_bounds__(256) lc_dec_sync_kernel(LcDecParams P, const LcSeg *__restrict__ prev,
@@ -193,52 +276,95 @@ __global__ void __launch_bounds__(256) lc_dec_sync_kernel(LcDecParams P, const L
                                                          int *__restrict__ changed)
 {
     __shared__ LcDecTables Ts;
-    for (int i = threadIdx.x; i < (int)(sizeof(LcDecTables) / 4); i += blockDim.x)
-        reinterpret_cast<uint32_t *>(&Ts)[i] = reinterpret_cast<const uint32_t *>(P.T)[i];
-    __syncthreads();
+    lc_load_tables(Ts, P.T);
     const unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= P.nseg) return;
-    const unsigned long long seg_beg = t * LC_SEG_BITS, seg_end = seg_beg + LC_SEG_BITS;
-    unsigned long long start;
-    if (first_pass) start = seg_beg;
-    else if (t == 0) start = 0;
-    else {
-        const LcSeg pp = prev[t - 1];
-        // predecessor stopped early (anomaly / end): nothing real starts here
-        start = pp.term ? ~0ULL : pp.exit;
-        if (start == prev[t].start) { cur[t] = prev[t]; return; }
-    }
+    const unsigned long long seg_base = t * LC_SEG_BITS, seg_end = seg_base + LC_SEG_BITS;
     LcSeg S;
-    if (start == ~0ULL) { S.start = ~0ULL; S.exit = ~0ULL; S.count = 0; S.term = 8; }
-    else lc_walk(P, Ts, Ts.max_len, start, seg_end, S, nullptr, 0, 0, 0, nullptr, 0);
-    if (!first_pass && (S.exit != prev[t].exit || S.term != prev[t].term)) atomicExch(changed, 1);
-    if (first_pass) atomicExch(changed, 1);
+    if (first_pass) {
+        lc_walk_full(P, Ts, Ts.max_len, seg_base, seg_base, seg_end, S);
+        cur[t] = S;
+        return;
+    }
+    S = prev[t];
+    unsigned long long start = 0;
+    if (t > 0) {
+        const LcSeg pp = prev[t - 1];
+        start = pp.term ? ~0ULL : pp.exit;       // anomaly / end before here: nothing starts here
+    }
+    if (start == S.start) { cur[t] = S; return; }
+    const unsigned long long old_exit = S.exit;
+    const int old_term = S.term;
+    if (start == ~0ULL) {
+        S.start = ~0ULL; S.exit = ~0ULL; S.count = 0; S.term = 8; S.nbnd = 0;
+    } else {
+        lc_walk_resync(P, Ts, Ts.max_len, start, seg_base, seg_end, S);
+    }
+    if (S.exit != old_exit || S.term != old_term) atomicExch(changed, 1);
     cur[t] = S;
 }
 
-// exclusive scan of segment counts (single block, sequential chunks)
-__global__ void __launch_bounds__(1024) lc_dec_scan_kernel(const LcSeg *__restrict__ seg, unsigned long long nseg,
-                                                          unsigned long long *__restrict__ off,
-                                                          unsigned long long *__restrict__ total_and_term)
+// Device-wide exclusive scan of segment counts (decoupled look-back) and the
+// first anomaly on the decode path.
+struct LcScanDesc { int st; int pad; unsigned long long agg, incl; };
+
+__global__ void __launch_bounds__(LC_TPB) lc_dec_scan_kernel(const LcSeg *__restrict__ seg, unsigned long long nseg,
+                                                            unsigned long long *__restrict__ off,
+                                                            LcScanDesc *__restrict__ desc,
+                                                            unsigned int *__restrict__ tile_counter,
+                                                            unsigned long long *__restrict__ total_and_term)
 {
-    typedef cub::BlockScan<unsigned long long, 1024> Scan;
+    typedef cub::BlockScan<unsigned long long, LC_TPB> Scan;
     __shared__ typename Scan::TempStorage tmp;
-    __shared__ unsigned long long carry;
-    __shared__ unsigned long long first_term;
-    if (threadIdx.x == 0) { carry = 0; first_term = ~0ULL; }
-    __syncthreads();
-    for (unsigned long long b = 0; b < nseg; b += 1024) {
-        const unsigned long long i = b + threadIdx.x;
-        const unsigned long long c = i < nseg ? seg[i].count : 0;
-        if (i < nseg && seg[i].term && seg[i].term != 8) atomicMin(&first_term, i);
+    __shared__ long long sh_tile;
+    __shared__ unsigned long long lb_u[LC_TPB / 32], lb_res, sh_in;
+    __shared__ int sh_j;
+    const int tid = threadIdx.x;
+    const int IPT = 8;
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) sh_tile = atomicAdd(tile_counter, 1u);
+        __syncthreads();
+        const long long t = sh_tile;
+        const unsigned long long base = (unsigned long long)t * LC_TPB * IPT;
+        if (base >= nseg) break;
+        unsigned long long c[IPT], sum = 0;
+        for (int k = 0; k < IPT; ++k) {
+            const unsigned long long i = base + (unsigned long long)tid * IPT + k;
+            c[k] = 0;
+            if (i < nseg) {
+                const LcSeg S = seg[i];
+                c[k] = S.count;
+                if (S.term && S.term != 8) atomicMin(&total_and_term[1], i);
+            }
+            sum += c[k];
+        }
         unsigned long long ex, agg;
-        Scan(tmp).ExclusiveSum(c, ex, agg);
-        if (i < nseg) off[i] = carry + ex;
+        Scan(tmp).ExclusiveSum(sum, ex, agg);
+        unsigned long long in = 0;
+        if (t > 0) {
+            if (tid == 0) { __stcg(&desc[t].agg, agg); st_release(&desc[t].st, 1); }
+            in = lc_lookback_block<unsigned long long>(
+                t, 0ULL, [](unsigned long long a, unsigned long long b) { return a + b; },
+                [](unsigned long long v, int o) { return __shfl_down_sync(0xffffffffu, v, o); },
+                [&](long long k) { return &desc[k].st; },
+                [&](long long k, int st) { return st == 2 ? __ldcg(&desc[k].incl) : __ldcg(&desc[k].agg); },
+                lb_u, &sh_j, &lb_res);
+        }
+        if (tid == 0) {
+            __stcg(&desc[t].incl, in + agg);
+            st_release(&desc[t].st, 2);
+            sh_in = in;
+            if ((base + (unsigned long long)LC_TPB * IPT) >= nseg) total_and_term[0] = in + agg;
+        }
         __syncthreads();
-        if (threadIdx.x == 0) carry += agg;
-        __syncthreads();
+        unsigned long long o = sh_in + ex;
+        for (int k = 0; k < IPT; ++k) {
+            const unsigned long long i = base + (unsigned long long)tid * IPT + k;
+            if (i < nseg) off[i] = o;
+            o += c[k];
+        }
     }
-    if (threadIdx.x == 0) { total_and_term[0] = carry; total_and_term[1] = first_term; }
 }
 
 __global__ void __launch_bounds__(256) lc_dec_write_kernel(LcDecParams P, const LcSeg *__restrict__ seg,
@@ -247,17 +373,30 @@ __global__ void __launch_bounds__(256) lc_dec_write_kernel(LcDecParams P, const 
                                                           unsigned long long *__restrict__ end_pos)
 {
     __shared__ LcDecTables Ts;
-    for (int i = threadIdx.x; i < (int)(sizeof(LcDecTables) / 4); i += blockDim.x)
-        reinterpret_cast<uint32_t *>(&Ts)[i] = reinterpret_cast<const uint32_t *>(P.T)[i];
-    __syncthreads();
+    lc_load_tables(Ts, P.T);
     const unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= P.nseg) return;
     const LcSeg S0 = seg[t];
     if (S0.start == ~0ULL || S0.count == 0) return;
-    const unsigned long long o = off[t];
+    unsigned long long o = off[t];
     if (o >= m) return;
-    LcSeg S;
-    lc_walk(P, Ts, Ts.max_len, S0.start, (t + 1) * LC_SEG_BITS, S, out, out_bytes, o, m, end_pos, m - 1);
+    const unsigned long long seg_end = (t + 1) * LC_SEG_BITS;
+    const int max_len = Ts.max_len;
+    LcBitReader br;
+    br.init(P.payload, S0.start);
+    unsigned int cnt = 0;
+    while (br.pos < seg_end && cnt < S0.count && o < m) {
+        uint32_t sym;
+        int term = 0;
+        const int l = lc_next_symbol(P, Ts, max_len, br, &sym, &term);
+        if (!l) break;
+        if (out_bytes == 2) ((uint16_t *)out)[o] = (uint16_t)sym;
+        else ((uint32_t *)out)[o] = sym;
+        br.consume(l);
+        if (o == m - 1) *end_pos = br.pos;
+        ++o;
+        ++cnt;
+    }
 }
 
 // Resolve the reference status (huffman.py:114-132) from the segment walk.
@@ -475,20 +614,42 @@ __global__ void __launch_bounds__(LC_TPB, 2) lc_recon_kernel(LcRecParams P)
         if (len > 0) {
             double r = g0;
             long long e = before.cnt;
-            H = lc_map_identity(lc_ulp(g0));
+            LcEvents E;
+            lc_events_init(E, g0);
+            bool pend = false;
+            double pr = 0.0, pc = 0.0, prn = 0.0;
             for (int j = 0; j < len; ++j) {
                 const uint32_t code = crow[j];
-                if (code == 0) {
-                    r = e < (long long)P.n_esc ? P.esc_val[e] : 0.0;
-                    ++e;
-                    H = lc_map_const(0.0);
-                } else {
-                    const int64_t m = lc_code_m(code);
-                    if (m != 0) {
-                        const double inc_ = LC_MUL((double)m, P.delta);
-                        const double rn = LC_ADD(r, inc_);
-                        lc_map_step(H, r, inc_, rn);
-                        r = rn;
+                const bool esc = code == 0;
+                const int64_t m = lc_code_m(code);
+                const double inc_ = LC_MUL((double)m, P.delta);
+                double rn = m != 0 ? LC_ADD(r, inc_) : r;
+                if (esc) { rn = e < (long long)P.n_esc ? P.esc_val[e] : 0.0; ++e; }
+                lc_events_step_if(E, pend, pr, pc, prn);
+                lc_events_escape_if(E, esc);
+                pend = !esc && m != 0;
+                pr = r; pc = inc_; prn = rn;
+                r = rn;
+            }
+            lc_events_step_if(E, pend, pr, pc, prn);
+            if (!lc_events_finish(E, g0, H)) {
+                double r2 = g0;
+                long long e2 = before.cnt;
+                H = lc_map_identity(lc_ulp(g0));
+                for (int j = 0; j < len; ++j) {
+                    const uint32_t code = crow[j];
+                    if (code == 0) {
+                        r2 = e2 < (long long)P.n_esc ? P.esc_val[e2] : 0.0;
+                        ++e2;
+                        H = lc_map_const(0.0);
+                    } else {
+                        const int64_t m = lc_code_m(code);
+                        if (m != 0) {
+                            const double inc_ = LC_MUL((double)m, P.delta);
+                            const double rn = LC_ADD(r2, inc_);
+                            lc_map_step(H, r2, inc_, rn);
+                            r2 = rn;
+                        }
                     }
                 }
             }
@@ -650,15 +811,18 @@ int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_valu
     const int code_bytes = n_lengths <= 65536 ? 2 : 4;
     LC_CUDA_OK(lc_reserve(bcodes, m * code_bytes + 16));
     const unsigned long long nseg = (payload_bits + LC_SEG_BITS - 1) / LC_SEG_BITS + 1;
-    LC_CUDA_OK(lc_reserve(bsync, 2 * nseg * sizeof(LcSeg) + nseg * 8 + 64));
+    const unsigned long long scan_tiles = (nseg + LC_TPB * 8 - 1) / (LC_TPB * 8);
+    LC_CUDA_OK(lc_reserve(bsync, 2 * nseg * sizeof(LcSeg) + nseg * 8 + scan_tiles * sizeof(LcScanDesc) + 64));
     LcSeg *sa = (LcSeg *)bsync.p, *sb = sa + nseg;
     unsigned long long *offs = (unsigned long long *)(sb + nseg);
+    LcScanDesc *sdesc = (LcScanDesc *)(offs + nseg);
     LC_CUDA_OK(lc_reserve(baux, 256));
     int *changed = (int *)baux.p;
     unsigned long long *tot = (unsigned long long *)((char *)baux.p + 16);
     unsigned long long *endpos = (unsigned long long *)((char *)baux.p + 48);
     int *status = (int *)((char *)baux.p + 64);
     int *esc_flags = (int *)((char *)baux.p + 80);
+    unsigned int *scan_counter = (unsigned int *)((char *)baux.p + 128);
     LcDecParams DP;
     DP.payload = (const uint32_t *)bpay.p;
     DP.bits = payload_bits;
@@ -667,24 +831,29 @@ int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_valu
     DP.nseg = nseg;
     const int sblocks = (int)((nseg + 255) / 256);
     int *hchanged = (int *)lc_pinned(ctx);
-    LC_CUDA_OK(cudaMemsetAsync(changed, 0, 4, st));
     lc_dec_sync_kernel<<<sblocks, 256, 0, st>>>(DP, sa, sa, 1, changed);
     { int _rc = lc_debug_check(ctx, "lc_dec_sync_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+    lc_count_launch(ctx, 1);
     LcSeg *prev = sa, *cur = sb;
-    for (int it = 0; it < 100000; ++it) {
+    for (int it = 0; it < 1000000; ++it) {
         LC_CUDA_OK(cudaMemsetAsync(changed, 0, 4, st));
         lc_dec_sync_kernel<<<sblocks, 256, 0, st>>>(DP, prev, cur, 0, changed);
         { int _rc = lc_debug_check(ctx, "lc_dec_sync_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
         lc_count_launch(ctx, 1);
         LcSeg *tmp = prev; prev = cur; cur = tmp;
-        if (it % 2 == 1 || it > 8) {
-            LC_CUDA_OK(cudaMemcpyAsync(hchanged, changed, 4, cudaMemcpyDeviceToHost, st));
-            LC_CUDA_OK(cudaStreamSynchronize(st));
-            if (!*hchanged) break;
-        }
+        LC_CUDA_OK(cudaMemcpyAsync(hchanged, changed, 4, cudaMemcpyDeviceToHost, st));
+        LC_CUDA_OK(cudaStreamSynchronize(st));
+        if (!*hchanged) break;
     }
     LC_CUDA_OK(cudaEventRecord(lc_phase_ev(ctx, 8), st));
-    lc_dec_scan_kernel<<<1, 1024, 0, st>>>(prev, nseg, offs, tot);
+    LC_CUDA_OK(cudaMemsetAsync(sdesc, 0, scan_tiles * sizeof(LcScanDesc), st));
+    LC_CUDA_OK(cudaMemsetAsync(scan_counter, 0, 4, st));
+    LC_CUDA_OK(cudaMemsetAsync(tot + 1, 0xff, 8, st));
+    {
+        const int g = (int)(scan_tiles < (unsigned long long)(2 * lc_sm_count(ctx)) ? scan_tiles : 2 * lc_sm_count(ctx));
+        lc_dec_scan_kernel<<<g, LC_TPB, 0, st>>>(prev, nseg, offs, sdesc, scan_counter, tot);
+        { int _rc = lc_debug_check(ctx, "lc_dec_scan_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+    }
     LC_CUDA_OK(cudaEventRecord(lc_phase_ev(ctx, 9), st));
     LC_CUDA_OK(cudaMemsetAsync(endpos, 0xff, 8, st));
     lc_dec_write_kernel<<<sblocks, 256, 0, st>>>(DP, prev, offs, bcodes.p, code_bytes, m, endpos);

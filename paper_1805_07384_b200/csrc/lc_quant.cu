@@ -206,13 +206,31 @@ __global__ void __launch_bounds__(LC_TPB, 2) lc_quant_kernel(LcQuantParams P, Co
         OffMap H;
         if (len > 0) {
             double r = g0;
-            H = lc_map_identity(lc_ulp(g0));
+            LcEvents E;
+            lc_events_init(E, g0);
+            // software-pipelined: the event test of step j-1 overlaps the chain of step j
+            bool pend = false;
+            double pr = 0.0, pc = 0.0, prn = 0.0;
             for (int j = 0; j < len; ++j) {
                 int esc; double inc;
                 const double rn = lc_step_guess(P.Q, row[j], r, &esc, &inc);
-                if (esc) H = lc_map_const(0.0);
-                else if (inc != 0.0) lc_map_step(H, r, inc, rn);
+                lc_events_step_if(E, pend, pr, pc, prn);
+                lc_events_escape_if(E, esc);
+                pend = !esc && inc != 0.0;
+                pr = r; pc = inc; prn = rn;
                 r = rn;
+            }
+            lc_events_step_if(E, pend, pr, pc, prn);
+            if (!lc_events_finish(E, g0, H)) {          // many events: exact tracking, step by step
+                double r2 = g0;
+                H = lc_map_identity(lc_ulp(g0));
+                for (int j = 0; j < len; ++j) {
+                    int esc; double inc;
+                    const double rn = lc_step_guess(P.Q, row[j], r2, &esc, &inc);
+                    if (esc) H = lc_map_const(0.0);
+                    else if (inc != 0.0) lc_map_step(H, r2, inc, rn);
+                    r2 = rn;
+                }
             }
             if (c + 1 < P.nchunks) lc_map_shift_out(H, LC_SUB(r, g1));
         } else {
@@ -275,15 +293,30 @@ __global__ void __launch_bounds__(LC_TPB, 2) lc_quant_kernel(LcQuantParams P, Co
         {
             double r = start;
             uint32_t *crow = reinterpret_cast<uint32_t *>(xs + tid * LC_ROW);
+            bool ok = true;
             for (int j = 0; j < len; ++j) {
                 uint32_t code; int esc; double inc, pe;
-                const double rn = lc_step(P.Q, row[j], r, &code, &esc, &inc, &pe);
+                const double rn = lc_step_nb(P.Q, row[j], r, &code, &inc, &esc, &pe, ok);
                 crow[j] = code;
                 if (P.pe) {
                     P.pe[p0 + j] = pe;
                     P.pe_rec[p0 + j] = LC_SUB(rn, r);
                 }
                 r = rn;
+            }
+            if (!ok) {                                        // a quotient was not certified: IEEE path
+                // x values of this row were partly overwritten by codes: reload from global
+                r = start;
+                for (int j = 0; j < len; ++j) {
+                    uint32_t code; int esc; double inc, pe;
+                    const double rn = lc_step(P.Q, P.x[p0 + 1 + j], r, &code, &esc, &inc, &pe);
+                    crow[j] = code;
+                    if (P.pe) {
+                        P.pe[p0 + j] = pe;
+                        P.pe_rec[p0 + j] = LC_SUB(rn, r);
+                    }
+                    r = rn;
+                }
             }
             if (len > 0 && c + 1 < P.nchunks && lc_bits(r) != lc_bits(next_pred)) {
                 P.bad_end[c] = r;

@@ -20,6 +20,7 @@ int64_t sim_predict(const double *x, int64_t n, double eb, int64_t nbh, int L,
     std::vector<OffMap> maps(nc);
     const double x0 = x[0];
     int64_t events = 0;
+    *n_events = 0;
     for (int64_t c = 0; c < nc; ++c) {
         const int64_t s = c * L;
         double g;
@@ -35,17 +36,28 @@ int64_t sim_predict(const double *x, int64_t n, double eb, int64_t nbh, int L,
         const int64_t e = (s + L < n - 1) ? s + L : n - 1;
         double r = guess[c];
         OffMap H = lc_map_identity(lc_ulp(r));
+        LcEvents E; lc_events_init(E, r);
+        const double g0 = r;
         for (int64_t i = s + 1; i <= e; ++i) {
             uint32_t code; double inc; int esc; double pe;
             const double rn = lc_step(Q, x[i], r, &code, &esc, &inc, &pe);
-            if (esc) H = lc_map_const(0.0);
+            if (esc) { H = lc_map_const(0.0); lc_events_escape(E); }
             else if (inc != 0.0) {
                 const int kb = H.kind;
                 const double Bb = H.B;
                 lc_map_step(H, r, inc, rn);
+                lc_events_step(E, r, inc, rn);
                 if (H.kind != kb || H.B != Bb) ++events;
             }
             r = rn;
+        }
+        {   // the deferred tracker must reproduce the step-by-step map exactly
+            OffMap H2;
+            if (lc_events_finish(E, g0, H2)) {
+                if (H2.kind != H.kind || lc_bits(H2.y) != lc_bits(H.y) || lc_bits(H2.t0) != lc_bits(H.t0) ||
+                    lc_bits(H2.t1) != lc_bits(H.t1) || lc_bits(H2.B) != lc_bits(H.B))
+                    *n_events = -1000000000;
+            }
         }
         rend[c] = r;
         if (c + 1 < nc) lc_map_shift_out(H, r - guess[c + 1]);
@@ -79,7 +91,7 @@ int64_t sim_predict(const double *x, int64_t n, double eb, int64_t nbh, int L,
             r = lc_step(Q, x[i], r, &code, &esc, &inc, &pe);
         }
     }
-    *n_events = events;
+    if (*n_events >= 0) *n_events = events;
     return bad;
 }
 
@@ -266,5 +278,28 @@ int64_t sim_tree_debug2(const double *x, int64_t n, double eb, int L)
         pre.swap(tmp);
     }
     return 0;
+}
+}
+extern "C" {
+// histogram of recorded events per chunk (deferred tracker), hist[0..15]
+void sim_event_hist(const double *x, int64_t n, double eb, int L, int64_t *hist)
+{
+    LcQuant Q;
+    Q.delta = 2.0 * eb; Q.eb = eb; Q.max_m = 32767.0; Q.max_m1 = 32768.0; Q.inv = 1.0 / Q.delta;
+    const int64_t nc = (n - 1 + L - 1) / L;
+    const double x0 = x[0];
+    for (int i = 0; i < 16; ++i) hist[i] = 0;
+    for (int64_t c = 0; c < nc; ++c) {
+        const int64_t s = c * L, e = (s + L < n - 1) ? s + L : n - 1;
+        double r = c == 0 ? x0 : x0 + floor((x[s] - x0) / Q.delta + 0.5) * Q.delta;
+        LcEvents E; lc_events_init(E, r);
+        for (int64_t i = s + 1; i <= e; ++i) {
+            uint32_t code; double inc; int esc; double pe;
+            const double rn = lc_step(Q, x[i], r, &code, &esc, &inc, &pe);
+            if (esc) lc_events_escape(E); else if (inc != 0.0) lc_events_step(E, r, inc, rn);
+            r = rn;
+        }
+        hist[E.n < 15 ? E.n : 15]++;
+    }
 }
 }
