@@ -38,7 +38,11 @@ struct lc_ctx {
     uint64_t launches = 0;
     // scratch
     LcBuf xbuf, codes, hist, desc, counters, bad_end, pe, pe_rec, lengths, cw, gkeys, ifreq,
-        parent, cbout, payload, esc_idx, esc_val, encdesc, range_parts, small;
+        parent, cbout, payload, esc_idx, esc_val, encdesc, range_parts, small, pred, tiles;
+    // last lc_range_f64 on device data (lets compress skip the anchor pass)
+    const void *rng_ptr = nullptr;
+    uint64_t rng_n = 0;
+    double rng_maxstep = INFINITY;
     void *pinned = nullptr;         // small pinned staging
     // last compress result
     uint64_t n = 0;
@@ -111,6 +115,12 @@ int lc_ctx_create(lc_ctx **out, int device, void *stream)
                                     (int)lc_quant_smem_bytes()));
     LC_CUDA_OK(cudaFuncSetAttribute(lc_quant_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)lc_quant_smem_bytes()));
+    LC_CUDA_OK(cudaFuncSetAttribute(lc_quant_a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)lc_quant_a_smem_bytes()));
+    LC_CUDA_OK(cudaFuncSetAttribute(lc_quant_b_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)lc_quant_b_smem_bytes()));
+    LC_CUDA_OK(cudaFuncSetAttribute(lc_quant_b_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)lc_quant_b_smem_bytes()));
     LC_CUDA_OK(cudaFuncSetAttribute(lc_codebook_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)lc_codebook_smem_bytes()));
     LC_CUDA_OK(cudaFuncSetAttribute(lc_encode_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -128,7 +138,7 @@ void lc_ctx_destroy(lc_ctx *ctx)
     LcBuf *bufs[] = {&ctx->xbuf, &ctx->codes, &ctx->hist, &ctx->desc, &ctx->counters, &ctx->bad_end,
                      &ctx->pe, &ctx->pe_rec, &ctx->lengths, &ctx->cw, &ctx->gkeys, &ctx->ifreq,
                      &ctx->parent, &ctx->cbout, &ctx->payload, &ctx->esc_idx, &ctx->esc_val,
-                     &ctx->encdesc, &ctx->range_parts, &ctx->small, &ctx->dec[0], &ctx->dec[1],
+                     &ctx->encdesc, &ctx->range_parts, &ctx->small, &ctx->pred, &ctx->tiles, &ctx->dec[0], &ctx->dec[1],
                      &ctx->dec[2], &ctx->dec[3], &ctx->dec[4], &ctx->dec[5], &ctx->dec[6],
                      &ctx->dec[7], &ctx->dec[8], &ctx->dec[9]};
     for (LcBuf *b : bufs)
@@ -182,6 +192,9 @@ int lc_range_f64(lc_ctx *ctx, const double *x, uint64_t n, int x_on_device, doub
     *vmin = h->vmin;
     *vmax = h->vmax;
     *nonfinite = h->nonfinite;
+    ctx->rng_ptr = x_on_device ? (const void *)x : nullptr;
+    ctx->rng_n = n;
+    ctx->rng_maxstep = h->maxstep;
     return 0;
 }
 
@@ -242,19 +255,47 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     LC_CUDA_OK(cudaStreamSynchronize(st));
     LC_CUDA_OK(cudaMemsetAsync(P.hist, 0, nbins * sizeof(uint32_t), st));
 
-    const int grid_cap = 2 * ctx->sm_count;
     unsigned long long *hbad = (unsigned long long *)ctx->pinned;
     uint32_t relaunches = 0;
     LC_CUDA_OK(cudaEventRecord(ctx->pev[1], st));
+    // split-pass buffers
+    LC_CUDA_OK(lc_reserve(ctx->pred, (size_t)nchunks * (sizeof(int) + 5 * sizeof(double)) + 64));
+    {
+        char *pp = (char *)ctx->pred.p;
+        P.pred.B = (double *)pp;
+        P.pred.t0 = P.pred.B + nchunks;
+        P.pred.t1 = P.pred.t0 + nchunks;
+        P.pred.y = P.pred.t1 + nchunks;
+        P.pred.g0 = P.pred.y + nchunks;
+        P.pred.kind = (int *)(P.pred.g0 + nchunks);
+    }
+    LC_CUDA_OK(lc_reserve(ctx->tiles, (size_t)(ntiles + 1) * (sizeof(OffMap) + sizeof(double) + 2 * sizeof(long long))));
+    P.tile_agg = (OffMap *)ctx->tiles.p;
+    P.tile_D = (double *)(P.tile_agg + ntiles + 1);
+    P.tile_last_esc = (long long *)(P.tile_D + ntiles + 1);
+    P.anc_in = (const long long *)(P.tile_last_esc + ntiles + 1);
+    long long *anc_in = (long long *)(P.tile_last_esc + ntiles + 1);
+    // definite escapes possible?  Same test as lc_definite_escape on the largest step.
+    P.use_anchors = 1;
+    if (ctx->rng_ptr == (const void *)dx && ctx->rng_n == n) {
+        const double ms = ctx->rng_maxstep;
+        P.use_anchors = ((ms * (1.0 - 0x1p-50)) - (eb_abs * (1.0 + 0x1p-50))) >= P.esc_thresh || !isfinite(ms);
+    }
+    const int ga = 2 * ctx->sm_count, gb = 3 * ctx->sm_count;
     for (;;) {
         P.ntiles = (nchunks - P.first_chunk + LC_TPB - 1) / LC_TPB;
-        LC_CUDA_OK(cudaMemsetAsync(P.desc, 0, P.ntiles * sizeof(LcTileDesc), st));
-        LC_CUDA_OK(cudaMemsetAsync(ctx->counters.p, 0, 16, st));
         LC_CUDA_OK(cudaMemsetAsync(first_bad, 0xff, 8, st));
-        const int grid = (int)(P.ntiles < grid_cap ? P.ntiles : grid_cap);
-        lc_quant_kernel<CodeT><<<grid, LC_TPB, lc_quant_smem_bytes(), st>>>(P, codes);
-        { int _rc = lc_debug_check(ctx, "lc_quant_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
-        ctx->launches += 1;
+        if (P.use_anchors) {
+            lc_anchor_tiles_kernel<<<(int)(P.ntiles < ga ? P.ntiles : ga), LC_TPB, 0, st>>>(P);
+            lc_anchor_scan_kernel<<<1, 1024, 0, st>>>(P.tile_last_esc, anc_in, P.ntiles, P.first_chunk * LC_L);
+            ctx->launches += 2;
+        }
+        lc_quant_a_kernel<<<(int)(P.ntiles < ga ? P.ntiles : ga), LC_TPB, lc_quant_a_smem_bytes(), st>>>(P);
+        { int _rc = lc_debug_check(ctx, "lc_quant_a_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+        lc_map_scan_kernel<<<1, 1024, 0, st>>>(P.tile_agg, P.tile_D, P.ntiles);
+        lc_quant_b_kernel<CodeT><<<(int)(P.ntiles < gb ? P.ntiles : gb), LC_TPB, lc_quant_b_smem_bytes(), st>>>(P, codes);
+        { int _rc = lc_debug_check(ctx, "lc_quant_b_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+        ctx->launches += 3;
         LC_CUDA_OK(cudaMemcpyAsync(hbad, first_bad, 8, cudaMemcpyDeviceToHost, st));
         LC_CUDA_OK(cudaStreamSynchronize(st));
         const unsigned long long fb = *hbad;

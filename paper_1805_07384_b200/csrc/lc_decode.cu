@@ -744,6 +744,310 @@ __global__ void __launch_bounds__(LC_TPB, 2) lc_recon_kernel(LcRecParams P)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Split reconstruction (no inter-tile waiting): R0 segmented m-prefix per tile,
+// R0 scan, RA guess chains + maps, map scan (lc_map_scan_kernel), RB exact chain.
+
+struct LcRecSplit {
+    LcSegScan *tile_seg;      // [ntiles] R0 output (tile aggregate)
+    LcSegScan *tile_in;       // [ntiles] R0 scan output (state at each tile start)
+    OffMap *tile_agg;         // [ntiles] RA output
+    double *tile_D;           // [ntiles + 1] map scan output
+    LcChunkPred pred;         // RA -> RB
+};
+
+__device__ __forceinline__ void lc_load_codes_tile(const LcRecParams &P, long long pbeg, uint32_t *cs)
+{
+    const int tid = threadIdx.x;
+    const long long nel = (long long)P.n - 1;
+#pragma unroll 8
+    for (int k = 0; k < LC_L; ++k) {
+        const int off = k * LC_TPB + tid;
+        const long long pos = pbeg + off;
+        uint32_t v = 0;
+        if (pos < nel) v = P.code_bytes == 2 ? (uint32_t)reinterpret_cast<const uint16_t *>(P.codes)[pos]
+                                             : reinterpret_cast<const uint32_t *>(P.codes)[pos];
+        cs[(off >> 5) * LC_ROW + (off & 31)] = v;
+    }
+}
+
+__device__ __forceinline__ LcSegScan lc_chunk_segscan(const uint32_t *crow, int len)
+{
+    LcSegScan mine; mine.sum = 0; mine.cnt = 0; mine.has = 0; mine.moved = 0;
+    for (int j = 0; j < len; ++j) {
+        const uint32_t code = crow[j];
+        if (code == 0) { mine.sum = 0; mine.cnt += 1; mine.has = 1; mine.moved = 0; }
+        else { const int64_t mm = lc_code_m(code); mine.sum += mm; mine.moved |= (mm != 0); }
+    }
+    return mine;
+}
+
+__device__ __forceinline__ LcSegScan lc_shfl_up_seg(const LcSegScan &v, int o)
+{
+    LcSegScan r;
+    r.sum = __shfl_up_sync(0xffffffffu, v.sum, o);
+    r.cnt = __shfl_up_sync(0xffffffffu, v.cnt, o);
+    r.has = __shfl_up_sync(0xffffffffu, v.has, o);
+    r.moved = __shfl_up_sync(0xffffffffu, v.moved, o);
+    return r;
+}
+
+// block-wide exclusive scan of chunk segscan states; returns exclusive, *agg = tile total
+__device__ __forceinline__ LcSegScan lc_block_segscan(const LcSegScan &mine, LcSegScan *wseg, LcSegScan *agg)
+{
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    LcSegScan inc = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const LcSegScan up = lc_shfl_up_seg(inc, o);
+        if (lane >= o) inc = lc_segscan_op(up, inc);
+    }
+    if (lane == 31) wseg[wid] = inc;
+    __syncthreads();
+    if (tid == 0)
+        for (int w = 1; w < LC_TPB / 32; ++w) wseg[w] = lc_segscan_op(wseg[w - 1], wseg[w]);
+    __syncthreads();
+    if (wid > 0) inc = lc_segscan_op(wseg[wid - 1], inc);
+    LcSegScan exc = lc_shfl_up_seg(inc, 1);
+    if (lane == 0) {
+        if (wid > 0) exc = wseg[wid - 1];
+        else { exc.sum = 0; exc.cnt = 0; exc.has = 0; exc.moved = 0; }
+    }
+    *agg = wseg[LC_TPB / 32 - 1];
+    return exc;
+}
+
+__global__ void __launch_bounds__(LC_TPB) lc_rec0_kernel(LcRecParams P, LcRecSplit S)
+{
+    __shared__ uint32_t cs[LC_TPB * LC_ROW];
+    __shared__ LcSegScan wseg[LC_TPB / 32];
+    const int tid = threadIdx.x;
+    const long long nel = (long long)P.n - 1;
+    for (long long t = blockIdx.x; t < P.ntiles; t += gridDim.x) {
+        const long long cbeg = P.first_chunk + t * LC_TPB;
+        const long long c = cbeg + tid;
+        const int len = (c < P.nchunks) ? (int)min((long long)LC_L, nel - c * LC_L) : 0;
+        __syncthreads();
+        lc_load_codes_tile(P, cbeg * LC_L, cs);
+        __syncthreads();
+        const LcSegScan mine = lc_chunk_segscan(cs + tid * LC_ROW, len);
+        LcSegScan agg;
+        lc_block_segscan(mine, wseg, &agg);
+        if (tid == 0) S.tile_seg[t] = agg;
+    }
+}
+
+__global__ void __launch_bounds__(1024) lc_rec0_scan_kernel(LcRecSplit S, long long ntiles, long long anchor_cnt)
+{
+    // sequential runs per thread + block scan of the runs (LcSegScan is a monoid)
+    __shared__ LcSegScan wsum[32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const long long per = (ntiles + 1023) / 1024;
+    const long long b0 = (long long)tid * per, b1 = min(ntiles, b0 + per);
+    LcSegScan run; run.sum = 0; run.cnt = 0; run.has = 0; run.moved = 0;
+    for (long long t = b0; t < b1; ++t) run = lc_segscan_op(run, S.tile_seg[t]);
+    LcSegScan inc = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const LcSegScan up = lc_shfl_up_seg(inc, o);
+        if (lane >= o) inc = lc_segscan_op(up, inc);
+    }
+    if (lane == 31) wsum[wid] = inc;
+    __syncthreads();
+    if (tid == 0)
+        for (int w = 1; w < 32; ++w) wsum[w] = lc_segscan_op(wsum[w - 1], wsum[w]);
+    __syncthreads();
+    if (wid > 0) inc = lc_segscan_op(wsum[wid - 1], inc);
+    LcSegScan exc = lc_shfl_up_seg(inc, 1);
+    if (lane == 0) {
+        if (wid > 0) exc = wsum[wid - 1];
+        else { exc.sum = 0; exc.cnt = 0; exc.has = 0; exc.moved = 0; }
+    }
+    LcSegScan st; st.sum = 0; st.cnt = anchor_cnt; st.has = 1; st.moved = 0;   // launch anchor
+    st = lc_segscan_op(st, exc);
+    for (long long t = b0; t < b1; ++t) {
+        S.tile_in[t] = st;
+        st = lc_segscan_op(st, S.tile_seg[t]);
+    }
+}
+
+__global__ void __launch_bounds__(LC_TPB, 2) lc_rec_a_kernel(LcRecParams P, LcRecSplit S)
+{
+    __shared__ uint32_t cs[LC_TPB * LC_ROW];
+    __shared__ LcSegScan wseg[LC_TPB / 32];
+    __shared__ OffMap warp_agg[LC_TPB / 32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const long long nel = (long long)P.n - 1;
+    for (long long t = blockIdx.x; t < P.ntiles; t += gridDim.x) {
+        const long long cbeg = P.first_chunk + t * LC_TPB;
+        const long long c = cbeg + tid;
+        const int len = (c < P.nchunks) ? (int)min((long long)LC_L, nel - c * LC_L) : 0;
+        __syncthreads();
+        lc_load_codes_tile(P, cbeg * LC_L, cs);
+        __syncthreads();
+        const uint32_t *crow = cs + tid * LC_ROW;
+        const LcSegScan mine = lc_chunk_segscan(crow, len);
+        LcSegScan agg;
+        const LcSegScan exc = lc_block_segscan(mine, wseg, &agg);
+        const LcSegScan before = lc_segscan_op(S.tile_in[t], exc);
+        const LcSegScan after = lc_segscan_op(before, mine);
+        auto anchor_of = [&](const LcSegScan &s) -> double {
+            if (s.cnt > P.anchor_cnt) {
+                const long long e = s.cnt - 1;
+                return e < (long long)P.n_esc ? P.esc_val[e] : 0.0;
+            }
+            return P.anchor_val;
+        };
+        auto guess_of = [&](const LcSegScan &s) -> double {
+            const double a = anchor_of(s);
+            if (!s.moved) return a;
+            const double g = LC_ADD(a, LC_MUL((double)s.sum, P.delta));
+            return isfinite(g) ? g : a;
+        };
+        const double g0 = guess_of(before);
+        const double g1 = guess_of(after);
+        OffMap H;
+        if (len > 0) {
+            P.chunk_esc[c] = before.cnt;
+            double r = g0;
+            long long e = before.cnt;
+            LcEvents E;
+            lc_events_init(E, g0);
+            bool pend = false;
+            double pr = 0.0, pc = 0.0, prn = 0.0;
+            for (int j = 0; j < len; ++j) {
+                const uint32_t code = crow[j];
+                const bool esc = code == 0;
+                const int64_t m = lc_code_m(code);
+                const double inc_ = LC_MUL((double)m, P.delta);
+                double rn = m != 0 ? LC_ADD(r, inc_) : r;
+                if (esc) { rn = e < (long long)P.n_esc ? P.esc_val[e] : 0.0; ++e; }
+                lc_events_step_if(E, pend, pr, pc, prn);
+                lc_events_escape_if(E, esc);
+                pend = !esc && m != 0;
+                pr = r; pc = inc_; prn = rn;
+                r = rn;
+            }
+            lc_events_step_if(E, pend, pr, pc, prn);
+            if (!lc_events_finish(E, g0, H)) {
+                double r2 = g0;
+                long long e2 = before.cnt;
+                H = lc_map_identity(lc_ulp(g0));
+                for (int j = 0; j < len; ++j) {
+                    const uint32_t code = crow[j];
+                    if (code == 0) {
+                        r2 = e2 < (long long)P.n_esc ? P.esc_val[e2] : 0.0;
+                        ++e2;
+                        H = lc_map_const(0.0);
+                    } else {
+                        const int64_t m = lc_code_m(code);
+                        if (m != 0) {
+                            const double inc_ = LC_MUL((double)m, P.delta);
+                            const double rn = LC_ADD(r2, inc_);
+                            lc_map_step(H, r2, inc_, rn);
+                            r2 = rn;
+                        }
+                    }
+                }
+            }
+            if (c + 1 < P.nchunks) lc_map_shift_out(H, LC_SUB(r, g1));
+        } else {
+            H = lc_map_neutral();
+        }
+        OffMap inc_map = H;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const OffMap up = lc_shfl_up_map(inc_map, o);
+            if (lane >= o) inc_map = lc_map_compose(inc_map, up);
+        }
+        if (lane == 31) warp_agg[wid] = inc_map;
+        __syncthreads();
+        if (tid == 0)
+            for (int w = 1; w < LC_TPB / 32; ++w) warp_agg[w] = lc_map_compose(warp_agg[w], warp_agg[w - 1]);
+        __syncthreads();
+        if (wid > 0) inc_map = lc_map_compose(inc_map, warp_agg[wid - 1]);
+        OffMap exc_map = lc_shfl_up_map(inc_map, 1);
+        if (lane == 0) exc_map = wid > 0 ? warp_agg[wid - 1] : lc_map_neutral();
+        if (len > 0) {
+            S.pred.kind[c] = exc_map.kind;
+            S.pred.B[c] = exc_map.B;
+            S.pred.t0[c] = exc_map.t0;
+            S.pred.t1[c] = exc_map.t1;
+            S.pred.y[c] = exc_map.y;
+            S.pred.g0[c] = g0;
+        }
+        if (tid == 0) S.tile_agg[t] = warp_agg[LC_TPB / 32 - 1];
+    }
+}
+
+__global__ void __launch_bounds__(LC_TPB, 2) lc_rec_b_kernel(LcRecParams P, LcRecSplit S)
+{
+    extern __shared__ __align__(16) unsigned char lc_dyn_smem[];
+    double *ys = reinterpret_cast<double *>(lc_dyn_smem);
+    uint32_t *cs = reinterpret_cast<uint32_t *>(ys + LC_TPB * LC_ROW);
+    __shared__ double starts[LC_TPB + 1];
+    const int tid = threadIdx.x;
+    const long long nel = (long long)P.n - 1;
+    for (long long t = blockIdx.x; t < P.ntiles; t += gridDim.x) {
+        const long long cbeg = P.first_chunk + t * LC_TPB;
+        const long long pbeg = cbeg * LC_L;
+        const long long c = cbeg + tid;
+        const long long p0 = c * LC_L;
+        const int len = (c < P.nchunks) ? (int)min((long long)LC_L, nel - p0) : 0;
+        __syncthreads();
+        lc_load_codes_tile(P, pbeg, cs);
+        const double Dt = S.tile_D[t];
+        double start = 0.0;
+        if (len > 0) {
+            OffMap m;
+            m.kind = S.pred.kind[c]; m.B = S.pred.B[c]; m.t0 = S.pred.t0[c]; m.t1 = S.pred.t1[c]; m.y = S.pred.y[c];
+            m.v = 0.0; m.og = 0.0;
+            start = lc_apply_offset(S.pred.g0[c], lc_map_eval(m, Dt));
+        }
+        starts[tid] = start;
+        if (tid == LC_TPB - 1) {
+            const long long cn = cbeg + LC_TPB;
+            starts[LC_TPB] = (cn < P.nchunks) ? lc_apply_offset(S.pred.g0[cn], S.tile_D[t + 1]) : 0.0;
+        }
+        __syncthreads();
+        const uint32_t *crow = cs + tid * LC_ROW;
+        double *yrow = ys + tid * LC_ROW;
+        if (len > 0) {
+            double r = start;
+            long long e = P.chunk_esc[c];
+            for (int j = 0; j < len; ++j) {
+                const uint32_t code = crow[j];
+                const int64_t m = lc_code_m(code);
+                double rn = m != 0 ? LC_ADD(r, LC_MUL((double)m, P.delta)) : r;   // compressor.py:371-374
+                if (code == 0) {                                                   // :365-369
+                    if (e < (long long)P.n_esc) {
+                        rn = P.esc_val[e];
+                        if (P.esc_idx[e] != (unsigned long long)(p0 + j + 1)) atomicExch(&P.esc_flags[1], 1);
+                    } else {
+                        atomicExch(&P.esc_flags[0], 1);
+                    }
+                    ++e;
+                }
+                yrow[j] = rn;
+                r = rn;
+            }
+            if (c + 1 < P.nchunks && lc_bits(r) != lc_bits(starts[tid + 1])) {
+                P.bad_end[c] = r;
+                atomicMin(P.first_bad, (unsigned long long)(c + 1));
+            }
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int k = 0; k < LC_L; ++k) {
+            const int off = k * LC_TPB + tid;
+            const long long pos = pbeg + 1 + off;
+            if (pos <= nel) __stcs(P.out + pos, ys[(off >> 5) * LC_ROW + (off & 31)]);
+        }
+    }
+}
+
+size_t lc_rec_b_smem_bytes() { return sizeof(double) * LC_TPB * LC_ROW + sizeof(uint32_t) * LC_TPB * LC_ROW; }
+
 size_t lc_recon_smem_bytes() { return sizeof(double) * LC_TPB * LC_ROW + sizeof(uint32_t) * LC_TPB * LC_ROW; }
 
 __global__ void lc_set_first_kernel(double *out, double v) { out[0] = v; }
@@ -874,7 +1178,8 @@ int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_valu
     }
     const int64_t nchunks = (int64_t)((m + LC_L - 1) / LC_L);
     const int64_t ntiles = (nchunks + LC_TPB - 1) / LC_TPB;
-    LC_CUDA_OK(lc_reserve(baux2, ntiles * sizeof(LcRecDesc) + nchunks * 16 + 64));
+    LC_CUDA_OK(lc_reserve(baux2, (size_t)(ntiles + 1) * (2 * sizeof(LcSegScan) + sizeof(OffMap) + sizeof(double))
+                                 + (size_t)nchunks * (16 + sizeof(int) + 5 * sizeof(double)) + 256));
     LcRecParams R;
     R.codes = bcodes.p;
     R.code_bytes = code_bytes;
@@ -888,13 +1193,33 @@ int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_valu
     R.anchor_val = first_value;
     R.anchor_cnt = 0;
     R.nchunks = nchunks;
-    R.desc = (LcRecDesc *)baux2.p;
-    R.tile_counter = (unsigned int *)((char *)baux.p + 96);
+    R.desc = nullptr;
+    R.tile_counter = nullptr;
     R.out = dout;
     R.first_bad = (unsigned long long *)((char *)baux.p + 112);
-    R.bad_end = (double *)((char *)baux2.p + ntiles * sizeof(LcRecDesc));
-    R.chunk_esc = (long long *)(R.bad_end + nchunks);
     R.esc_flags = esc_flags;
+    LcRecSplit RS;
+    {
+        char *pp = (char *)baux2.p;
+        RS.tile_seg = (LcSegScan *)pp;           pp += (ntiles + 1) * sizeof(LcSegScan);
+        RS.tile_in = (LcSegScan *)pp;            pp += (ntiles + 1) * sizeof(LcSegScan);
+        RS.tile_agg = (OffMap *)pp;              pp += (ntiles + 1) * sizeof(OffMap);
+        RS.tile_D = (double *)pp;                pp += (ntiles + 1) * sizeof(double);
+        R.bad_end = (double *)pp;                pp += nchunks * sizeof(double);
+        R.chunk_esc = (long long *)pp;           pp += nchunks * sizeof(long long);
+        RS.pred.B = (double *)pp;                pp += nchunks * sizeof(double);
+        RS.pred.t0 = (double *)pp;               pp += nchunks * sizeof(double);
+        RS.pred.t1 = (double *)pp;               pp += nchunks * sizeof(double);
+        RS.pred.y = (double *)pp;                pp += nchunks * sizeof(double);
+        RS.pred.g0 = (double *)pp;               pp += nchunks * sizeof(double);
+        RS.pred.kind = (int *)pp;
+    }
+    static bool attr_b = false;
+    if (!attr_b) {
+        LC_CUDA_OK(cudaFuncSetAttribute(lc_rec_b_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)lc_rec_b_smem_bytes()));
+        attr_b = true;
+    }
     LC_CUDA_OK(cudaMemsetAsync(esc_flags, 0, 8, st));
     lc_set_first_kernel<<<1, 1, 0, st>>>(dout, first_value);
     lc_count_launch(ctx, 1);
@@ -903,13 +1228,16 @@ int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_valu
     int relaunches = 0;
     for (;;) {
         R.ntiles = (nchunks - R.first_chunk + LC_TPB - 1) / LC_TPB;
-        LC_CUDA_OK(cudaMemsetAsync(R.desc, 0, R.ntiles * sizeof(LcRecDesc), st));
-        LC_CUDA_OK(cudaMemsetAsync(R.tile_counter, 0, 4, st));
         LC_CUDA_OK(cudaMemsetAsync(R.first_bad, 0xff, 8, st));
         const int grid = (int)(R.ntiles < grid_cap ? R.ntiles : grid_cap);
-        lc_recon_kernel<<<grid, LC_TPB, lc_recon_smem_bytes(), st>>>(R);
-        { int _rc = lc_debug_check(ctx, "lc_recon_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
-        lc_count_launch(ctx, 1);
+        lc_rec0_kernel<<<(int)(R.ntiles < 3 * grid_cap ? R.ntiles : 3 * grid_cap), LC_TPB, 0, st>>>(R, RS);
+        lc_rec0_scan_kernel<<<1, 1024, 0, st>>>(RS, R.ntiles, R.anchor_cnt);
+        lc_rec_a_kernel<<<grid, LC_TPB, 0, st>>>(R, RS);
+        { int _rc = lc_debug_check(ctx, "lc_rec_a_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+        lc_map_scan_kernel<<<1, 1024, 0, st>>>(RS.tile_agg, RS.tile_D, R.ntiles);
+        lc_rec_b_kernel<<<grid, LC_TPB, lc_rec_b_smem_bytes(), st>>>(R, RS);
+        { int _rc = lc_debug_check(ctx, "lc_rec_b_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+        lc_count_launch(ctx, 5);
         LC_CUDA_OK(cudaMemcpyAsync(hbad, R.first_bad, 8, cudaMemcpyDeviceToHost, st));
         LC_CUDA_OK(cudaStreamSynchronize(st));
         if (*hbad == ~0ULL) break;
@@ -929,12 +1257,11 @@ int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_valu
     long long total_esc;
     LC_CUDA_OK(cudaMemcpy(hflags, esc_flags, 8, cudaMemcpyDeviceToHost));
     {
-        // total escape codes = tile-inclusive count of the last tile of the first launch chain
-        LcSegScan s;
-        LcRecDesc last;
-        (void)s;
-        LC_CUDA_OK(cudaMemcpy(&last, R.desc + (R.ntiles - 1), sizeof(LcRecDesc), cudaMemcpyDeviceToHost));
-        total_esc = last.seg_inc_cnt;
+        // total escape codes = state at the last tile start + that tile's aggregate
+        LcSegScan a, b;
+        LC_CUDA_OK(cudaMemcpy(&a, RS.tile_in + (R.ntiles - 1), sizeof(LcSegScan), cudaMemcpyDeviceToHost));
+        LC_CUDA_OK(cudaMemcpy(&b, RS.tile_seg + (R.ntiles - 1), sizeof(LcSegScan), cudaMemcpyDeviceToHost));
+        total_esc = a.cnt + b.cnt;
     }
     LC_CUDA_OK(cudaEventRecord(lc_phase_ev(ctx, 7), st));
     lc_set_kind(ctx, 2);

@@ -3,7 +3,14 @@
 #pragma once
 #include "lc_common.cuh"
 
-struct LcRangePart { double vmin, vmax; int nonfinite; };
+struct LcRangePart { double vmin, vmax, maxstep; int nonfinite; };
+
+// Per-chunk prediction data written by pass A, read by pass B (SoA, [nchunks]).
+struct LcChunkPred {
+    int *kind;               // exclusive in-tile prefix map of the chunk (evaluation fields)
+    double *B, *t0, *t1, *y;
+    double *g0;              // guess of the chain value at the chunk start
+};
 
 struct LcQuantParams {
     const double *x;
@@ -23,6 +30,13 @@ struct LcQuantParams {
     double *bad_end;         // per chunk: exact end value when its successor failed
     double *pe, *pe_rec;     // optional traces
     unsigned long long *timeline;  // optional: 8 globaltimer stamps per tile (profiling)
+    // split-pass data
+    int use_anchors;             // 0: no definite escape possible (range pass), anchor = launch anchor
+    const long long *anc_in;     // [ntiles] last definite escape before each tile (>= launch anchor)
+    long long *tile_last_esc;    // [ntiles] pass 0 output
+    LcChunkPred pred;            // pass A -> pass B
+    OffMap *tile_agg;            // [ntiles] pass A -> scan
+    double *tile_D;              // [ntiles + 1] scan -> pass B (offset at each tile start)
 };
 
 struct LcCodebookOut {
@@ -58,6 +72,14 @@ struct LcEncParams {
 __global__ void lc_range_kernel(const double *__restrict__ x, uint64_t n, LcRangePart *__restrict__ parts);
 __global__ void lc_range_final_kernel(const LcRangePart *__restrict__ parts, int np, LcRangePart *__restrict__ out);
 template <typename CodeT> __global__ void lc_quant_kernel(LcQuantParams P, CodeT *__restrict__ codes);
+__global__ void lc_anchor_tiles_kernel(LcQuantParams P);
+__global__ void lc_anchor_scan_kernel(const long long *__restrict__ last, long long *__restrict__ incoming,
+                                      long long ntiles, long long launch_pos);
+__global__ void lc_quant_a_kernel(LcQuantParams P);
+__global__ void lc_map_scan_kernel(const OffMap *__restrict__ agg, double *__restrict__ tileD, long long ntiles);
+template <typename CodeT> __global__ void lc_quant_b_kernel(LcQuantParams P, CodeT *__restrict__ codes);
+size_t lc_quant_a_smem_bytes();
+size_t lc_quant_b_smem_bytes();
 template <typename CodeT> __global__ void lc_quant_serial_kernel(LcQuantParams P, CodeT *__restrict__ codes);
 template <typename CodeT>
 __global__ void lc_hist_kernel(const CodeT *__restrict__ codes, uint64_t m, uint32_t *__restrict__ hist, uint32_t nbins);

@@ -21,39 +21,43 @@
 __global__ void __launch_bounds__(256) lc_range_kernel(const double *__restrict__ x, uint64_t n,
                                                       LcRangePart *__restrict__ parts)
 {
-    double mn = INFINITY, mx = -INFINITY;
+    // min, max, non-finite flag and max |x_i - x_{i-1}| (decides whether definite
+    // escapes are possible, lc_compress_f64).  Grid-stride over warp-contiguous
+    // runs; the predecessor comes from the neighbouring lane.
+    double mn = INFINITY, mx = -INFINITY, ms = 0.0;
     int nf = 0;
+    const int lane = threadIdx.x & 31;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    // 2-way unrolled grid-stride loop (coalesced 8-byte loads)
-    for (; i + stride < n; i += 2 * stride) {
-        const double a = __ldcs(x + i), b = __ldcs(x + i + stride);
-        nf |= !isfinite(a) | !isfinite(b);
-        mn = fmin(mn, fmin(a, b));
-        mx = fmax(mx, fmax(a, b));
-    }
-    if (i < n) {
-        const double a = __ldcs(x + i);
-        nf |= !isfinite(a);
-        mn = fmin(mn, a);
-        mx = fmax(mx, a);
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n; base += stride) {
+        const uint64_t i = base + lane;
+        const double a = i < n ? __ldcs(x + i) : 0.0;
+        double prev = __shfl_up_sync(0xffffffffu, a, 1);
+        if (lane == 0) prev = base > 0 ? x[base - 1] : a;
+        if (i < n) {
+            nf |= !isfinite(a);
+            mn = fmin(mn, a);
+            mx = fmax(mx, a);
+            ms = fmax(ms, fabs(__dsub_rn(a, prev)));
+        }
     }
     for (int o = 16; o; o >>= 1) {
         mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
         mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        ms = fmax(ms, __shfl_xor_sync(0xffffffffu, ms, o));
         nf |= __shfl_xor_sync(0xffffffffu, nf, o);
     }
-    __shared__ double smn[8], smx[8];
+    __shared__ double smn[8], smx[8], sms[8];
     __shared__ int snf[8];
     const int w = threadIdx.x >> 5;
-    if ((threadIdx.x & 31) == 0) { smn[w] = mn; smx[w] = mx; snf[w] = nf; }
+    if (lane == 0) { smn[w] = mn; smx[w] = mx; sms[w] = ms; snf[w] = nf; }
     __syncthreads();
     if (threadIdx.x == 0) {
         for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
-            mn = fmin(mn, smn[k]); mx = fmax(mx, smx[k]); nf |= snf[k];
+            mn = fmin(mn, smn[k]); mx = fmax(mx, smx[k]); ms = fmax(ms, sms[k]); nf |= snf[k];
         }
         parts[blockIdx.x].vmin = mn;
         parts[blockIdx.x].vmax = mx;
+        parts[blockIdx.x].maxstep = ms;
         parts[blockIdx.x].nonfinite = nf;
     }
 }
@@ -62,17 +66,19 @@ __global__ void __launch_bounds__(256) lc_range_kernel(const double *__restrict_
 __global__ void lc_range_final_kernel(const LcRangePart *__restrict__ parts, int np,
                                       LcRangePart *__restrict__ out)
 {
-    double mn = INFINITY, mx = -INFINITY;
+    double mn = INFINITY, mx = -INFINITY, ms = 0.0;
     int nf = 0;
     for (int i = threadIdx.x; i < np; i += blockDim.x) {
-        mn = fmin(mn, parts[i].vmin); mx = fmax(mx, parts[i].vmax); nf |= parts[i].nonfinite;
+        mn = fmin(mn, parts[i].vmin); mx = fmax(mx, parts[i].vmax); ms = fmax(ms, parts[i].maxstep);
+        nf |= parts[i].nonfinite;
     }
     for (int o = 16; o; o >>= 1) {
         mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
         mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        ms = fmax(ms, __shfl_xor_sync(0xffffffffu, ms, o));
         nf |= __shfl_xor_sync(0xffffffffu, nf, o);
     }
-    if (threadIdx.x == 0) { out->vmin = mn; out->vmax = mx; out->nonfinite = nf; }
+    if (threadIdx.x == 0) { out->vmin = mn; out->vmax = mx; out->maxstep = ms; out->nonfinite = nf; }
 }
 
 // ---------------------------------------------------------------------------
@@ -353,6 +359,318 @@ __global__ void __launch_bounds__(LC_TPB, 2) lc_quant_kernel(LcQuantParams P, Co
             if (hs[i]) atomicAdd(&P.hist[i], hs[i]);
     }
 }
+
+// ---------------------------------------------------------------------------
+// Split quantizer: pass 0 (anchors, only when escapes are possible), pass A
+// (guess chains + maps + in-tile scan), map scan over tiles, pass B (exact
+// chain).  No tile ever waits for another tile.
+
+// Load one tile of x into padded smem rows; xhalo[LC_L] = x[tile start].
+__device__ __forceinline__ void lc_load_x_tile(const LcQuantParams &P, long long pbeg, double *xs, double *xhalo)
+{
+    const int tid = threadIdx.x;
+    const long long nel = (long long)P.n - 1;
+#pragma unroll 8
+    for (int k = 0; k < LC_L; ++k) {
+        const int off = k * LC_TPB + tid;
+        const long long pos = pbeg + 1 + off;
+        if (pos <= nel) xs[(off >> 5) * LC_ROW + (off & 31)] = __ldcs(P.x + pos);
+    }
+    if (tid <= LC_L) {
+        const long long pos = pbeg - LC_L + tid;
+        xhalo[tid] = pos >= 0 ? P.x[pos] : 0.0;
+    }
+}
+
+__global__ void __launch_bounds__(LC_TPB) lc_anchor_tiles_kernel(LcQuantParams P)
+{
+    // last definite escape position of every tile (escapes certain from the data)
+    __shared__ long long wmax[LC_TPB / 32];
+    const int tid = threadIdx.x;
+    const long long nel = (long long)P.n - 1;
+    for (long long t = blockIdx.x; t < P.ntiles; t += gridDim.x) {
+        const long long pbeg = (P.first_chunk + t * LC_TPB) * LC_L;
+        long long last = -1;
+        for (int k = 0; k < LC_L; ++k) {
+            const long long pos = pbeg + 1 + k * LC_TPB + tid;
+            if (pos <= nel && lc_definite_escape(P.x[pos], P.x[pos - 1], P)) last = max(last, pos);
+        }
+        for (int o = 16; o; o >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
+        if ((tid & 31) == 0) wmax[tid >> 5] = last;
+        __syncthreads();
+        if (tid == 0) {
+            for (int w = 0; w < LC_TPB / 32; ++w) last = max(last, wmax[w]);
+            P.tile_last_esc[t] = last;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(1024) lc_anchor_scan_kernel(const long long *__restrict__ last,
+                                                             long long *__restrict__ incoming, long long ntiles,
+                                                             long long launch_pos)
+{
+    typedef cub::BlockScan<long long, 1024> Scan;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ long long carry;
+    if (threadIdx.x == 0) carry = launch_pos;
+    __syncthreads();
+    struct MaxOp { __device__ long long operator()(long long a, long long b) const { return a > b ? a : b; } };
+    for (long long b = 0; b < ntiles; b += 1024) {
+        const long long i = b + threadIdx.x;
+        const long long v = i < ntiles ? last[i] : -1;
+        long long ex, agg;
+        Scan(tmp).ExclusiveScan(v, ex, -1LL, MaxOp(), agg);
+        const long long c = carry;
+        if (i < ntiles) incoming[i] = max(c, ex);
+        __syncthreads();
+        if (threadIdx.x == 0) carry = max(c, agg);
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(LC_TPB, 2) lc_quant_a_kernel(LcQuantParams P)
+{
+    typedef cub::BlockScan<long long, LC_TPB> ScanLL;
+    extern __shared__ __align__(16) unsigned char lc_dyn_smem[];
+    double *xs = reinterpret_cast<double *>(lc_dyn_smem);
+    __shared__ double xhalo[LC_L + 1];
+    __shared__ typename ScanLL::TempStorage scan_tmp;
+    __shared__ OffMap warp_agg[LC_TPB / 32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const long long nel = (long long)P.n - 1;
+    const long long launch_apos = P.first_chunk * LC_L;
+
+    for (long long t = blockIdx.x; t < P.ntiles; t += gridDim.x) {
+        const long long cbeg = P.first_chunk + t * LC_TPB;
+        const long long pbeg = cbeg * LC_L;
+        const long long c = cbeg + tid;
+        const long long p0 = c * LC_L;
+        const int len = (c < P.nchunks) ? (int)min((long long)LC_L, nel - p0) : 0;
+        __syncthreads();
+        lc_load_x_tile(P, pbeg, xs, xhalo);
+        __syncthreads();
+        const double *row = xs + tid * LC_ROW;
+        const double xstart = tid == 0 ? xhalo[LC_L] : xs[(tid - 1) * LC_ROW + LC_L - 1];
+
+        // anchors
+        long long apos, apos_next;
+        if (P.use_anchors) {
+            long long last_esc = -1;
+            double xp = xstart;
+            for (int j = 0; j < len; ++j) {
+                const double xi = row[j];
+                if (lc_definite_escape(xi, xp, P)) last_esc = p0 + 1 + j;
+                xp = xi;
+            }
+            struct MaxOp { __device__ long long operator()(long long a, long long b) const { return a > b ? a : b; } };
+            long long esc_excl;
+            ScanLL(scan_tmp).ExclusiveScan(last_esc, esc_excl, -1LL, MaxOp());
+            const long long in = P.anc_in[t];
+            apos = max(in, esc_excl);
+            apos_next = max(apos, last_esc);
+        } else {
+            apos = apos_next = launch_apos;
+        }
+        const double aval = (apos == launch_apos) ? P.anchor_val : P.x[apos];
+        const double aval_next = (apos_next == launch_apos) ? P.anchor_val : P.x[apos_next];
+        const double xend = len > 0 ? row[len - 1] : xstart;
+        const double g0 = lc_guess(P, xstart, p0, apos, aval);
+        const double g1 = lc_guess(P, xend, p0 + len, apos_next, aval_next);
+
+        // guess chain -> chunk map (software-pipelined event detection)
+        OffMap H;
+        if (len > 0) {
+            double r = g0;
+            LcEvents E;
+            lc_events_init(E, g0);
+            bool pend = false;
+            double pr = 0.0, pc = 0.0, prn = 0.0;
+            for (int j = 0; j < len; ++j) {
+                int esc; double inc;
+                const double rn = lc_step_guess(P.Q, row[j], r, &esc, &inc);
+                lc_events_step_if(E, pend, pr, pc, prn);
+                lc_events_escape_if(E, esc);
+                pend = !esc && inc != 0.0;
+                pr = r; pc = inc; prn = rn;
+                r = rn;
+            }
+            lc_events_step_if(E, pend, pr, pc, prn);
+            if (!lc_events_finish(E, g0, H)) {
+                double r2 = g0;
+                H = lc_map_identity(lc_ulp(g0));
+                for (int j = 0; j < len; ++j) {
+                    int esc; double inc;
+                    const double rn = lc_step_guess(P.Q, row[j], r2, &esc, &inc);
+                    if (esc) H = lc_map_const(0.0);
+                    else if (inc != 0.0) lc_map_step(H, r2, inc, rn);
+                    r2 = rn;
+                }
+            }
+            if (c + 1 < P.nchunks) lc_map_shift_out(H, LC_SUB(r, g1));
+        } else {
+            H = lc_map_neutral();
+        }
+
+        // in-tile inclusive scan of maps
+        OffMap inc_map = H;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const OffMap up = lc_shfl_up_map(inc_map, o);
+            if (lane >= o) inc_map = lc_map_compose(inc_map, up);
+        }
+        if (lane == 31) warp_agg[wid] = inc_map;
+        __syncthreads();
+        if (tid == 0)
+            for (int w = 1; w < LC_TPB / 32; ++w) warp_agg[w] = lc_map_compose(warp_agg[w], warp_agg[w - 1]);
+        __syncthreads();
+        if (wid > 0) inc_map = lc_map_compose(inc_map, warp_agg[wid - 1]);
+        OffMap exc_map = lc_shfl_up_map(inc_map, 1);
+        if (lane == 0) exc_map = wid > 0 ? warp_agg[wid - 1] : lc_map_neutral();
+        if (len > 0) {
+            P.pred.kind[c] = exc_map.kind;
+            P.pred.B[c] = exc_map.B;
+            P.pred.t0[c] = exc_map.t0;
+            P.pred.t1[c] = exc_map.t1;
+            P.pred.y[c] = exc_map.y;
+            P.pred.g0[c] = g0;
+        }
+        if (tid == 0) P.tile_agg[t] = warp_agg[LC_TPB / 32 - 1];
+    }
+}
+
+// Offsets at every tile start: D_0 = 0, D_{t+1} = agg_t(D_t).  One CTA: each
+// thread composes a run of tiles, a block scan composes the runs.
+__global__ void __launch_bounds__(1024) lc_map_scan_kernel(const OffMap *__restrict__ agg, double *__restrict__ tileD,
+                                                          long long ntiles)
+{
+    __shared__ OffMap wsum[32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const long long per = (ntiles + 1023) / 1024;
+    const long long b0 = (long long)tid * per, b1 = min(ntiles, b0 + per);
+    OffMap run = lc_map_neutral();
+    for (long long t = b0; t < b1; ++t) run = lc_map_compose(agg[t], run);
+    OffMap inc = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const OffMap up = lc_shfl_up_map(inc, o);
+        if (lane >= o) inc = lc_map_compose(inc, up);
+    }
+    if (lane == 31) wsum[wid] = inc;
+    __syncthreads();
+    if (tid == 0)
+        for (int w = 1; w < 32; ++w) wsum[w] = lc_map_compose(wsum[w], wsum[w - 1]);
+    __syncthreads();
+    if (wid > 0) inc = lc_map_compose(inc, wsum[wid - 1]);
+    OffMap exc = lc_shfl_up_map(inc, 1);
+    if (lane == 0) exc = wid > 0 ? wsum[wid - 1] : lc_map_neutral();
+    double D = lc_map_eval(exc, 0.0);
+    for (long long t = b0; t < b1; ++t) {
+        tileD[t] = D;
+        D = lc_map_eval(agg[t], D);
+    }
+    if (b1 == ntiles && b0 < b1) tileD[ntiles] = D;
+}
+
+template <typename CodeT>
+__global__ void __launch_bounds__(LC_TPB, 3) lc_quant_b_kernel(LcQuantParams P, CodeT *__restrict__ codes)
+{
+    extern __shared__ __align__(16) unsigned char lc_dyn_smem[];
+    double *xs = reinterpret_cast<double *>(lc_dyn_smem);
+    uint32_t *hs = reinterpret_cast<uint32_t *>(xs + LC_TPB * LC_ROW);
+    __shared__ double xhalo[LC_L + 1];
+    __shared__ double starts[LC_TPB + 1];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const long long nel = (long long)P.n - 1;
+    const uint32_t hb = P.nbins < LC_HBINS_B ? P.nbins : LC_HBINS_B;
+    for (uint32_t i = tid; i < LC_HBINS_B; i += LC_TPB) hs[i] = 0;
+
+    for (long long t = blockIdx.x; t < P.ntiles; t += gridDim.x) {
+        const long long cbeg = P.first_chunk + t * LC_TPB;
+        const long long pbeg = cbeg * LC_L;
+        const long long c = cbeg + tid;
+        const long long p0 = c * LC_L;
+        const int len = (c < P.nchunks) ? (int)min((long long)LC_L, nel - p0) : 0;
+        __syncthreads();
+        lc_load_x_tile(P, pbeg, xs, xhalo);
+        const double Dt = P.tile_D[t];
+        double start = 0.0;
+        if (len > 0) {
+            OffMap m;
+            m.kind = P.pred.kind[c]; m.B = P.pred.B[c]; m.t0 = P.pred.t0[c]; m.t1 = P.pred.t1[c]; m.y = P.pred.y[c];
+            m.v = 0.0; m.og = 0.0;
+            start = lc_apply_offset(P.pred.g0[c], lc_map_eval(m, Dt));
+        }
+        starts[tid] = start;
+        if (tid == LC_TPB - 1) {
+            const long long cn = cbeg + LC_TPB;          // first chunk of the next tile
+            starts[LC_TPB] = (cn < P.nchunks) ? lc_apply_offset(P.pred.g0[cn], P.tile_D[t + 1]) : 0.0;
+        }
+        __syncthreads();
+        const double *row = xs + tid * LC_ROW;
+        {
+            double r = start;
+            uint32_t *crow = reinterpret_cast<uint32_t *>(xs + tid * LC_ROW);
+            bool ok = true;
+            for (int j = 0; j < len; ++j) {
+                uint32_t code; int esc; double inc, pe;
+                const double rn = lc_step_nb(P.Q, row[j], r, &code, &inc, &esc, &pe, ok);
+                crow[j] = code;
+                if (P.pe) {
+                    P.pe[p0 + j] = pe;
+                    P.pe_rec[p0 + j] = LC_SUB(rn, r);
+                }
+                r = rn;
+            }
+            if (!ok) {                                        // a quotient was not certified: IEEE path
+                r = start;
+                for (int j = 0; j < len; ++j) {
+                    uint32_t code; int esc; double inc, pe;
+                    const double rn = lc_step(P.Q, P.x[p0 + 1 + j], r, &code, &esc, &inc, &pe);
+                    crow[j] = code;
+                    if (P.pe) {
+                        P.pe[p0 + j] = pe;
+                        P.pe_rec[p0 + j] = LC_SUB(rn, r);
+                    }
+                    r = rn;
+                }
+            }
+            if (len > 0 && c + 1 < P.nchunks && lc_bits(r) != lc_bits(starts[tid + 1])) {
+                P.bad_end[c] = r;
+                atomicMin(P.first_bad, (unsigned long long)(c + 1));
+            }
+        }
+        __syncthreads();
+        // histogram (warp-aggregated) + coalesced code store
+#pragma unroll 4
+        for (int k = 0; k < LC_L; ++k) {
+            const int off = k * LC_TPB + tid;
+            const long long pos = pbeg + off;
+            const bool valid = pos < nel;
+            const uint32_t code = valid ? reinterpret_cast<const uint32_t *>(xs)[(off >> 5) * (2 * LC_ROW) + (off & 31)]
+                                        : 0xffffffffu;
+            if (valid) codes[pos] = (CodeT)code;
+            if (P.count_hist) {
+                const unsigned peers = __match_any_sync(0xffffffffu, code);
+                if (valid && (int)(__ffs(peers) - 1) == lane) {
+                    const unsigned cnt = __popc(peers);
+                    if (code < hb) atomicAdd(&hs[code], cnt);
+                    else atomicAdd(&P.hist[code], cnt);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (P.count_hist)
+        for (uint32_t i = tid; i < hb; i += LC_TPB)
+            if (hs[i]) atomicAdd(&P.hist[i], hs[i]);
+}
+
+size_t lc_quant_a_smem_bytes() { return sizeof(double) * LC_TPB * LC_ROW; }
+size_t lc_quant_b_smem_bytes() { return sizeof(double) * LC_TPB * LC_ROW + sizeof(uint32_t) * LC_HBINS_B; }
+
+template __global__ void lc_quant_b_kernel<uint16_t>(LcQuantParams, uint16_t *);
+template __global__ void lc_quant_b_kernel<uint32_t>(LcQuantParams, uint32_t *);
 
 // Sequential exact chain from chunk `first_chunk` (fallback for inputs whose
 // chunk predictions keep failing).  One thread; correct for every input.
