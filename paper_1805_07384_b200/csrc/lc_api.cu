@@ -111,10 +111,6 @@ int lc_ctx_create(lc_ctx **out, int device, void *stream)
     LC_CUDA_OK(cudaEventCreate(&ctx->ev1));
     for (int i = 0; i < 12; ++i) LC_CUDA_OK(cudaEventCreate(&ctx->pev[i]));
     LC_CUDA_OK(cudaMallocHost(&ctx->pinned, 4096));
-    LC_CUDA_OK(cudaFuncSetAttribute(lc_quant_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)lc_quant_smem_bytes()));
-    LC_CUDA_OK(cudaFuncSetAttribute(lc_quant_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)lc_quant_smem_bytes()));
     LC_CUDA_OK(cudaFuncSetAttribute(lc_quant_a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)lc_quant_a_smem_bytes()));
     LC_CUDA_OK(cudaFuncSetAttribute(lc_quant_b_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,

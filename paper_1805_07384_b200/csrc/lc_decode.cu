@@ -468,282 +468,6 @@ struct LcRecParams {
 
 __device__ __forceinline__ int64_t lc_code_m(uint32_t code) { return lc_unzigzag(code); }
 
-__global__ void __launch_bounds__(LC_TPB, 2) lc_recon_kernel(LcRecParams P)
-{
-    typedef cub::BlockScan<long long, LC_TPB> ScanLL;
-    extern __shared__ __align__(16) unsigned char lc_dyn_smem[];
-    double *ys = reinterpret_cast<double *>(lc_dyn_smem);            // outputs, padded rows
-    uint32_t *cs = reinterpret_cast<uint32_t *>(ys + LC_TPB * LC_ROW); // codes, padded rows
-    __shared__ typename ScanLL::TempStorage scan_tmp;
-    __shared__ OffMap warp_agg[LC_TPB / 32];
-    __shared__ LcSegScan warp_seg[LC_TPB / 32];
-    __shared__ long long sh_tile;
-    __shared__ LcSegScan sh_seg_in;
-    __shared__ LcSegScan lb_seg[LC_TPB / 32], lb_seg_res;
-    __shared__ OffMap lb_map[LC_TPB / 32], lb_map_res;
-    __shared__ int sh_j;
-    __shared__ double sh_Din;
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-
-    for (;;) {
-        __syncthreads();
-        if (tid == 0) sh_tile = atomicAdd(P.tile_counter, 1u);
-        __syncthreads();
-        const long long t = sh_tile;
-        if (t >= P.ntiles) break;
-        const long long cbeg = P.first_chunk + t * LC_TPB;
-        const long long pbeg = cbeg * LC_L;
-        const long long c = cbeg + tid;
-        const long long p0 = c * LC_L;
-        const long long nel = (long long)P.n - 1;
-        const int len = (c < P.nchunks) ? (int)min((long long)LC_L, nel - p0) : 0;
-#pragma unroll 8
-        for (int k = 0; k < LC_L; ++k) {
-            const int off = k * LC_TPB + tid;
-            const long long pos = pbeg + off;          // code index (element pos+1)
-            uint32_t v = 0;
-            if (pos < nel) v = P.code_bytes == 2 ? (uint32_t)reinterpret_cast<const uint16_t *>(P.codes)[pos]
-                                                 : reinterpret_cast<const uint32_t *>(P.codes)[pos];
-            cs[(off >> 5) * LC_ROW + (off & 31)] = v;
-        }
-        __syncthreads();
-        const uint32_t *crow = cs + tid * LC_ROW;
-
-        // ---- escape-segmented m prefix ----------------------------------------------
-        LcSegScan mine; mine.sum = 0; mine.cnt = 0; mine.has = 0; mine.moved = 0;
-        for (int j = 0; j < len; ++j) {
-            const uint32_t code = crow[j];
-            if (code == 0) { mine.sum = 0; mine.cnt += 1; mine.has = 1; mine.moved = 0; }
-            else { const int64_t mm = lc_code_m(code); mine.sum += mm; mine.moved |= (mm != 0); }
-        }
-        LcSegScan inc = mine;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            LcSegScan up;
-            up.sum = __shfl_up_sync(0xffffffffu, inc.sum, o);
-            up.cnt = __shfl_up_sync(0xffffffffu, inc.cnt, o);
-            up.has = __shfl_up_sync(0xffffffffu, inc.has, o);
-            up.moved = __shfl_up_sync(0xffffffffu, inc.moved, o);
-            if (lane >= o) inc = lc_segscan_op(up, inc);
-        }
-        if (lane == 31) warp_seg[wid] = inc;
-        __syncthreads();
-        if (tid == 0)
-            for (int w = 1; w < LC_TPB / 32; ++w) warp_seg[w] = lc_segscan_op(warp_seg[w - 1], warp_seg[w]);
-        __syncthreads();
-        if (wid > 0) inc = lc_segscan_op(warp_seg[wid - 1], inc);
-        LcSegScan exc;
-        exc.sum = __shfl_up_sync(0xffffffffu, inc.sum, 1);
-        exc.cnt = __shfl_up_sync(0xffffffffu, inc.cnt, 1);
-        exc.has = __shfl_up_sync(0xffffffffu, inc.has, 1);
-        exc.moved = __shfl_up_sync(0xffffffffu, inc.moved, 1);
-        if (lane == 0) {
-            if (wid > 0) exc = warp_seg[wid - 1];
-            else { exc.sum = 0; exc.cnt = 0; exc.has = 0; exc.moved = 0; }
-        }
-        {
-            LcRecDesc *d = P.desc + t;
-            const LcSegScan agg = warp_seg[LC_TPB / 32 - 1];
-            LcSegScan in;
-            if (t == 0) {
-                in.sum = 0; in.cnt = P.anchor_cnt; in.has = 1; in.moved = 0;   // anchored at the launch start
-            } else {
-                if (tid == 0) {
-                    __stcg(&d->seg_agg_sum, agg.sum); __stcg(&d->seg_agg_cnt, agg.cnt);
-                    __stcg(&d->seg_agg_has, agg.has | (agg.moved << 1));
-                    st_release(&d->st_seg, 1);
-                }
-                LcSegScan ident; ident.sum = 0; ident.cnt = 0; ident.has = 0; ident.moved = 0;
-                in = lc_lookback_block<LcSegScan>(
-                    t, ident, [](const LcSegScan &x, const LcSegScan &y) { return lc_segscan_op(x, y); },
-                    [](const LcSegScan &v, int o) {
-                        LcSegScan r;
-                        r.sum = __shfl_down_sync(0xffffffffu, v.sum, o);
-                        r.cnt = __shfl_down_sync(0xffffffffu, v.cnt, o);
-                        r.has = __shfl_down_sync(0xffffffffu, v.has, o);
-                        r.moved = __shfl_down_sync(0xffffffffu, v.moved, o);
-                        return r;
-                    },
-                    [&](long long k) { return &P.desc[k].st_seg; },
-                    [&](long long k, int st) {
-                        LcSegScan v;
-                        int hm;
-                        if (st == 2) {
-                            v.sum = __ldcg(&P.desc[k].seg_inc_sum); v.cnt = __ldcg(&P.desc[k].seg_inc_cnt);
-                            hm = __ldcg(&P.desc[k].seg_inc_has);
-                        } else {
-                            v.sum = __ldcg(&P.desc[k].seg_agg_sum); v.cnt = __ldcg(&P.desc[k].seg_agg_cnt);
-                            hm = __ldcg(&P.desc[k].seg_agg_has);
-                        }
-                        v.has = hm & 1; v.moved = hm >> 1;
-                        return v;
-                    },
-                    lb_seg, &sh_j, &lb_seg_res);
-            }
-            if (tid == 0) {
-                const LcSegScan incl = lc_segscan_op(in, agg);
-                __stcg(&d->seg_inc_sum, incl.sum); __stcg(&d->seg_inc_cnt, incl.cnt);
-                __stcg(&d->seg_inc_has, incl.has | (incl.moved << 1));
-                st_release(&d->st_seg, 2);
-                sh_seg_in = in;
-            }
-        }
-        __syncthreads();
-        const LcSegScan before = lc_segscan_op(sh_seg_in, exc);    // state at position cL
-        const LcSegScan after = lc_segscan_op(before, mine);       // state at position cL + len
-        // anchor: the last escape value (or the launch anchor when none since)
-        auto anchor_of = [&](const LcSegScan &s) -> double {
-            if (s.cnt > P.anchor_cnt) {
-                const long long e = s.cnt - 1;
-                return e < (long long)P.n_esc ? P.esc_val[e] : 0.0;
-            }
-            return P.anchor_val;
-        };
-        auto guess_of = [&](const LcSegScan &s) -> double {
-            const double a = anchor_of(s);
-            if (!s.moved) return a;                  // chain still sits on the anchor value
-            const double g = LC_ADD(a, LC_MUL((double)s.sum, P.delta));
-            return isfinite(g) ? g : a;
-        };
-        const double g0 = guess_of(before);
-        const double g1 = guess_of(after);
-        if (len > 0) P.chunk_esc[c] = before.cnt;
-
-        // ---- phase A: guess chain -> offset map ---------------------------------------
-        OffMap H;
-        if (len > 0) {
-            double r = g0;
-            long long e = before.cnt;
-            LcEvents E;
-            lc_events_init(E, g0);
-            bool pend = false;
-            double pr = 0.0, pc = 0.0, prn = 0.0;
-            for (int j = 0; j < len; ++j) {
-                const uint32_t code = crow[j];
-                const bool esc = code == 0;
-                const int64_t m = lc_code_m(code);
-                const double inc_ = LC_MUL((double)m, P.delta);
-                double rn = m != 0 ? LC_ADD(r, inc_) : r;
-                if (esc) { rn = e < (long long)P.n_esc ? P.esc_val[e] : 0.0; ++e; }
-                lc_events_step_if(E, pend, pr, pc, prn);
-                lc_events_escape_if(E, esc);
-                pend = !esc && m != 0;
-                pr = r; pc = inc_; prn = rn;
-                r = rn;
-            }
-            lc_events_step_if(E, pend, pr, pc, prn);
-            if (!lc_events_finish(E, g0, H)) {
-                double r2 = g0;
-                long long e2 = before.cnt;
-                H = lc_map_identity(lc_ulp(g0));
-                for (int j = 0; j < len; ++j) {
-                    const uint32_t code = crow[j];
-                    if (code == 0) {
-                        r2 = e2 < (long long)P.n_esc ? P.esc_val[e2] : 0.0;
-                        ++e2;
-                        H = lc_map_const(0.0);
-                    } else {
-                        const int64_t m = lc_code_m(code);
-                        if (m != 0) {
-                            const double inc_ = LC_MUL((double)m, P.delta);
-                            const double rn = LC_ADD(r2, inc_);
-                            lc_map_step(H, r2, inc_, rn);
-                            r2 = rn;
-                        }
-                    }
-                }
-            }
-            if (c + 1 < P.nchunks) lc_map_shift_out(H, LC_SUB(r, g1));
-        } else {
-            H = lc_map_neutral();
-        }
-        OffMap inc_map = H;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const OffMap up = lc_shfl_up_map(inc_map, o);
-            if (lane >= o) inc_map = lc_map_compose(inc_map, up);
-        }
-        if (lane == 31) warp_agg[wid] = inc_map;
-        __syncthreads();
-        if (tid == 0)
-            for (int w = 1; w < LC_TPB / 32; ++w) warp_agg[w] = lc_map_compose(warp_agg[w], warp_agg[w - 1]);
-        __syncthreads();
-        if (wid > 0) inc_map = lc_map_compose(inc_map, warp_agg[wid - 1]);
-        OffMap exc_map = lc_shfl_up_map(inc_map, 1);
-        if (lane == 0) exc_map = wid > 0 ? warp_agg[wid - 1] : lc_map_neutral();
-        {
-            LcRecDesc *d = P.desc + t;
-            const OffMap agg = warp_agg[LC_TPB / 32 - 1];
-            double Din = 0.0;
-            if (t > 0) {
-                if (tid == 0) {
-                    d->map_kind = agg.kind; d->mv = agg.v; d->mB = agg.B; d->mt0 = agg.t0; d->mt1 = agg.t1;
-                    d->my = agg.y; d->mog = agg.og;
-                    st_release(&d->st_map, 1);
-                }
-                const OffMap pre = lc_lookback_block<OffMap>(
-                    t, lc_map_neutral(), [](const OffMap &x, const OffMap &y) { return lc_map_compose(y, x); },
-                    [](const OffMap &v, int o) { return lc_shfl_down_map(v, o); },
-                    [&](long long k) { return &P.desc[k].st_map; },
-                    [&](long long k, int st) {
-                        if (st == 2) return lc_map_const(__ldcg(&P.desc[k].incl_D));
-                        const LcRecDesc *dk = P.desc + k;
-                        OffMap mk;
-                        mk.kind = __ldcg(&dk->map_kind); mk.v = __ldcg(&dk->mv); mk.B = __ldcg(&dk->mB);
-                        mk.t0 = __ldcg(&dk->mt0); mk.t1 = __ldcg(&dk->mt1); mk.y = __ldcg(&dk->my);
-                        mk.og = __ldcg(&dk->mog);
-                        return mk;
-                    },
-                    lb_map, &sh_j, &lb_map_res);
-                Din = pre.y;
-            }
-            if (tid == 0) {
-                __stcg(&d->incl_D, lc_map_eval(agg, Din));
-                st_release(&d->st_map, 2);
-                sh_Din = Din;
-            }
-        }
-        __syncthreads();
-        const double Din = sh_Din;
-        const double start = lc_apply_offset(g0, lc_map_eval(exc_map, Din));
-        const double next_pred = lc_apply_offset(g1, lc_map_eval(inc_map, Din));
-
-        // ---- phase B: exact chain (compressor.py:358-376) ----------------------------
-        {
-            double r = start;
-            long long e = before.cnt;
-            double *yrow = ys + tid * LC_ROW;
-            for (int j = 0; j < len; ++j) {
-                const uint32_t code = crow[j];
-                if (code == 0) {
-                    if (e < (long long)P.n_esc) {
-                        r = P.esc_val[e];
-                        if (P.esc_idx[e] != (unsigned long long)(p0 + j + 1)) atomicExch(&P.esc_flags[1], 1);
-                    } else {
-                        atomicExch(&P.esc_flags[0], 1);
-                    }
-                    ++e;
-                } else {
-                    const int64_t m = lc_code_m(code);
-                    if (m != 0) r = LC_ADD(r, LC_MUL((double)m, P.delta));
-                }
-                yrow[j] = r;
-            }
-            if (len > 0 && c + 1 < P.nchunks && lc_bits(r) != lc_bits(next_pred)) {
-                P.bad_end[c] = r;
-                atomicMin(P.first_bad, (unsigned long long)(c + 1));
-            }
-        }
-        __syncthreads();
-#pragma unroll 8
-        for (int k = 0; k < LC_L; ++k) {
-            const int off = k * LC_TPB + tid;
-            const long long pos = pbeg + 1 + off;        // element index
-            if (pos <= nel) __stcs(P.out + pos, ys[(off >> 5) * LC_ROW + (off & 31)]);
-        }
-    }
-}
-
 // ---------------------------------------------------------------------------
 // Split reconstruction (no inter-tile waiting): R0 segmented m-prefix per tile,
 // R0 scan, RA guess chains + maps, map scan (lc_map_scan_kernel), RB exact chain.
@@ -873,7 +597,8 @@ __global__ void __launch_bounds__(1024) lc_rec0_scan_kernel(LcRecSplit S, long l
 
 __global__ void __launch_bounds__(LC_TPB, 2) lc_rec_a_kernel(LcRecParams P, LcRecSplit S)
 {
-    __shared__ uint32_t cs[LC_TPB * LC_ROW];
+    extern __shared__ __align__(16) unsigned char lc_dyn_smem[];
+    uint32_t *cs = reinterpret_cast<uint32_t *>(lc_dyn_smem);
     __shared__ LcSegScan wseg[LC_TPB / 32];
     __shared__ OffMap warp_agg[LC_TPB / 32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -922,31 +647,22 @@ __global__ void __launch_bounds__(LC_TPB, 2) lc_rec_a_kernel(LcRecParams P, LcRe
                 const double inc_ = LC_MUL((double)m, P.delta);
                 double rn = m != 0 ? LC_ADD(r, inc_) : r;
                 if (esc) { rn = e < (long long)P.n_esc ? P.esc_val[e] : 0.0; ++e; }
-                lc_events_step_if(E, pend, pr, pc, prn);
+                lc_events_step_if(E, pend, j - 1, pr, pc, prn);
                 lc_events_escape_if(E, esc);
                 pend = !esc && m != 0;
                 pr = r; pc = inc_; prn = rn;
                 r = rn;
             }
-            lc_events_step_if(E, pend, pr, pc, prn);
-            if (!lc_events_finish(E, g0, H)) {
+            lc_events_step_if(E, pend, len - 1, pr, pc, prn);
+            if (!lc_events_finish(E, g0, H)) {          // events: replay, compose at flagged steps
                 double r2 = g0;
-                long long e2 = before.cnt;
-                H = lc_map_identity(lc_ulp(g0));
                 for (int j = 0; j < len; ++j) {
-                    const uint32_t code = crow[j];
-                    if (code == 0) {
-                        r2 = e2 < (long long)P.n_esc ? P.esc_val[e2] : 0.0;
-                        ++e2;
-                        H = lc_map_const(0.0);
-                    } else {
-                        const int64_t m = lc_code_m(code);
-                        if (m != 0) {
-                            const double inc_ = LC_MUL((double)m, P.delta);
-                            const double rn = LC_ADD(r2, inc_);
-                            lc_map_step(H, r2, inc_, rn);
-                            r2 = rn;
-                        }
+                    const int64_t m = lc_code_m(crow[j]);  // no escape here (E.esc would be set)
+                    if (m != 0) {
+                        const double inc_ = LC_MUL((double)m, P.delta);
+                        const double rn = LC_ADD(r2, inc_);
+                        if ((E.mask >> j) & 1u) lc_map_step(H, r2, inc_, rn);
+                        r2 = rn;
                     }
                 }
             }
@@ -1046,9 +762,9 @@ __global__ void __launch_bounds__(LC_TPB, 2) lc_rec_b_kernel(LcRecParams P, LcRe
     }
 }
 
+size_t lc_rec_a_smem_bytes() { return sizeof(uint32_t) * LC_TPB * LC_ROW; }
 size_t lc_rec_b_smem_bytes() { return sizeof(double) * LC_TPB * LC_ROW + sizeof(uint32_t) * LC_TPB * LC_ROW; }
 
-size_t lc_recon_smem_bytes() { return sizeof(double) * LC_TPB * LC_ROW + sizeof(uint32_t) * LC_TPB * LC_ROW; }
 
 __global__ void lc_set_first_kernel(double *out, double v) { out[0] = v; }
 
@@ -1076,12 +792,6 @@ int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_valu
                        int out_on_device, int64_t *esc_used)
 {
     if (n < 2 || n_lengths == 0 || payload_bits > 8 * payload_bytes) return 12;
-    static bool attr_done = false;
-    if (!attr_done) {
-        LC_CUDA_OK(cudaFuncSetAttribute(lc_recon_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)lc_recon_smem_bytes()));
-        attr_done = true;
-    }
     cudaStream_t st = lc_stream(ctx);
     LcBuf *B = lc_dec_bufs(ctx);      // ctx->dec[10]
     LcBuf &bpay = B[0], &blen = B[1], &beidx = B[2], &beval = B[3], &bout = B[4], &bcodes = B[5], &btab = B[6],
@@ -1216,6 +926,8 @@ int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_valu
     }
     static bool attr_b = false;
     if (!attr_b) {
+        LC_CUDA_OK(cudaFuncSetAttribute(lc_rec_a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)lc_rec_a_smem_bytes()));
         LC_CUDA_OK(cudaFuncSetAttribute(lc_rec_b_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)lc_rec_b_smem_bytes()));
         attr_b = true;
@@ -1232,7 +944,7 @@ int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_valu
         const int grid = (int)(R.ntiles < grid_cap ? R.ntiles : grid_cap);
         lc_rec0_kernel<<<(int)(R.ntiles < 3 * grid_cap ? R.ntiles : 3 * grid_cap), LC_TPB, 0, st>>>(R, RS);
         lc_rec0_scan_kernel<<<1, 1024, 0, st>>>(RS, R.ntiles, R.anchor_cnt);
-        lc_rec_a_kernel<<<grid, LC_TPB, 0, st>>>(R, RS);
+        lc_rec_a_kernel<<<grid, LC_TPB, lc_rec_a_smem_bytes(), st>>>(R, RS);
         { int _rc = lc_debug_check(ctx, "lc_rec_a_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
         lc_map_scan_kernel<<<1, 1024, 0, st>>>(RS.tile_agg, RS.tile_D, R.ntiles);
         lc_rec_b_kernel<<<grid, LC_TPB, lc_rec_b_smem_bytes(), st>>>(R, RS);

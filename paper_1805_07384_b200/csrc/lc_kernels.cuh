@@ -71,7 +71,6 @@ struct LcEncParams {
 
 __global__ void lc_range_kernel(const double *__restrict__ x, uint64_t n, LcRangePart *__restrict__ parts);
 __global__ void lc_range_final_kernel(const LcRangePart *__restrict__ parts, int np, LcRangePart *__restrict__ out);
-template <typename CodeT> __global__ void lc_quant_kernel(LcQuantParams P, CodeT *__restrict__ codes);
 __global__ void lc_anchor_tiles_kernel(LcQuantParams P);
 __global__ void lc_anchor_scan_kernel(const long long *__restrict__ last, long long *__restrict__ incoming,
                                       long long ntiles, long long launch_pos);
@@ -88,6 +87,5 @@ __global__ void lc_codebook_kernel(const uint32_t *__restrict__ hist, uint32_t n
                                    unsigned long long *__restrict__ ifreq, int *__restrict__ parent, LcCodebookOut *out);
 __global__ void lc_zero_words_kernel(uint32_t *__restrict__ p, const LcCodebookOut *__restrict__ cb);
 template <typename CodeT> __global__ void lc_encode_kernel(LcEncParams P);
-size_t lc_quant_smem_bytes();
 size_t lc_codebook_smem_bytes();
 size_t lc_encode_smem_bytes();

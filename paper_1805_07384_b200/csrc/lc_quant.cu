@@ -104,262 +104,6 @@ __device__ __forceinline__ double lc_guess(const LcQuantParams &P, double xpos, 
     return isfinite(g) ? g : xpos;
 }
 
-template <typename CodeT>
-__global__ void __launch_bounds__(LC_TPB, 2) lc_quant_kernel(LcQuantParams P, CodeT *__restrict__ codes)
-{
-    typedef cub::BlockScan<long long, LC_TPB> ScanLL;
-    extern __shared__ __align__(16) unsigned char lc_dyn_smem[];
-    // x tile with padded rows; phase B overwrites each row with its codes
-    // (uint32 slot j of a row aliases x[j/2] of the same row, already consumed)
-    double *xs = reinterpret_cast<double *>(lc_dyn_smem);
-    uint32_t *hs = reinterpret_cast<uint32_t *>(xs + LC_TPB * LC_ROW);
-    __shared__ double xhalo[LC_L + 1];            // x[tile_start-32 .. tile_start]
-    __shared__ typename ScanLL::TempStorage scan_tmp;
-    __shared__ OffMap warp_agg[LC_TPB / 32];
-    __shared__ long long sh_tile, sh_anchor_in;
-    __shared__ long long lb_ll[LC_TPB / 32], lb_ll_res;
-    __shared__ OffMap lb_map[LC_TPB / 32], lb_map_res;
-    __shared__ int sh_j;
-    __shared__ double sh_Din;
-
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    for (int i = tid; i < LC_HBINS; i += LC_TPB) hs[i] = 0;
-
-    for (;;) {
-        __syncthreads();
-        if (tid == 0) sh_tile = atomicAdd(P.tile_counter, 1u);
-        __syncthreads();
-        const long long t = sh_tile;
-        if (t >= P.ntiles) break;
-        const long long cbeg = P.first_chunk + t * LC_TPB;   // first chunk of the tile
-        const long long pbeg = cbeg * LC_L;                   // its start position
-        const long long c = cbeg + tid;                       // this thread's chunk
-        const long long p0 = c * LC_L;
-        const long long nel = (long long)P.n - 1;            // last element index
-        const int len = (c < P.nchunks) ? (int)min((long long)LC_L, nel - p0) : 0;
-        unsigned long long *tl = P.timeline ? P.timeline + 16 * t : nullptr;
-#define LC_STAMP(i) do { if (tl && tid == 0) tl[i] = lc_gtimer(); } while (0)
-        LC_STAMP(0);
-
-        // ---- load tile (coalesced) -------------------------------------------------
-#pragma unroll 8
-        for (int k = 0; k < LC_L; ++k) {
-            const int off = k * LC_TPB + tid;
-            const long long pos = pbeg + 1 + off;
-            if (pos <= nel) xs[(off >> 5) * LC_ROW + (off & 31)] = __ldcs(P.x + pos);
-        }
-        if (tid <= LC_L) {
-            const long long pos = pbeg - LC_L + tid;
-            xhalo[tid] = pos >= 0 ? P.x[pos] : 0.0;
-        }
-        __syncthreads();
-        const double *row = xs + tid * LC_ROW;
-        const double xstart = tid == 0 ? xhalo[LC_L] : xs[(tid - 1) * LC_ROW + LC_L - 1];
-        LC_STAMP(1);
-
-        // ---- phase 0: definite escapes -> anchors ------------------------------------
-        long long last_esc = -1;
-        {
-            double xp = xstart;
-            for (int j = 0; j < len; ++j) {
-                const double xi = row[j];
-                if (lc_definite_escape(xi, xp, P)) last_esc = p0 + 1 + j;
-                xp = xi;
-            }
-        }
-        long long esc_excl, esc_agg;
-        {
-            struct MaxOp { __device__ long long operator()(long long a, long long b) const { return a > b ? a : b; } };
-            ScanLL(scan_tmp).ExclusiveScan(last_esc, esc_excl, -1LL, MaxOp(), esc_agg);
-        }
-        {
-            LcTileDesc *d = P.desc + t;
-            long long in;
-            if (t == 0) {
-                in = pbeg;                                   // launch anchor position
-            } else {
-                if (tid == 0) {
-                    __stcg(&d->anc_agg, esc_agg);
-                    st_release(&d->st_anchor, 1);
-                }
-                in = lc_lookback_block<long long>(
-                    t, -1LL, [](long long a, long long b) { return a > b ? a : b; },
-                    [](long long v, int o) { return __shfl_down_sync(0xffffffffu, v, o); },
-                    [&](long long k) { return &P.desc[k].st_anchor; },
-                    [&](long long k, int st) {
-                        return st == 2 ? __ldcg(&P.desc[k].anc_incl) : __ldcg(&P.desc[k].anc_agg);
-                    },
-                    lb_ll, &sh_j, &lb_ll_res);
-            }
-            if (tid == 0) {
-                __stcg(&d->anc_incl, max(in, esc_agg));
-                st_release(&d->st_anchor, 2);
-                sh_anchor_in = in;
-            }
-        }
-        __syncthreads();
-        LC_STAMP(2);
-        const long long launch_apos = P.first_chunk * LC_L;
-        const long long apos = max(sh_anchor_in, esc_excl);
-        const double aval = (apos == launch_apos) ? P.anchor_val : P.x[apos];
-        const long long apos_next = max(apos, last_esc);
-        const double aval_next = (apos_next == launch_apos) ? P.anchor_val : P.x[apos_next];
-        const double xend = len > 0 ? row[len - 1] : xstart;
-        const double g0 = lc_guess(P, xstart, p0, apos, aval);
-        const double g1 = lc_guess(P, xend, p0 + len, apos_next, aval_next);
-
-        // ---- phase A: guess chain -> offset map ---------------------------------------
-        OffMap H;
-        if (len > 0) {
-            double r = g0;
-            LcEvents E;
-            lc_events_init(E, g0);
-            // software-pipelined: the event test of step j-1 overlaps the chain of step j
-            bool pend = false;
-            double pr = 0.0, pc = 0.0, prn = 0.0;
-            for (int j = 0; j < len; ++j) {
-                int esc; double inc;
-                const double rn = lc_step_guess(P.Q, row[j], r, &esc, &inc);
-                lc_events_step_if(E, pend, pr, pc, prn);
-                lc_events_escape_if(E, esc);
-                pend = !esc && inc != 0.0;
-                pr = r; pc = inc; prn = rn;
-                r = rn;
-            }
-            lc_events_step_if(E, pend, pr, pc, prn);
-            if (!lc_events_finish(E, g0, H)) {          // many events: exact tracking, step by step
-                double r2 = g0;
-                H = lc_map_identity(lc_ulp(g0));
-                for (int j = 0; j < len; ++j) {
-                    int esc; double inc;
-                    const double rn = lc_step_guess(P.Q, row[j], r2, &esc, &inc);
-                    if (esc) H = lc_map_const(0.0);
-                    else if (inc != 0.0) lc_map_step(H, r2, inc, rn);
-                    r2 = rn;
-                }
-            }
-            if (c + 1 < P.nchunks) lc_map_shift_out(H, LC_SUB(r, g1));
-        } else {
-            H = lc_map_neutral();
-        }
-
-        // ---- block inclusive scan of maps (apply earlier chunks first) ----------------
-        OffMap inc_map = H;
-        LC_STAMP(3);
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const OffMap up = lc_shfl_up_map(inc_map, o);
-            if (lane >= o) inc_map = lc_map_compose(inc_map, up);
-        }
-        if (lane == 31) warp_agg[wid] = inc_map;
-        __syncthreads();
-        if (tid == 0) {
-            for (int w = 1; w < LC_TPB / 32; ++w) warp_agg[w] = lc_map_compose(warp_agg[w], warp_agg[w - 1]);
-        }
-        __syncthreads();
-        if (wid > 0) inc_map = lc_map_compose(inc_map, warp_agg[wid - 1]);
-        OffMap exc_map = lc_shfl_up_map(inc_map, 1);
-        if (lane == 0) exc_map = wid > 0 ? warp_agg[wid - 1] : lc_map_neutral();
-        LC_STAMP(4);
-
-        // ---- look-back over tile aggregates -> offset at the tile start -------------
-        {
-            LcTileDesc *d = P.desc + t;
-            const OffMap agg = warp_agg[LC_TPB / 32 - 1];
-            double Din = 0.0;                                // tile 0 starts exactly at the anchor
-            if (t > 0) {
-                if (tid == 0) {
-                    lc_store_map(d, agg);
-                    st_release(&d->st_map, 1);
-                }
-                const OffMap pre = lc_lookback_block<OffMap>(
-                    t, lc_map_neutral(), [](const OffMap &a, const OffMap &b) { return lc_map_compose(b, a); },
-                    [](const OffMap &v, int o) { return lc_shfl_down_map(v, o); },
-                    [&](long long k) { return &P.desc[k].st_map; },
-                    [&](long long k, int st) {
-                        return st == 2 ? lc_map_const(__ldcg(&P.desc[k].incl_D)) : lc_load_map(P.desc + k);
-                    },
-                    lb_map, &sh_j, &lb_map_res, tl ? tl + 8 : nullptr);
-                Din = pre.y;                                 // a constant map: the offset itself
-            }
-            if (tid == 0) {
-                __stcg(&d->incl_D, lc_map_eval(agg, Din));
-                st_release(&d->st_map, 2);
-                sh_Din = Din;
-            }
-        }
-        __syncthreads();
-        LC_STAMP(5);
-        const double Din = sh_Din;
-        const double Dc = lc_map_eval(exc_map, Din);
-        const double start = lc_apply_offset(g0, Dc);
-        const double next_pred = lc_apply_offset(g1, lc_map_eval(inc_map, Din));
-
-        // ---- phase B: exact chain from the predicted start ---------------------------
-        {
-            double r = start;
-            uint32_t *crow = reinterpret_cast<uint32_t *>(xs + tid * LC_ROW);
-            bool ok = true;
-            for (int j = 0; j < len; ++j) {
-                uint32_t code; int esc; double inc, pe;
-                const double rn = lc_step_nb(P.Q, row[j], r, &code, &inc, &esc, &pe, ok);
-                crow[j] = code;
-                if (P.pe) {
-                    P.pe[p0 + j] = pe;
-                    P.pe_rec[p0 + j] = LC_SUB(rn, r);
-                }
-                r = rn;
-            }
-            if (!ok) {                                        // a quotient was not certified: IEEE path
-                // x values of this row were partly overwritten by codes: reload from global
-                r = start;
-                for (int j = 0; j < len; ++j) {
-                    uint32_t code; int esc; double inc, pe;
-                    const double rn = lc_step(P.Q, P.x[p0 + 1 + j], r, &code, &esc, &inc, &pe);
-                    crow[j] = code;
-                    if (P.pe) {
-                        P.pe[p0 + j] = pe;
-                        P.pe_rec[p0 + j] = LC_SUB(rn, r);
-                    }
-                    r = rn;
-                }
-            }
-            if (len > 0 && c + 1 < P.nchunks && lc_bits(r) != lc_bits(next_pred)) {
-                P.bad_end[c] = r;
-                atomicMin(P.first_bad, (unsigned long long)(c + 1));
-            }
-        }
-        __syncthreads();
-        LC_STAMP(6);
-
-        // ---- histogram + coalesced code store ------------------------------------------
-#pragma unroll 4
-        for (int k = 0; k < LC_L; ++k) {
-            const int off = k * LC_TPB + tid;
-            const long long pos = pbeg + off;                // code index = element - 1
-            const bool valid = pos < nel;
-            const uint32_t code = valid ? reinterpret_cast<const uint32_t *>(xs)[(off >> 5) * (2 * LC_ROW) + (off & 31)]
-                                        : 0xffffffffu;
-            if (valid) codes[pos] = (CodeT)code;
-            if (P.count_hist) {
-                const unsigned peers = __match_any_sync(0xffffffffu, code);
-                if (valid && (int)(__ffs(peers) - 1) == lane) {
-                    const unsigned cnt = __popc(peers);
-                    if (code < LC_HBINS) atomicAdd(&hs[code], cnt);
-                    else atomicAdd(&P.hist[code], cnt);
-                }
-            }
-        }
-        LC_STAMP(7);
-    }
-    __syncthreads();
-    if (P.count_hist) {
-        const uint32_t lim = P.nbins < LC_HBINS ? P.nbins : LC_HBINS;
-        for (uint32_t i = tid; i < lim; i += LC_TPB)
-            if (hs[i]) atomicAdd(&P.hist[i], hs[i]);
-    }
-}
-
 // ---------------------------------------------------------------------------
 // Split quantizer: pass 0 (anchors, only when escapes are possible), pass A
 // (guess chains + maps + in-tile scan), map scan over tiles, pass B (exact
@@ -489,21 +233,19 @@ __global__ void __launch_bounds__(LC_TPB, 2) lc_quant_a_kernel(LcQuantParams P)
             for (int j = 0; j < len; ++j) {
                 int esc; double inc;
                 const double rn = lc_step_guess(P.Q, row[j], r, &esc, &inc);
-                lc_events_step_if(E, pend, pr, pc, prn);
+                lc_events_step_if(E, pend, j - 1, pr, pc, prn);
                 lc_events_escape_if(E, esc);
                 pend = !esc && inc != 0.0;
                 pr = r; pc = inc; prn = rn;
                 r = rn;
             }
-            lc_events_step_if(E, pend, pr, pc, prn);
-            if (!lc_events_finish(E, g0, H)) {
+            lc_events_step_if(E, pend, len - 1, pr, pc, prn);
+            if (!lc_events_finish(E, g0, H)) {          // events: replay, compose at flagged steps
                 double r2 = g0;
-                H = lc_map_identity(lc_ulp(g0));
                 for (int j = 0; j < len; ++j) {
                     int esc; double inc;
                     const double rn = lc_step_guess(P.Q, row[j], r2, &esc, &inc);
-                    if (esc) H = lc_map_const(0.0);
-                    else if (inc != 0.0) lc_map_step(H, r2, inc, rn);
+                    if ((E.mask >> j) & 1u) lc_map_step(H, r2, inc, rn);
                     r2 = rn;
                 }
             }
@@ -708,10 +450,6 @@ __global__ void __launch_bounds__(256) lc_hist_kernel(const CodeT *__restrict__ 
         if (hs[i]) atomicAdd(&hist[i], hs[i]);
 }
 
-size_t lc_quant_smem_bytes() { return sizeof(double) * LC_TPB * LC_ROW + sizeof(uint32_t) * LC_HBINS; }
-
-template __global__ void lc_quant_kernel<uint16_t>(LcQuantParams, uint16_t *);
-template __global__ void lc_quant_kernel<uint32_t>(LcQuantParams, uint32_t *);
 template __global__ void lc_quant_serial_kernel<uint16_t>(LcQuantParams, uint16_t *);
 template __global__ void lc_quant_serial_kernel<uint32_t>(LcQuantParams, uint32_t *);
 template __global__ void lc_hist_kernel<uint16_t>(const uint16_t *, uint64_t, uint32_t *, uint32_t);

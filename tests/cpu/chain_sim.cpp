@@ -38,6 +38,7 @@ int64_t sim_predict(const double *x, int64_t n, double eb, int64_t nbh, int L,
         OffMap H = lc_map_identity(lc_ulp(r));
         LcEvents E; lc_events_init(E, r);
         const double g0 = r;
+        int jj = 0;
         for (int64_t i = s + 1; i <= e; ++i) {
             uint32_t code; double inc; int esc; double pe;
             const double rn = lc_step(Q, x[i], r, &code, &esc, &inc, &pe);
@@ -46,14 +47,25 @@ int64_t sim_predict(const double *x, int64_t n, double eb, int64_t nbh, int L,
                 const int kb = H.kind;
                 const double Bb = H.B;
                 lc_map_step(H, r, inc, rn);
-                lc_events_step(E, r, inc, rn);
+                lc_events_step_if(E, true, jj, r, inc, rn);
                 if (H.kind != kb || H.B != Bb) ++events;
             }
             r = rn;
+            ++jj;
         }
         {   // the deferred tracker must reproduce the step-by-step map exactly
             OffMap H2;
-            if (lc_events_finish(E, g0, H2)) {
+            if (!lc_events_finish(E, g0, H2)) {      // replay at flagged steps
+                double r2 = g0;
+                int j2 = 0;
+                for (int64_t i = s + 1; i <= e; ++i, ++j2) {
+                    uint32_t code; double inc; int esc; double pe;
+                    const double rn = lc_step(Q, x[i], r2, &code, &esc, &inc, &pe);
+                    if ((E.mask >> j2) & 1u) lc_map_step(H2, r2, inc, rn);
+                    r2 = rn;
+                }
+            }
+            {
                 if (H2.kind != H.kind || lc_bits(H2.y) != lc_bits(H.y) || lc_bits(H2.t0) != lc_bits(H.t0) ||
                     lc_bits(H2.t1) != lc_bits(H.t1) || lc_bits(H2.B) != lc_bits(H.B))
                     *n_events = -1000000000;
@@ -293,13 +305,15 @@ void sim_event_hist(const double *x, int64_t n, double eb, int L, int64_t *hist)
         const int64_t s = c * L, e = (s + L < n - 1) ? s + L : n - 1;
         double r = c == 0 ? x0 : x0 + floor((x[s] - x0) / Q.delta + 0.5) * Q.delta;
         LcEvents E; lc_events_init(E, r);
-        for (int64_t i = s + 1; i <= e; ++i) {
+        int jj = 0;
+        for (int64_t i = s + 1; i <= e; ++i, ++jj) {
             uint32_t code; double inc; int esc; double pe;
             const double rn = lc_step(Q, x[i], r, &code, &esc, &inc, &pe);
-            if (esc) lc_events_escape(E); else if (inc != 0.0) lc_events_step(E, r, inc, rn);
+            if (esc) lc_events_escape(E); else if (inc != 0.0) lc_events_step_if(E, true, jj, r, inc, rn);
             r = rn;
         }
-        hist[E.n < 15 ? E.n : 15]++;
+        const int ne = __builtin_popcount(E.mask);
+        hist[ne < 15 ? ne : 15]++;
     }
 }
 }
