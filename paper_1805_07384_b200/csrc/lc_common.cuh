@@ -206,3 +206,30 @@ __device__ __forceinline__ T lc_lookback_block(long long t, T ident, Op op, Shfl
     }
     return acc;
 }
+
+// ---- bulk async copy (TMA engine) global -> shared, completion on an mbarrier
+__device__ __forceinline__ void lc_mbar_init(unsigned long long *bar, unsigned count)
+{
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// one thread: expect `bytes` and start the copy (16-byte aligned, multiple of 16)
+__device__ __forceinline__ void lc_bulk_load(void *dst, const void *src, unsigned bytes, unsigned long long *bar)
+{
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(d), "l"(src), "r"(bytes), "r"(b) : "memory");
+}
+__device__ __forceinline__ void lc_mbar_wait(unsigned long long *bar, unsigned phase)
+{
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    unsigned ok = 0;
+    do {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(ok) : "r"(b), "r"(phase) : "memory");
+    } while (!ok);
+}

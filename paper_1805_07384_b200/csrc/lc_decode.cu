@@ -6,11 +6,17 @@
 // compressor.decompress (compressor.py:358-376, 420-440).
 //
 // Huffman decode of a v1 (LCKP0001) bitstream, which has no sync points:
-//   * the bitstream is cut into S-bit segments, one thread each;
-//   * sync passes: each segment decodes from its predecessor's exit position
-//     (initially its own start) until it crosses its end; passes repeat until
-//     no exit moves (canonical codes resynchronise within a few codewords);
+//   * the bitstream is cut into 128-bit segments, one thread each, 256
+//     consecutive segments per CTA;
+//   * every segment first decodes from its own base; a segment records the
+//     positions of its codeword starts as a 128-bit mask.  Re-decoding from a
+//     corrected start stops at the first start shared with the previous walk
+//     (from there both walks coincide), so corrections are cheap;
+//   * corrections are propagated inside the CTA in shared memory until no
+//     exit moves, then across CTAs by short host-driven passes (canonical
+//     codes resynchronise within a few codewords, so one pass is typical);
 //   * counts are scanned to output offsets and a final pass writes symbols;
+//     a 12-bit table yields every codeword that fits in the next 12 bits;
 //   * the first decoding anomaly on the true path reproduces the reference
 //     status (1 invalid codeword, 2 exhausted, 3 trailing bits).
 // Reconstruction runs the same chunked exact chain as the encoder
@@ -20,8 +26,9 @@
 #include "lc_kernels.cuh"
 #include "../../include/lossyckpt_b200.h"
 
-#define LC_SEG_BITS 1024
 #define LC_LUT_BITS 12
+#define LC_DEC_TPB 256
+#define LC_SEG_DEAD 0xffffu
 
 struct LcDecTables {
     int max_len;
@@ -31,7 +38,11 @@ struct LcDecTables {
     unsigned long long first_code[66];
     unsigned long long count[66];
     unsigned long long offset[66];
-    unsigned int lut[1 << LC_LUT_BITS];  // (len << 24) | sym; ~0 = no code of length <= LUT_BITS
+    unsigned int lut[1 << LC_LUT_BITS];   // (len << 24) | sym; ~0 = no code of length <= LUT_BITS
+    unsigned int lut2[1 << LC_LUT_BITS];  // codewords inside the 12 bits: (n << 16) | (bits << 12) | start mask
+    unsigned long long lim[34];      // left-justified 32-bit code limits per length (canonical codes, l <= 32)
+    int canon;                       // Kraft <= 1 and max_len <= 32: lengths follow from lim[]
+    int pad2[3];
 };
 
 // lengths[nl] -> tables + sorted symbols (canonical order)
@@ -43,11 +54,11 @@ __global__ void __launch_bounds__(1024) lc_dec_tables_kernel(const uint8_t *__re
     __shared__ int s_wcnt[32][66];
     __shared__ int s_max;
     __shared__ unsigned long long s_first[66], s_off[66];
+    __shared__ unsigned int s_lut[1 << LC_LUT_BITS];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
     if (tid < 66) s_cnt[tid] = 0;
     if (tid == 0) s_max = 0;
     for (int i = tid; i < 32 * 66; i += blockDim.x) (&s_wcnt[0][0])[i] = 0;
-    for (int i = tid; i < (1 << LC_LUT_BITS); i += blockDim.x) T->lut[i] = 0xffffffffu;
     __syncthreads();
     const uint32_t span = (nl + nw - 1) / nw;
     const uint32_t sb = wid * span, se = min(nl, sb + span);
@@ -78,6 +89,20 @@ __global__ void __launch_bounds__(1024) lc_dec_tables_kernel(const uint8_t *__re
         T->max_len = ml;
         T->used = used;
         T->status = ml > 64 ? 1 : 0;
+        // canonical ranges are contiguous and ordered by length when no
+        // length overflows its code space (Kraft <= 1)
+        int canon = ml <= 32;
+        for (int l = 1; l <= 32; ++l)
+            if (s_first[l] + (unsigned long long)s_cnt[l] > (1ULL << l)) canon = 0;
+        for (int l = 0; l <= 33; ++l) {
+            unsigned long long v = ~0ULL;
+            if (canon && l >= 1 && l <= 32 && l < ml)
+                v = (s_first[l] + (unsigned long long)s_cnt[l]) << (32 - l);
+            else if (canon && l == ml)
+                v = (s_first[l] + (unsigned long long)s_cnt[l]) << (32 - l);
+            T->lim[l] = v;
+        }
+        T->canon = canon;
     }
     __syncthreads();
     if (tid >= 1 && tid <= 64 && s_cnt[tid]) {
@@ -96,32 +121,47 @@ __global__ void __launch_bounds__(1024) lc_dec_tables_kernel(const uint8_t *__re
         if (l > 0 && l <= 64) {
             const int rank = s_wcnt[wid][l] + __popc(peers & ((1u << lane) - 1u));
             sorted[s_off[l] + rank] = s;
-            const unsigned long long cw = s_first[l] + rank;
-            // shortest length wins on a shared prefix (the reference tries
-            // lengths in increasing order); codes that overflow l bits never match
-            if (l <= LC_LUT_BITS && cw < (1ULL << l)) {
-                const uint32_t lo = (uint32_t)(cw << (LC_LUT_BITS - l));
-                const uint32_t nfill = 1u << (LC_LUT_BITS - l);
-                for (uint32_t f = 0; f < nfill; ++f) atomicMin(&T->lut[lo + f], ((uint32_t)l << 24) | s);
-            }
         }
         __syncwarp();
         if (l > 0 && l <= 64 && (int)(__ffs(peers) - 1) == lane) s_wcnt[wid][l] += __popc(peers);
         __syncwarp();
     }
-}
-
-// 64 bits of the MSB-first stream starting at bit p (payload padded by >= 16 bytes)
-__device__ __forceinline__ unsigned long long lc_peek64(const uint32_t *__restrict__ w, unsigned long long p)
-{
-    const unsigned long long wi = p >> 5;
-    const int sh = (int)(p & 31);
-    const unsigned long long a = __byte_perm(__ldg(w + wi), 0, 0x0123);
-    const unsigned long long b = __byte_perm(__ldg(w + wi + 1), 0, 0x0123);
-    const unsigned long long hi = (a << 32) | b;
-    if (!sh) return hi;
-    const unsigned long long c = __byte_perm(__ldg(w + wi + 2), 0, 0x0123);
-    return (hi << sh) | (c >> (32 - sh));
+    __syncthreads();
+    // single-codeword table: the reference tries lengths in increasing order
+    // (huffman.py:117-125), so the shortest matching length wins; codes that
+    // overflow their length never match
+    for (int w = tid; w < (1 << LC_LUT_BITS); w += blockDim.x) {
+        unsigned e = 0xffffffffu;
+        for (int l = 1; l <= LC_LUT_BITS; ++l) {
+            const unsigned long long v = (unsigned long long)(w >> (LC_LUT_BITS - l));
+            const unsigned long long rel = v - s_first[l];
+            if (s_cnt[l] && v >= s_first[l] && rel < (unsigned long long)s_cnt[l]) {
+                e = ((unsigned)l << 24) | sorted[s_off[l] + rel];
+                break;
+            }
+        }
+        s_lut[w] = e;
+    }
+    __syncthreads();
+    // Multi-codeword entries.  A codeword found with padded (unknown) low bits
+    // is exact when it ends inside the known bits: every shorter codeword
+    // depends on known bits only, and the table keeps the shortest match.
+    for (int w = tid; w < (1 << LC_LUT_BITS); w += blockDim.x) {
+        const unsigned e0 = s_lut[w];
+        T->lut[w] = e0;
+        unsigned sm = 0;
+        int pos = 0, n = 0;
+        while (pos < LC_LUT_BITS) {
+            const unsigned e = s_lut[(w << pos) & ((1 << LC_LUT_BITS) - 1)];
+            if (e == 0xffffffffu) break;
+            const int l = (int)(e >> 24);
+            if (pos + l > LC_LUT_BITS) break;
+            sm |= 1u << pos;
+            pos += l;
+            ++n;
+        }
+        T->lut2[w] = n ? ((unsigned)n << 16) | ((unsigned)pos << 12) | sm : 0u;
+    }
 }
 
 // Decode one codeword at bit p.  Returns its length (>0) and *sym, or 0 for
@@ -139,19 +179,18 @@ __device__ __forceinline__ int lc_decode_one(const LcDecTables &T, const uint32_
     return 0;
 }
 
-#define LC_SYNC_K 16
+// Per-segment decode state (8 bytes).  Positions are relative to the
+// segment base; `start` == LC_SEG_DEAD: the decode path ended before it.
+struct __align__(8) LcSeg {
+    unsigned short start;        // first codeword start
+    unsigned short exit;         // first codeword start >= segment end, or stop point
+    unsigned short count;        // codewords started in [start, exit)
+    unsigned char term;          // 0 none, 1 invalid, 2 exhausted, 4 clean end at bit_length, 8 dead
+    unsigned char pad;
+};
 
-// Per-segment decode state.  bnd[] holds the first codeword starts (bit
-// offsets from the segment base) of the last full decode: a later re-decode
-// from a different start that lands on one of them is synchronised.
-struct __align__(16) LcSeg {
-    unsigned long long start;   // bit where this segment's first codeword starts (~0: dead)
-    unsigned long long exit;    // first codeword start >= segment end (or stop point)
-    unsigned int count;         // codewords started in [start, exit)
-    int term;                   // 0 none, 1 invalid, 2 exhausted, 4 clean end at bit_length, 8 dead
-    unsigned short bnd[LC_SYNC_K];
-    int nbnd;
-    unsigned int full_count;    // codewords of the full decode that recorded bnd[] (from bnd[0])
+struct LcBlkOut {                // exit of a CTA's last segment (absolute; ~0 when it terminated)
+    unsigned long long exit;
 };
 
 struct LcDecParams {
@@ -160,148 +199,279 @@ struct LcDecParams {
     const LcDecTables *T;
     const uint32_t *sorted;
     unsigned long long nseg;
+    long long nblk;             // CTAs of LC_DEC_TPB segments
+    int seg_bits;               // 64 * sub-segments
+    unsigned long long nwords;  // payload words readable (padded)
 };
 
-// MSB-first bit reader: the top nb bits of buf are valid (nb in (32, 64] after refill).
-struct LcBitReader {
+// staged words beyond a CTA's segments: the last walk reads at most one
+// codeword (<= 64 bits) past its segment plus the reader's 64-bit lookahead
+#define LC_DEC_STAGE_PAD 8
+#define LC_DEAD32 0xffffffffu
+
+static size_t lc_dec_stage_bytes(int ns)
+{
+    return sizeof(uint32_t) * (LC_DEC_TPB * 2 * ns + LC_DEC_STAGE_PAD) + 8ull * LC_DEC_TPB * ns;
+}
+
+// Payload word sources for the bit reader (32-bit word index relative to a
+// base the caller chose): global memory, or a CTA range staged in shared
+// memory.  Words are big-endian byte streams.
+struct LcGlobSrc {
     const uint32_t *w;
-    unsigned long long buf, pos, next;
+    __device__ __forceinline__ uint32_t word(unsigned i) const { return __byte_perm(__ldg(w + i), 0, 0x0123); }
+};
+struct LcSmemSrc {
+    const uint32_t *w;
+    __device__ __forceinline__ uint32_t word(unsigned i) const { return __byte_perm(w[i], 0, 0x0123); }
+};
+
+// MSB-first bit reader over relative bit positions: the top nb bits of buf
+// are valid (nb in (32, 64] after refill).
+template <class Src>
+struct LcBitReader {
+    Src src;
+    unsigned long long buf;
+    unsigned pos, next;
     int nb;
-    __device__ __forceinline__ void init(const uint32_t *words, unsigned long long p)
+    __device__ __forceinline__ void seek(unsigned p)
     {
-        w = words;
         pos = p;
-        const unsigned long long wi = p >> 5;
+        const unsigned wi = p >> 5;
         const int sh = (int)(p & 31);
-        const unsigned long long a = __byte_perm(__ldg(w + wi), 0, 0x0123);
-        const unsigned long long b = __byte_perm(__ldg(w + wi + 1), 0, 0x0123);
-        buf = ((a << 32) | b) << sh;
+        buf = (((unsigned long long)src.word(wi) << 32) | src.word(wi + 1)) << sh;
         nb = 64 - sh;
         next = wi + 2;
         if (nb <= 32) refill();
     }
     __device__ __forceinline__ void refill()
     {
-        buf |= (unsigned long long)__byte_perm(__ldg(w + next), 0, 0x0123) << (32 - nb);
+        buf |= (unsigned long long)src.word(next) << (32 - nb);
         ++next;
         nb += 32;
     }
     __device__ __forceinline__ void consume(int l)
     {
-        if (l >= nb) { init(w, pos + l); return; }   // only for codes longer than the buffer
+        if (l >= nb) { seek(pos + l); return; }      // only for codes longer than the buffer
         buf <<= l;
         nb -= l;
         pos += l;
         if (nb <= 32) refill();
     }
+    // 64 bits from pos (for codes longer than the buffered bits)
     __device__ __forceinline__ unsigned long long window(int max_len) const
     {
-        return max_len > nb ? lc_peek64(w, pos) : buf;
+        if (max_len <= nb) return buf;
+        const unsigned wi = pos >> 5;
+        const int sh = (int)(pos & 31);
+        const unsigned long long hi = ((unsigned long long)src.word(wi) << 32) | src.word(wi + 1);
+        if (!sh) return hi;
+        return (hi << sh) | ((unsigned long long)src.word(wi + 2) >> (32 - sh));
     }
 };
 
+// bit_length relative to a base bit (clamped; 0 when the stream ended before it)
+__device__ __forceinline__ unsigned lc_bits_rel(unsigned long long bits, unsigned long long base)
+{
+    if (bits <= base) return 0u;
+    const unsigned long long r = bits - base;
+    return r > 0x7fffffffull ? 0x7fffffffu : (unsigned)r;
+}
+
 // One codeword at the reader; returns its length, 0 for "no codeword within
 // max_len bits"; sets *term for anomalies exactly like huffman.py:114-129.
-__device__ __forceinline__ int lc_next_symbol(const LcDecParams &P, const LcDecTables &T, int max_len,
-                                              const LcBitReader &br, uint32_t *sym, int *term)
+template <class BR>
+__device__ __forceinline__ int lc_next_symbol(const LcDecTables &T, const uint32_t *__restrict__ sorted,
+                                              const BR &br, unsigned bits_rel, uint32_t *sym, int *term)
 {
-    if (br.pos >= P.bits) { *term = 4; return 0; }
-    const unsigned long long remaining = P.bits - br.pos;
-    const int l = lc_decode_one(T, P.sorted, br.window(max_len), max_len, sym);
-    if (l == 0) { *term = remaining > (unsigned long long)max_len ? 1 : 2; return 0; }
-    if ((unsigned long long)l > remaining) { *term = 2; return 0; }
+    if (br.pos >= bits_rel) { *term = 4; return 0; }
+    const unsigned remaining = bits_rel - br.pos;
+    const int max_len = T.max_len;
+    const int l = lc_decode_one(T, sorted, br.window(max_len), max_len, sym);
+    if (l == 0) { *term = remaining > (unsigned)max_len ? 1 : 2; return 0; }
+    if ((unsigned)l > remaining) { *term = 2; return 0; }
     return l;
 }
 
-// Full decode of [start, seg_end): records boundaries, count, exit, anomaly.
-__device__ void lc_walk_full(const LcDecParams &P, const LcDecTables &T, int max_len, unsigned long long start,
-                             unsigned long long seg_base, unsigned long long seg_end, LcSeg &S)
+// Length of a codeword longer than LC_LUT_BITS for canonical codes (T.canon):
+// the first length whose left-justified limit exceeds the window.  Returns 0
+// when the window is past every code (the exact path then decides).
+__device__ __forceinline__ int lc_long_len(const LcDecTables &T, unsigned long long buf)
 {
-    LcBitReader br;
-    br.init(P.payload, start);
-    unsigned int cnt = 0;
-    int term = 0, nb = 0;
-    while (br.pos < seg_end) {
-        uint32_t sym;
-        const int l = lc_next_symbol(P, T, max_len, br, &sym, &term);
-        if (!l) break;
-        if (nb < LC_SYNC_K) S.bnd[nb++] = (unsigned short)(br.pos - seg_base);
-        br.consume(l);
-        ++cnt;
-    }
-    S.start = start;
-    S.exit = br.pos;
-    S.count = cnt;
-    S.full_count = cnt;
-    S.term = term;
-    S.nbnd = nb;
+    const unsigned long long w = buf >> 32;
+    if (!T.canon || w >= T.lim[T.max_len]) return 0;
+    int l = LC_LUT_BITS + 1;                 // long codes are rare and mostly just over 12 bits
+#pragma unroll 1
+    while (w >= T.lim[l]) ++l;
+    return l;
 }
 
-// Re-decode from a new start; stops as soon as it lands on a boundary of the
-// previous full decode (the remainder is then identical).
-__device__ void lc_walk_resync(const LcDecParams &P, const LcDecTables &T, int max_len, unsigned long long start,
-                               unsigned long long seg_base, unsigned long long seg_end, LcSeg &S)
+__device__ __forceinline__ void lc_seg_dead(LcSeg &S)
 {
-    LcBitReader br;
-    br.init(P.payload, start);
-    unsigned int n_new = 0;
-    int j = 0;
-    while (br.pos < seg_end) {
-        while (j < S.nbnd && seg_base + S.bnd[j] < br.pos) ++j;
-        if (j < S.nbnd && seg_base + S.bnd[j] == br.pos) {      // synchronised
-            S.count = n_new + (S.full_count - (unsigned int)j);
-            S.start = start;
-            return;
+    S.start = S.exit = LC_SEG_DEAD;
+    S.count = 0;
+    S.term = 8;
+}
+
+// Walk codewords from `start` (CTA-relative bit) until the first codeword
+// start >= segment end (the exit) or an anomaly.  The segment is NS
+// sub-segments of 64 bits; Ms[k * LC_DEC_TPB] (shared memory, conflict-free
+// across the warp) holds the codeword-start mask of sub-segment k: the
+// previous walk's when `resync`, replaced by this one's.  With `resync` the
+// walk stops at the first start both walks share: from there on they
+// coincide (count, exit and status carry over).
+template <int NS>
+__device__ void lc_seg_walk(const LcDecTables &T, const uint32_t *__restrict__ sorted, const LcSmemSrc &src,
+                            unsigned bits_rel, unsigned seg_rel, unsigned start, bool resync, LcSeg &S,
+                            unsigned long long *Ms)
+{
+    LcBitReader<LcSmemSrc> br;
+    br.src = src;
+    br.seek(start);
+    int cnt = 0, term = 0, k = 0;
+    bool merged = false, stopped = false;
+    for (; k < NS; ++k) {
+        const unsigned sub_base = seg_rel + 64u * k, sub_end = sub_base + 64u;
+        unsigned long long *mw = Ms + k * LC_DEC_TPB;
+        const unsigned long long old = resync ? *mw : 0ull;
+        unsigned long long mask = 0;
+        while (br.pos < sub_end) {
+            if (br.pos >= bits_rel) { term = 4; stopped = true; break; }
+            const unsigned e2 = T.lut2[br.buf >> (64 - LC_LUT_BITS)];
+            int adv = (int)((e2 >> 12) & 15u);
+            unsigned sm = e2 & 0xfffu;
+            if (!e2 || br.pos + (unsigned)adv > bits_rel) {
+                adv = e2 ? 0 : lc_long_len(T, br.buf);
+                if (!adv || br.pos + (unsigned)adv > bits_rel) {
+                    uint32_t sym;
+                    adv = lc_next_symbol(T, sorted, br, bits_rel, &sym, &term);
+                    if (!adv) { stopped = true; break; }
+                }
+                sm = 1u;
+            }
+            const unsigned lim = sub_end - br.pos;
+            const unsigned inside = lim >= LC_LUT_BITS ? sm : (sm & ((1u << lim) - 1u));
+            const unsigned long long news = (unsigned long long)inside << (br.pos - sub_base);
+            const unsigned long long hit = news & old;
+            if (hit) {                                   // synchronised with the previous walk
+                const unsigned long long below = (hit & (~hit + 1ull)) - 1ull;
+                mask = mask | (news & below) | (old & ~below);
+                merged = true;
+                break;
+            }
+            mask |= news;
+            const unsigned beyond = sm ^ inside;
+            if (beyond) { br.consume(__ffs(beyond) - 1); break; }
+            br.consume(adv);
         }
-        if (j >= S.nbnd && S.nbnd < LC_SYNC_K) break;            // old decode ended before here
-        uint32_t sym;
-        int term = 0;
-        const int l = lc_next_symbol(P, T, max_len, br, &sym, &term);
-        if (!l) { S.start = start; S.exit = br.pos; S.count = n_new; S.term = term; S.nbnd = 0; return; }
-        br.consume(l);
-        ++n_new;
+        cnt += __popcll(mask);
+        *mw = mask;
+        if (merged || stopped) break;
     }
-    lc_walk_full(P, T, max_len, start, seg_base, seg_end, S);    // no sync: decode afresh
+    for (int j = k + 1; j < NS; ++j) {
+        unsigned long long *mw = Ms + j * LC_DEC_TPB;
+        if (merged) cnt += __popcll(*mw);             // old starts carry over
+        else *mw = 0ull;
+    }
+    S.count = (unsigned short)cnt;
+    S.start = (unsigned short)(start - seg_rel);
+    if (!merged) {
+        S.exit = (unsigned short)(br.pos - seg_rel);
+        S.term = (unsigned char)term;
+    }
 }
 
 __device__ __forceinline__ void lc_load_tables(LcDecTables &Ts, const LcDecTables *T)
 {
-    for (int i = threadIdx.x; i < (int)(sizeof(LcDecTables) / 4); i += blockDim.x)
-        reinterpret_cast<uint32_t *>(&Ts)[i] = reinterpret_cast<const uint32_t *>(T)[i];
+    for (int i = threadIdx.x; i < (int)(sizeof(LcDecTables) / 16); i += blockDim.x)
+        reinterpret_cast<uint4 *>(&Ts)[i] = __ldg(reinterpret_cast<const uint4 *>(T) + i);
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) lc_dec_sync_kernel(LcDecParams P, const LcSeg *__restrict__ prev,
-                                                         LcSeg *__restrict__ cur, int first_pass,
-                                                         int *__restrict__ changed)
+// One sync pass.  First pass: every segment walks from its own base, then
+// exits are propagated inside each CTA until nothing moves (re-walks stop at
+// the first codeword start shared with the previous walk).  Later passes: a
+// CTA whose entry (the previous CTA's exit from the last pass) differs from
+// its first segment's start re-walks from it and propagates again; *changed
+// is set when a CTA's own exit moves (the next CTA then needs another pass).
+// The CTA's payload range is staged in shared memory by one bulk copy and
+// all positions are 32-bit, relative to the CTA's first bit.
+template <int NS>
+__global__ void __launch_bounds__(LC_DEC_TPB) lc_dec_sync_kernel(LcDecParams P, LcSeg *__restrict__ seg,
+                                                                const LcBlkOut *__restrict__ bprev,
+                                                                LcBlkOut *__restrict__ bcur, int first_pass,
+                                                                int *__restrict__ changed)
 {
     __shared__ LcDecTables Ts;
+    __shared__ unsigned s_exit[LC_DEC_TPB];
+    __shared__ int s_skip;
+    __shared__ unsigned long long s_bar;
+    extern __shared__ __align__(16) uint32_t s_words[];   // lc_dec_stage_bytes(NS): payload, then masks
+    constexpr int NW = LC_DEC_TPB * 2 * NS + LC_DEC_STAGE_PAD;
+    constexpr unsigned SEGB = 64u * NS;
+    if (threadIdx.x == 0) lc_mbar_init(&s_bar, 1);
+    unsigned phase = 0;
     lc_load_tables(Ts, P.T);
-    const unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= P.nseg) return;
-    const unsigned long long seg_base = t * LC_SEG_BITS, seg_end = seg_base + LC_SEG_BITS;
-    LcSeg S;
-    if (first_pass) {
-        lc_walk_full(P, Ts, Ts.max_len, seg_base, seg_base, seg_end, S);
-        cur[t] = S;
-        return;
+    const int tid = threadIdx.x;
+    unsigned long long *M = reinterpret_cast<unsigned long long *>(s_words + NW) + tid;
+    LcSmemSrc src;
+    src.w = s_words;
+    const unsigned seg_rel = tid * SEGB;
+    for (long long b = blockIdx.x; b < P.nblk; b += gridDim.x) {
+        const unsigned long long t = (unsigned long long)b * LC_DEC_TPB + tid;
+        const bool live = t < P.nseg;
+        const unsigned long long cbit = (unsigned long long)b * LC_DEC_TPB * SEGB;
+        const unsigned bits_rel = lc_bits_rel(P.bits, cbit);
+        LcSeg S;
+        bool have_mask = false;
+        unsigned my_start = seg_rel, entry = 0u;
+        if (!first_pass) {
+            if (live) {
+                S = seg[t];
+                my_start = S.start == LC_SEG_DEAD ? LC_DEAD32 : seg_rel + S.start;
+            }
+            if (tid == 0) {
+                const unsigned long long ex = b > 0 ? bprev[b - 1].exit : 0ull;
+                entry = ex == ~0ull ? LC_DEAD32 : (unsigned)(ex - cbit);
+                s_skip = entry == my_start;
+            }
+            __syncthreads();
+            const int skip = s_skip;
+            if (skip) {
+                __syncthreads();
+                if (tid == 0) bcur[b] = bprev[b];
+                continue;
+            }
+        }
+        // stage this CTA's payload range (+ lookahead) with one bulk copy; the
+        // payload buffer is padded to whole CTA ranges
+        if (tid == 0) lc_bulk_load(s_words, P.payload + cbit / 32, (unsigned)(NW * 4), &s_bar);
+        lc_mbar_wait(&s_bar, phase);
+        phase ^= 1u;
+        if (first_pass && live) {
+            lc_seg_walk<NS>(Ts, P.sorted, src, bits_rel, seg_rel, seg_rel, false, S, M);
+            have_mask = true;
+        }
+        for (;;) {
+            s_exit[tid] = (live && !S.term) ? seg_rel + S.exit : LC_DEAD32;
+            __syncthreads();
+            const unsigned want = tid == 0 ? (first_pass ? 0u : entry) : s_exit[tid - 1];
+            bool ch = false;
+            if (live && want != my_start) {
+                if (want == LC_DEAD32) { lc_seg_dead(S); have_mask = false; }
+                else { lc_seg_walk<NS>(Ts, P.sorted, src, bits_rel, seg_rel, want, have_mask, S, M); have_mask = true; }
+                my_start = want;
+                ch = true;
+            }
+            if (!__syncthreads_or(ch)) break;
+        }
+        if (live) seg[t] = S;
+        if (tid == LC_DEC_TPB - 1) {
+            const unsigned long long ex = (live && !S.term) ? cbit + seg_rel + S.exit : ~0ull;
+            bcur[b].exit = ex;
+            if (!first_pass && ex != bprev[b].exit) atomicExch(changed, 1);
+        }
     }
-    S = prev[t];
-    unsigned long long start = 0;
-    if (t > 0) {
-        const LcSeg pp = prev[t - 1];
-        start = pp.term ? ~0ULL : pp.exit;       // anomaly / end before here: nothing starts here
-    }
-    if (start == S.start) { cur[t] = S; return; }
-    const unsigned long long old_exit = S.exit;
-    const int old_term = S.term;
-    if (start == ~0ULL) {
-        S.start = ~0ULL; S.exit = ~0ULL; S.count = 0; S.term = 8; S.nbnd = 0;
-    } else {
-        lc_walk_resync(P, Ts, Ts.max_len, start, seg_base, seg_end, S);
-    }
-    if (S.exit != old_exit || S.term != old_term) atomicExch(changed, 1);
-    cur[t] = S;
 }
 
 // Device-wide exclusive scan of segment counts (decoupled look-back) and the
@@ -367,36 +537,126 @@ __global__ void __launch_bounds__(LC_TPB) lc_dec_scan_kernel(const LcSeg *__rest
     }
 }
 
-__global__ void __launch_bounds__(256) lc_dec_write_kernel(LcDecParams P, const LcSeg *__restrict__ seg,
-                                                          const unsigned long long *__restrict__ off,
-                                                          void *out, int out_bytes, unsigned long long m,
-                                                          unsigned long long *__restrict__ end_pos)
+// Write pass.  A warp owns 32 consecutive segments, whose symbols form one
+// contiguous output range: each lane decodes its segment into a shared-memory
+// window of `cap` symbols at its output offset, then the warp copies the
+// window to global memory with 16-byte stores.  Ranges longer than the window
+// take several rounds (lanes pause at the window end; the <= 11 symbols a
+// step spills past it move to the front of the next window).
+template <typename CodeT>
+__global__ void __launch_bounds__(LC_DEC_TPB) lc_dec_write_kernel(LcDecParams P, const LcSeg *__restrict__ seg,
+                                                                 const unsigned long long *__restrict__ off,
+                                                                 void *out, unsigned long long m,
+                                                                 unsigned long long *__restrict__ end_pos, int cap)
 {
     __shared__ LcDecTables Ts;
+    extern __shared__ __align__(16) unsigned char s_dyn[];
     lc_load_tables(Ts, P.T);
-    const unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= P.nseg) return;
-    const LcSeg S0 = seg[t];
-    if (S0.start == ~0ULL || S0.count == 0) return;
-    unsigned long long o = off[t];
-    if (o >= m) return;
-    const unsigned long long seg_end = (t + 1) * LC_SEG_BITS;
-    const int max_len = Ts.max_len;
-    LcBitReader br;
-    br.init(P.payload, S0.start);
-    unsigned int cnt = 0;
-    while (br.pos < seg_end && cnt < S0.count && o < m) {
-        uint32_t sym;
-        int term = 0;
-        const int l = lc_next_symbol(P, Ts, max_len, br, &sym, &term);
-        if (!l) break;
-        if (out_bytes == 2) ((uint16_t *)out)[o] = (uint16_t)sym;
-        else ((uint32_t *)out)[o] = sym;
-        br.consume(l);
-        if (o == m - 1) *end_pos = br.pos;
-        ++o;
-        ++cnt;
+    constexpr int VEC = 16 / sizeof(CodeT);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    CodeT *stage = reinterpret_cast<CodeT *>(s_dyn) + (size_t)wid * (cap + 2 * VEC + 16);
+    CodeT *gout = reinterpret_cast<CodeT *>(out);
+    const unsigned long long nwt = (P.nseg + 31) / 32;
+    const unsigned long long nwarps = (unsigned long long)gridDim.x * (blockDim.x >> 5);
+    const unsigned segb = (unsigned)P.seg_bits;
+    for (unsigned long long wt = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + wid; wt < nwt; wt += nwarps) {
+        const unsigned long long t = wt * 32 + lane;
+        unsigned long long o = 0;
+        unsigned todo = 0;
+        LcSeg S0;
+        S0.start = LC_SEG_DEAD;
+        if (t < P.nseg) {
+            S0 = seg[t];
+            o = off[t];
+            if (S0.start != LC_SEG_DEAD) todo = S0.count;
+        }
+        if (o >= m) todo = 0;
+        else if ((unsigned long long)todo > m - o) todo = (unsigned)(m - o);
+        const unsigned long long wlo = __shfl_sync(0xffffffffu, o, 0);
+        // warp-relative output slots (a warp covers <= 32 * 1024 symbols)
+        unsigned orel = (unsigned)(o - wlo), whi = todo ? orel + todo : 0u;
+        whi = __reduce_max_sync(0xffffffffu, whi);
+        if (!whi) continue;
+        const int a = (int)(wlo & (VEC - 1));
+        const bool last = todo && o + todo == m;
+        // segment-relative bit positions
+        const unsigned long long sbit = t * (unsigned long long)segb;
+        const unsigned bits_rel = lc_bits_rel(P.bits, sbit);
+        LcBitReader<LcGlobSrc> br;
+        br.src.w = P.payload + sbit / 32;
+        if (todo) br.seek(S0.start);
+        for (unsigned wb = 0; wb < whi; wb += (unsigned)cap) {
+            const unsigned wend = wb + (unsigned)cap;
+            CodeT *st0 = stage + a - wb;
+            while (todo && orel < wend) {
+                CodeT *dst = st0 + orel;
+                const unsigned w12 = (unsigned)(br.buf >> (64 - LC_LUT_BITS));
+                const unsigned e1 = Ts.lut[w12];
+                const unsigned e2 = Ts.lut2[w12];
+                const unsigned n2 = e2 >> 16;
+                const unsigned L2 = (e2 >> 12) & 15u;
+                const bool fits = br.pos + L2 <= bits_rel;
+                if (n2 >= 2 && n2 <= todo && fits) {
+                    // several codewords in the next 12 bits; the first is e1
+                    dst[0] = (CodeT)(e1 & 0xffffffu);
+                    unsigned sm = (e2 & 0xfffu) & ((e2 & 0xfffu) - 1u);
+                    int k = 1;
+                    do {
+                        const int i = __ffs(sm) - 1;
+                        sm &= sm - 1;
+                        dst[k++] = (CodeT)(Ts.lut[(w12 << i) & ((1u << LC_LUT_BITS) - 1)] & 0xffffffu);
+                    } while (sm);
+                    br.consume((int)L2);
+                    orel += n2;
+                    todo -= n2;
+                } else {
+                    uint32_t sym;
+                    int l;
+                    if (e2 && fits) {                        // one codeword of <= 12 bits
+                        sym = e1 & 0xffffffu;
+                        l = (int)(e1 >> 24);
+                    } else {
+                        l = e2 ? 0 : lc_long_len(Ts, br.buf);
+                        if (l && br.pos + (unsigned)l <= bits_rel) {
+                            const unsigned long long v = (br.buf >> 32) >> (32 - l);
+                            sym = __ldg(P.sorted + Ts.offset[l] + (v - Ts.first_code[l]));
+                        } else {
+                            int term = 0;
+                            l = lc_next_symbol(Ts, P.sorted, br, bits_rel, &sym, &term);
+                            if (!l) { todo = 0; break; }     // cannot happen on the converged path
+                        }
+                    }
+                    dst[0] = (CodeT)sym;
+                    br.consume(l);
+                    ++orel;
+                    --todo;
+                }
+                if (last && !todo) *end_pos = sbit + br.pos;
+            }
+            __syncwarp();
+            const unsigned len = whi - wb < (unsigned)cap ? whi - wb : (unsigned)cap;
+            const int tot = a + (int)len;
+            CodeT *g = gout + (wlo + wb - a);
+            for (int i0 = lane * VEC; i0 < tot; i0 += 32 * VEC) {
+                if (i0 >= a && i0 + VEC <= tot) {
+                    *reinterpret_cast<uint4 *>(g + i0) = *reinterpret_cast<const uint4 *>(stage + i0);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < VEC; ++k)
+                        if (i0 + k >= a && i0 + k < tot) g[i0 + k] = stage[i0 + k];
+                }
+            }
+            __syncwarp();
+            if (len == (unsigned)cap && lane < 16) stage[a + lane] = stage[a + cap + lane];
+            __syncwarp();
+        }
     }
+}
+
+static size_t lc_dec_write_smem(int cap, int code_bytes)
+{
+    const int vec = 16 / code_bytes;
+    return (size_t)(LC_DEC_TPB / 32) * (size_t)(cap + 2 * vec + 16) * code_bytes;
 }
 
 // Resolve the reference status (huffman.py:114-132) from the segment walk.
@@ -799,8 +1059,10 @@ int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_valu
     LC_CUDA_OK(cudaEventRecord(lc_ev(ctx, 0), st));
     const uint64_t m = n - 1;
     const uint64_t words = (payload_bytes + 3) / 4 + 4;
-    LC_CUDA_OK(lc_reserve(bpay, words * 4));
-    LC_CUDA_OK(cudaMemsetAsync(bpay.p, 0, words * 4, st));
+    // padded to whole sync-CTA ranges (bulk copies of up to 256 * 32 + 8 words)
+    const uint64_t words_alloc = words + LC_DEC_TPB * 32 + LC_DEC_STAGE_PAD + 64;
+    LC_CUDA_OK(lc_reserve(bpay, words_alloc * 4));
+    LC_CUDA_OK(cudaMemsetAsync(bpay.p, 0, words_alloc * 4, st));
     LC_CUDA_OK(cudaMemcpyAsync(bpay.p, payload, payload_bytes,
                                inputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
     LC_CUDA_OK(lc_reserve(blen, n_lengths));
@@ -824,11 +1086,24 @@ int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_valu
     // Huffman decode
     const int code_bytes = n_lengths <= 65536 ? 2 : 4;
     LC_CUDA_OK(lc_reserve(bcodes, m * code_bytes + 16));
-    const unsigned long long nseg = (payload_bits + LC_SEG_BITS - 1) / LC_SEG_BITS + 1;
+    // segment size: ~40 average codewords (canonical codes resynchronise
+    // within a few codewords), 128..1024 bits, while keeping >= 2 waves of CTAs
+    int sub = 2;                                         // 64-bit sub-segments
+    {
+        const double bps = (double)payload_bits / (double)m;
+        while (sub < 16 && 64.0 * sub < 40.0 * bps &&
+               (payload_bits / (128ull * sub)) >= (unsigned long long)(2 * 256 * lc_sm_count(ctx)))
+            sub *= 2;
+    }
+    const int seg_bits = 64 * sub;
+    const unsigned long long nseg = (payload_bits + seg_bits - 1) / seg_bits + 1;
+    const long long nblk = (long long)((nseg + LC_DEC_TPB - 1) / LC_DEC_TPB);
     const unsigned long long scan_tiles = (nseg + LC_TPB * 8 - 1) / (LC_TPB * 8);
-    LC_CUDA_OK(lc_reserve(bsync, 2 * nseg * sizeof(LcSeg) + nseg * 8 + scan_tiles * sizeof(LcScanDesc) + 64));
-    LcSeg *sa = (LcSeg *)bsync.p, *sb = sa + nseg;
-    unsigned long long *offs = (unsigned long long *)(sb + nseg);
+    LC_CUDA_OK(lc_reserve(bsync, nseg * sizeof(LcSeg) + 2 * nblk * sizeof(LcBlkOut) + nseg * 8
+                                 + scan_tiles * sizeof(LcScanDesc) + 64));
+    LcSeg *segs = (LcSeg *)bsync.p;
+    LcBlkOut *bo_a = (LcBlkOut *)(segs + nseg), *bo_b = bo_a + nblk;
+    unsigned long long *offs = (unsigned long long *)(bo_b + nblk);
     LcScanDesc *sdesc = (LcScanDesc *)(offs + nseg);
     LC_CUDA_OK(lc_reserve(baux, 256));
     int *changed = (int *)baux.p;
@@ -843,18 +1118,36 @@ int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_valu
     DP.T = T;
     DP.sorted = sorted;
     DP.nseg = nseg;
-    const int sblocks = (int)((nseg + 255) / 256);
+    DP.nblk = nblk;
+    const int pgrid_ = (int)(nblk < (long long)(6 * lc_sm_count(ctx)) ? nblk : 6 * lc_sm_count(ctx));
+    DP.seg_bits = seg_bits;
+    DP.nwords = words;
+    const size_t ssm = lc_dec_stage_bytes(sub);
+    switch (sub) {
+    case 2: LC_CUDA_OK(cudaFuncSetAttribute(lc_dec_sync_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm)); break;
+    case 4: LC_CUDA_OK(cudaFuncSetAttribute(lc_dec_sync_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm)); break;
+    case 8: LC_CUDA_OK(cudaFuncSetAttribute(lc_dec_sync_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm)); break;
+    default: LC_CUDA_OK(cudaFuncSetAttribute(lc_dec_sync_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm)); break;
+    }
+    auto sync_launch = [&](LcBlkOut *bp, LcBlkOut *bc, int first) {
+        switch (sub) {
+        case 2: lc_dec_sync_kernel<2><<<pgrid_, LC_DEC_TPB, ssm, st>>>(DP, segs, bp, bc, first, changed); break;
+        case 4: lc_dec_sync_kernel<4><<<pgrid_, LC_DEC_TPB, ssm, st>>>(DP, segs, bp, bc, first, changed); break;
+        case 8: lc_dec_sync_kernel<8><<<pgrid_, LC_DEC_TPB, ssm, st>>>(DP, segs, bp, bc, first, changed); break;
+        default: lc_dec_sync_kernel<16><<<pgrid_, LC_DEC_TPB, ssm, st>>>(DP, segs, bp, bc, first, changed); break;
+        }
+    };
     int *hchanged = (int *)lc_pinned(ctx);
-    lc_dec_sync_kernel<<<sblocks, 256, 0, st>>>(DP, sa, sa, 1, changed);
+    sync_launch(bo_b, bo_a, 1);
     { int _rc = lc_debug_check(ctx, "lc_dec_sync_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
     lc_count_launch(ctx, 1);
-    LcSeg *prev = sa, *cur = sb;
-    for (int it = 0; it < 1000000; ++it) {
+    LcBlkOut *bprev = bo_a, *bcur = bo_b;
+    for (int it = 0; nblk > 1 && it < 1000000; ++it) {
         LC_CUDA_OK(cudaMemsetAsync(changed, 0, 4, st));
-        lc_dec_sync_kernel<<<sblocks, 256, 0, st>>>(DP, prev, cur, 0, changed);
+        sync_launch(bprev, bcur, 0);
         { int _rc = lc_debug_check(ctx, "lc_dec_sync_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
         lc_count_launch(ctx, 1);
-        LcSeg *tmp = prev; prev = cur; cur = tmp;
+        LcBlkOut *tmp = bprev; bprev = bcur; bcur = tmp;
         LC_CUDA_OK(cudaMemcpyAsync(hchanged, changed, 4, cudaMemcpyDeviceToHost, st));
         LC_CUDA_OK(cudaStreamSynchronize(st));
         if (!*hchanged) break;
@@ -865,13 +1158,30 @@ int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_valu
     LC_CUDA_OK(cudaMemsetAsync(tot + 1, 0xff, 8, st));
     {
         const int g = (int)(scan_tiles < (unsigned long long)(2 * lc_sm_count(ctx)) ? scan_tiles : 2 * lc_sm_count(ctx));
-        lc_dec_scan_kernel<<<g, LC_TPB, 0, st>>>(prev, nseg, offs, sdesc, scan_counter, tot);
+        lc_dec_scan_kernel<<<g, LC_TPB, 0, st>>>(segs, nseg, offs, sdesc, scan_counter, tot);
         { int _rc = lc_debug_check(ctx, "lc_dec_scan_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
     }
     LC_CUDA_OK(cudaEventRecord(lc_phase_ev(ctx, 9), st));
     LC_CUDA_OK(cudaMemsetAsync(endpos, 0xff, 8, st));
-    lc_dec_write_kernel<<<sblocks, 256, 0, st>>>(DP, prev, offs, bcodes.p, code_bytes, m, endpos);
-    lc_dec_status_kernel<<<1, 1, 0, st>>>(prev, offs, tot, endpos, m, payload_bits, status);
+    {
+        // output window per warp: the typical 32-segment range (+25%), <= 4096 symbols
+        const double syms_per_seg = (double)m * seg_bits / (double)(payload_bits ? payload_bits : 1);
+        long long cap = (long long)(1.25 * 32.0 * syms_per_seg);
+        cap = (cap + 63) / 64 * 64;
+        if (cap < 256) cap = 256;
+        if (cap > 4096) cap = 4096;
+        const size_t wsm = lc_dec_write_smem((int)cap, code_bytes);
+        const unsigned long long wb = (nseg + LC_DEC_TPB - 1) / LC_DEC_TPB;
+        const int wgrid = (int)(wb < (unsigned long long)(4 * lc_sm_count(ctx)) ? wb : 4 * lc_sm_count(ctx));
+        if (code_bytes == 2) {
+            LC_CUDA_OK(cudaFuncSetAttribute(lc_dec_write_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+            lc_dec_write_kernel<uint16_t><<<wgrid, LC_DEC_TPB, wsm, st>>>(DP, segs, offs, bcodes.p, m, endpos, (int)cap);
+        } else {
+            LC_CUDA_OK(cudaFuncSetAttribute(lc_dec_write_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+            lc_dec_write_kernel<uint32_t><<<wgrid, LC_DEC_TPB, wsm, st>>>(DP, segs, offs, bcodes.p, m, endpos, (int)cap);
+        }
+    }
+    lc_dec_status_kernel<<<1, 1, 0, st>>>(segs, offs, tot, endpos, m, payload_bits, status);
     { int _rc = lc_debug_check(ctx, "lc_dec_status_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
     lc_count_launch(ctx, 3);
     int *hstat = (int *)lc_pinned(ctx);
