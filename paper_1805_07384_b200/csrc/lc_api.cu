@@ -320,7 +320,7 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     // codebook
     LC_CUDA_OK(lc_reserve(ctx->lengths, nbins));
     LC_CUDA_OK(lc_reserve(ctx->cw, nbins * sizeof(unsigned long long)));
-    LC_CUDA_OK(lc_reserve(ctx->gkeys, 2 * (size_t)nbins * sizeof(unsigned long long)));
+    LC_CUDA_OK(lc_reserve(ctx->gkeys, 3 * (size_t)nbins * sizeof(unsigned long long)));
     LC_CUDA_OK(lc_reserve(ctx->ifreq, (size_t)nbins * sizeof(unsigned long long)));
     LC_CUDA_OK(lc_reserve(ctx->parent, 2 * (size_t)nbins * sizeof(int)));
     LC_CUDA_OK(lc_reserve(ctx->cbout, sizeof(LcCodebookOut)));
@@ -361,7 +361,8 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     E.desc = (LcEncDesc *)ctx->encdesc.p;
     E.tile_counter = tile_counter;
     E.ntiles = etiles;
-    const int egrid = (int)(etiles < (uint64_t)(3 * ctx->sm_count) ? etiles : 3 * ctx->sm_count);
+    E.max_len = ctx->cb.max_len;
+    const int egrid = (int)(etiles < (uint64_t)(4 * ctx->sm_count) ? etiles : 4 * ctx->sm_count);
     lc_encode_kernel<CodeT><<<egrid, LC_TPB, lc_encode_smem_bytes(), st>>>(E);
     { int _rc = lc_debug_check(ctx, "lc_encode_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
     ctx->launches += 2;
@@ -472,7 +473,7 @@ int lc_decompress_f64(lc_ctx *ctx, uint64_t n, double eb_abs, double first_value
 int lc_debug_copy(lc_ctx *ctx, int what, void *host, uint64_t bytes)
 {
     const void *src = what == 0 ? ctx->codes.p : what == 1 ? ctx->hist.p : what == 2 ? ctx->lengths.p
-                    : what == 3 ? ctx->cw.p : ctx->timeline.p;
+                    : what == 3 ? ctx->cw.p : what == 5 ? ctx->cbout.p : ctx->timeline.p;
     LC_CUDA_OK(cudaMemcpyAsync(host, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
     LC_CUDA_OK(cudaStreamSynchronize(ctx->stream));
     return 0;

@@ -45,11 +45,31 @@ struct LcDecTables {
     int pad2[3];
 };
 
-// lengths[nl] -> tables + sorted symbols (canonical order)
-__global__ void __launch_bounds__(1024) lc_dec_tables_kernel(const uint8_t *__restrict__ lengths, uint32_t nl,
+// lengths[nl] -> tables + sorted symbols (canonical order).  SM: the lengths
+// are first staged in shared memory with 16-byte loads (nl <= LC_DEC_LEN_SMEM).
+#define LC_DEC_LEN_SMEM 98304
+template <bool SM>
+__global__ void __launch_bounds__(1024) lc_dec_tables_kernel(const uint8_t *__restrict__ glengths, uint32_t nl,
                                                             LcDecTables *__restrict__ T,
                                                             uint32_t *__restrict__ sorted)
 {
+    extern __shared__ __align__(16) uint8_t s_lengths[];
+    if (SM) {
+        const uint32_t nv = (nl + 15) / 16;
+        const bool al = (reinterpret_cast<uintptr_t>(glengths) & 15) == 0;
+        for (uint32_t i = threadIdx.x; i < nv; i += blockDim.x) {
+            uint4 v;
+            if (al && 16 * i + 16 <= nl) {
+                v = __ldg(reinterpret_cast<const uint4 *>(glengths) + i);
+            } else {
+                uint8_t b[16];
+                for (int k = 0; k < 16; ++k) b[k] = 16 * i + k < nl ? glengths[16 * i + k] : 0;
+                v = *reinterpret_cast<uint4 *>(b);
+            }
+            reinterpret_cast<uint4 *>(s_lengths)[i] = v;
+        }
+    }
+    const uint8_t *lengths = SM ? s_lengths : glengths;
     __shared__ int s_cnt[66];
     __shared__ int s_wcnt[32][66];
     __shared__ int s_max;
@@ -1080,7 +1100,13 @@ int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_valu
     LC_CUDA_OK(lc_reserve(btab, sizeof(LcDecTables) + n_lengths * 4 + 64));
     LcDecTables *T = (LcDecTables *)btab.p;
     uint32_t *sorted = (uint32_t *)((char *)btab.p + sizeof(LcDecTables));
-    lc_dec_tables_kernel<<<1, 1024, 0, st>>>((const uint8_t *)blen.p, (uint32_t)n_lengths, T, sorted);
+    if (n_lengths <= LC_DEC_LEN_SMEM) {
+        const size_t lsm = (n_lengths + 15) / 16 * 16;
+        LC_CUDA_OK(cudaFuncSetAttribute(lc_dec_tables_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
+        lc_dec_tables_kernel<true><<<1, 1024, lsm, st>>>((const uint8_t *)blen.p, (uint32_t)n_lengths, T, sorted);
+    } else {
+        lc_dec_tables_kernel<false><<<1, 1024, 0, st>>>((const uint8_t *)blen.p, (uint32_t)n_lengths, T, sorted);
+    }
     { int _rc = lc_debug_check(ctx, "lc_dec_tables_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
     lc_count_launch(ctx, 2);
     // Huffman decode

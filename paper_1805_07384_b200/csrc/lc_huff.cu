@@ -19,141 +19,213 @@
 #include "lc_kernels.cuh"
 
 #define LC_CB_THREADS 1024
-#define LC_CB_SMEM_KEYS 8192
+#define LC_CB_SMEM_KEYS 4096
 #define LC_ENC_TAB 4096
 
 
-__device__ void lc_bitonic_sort(unsigned long long *a, int npow2)
+__device__ __forceinline__ void lc_bitonic_sort(unsigned long long *a, int npow2)
 {
+    const int half = npow2 >> 1;
     for (int k = 2; k <= npow2; k <<= 1) {
         for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < npow2; i += blockDim.x) {
-                const int ixj = i ^ j;
-                if (ixj > i) {
-                    const unsigned long long ai = a[i], aj = a[ixj];
-                    const bool up = (i & k) == 0;
-                    if ((ai > aj) == up) { a[i] = aj; a[ixj] = ai; }
-                }
+            for (int q = threadIdx.x; q < half; q += blockDim.x) {
+                const int i = ((q & ~(j - 1)) << 1) | (q & (j - 1));   // lower index of the pair
+                const int ixj = i | j;
+                const unsigned long long ai = a[i], aj = a[ixj];
+                const bool up = (i & k) == 0;
+                if ((ai > aj) == up) { a[i] = aj; a[ixj] = ai; }
             }
             __syncthreads();
         }
     }
 }
 
-// hist[nbins] -> lengths[nbins], codes[nbins], meta.  scratch holds
-// 3*nbins u64 + 2*nbins int32 (global fallback storage).
-__global__ void __launch_bounds__(LC_CB_THREADS) lc_codebook_kernel(
-    const uint32_t *__restrict__ hist, uint32_t nbins, uint8_t *__restrict__ lengths,
-    unsigned long long *__restrict__ codes, unsigned long long *__restrict__ gkeys,
-    unsigned long long *__restrict__ ifreq, int *__restrict__ parent, LcCodebookOut *out)
+// hist[nbins] -> lengths[nbins], codes[nbins], meta.  Working arrays live in
+// shared memory when at most LC_CB_SMEM_KEYS symbols are used (SMEM), else in
+// the global scratch (gkeys: 3*nbins u64, ifreq: nbins u64, parent: 2*nbins int).
+// Used symbols are numbered p = 0..k-1 in symbol order; sort keys are
+// (freq << 32 | p), so (freq, p) order is the reference's (freq, symbol) order.
+template <bool SMEM>
+__device__ __forceinline__ void lc_codebook_body(const uint32_t *__restrict__ hist, uint32_t nbins,
+                                                 uint8_t *__restrict__ lengths, unsigned long long *__restrict__ codes,
+                                                 unsigned long long *__restrict__ gkeys,
+                                                 unsigned long long *__restrict__ ifreq_g, int *__restrict__ parent_g,
+                                                 LcCodebookOut *out, int k, int wbase, uint32_t wsb, uint32_t wse,
+                                                 int *s_len_count, int *s_len_start, unsigned long long *s_first,
+                                                 unsigned long long *s_bits, int *s_wmax, int (*s_wcnt)[65])
 {
     extern __shared__ __align__(16) unsigned char lc_dyn_smem[];
-    unsigned long long *skeys = reinterpret_cast<unsigned long long *>(lc_dyn_smem);
-    __shared__ int s_used, s_len_count[66];
-    __shared__ unsigned long long s_first[66];
-    __shared__ unsigned long long s_bits[32];
-    const int tid = threadIdx.x;
-    if (tid == 0) s_used = 0;
-    if (tid < 66) s_len_count[tid] = 0;
-    __syncthreads();
-
-    // 1. used symbols (order irrelevant: sorted next)
-    int cnt = 0;
-    for (uint32_t s = tid; s < nbins; s += blockDim.x) cnt += hist[s] > 0;
-    const int base = atomicAdd(&s_used, cnt) ; (void)base;
-    __syncthreads();
-    const int k = s_used;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    constexpr int NWARP = LC_CB_THREADS / 32;
+    const int cap = SMEM ? LC_CB_SMEM_KEYS : (int)(2 * nbins);
+    unsigned long long *keys = SMEM ? reinterpret_cast<unsigned long long *>(lc_dyn_smem) : gkeys;
+    unsigned long long *ifreq = SMEM ? keys + LC_CB_SMEM_KEYS : ifreq_g;
+    int *parent = SMEM ? reinterpret_cast<int *>(ifreq + LC_CB_SMEM_KEYS) : parent_g;
+    uint32_t *syms = SMEM ? reinterpret_cast<uint32_t *>(parent + 2 * LC_CB_SMEM_KEYS)
+                          : reinterpret_cast<uint32_t *>(gkeys + cap);
+    uint8_t *lenp = reinterpret_cast<uint8_t *>(syms + (SMEM ? LC_CB_SMEM_KEYS : nbins));
     int npow2 = 1;
     while (npow2 < k) npow2 <<= 1;
-    unsigned long long *keys = (npow2 <= LC_CB_SMEM_KEYS) ? skeys : gkeys;
-    __syncthreads();
-    if (tid == 0) s_used = 0;
-    __syncthreads();
-    for (uint32_t s = tid; s < nbins; s += blockDim.x) {
-        lengths[s] = 0;
-        codes[s] = 0;
-        if (hist[s]) {
-            const int pos = atomicAdd(&s_used, 1);
-            keys[pos] = ((unsigned long long)hist[s] << 32) | s;
+    // 1b. compaction in symbol order (warp ranges, ballot ranks)
+    int wpos = wbase;
+    for (uint32_t s0 = wsb; s0 < wse; s0 += 32) {
+        const uint32_t sy = s0 + lane;
+        const uint32_t h = sy < wse ? __ldg(hist + sy) : 0u;
+        const unsigned bal = __ballot_sync(0xffffffffu, h != 0);
+        if (h) {
+            const int pp = wpos + __popc(bal & ((1u << lane) - 1u));
+            keys[pp] = ((unsigned long long)h << 32) | (uint32_t)pp;
+            syms[pp] = sy;
         }
+        wpos += __popc(bal);
     }
+    for (int i = k + tid; i < npow2; i += LC_CB_THREADS) keys[i] = ~0ULL;
     __syncthreads();
-    for (int i = k + tid; i < npow2; i += blockDim.x) keys[i] = ~0ULL;
-    __syncthreads();
-    if (k == 0) {
-        if (tid == 0) { out->total_bits = 0; out->n_esc = 0; out->max_len = 0; out->used = 0; out->status = 0; }
-        return;
-    }
     if (k == 1) {                                   // huffman.py:33-35
         if (tid == 0) {
-            const uint32_t s = (uint32_t)(keys[0] & 0xffffffffu);
-            lengths[s] = 1;
-            codes[s] = 0;
+            const uint32_t sy = syms[0];
+            lengths[sy] = 1;
+            codes[sy] = 0;
             out->total_bits = keys[0] >> 32;
             out->n_esc = hist[0];
             out->max_len = 1; out->used = 1; out->status = 0;
         }
         return;
     }
+    if (tid == 0) out->stamp[0] = lc_gtimer();
     // 2. sort by (freq, symbol)
     lc_bitonic_sort(keys, npow2);
+    if (tid == 0) out->stamp[1] = lc_gtimer();
 
-    // 3. two-queue merge (thread 0).  Leaves 0..k-1 in sorted order; internal
-    //    node m (0..k-2) has freq ifreq[m]; parent[] indexes internal nodes:
-    //    parent[leaf] at [0,k), parent[k + m] for internal node m.
-    if (tid == 0) {
-        int li = 0, ii = 0;                          // queue heads
+    // 3. two-queue merge.  Leaves 0..k-1 in sorted order; internal node m
+    //    (0..k-2) has freq ifreq[m]; parent[leaf] at [0,k), parent[k + m] for
+    //    internal node m.  A leaf wins ties: heapq pops (freq, counter) and
+    //    leaves were pushed first (huffman.py:36-48).  The first warp runs it
+    //    (lane-varying start values keep it off the uniform datapath; lane 0
+    //    stores); queue heads and their successors stay in registers.
+    if (wid == 0) {
+        const unsigned long long INF = ~0ULL;
+        int li = lane >> 5, ii = lane >> 5;          // 0, but not provably warp-uniform
+        unsigned long long lf0 = keys[0] >> 32, lf1 = keys[1] >> 32;   // k >= 2 here
+        unsigned long long if0 = INF, if1 = INF;
         for (int m = 0; m < k - 1; ++m) {
-            int pick[2];
+            int pk[2];
             unsigned long long f[2];
+#pragma unroll
             for (int q = 0; q < 2; ++q) {
-                const bool leaf_ok = li < k;
-                const bool int_ok = ii < m;
-                const unsigned long long lf = leaf_ok ? (keys[li] >> 32) : ~0ULL;
-                const unsigned long long nf = int_ok ? ifreq[ii] : ~0ULL;
-                if (leaf_ok && (!int_ok || lf <= nf)) { pick[q] = li; f[q] = lf; ++li; }
-                else { pick[q] = k + ii; f[q] = nf; ++ii; }
+                const bool tl = lf0 <= if0;
+                f[q] = tl ? lf0 : if0;
+                pk[q] = tl ? li : k + ii;
+                li += tl;
+                ii += !tl;
+                const unsigned long long lnext = li + 1 < k ? (keys[min(li + 1, k - 1)] >> 32) : INF;
+                const unsigned long long inext = ii + 1 < m ? ifreq[min(ii + 1, k - 2)] : INF;
+                lf0 = tl ? lf1 : lf0;
+                lf1 = tl ? lnext : lf1;
+                if0 = tl ? if0 : if1;
+                if1 = tl ? if1 : inext;
             }
-            ifreq[m] = f[0] + f[1];
-            parent[pick[0]] = m;
-            parent[pick[1]] = m;
+            const unsigned long long fm = f[0] + f[1];
+            if (lane == 0) {
+                ifreq[m] = fm;
+                parent[pk[0]] = m;
+                parent[pk[1]] = m;
+            }
+            if0 = ii == m ? fm : if0;
+            if1 = ii + 1 == m ? fm : if1;
         }
     }
     __syncthreads();
-    // 4. depths: internal nodes in reverse creation order (root = k-2)
-    int *depth = reinterpret_cast<int *>(ifreq);     // reuse (freqs no longer needed)
-    if (tid == 0) {
-        depth[k - 2] = 0;
-        for (int m = k - 3; m >= 0; --m) depth[m] = depth[parent[k + m]] + 1;
+    if (tid == 0) out->stamp[2] = lc_gtimer();
+    // 4. depths of internal nodes: pointer jumping (root k-2 has depth 0)
+    int *D = reinterpret_cast<int *>(ifreq);         // freqs no longer needed
+    int *A = D + k;
+    const int ni = k - 1;
+    constexpr int NJ = 8;
+    if (ni <= NJ * LC_CB_THREADS) {
+        for (int m = tid; m < ni; m += LC_CB_THREADS) {
+            const bool root = m == ni - 1;
+            D[m] = root ? 0 : 1;
+            A[m] = root ? -1 : parent[k + m];
+        }
+        __syncthreads();
+        for (int r = 1; r < ni; r <<= 1) {
+            int nd[NJ], na[NJ];
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) {
+                const int m = tid + j * LC_CB_THREADS;
+                nd[j] = 0; na[j] = -1;
+                if (m < ni) {
+                    const int a = A[m];
+                    nd[j] = D[m];
+                    if (a >= 0) { nd[j] += D[a]; na[j] = A[a]; }
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) {
+                const int m = tid + j * LC_CB_THREADS;
+                if (m < ni) { D[m] = nd[j]; A[m] = na[j]; }
+            }
+            __syncthreads();
+        }
+    } else {
+        if (tid == 0) {
+            D[ni - 1] = 0;
+            for (int m = ni - 2; m >= 0; --m) D[m] = D[parent[k + m]] + 1;
+        }
+        __syncthreads();
     }
-    __syncthreads();
+    if (tid == 0) out->stamp[3] = lc_gtimer();
+    // leaf lengths by symbol-order position
     int local_max = 0;
     unsigned long long local_bits = 0;
-    for (int i = tid; i < k; i += blockDim.x) {
-        const int d = depth[parent[i]] + 1;
-        const uint32_t s = (uint32_t)(keys[i] & 0xffffffffu);
-        lengths[s] = (uint8_t)(d > 255 ? 255 : d);
-        if (d <= 64) atomicAdd(&s_len_count[d], 1);
+    for (int i = tid; i < k; i += LC_CB_THREADS) {
+        const int d = D[parent[i]] + 1;
+        const unsigned long long key = keys[i];
+        lenp[(uint32_t)(key & 0xffffffffu)] = (uint8_t)(d > 255 ? 255 : d);
         local_max = max(local_max, d);
-        local_bits += (keys[i] >> 32) * (unsigned long long)d;
+        local_bits += (key >> 32) * (unsigned long long)d;
     }
     for (int o = 16; o; o >>= 1) {
         local_max = max(local_max, __shfl_xor_sync(0xffffffffu, local_max, o));
         local_bits += __shfl_xor_sync(0xffffffffu, local_bits, o);
     }
-    __shared__ int s_wmax[32];
-    if ((tid & 31) == 0) { s_wmax[tid >> 5] = local_max; s_bits[tid >> 5] = local_bits; }
+    if (lane == 0) { s_wmax[wid] = local_max; s_bits[wid] = local_bits; }
+    for (int i = tid; i < NWARP * 65; i += LC_CB_THREADS) (&s_wcnt[0][0])[i] = 0;
+    __syncthreads();
+    // 5. canonical codes (huffman.py:58-72): within a length, consecutive
+    //    codes in symbol order.  Warp w owns positions [w*span, (w+1)*span).
+    const int span = (k + NWARP - 1) / NWARP;
+    const int pb = min(k, wid * span), pe = min(k, pb + span);
+    for (int p0 = pb; p0 < pe; p0 += 32) {
+        const int pp = p0 + lane;
+        const int l = pp < pe ? lenp[pp] : 0;
+        if (l > 0 && l <= 64) atomicAdd(&s_wcnt[wid][l], 1);
+    }
     __syncthreads();
     if (tid == 0) {
         int mx = 0;
         unsigned long long tb = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { mx = max(mx, s_wmax[w]); tb += s_bits[w]; }
+        for (int w = 0; w < NWARP; ++w) { mx = max(mx, s_wmax[w]); tb += s_bits[w]; }
         out->max_len = mx;
         out->used = k;
         out->total_bits = tb;
         out->n_esc = hist[0];
         out->status = mx > 64 ? 13 : 0;
-        // canonical first codes per length (huffman.py:64-71)
+        s_wmax[0] = mx;
+    }
+    if (tid >= 1 && tid <= 64) {
+        int acc = 0;
+        for (int w = 0; w < NWARP; ++w) {
+            const int c0 = s_wcnt[w][tid];
+            s_wcnt[w][tid] = acc;                   // rank base of warp w within length tid
+            acc += c0;
+        }
+        s_len_count[tid] = acc;
+    }
+    __syncthreads();
+    if (tid == 0) {
         unsigned long long code = 0;
         int prev = 0;
         for (int l = 1; l <= 64; ++l) {
@@ -161,48 +233,65 @@ __global__ void __launch_bounds__(LC_CB_THREADS) lc_codebook_kernel(
             code = (l - prev) >= 64 ? 0 : (code << (l - prev));
             s_first[l] = code;
             code += (unsigned long long)s_len_count[l];
-            // last code of this length is code-1; the next length shifts it
             prev = l;
         }
+        out->stamp[4] = lc_gtimer();
     }
     __syncthreads();
-    if (out->status) return;
-    // 5. codes: symbols of one length get consecutive codes in symbol order.
-    //    Warp w owns a contiguous symbol range: count lengths, scan the counts
-    //    across warps, then assign ranks with match_any inside each group.
-    __shared__ int s_wcnt[LC_CB_THREADS / 32][65];
-    const int lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-    for (int i = tid; i < nw * 65; i += blockDim.x) (&s_wcnt[0][0])[i] = 0;
-    __syncthreads();
-    const uint32_t span = (nbins + nw - 1) / nw;
-    const uint32_t sb = wid * span, se = min(nbins, sb + span);
-    for (uint32_t s0 = sb; s0 < se; s0 += 32) {
-        const uint32_t s = s0 + lane;
-        const int l = s < se ? lengths[s] : 0;
-        if (l > 0) atomicAdd(&s_wcnt[wid][l], 1);
-    }
-    __syncthreads();
-    if (tid >= 1 && tid <= 64 && s_len_count[tid]) {
-        unsigned long long off = s_first[tid];
-        for (int w = 0; w < nw; ++w) {
-            const int c0 = s_wcnt[w][tid];
-            s_wcnt[w][tid] = (int)(off - s_first[tid]);   // exclusive rank base
-            off += c0;
-        }
-    }
-    __syncthreads();
-    for (uint32_t s0 = sb; s0 < se; s0 += 32) {
-        const uint32_t s = s0 + lane;
-        const int l = s < se ? lengths[s] : 0;
+    if (s_wmax[0] > 64) return;
+    for (int p0 = pb; p0 < pe; p0 += 32) {
+        const int pp = p0 + lane;
+        const int l = pp < pe ? lenp[pp] : 0;
         const unsigned peers = __match_any_sync(0xffffffffu, l);
         if (l > 0) {
-            const int rank = __popc(peers & ((1u << lane) - 1u));
-            codes[s] = s_first[l] + (unsigned long long)(s_wcnt[wid][l] + rank);
+            const uint32_t sy = syms[pp];
+            lengths[sy] = (uint8_t)l;
+            codes[sy] = s_first[l] + (unsigned long long)(s_wcnt[wid][l] + __popc(peers & ((1u << lane) - 1u)));
         }
         __syncwarp();
         if (l > 0 && (int)(__ffs(peers) - 1) == lane) s_wcnt[wid][l] += __popc(peers);
         __syncwarp();
     }
+    if (tid == 0) out->stamp[5] = lc_gtimer();
+}
+
+__global__ void __launch_bounds__(LC_CB_THREADS) lc_codebook_kernel(
+    const uint32_t *__restrict__ hist, uint32_t nbins, uint8_t *__restrict__ lengths,
+    unsigned long long *__restrict__ codes, unsigned long long *__restrict__ gkeys,
+    unsigned long long *__restrict__ ifreq_g, int *__restrict__ parent_g, LcCodebookOut *out)
+{
+    __shared__ int s_wcnt[LC_CB_THREADS / 32][65], s_len_count[66], s_len_start[66], s_wmax[32];
+    __shared__ unsigned long long s_first[66], s_bits[32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid < 66) s_len_count[tid] = 0;
+    // 1a. used symbols per warp range (coalesced), zero all lengths
+    const uint32_t span = ((nbins + LC_CB_THREADS / 32 - 1) / (LC_CB_THREADS / 32) + 31) & ~31u;
+    const uint32_t wsb = min(nbins, wid * span), wse = min(nbins, wsb + span);
+    int cnt = 0;
+    for (uint32_t s0 = wsb; s0 < wse; s0 += 32) {
+        const uint32_t sy = s0 + lane;
+        cnt += __popc(__ballot_sync(0xffffffffu, sy < wse && __ldg(hist + sy) != 0));
+    }
+    for (uint32_t sy = tid; sy < nbins; sy += LC_CB_THREADS) lengths[sy] = 0;
+    if (lane == 0) s_wcnt[wid][0] = cnt;
+    __syncthreads();
+    int wbase = 0, k = 0;
+    for (int w = 0; w < LC_CB_THREADS / 32; ++w) {
+        const int c = s_wcnt[w][0];
+        if (w < wid) wbase += c;
+        k += c;
+    }
+    __syncthreads();
+    if (k == 0) {
+        if (tid == 0) { out->total_bits = 0; out->n_esc = 0; out->max_len = 0; out->used = 0; out->status = 0; }
+        return;
+    }
+    if (k <= LC_CB_SMEM_KEYS)
+        lc_codebook_body<true>(hist, nbins, lengths, codes, gkeys, ifreq_g, parent_g, out, k, wbase, wsb, wse,
+                               s_len_count, s_len_start, s_first, s_bits, s_wmax, s_wcnt);
+    else
+        lc_codebook_body<false>(hist, nbins, lengths, codes, gkeys, ifreq_g, parent_g, out, k, wbase, wsb, wse,
+                                s_len_count, s_len_start, s_first, s_bits, s_wmax, s_wcnt);
 }
 
 // ---------------------------------------------------------------------------
@@ -224,14 +313,33 @@ __device__ __forceinline__ void lc_put_word(uint32_t *payload, uint64_t w, uint3
     else payload[w] = le;
 }
 
+// Encoder.  A tile of LC_TILE symbols per CTA iteration, 32 consecutive
+// symbols per thread held in registers.  Tile bit offsets come from a
+// decoupled look-back over (bits, escapes); the tile's bit string is
+// assembled in a shared-memory word buffer (thread-boundary words merged with
+// shared atomics) and written out with coalesced word stores, merging only
+// the tile's first and last words with the neighbouring tiles (the payload
+// is zeroed first).  huffman.encode (huffman.py:52-72) packs MSB-first.
+#define LC_ENC_WBUF 4096                 // tile buffer words (16 bits per symbol on average)
+
+template <typename CodeT>
+struct LcCodeRegs {
+    static constexpr int NW = LC_L * sizeof(CodeT) / 4;   // 32-bit words holding 32 symbols
+    uint32_t w[NW];
+    __device__ __forceinline__ uint32_t get(int j) const
+    {
+        if (sizeof(CodeT) == 2) return (w[j >> 1] >> (16 * (j & 1))) & 0xffffu;
+        return w[j];
+    }
+};
+
 template <typename CodeT>
 __global__ void __launch_bounds__(LC_TPB) lc_encode_kernel(LcEncParams P)
 {
     typedef cub::BlockScan<unsigned long long, LC_TPB> ScanU;
     extern __shared__ __align__(16) unsigned char lc_dyn_smem[];
-    unsigned long long *tcw = reinterpret_cast<unsigned long long *>(lc_dyn_smem);
-    uint32_t *cs = reinterpret_cast<uint32_t *>(tcw + LC_ENC_TAB);
-    uint8_t *tlen = reinterpret_cast<uint8_t *>(cs + LC_TPB * LC_ROW);
+    unsigned long long *tpk = reinterpret_cast<unsigned long long *>(lc_dyn_smem);   // (len << 32) | code
+    uint32_t *wbuf = reinterpret_cast<uint32_t *>(tpk + LC_ENC_TAB);
     __shared__ typename ScanU::TempStorage scan_tmp;
     __shared__ long long sh_tile;
     __shared__ unsigned long long sh_in_bits, sh_in_esc;
@@ -239,8 +347,13 @@ __global__ void __launch_bounds__(LC_TPB) lc_encode_kernel(LcEncParams P)
     __shared__ int sh_j;
     const int tid = threadIdx.x;
     const CodeT *codes = reinterpret_cast<const CodeT *>(P.codes);
+    const bool fast = P.max_len <= 32;
     const uint32_t tab = P.nbins < LC_ENC_TAB ? P.nbins : LC_ENC_TAB;
-    for (uint32_t s = tid; s < tab; s += LC_TPB) { tlen[s] = P.lengths[s]; tcw[s] = P.cw[s]; }
+    for (uint32_t s = tid; s < tab; s += LC_TPB)
+        tpk[s] = ((unsigned long long)P.lengths[s] << 32) | (fast ? (uint32_t)P.cw[s] : 0u);
+    auto entry = [&](uint32_t s) -> unsigned long long {
+        return s < LC_ENC_TAB ? tpk[s] : (((unsigned long long)P.lengths[s] << 32) | (uint32_t)P.cw[s]);
+    };
 
     for (;;) {
         __syncthreads();
@@ -248,34 +361,48 @@ __global__ void __launch_bounds__(LC_TPB) lc_encode_kernel(LcEncParams P)
         __syncthreads();
         const long long t = sh_tile;
         if (t >= (long long)P.ntiles) break;
-        const long long base = t * (long long)LC_TILE;
-#pragma unroll 8
-        for (int k = 0; k < LC_L; ++k) {
-            const int off = k * LC_TPB + tid;
-            const long long pos = base + off;
-            cs[(off >> 5) * LC_ROW + (off & 31)] = pos < (long long)P.m ? (uint32_t)codes[pos] : 0xffffffffu;
-        }
-        __syncthreads();
-        const uint32_t *row = cs + tid * LC_ROW;
-        const long long p0 = base + (long long)tid * LC_L;
+        const long long p0 = t * (long long)LC_TILE + (long long)tid * LC_L;
         const int len = (int)max(0LL, min((long long)LC_L, (long long)P.m - p0));
-        unsigned long long bits = 0, nesc = 0;
-        for (int j = 0; j < len; ++j) {
-            const uint32_t s = row[j];
-            bits += s < LC_ENC_TAB ? tlen[s] : P.lengths[s];
-            nesc += (s == 0);
+        LcCodeRegs<CodeT> C;
+        if (len == LC_L) {
+            const uint4 *src = reinterpret_cast<const uint4 *>(codes + p0);
+#pragma unroll
+            for (int k = 0; k < LcCodeRegs<CodeT>::NW / 4; ++k) {
+                const uint4 v = __ldcs(src + k);
+                C.w[4 * k] = v.x; C.w[4 * k + 1] = v.y; C.w[4 * k + 2] = v.z; C.w[4 * k + 3] = v.w;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < LcCodeRegs<CodeT>::NW; ++k) C.w[k] = 0;
+#pragma unroll
+            for (int j = 0; j < LC_L; ++j) {
+                if (j < len) {
+                    const uint32_t v = (uint32_t)codes[p0 + j];
+                    if (sizeof(CodeT) == 2) C.w[j >> 1] |= v << (16 * (j & 1));
+                    else C.w[j] = v;
+                }
+            }
         }
-        unsigned long long bex, eex, bagg, eagg;
-        ScanU(scan_tmp).ExclusiveSum(bits, bex, bagg);
-        __syncthreads();
-        ScanU(scan_tmp).ExclusiveSum(nesc, eex, eagg);
+        unsigned long long bits = 0, nesc = 0;
+#pragma unroll
+        for (int j = 0; j < LC_L; ++j) {
+            if (j < len) {
+                const uint32_t s = C.get(j);
+                bits += (uint32_t)(entry(s) >> 32);
+                nesc += (s == 0);
+            }
+        }
+        // per-tile bits < 2^20 and escapes < 2^14: one scan of (esc << 32 | bits)
+        unsigned long long ex, agg;
+        ScanU(scan_tmp).ExclusiveSum(bits | (nesc << 32), ex, agg);
+        const unsigned long long abits = agg & 0xffffffffull, aesc = agg >> 32;
         {
             LcEncDesc *d = P.desc + t;
             ulonglong2 in = make_ulonglong2(0, 0);
             if (t > 0) {
                 if (tid == 0) {
-                    __stcg(&d->agg_bits, bagg);
-                    __stcg(&d->agg_esc, eagg);
+                    __stcg(&d->agg_bits, abits);
+                    __stcg(&d->agg_esc, aesc);
                     st_release(&d->st, 1);
                 }
                 in = lc_lookback_block<ulonglong2>(
@@ -293,62 +420,100 @@ __global__ void __launch_bounds__(LC_TPB) lc_encode_kernel(LcEncParams P)
                     lb_u2, &sh_j, &lb_u2_res);
             }
             if (tid == 0) {
-                __stcg(&d->incl_bits, in.x + bagg);
-                __stcg(&d->incl_esc, in.y + eagg);
+                __stcg(&d->incl_bits, in.x + abits);
+                __stcg(&d->incl_esc, in.y + aesc);
                 st_release(&d->st, 2);
                 sh_in_bits = in.x; sh_in_esc = in.y;
             }
         }
         __syncthreads();
+        const unsigned long long B0 = sh_in_bits;
         // escapes (compressor.py:409-410): code index i-1 <-> element i
         if (nesc) {
-            unsigned long long e = sh_in_esc + eex;
-            for (int j = 0; j < len; ++j)
-                if (row[j] == 0) {
+            unsigned long long e = sh_in_esc + (ex >> 32);
+#pragma unroll
+            for (int j = 0; j < LC_L; ++j)
+                if (j < len && C.get(j) == 0) {
                     const unsigned long long el = (unsigned long long)(p0 + j + 1);
                     P.esc_idx[e] = el;
                     P.esc_val[e] = P.x ? P.x[el] : 0.0;
                     ++e;
                 }
         }
-        if (len == 0) continue;
-        // bit packing
-        const unsigned long long b0 = sh_in_bits + bex;
-        const unsigned long long b1 = b0 + bits;
-        const uint64_t w0 = b0 >> 5, wl = (b1 - 1) >> 5;
-        uint64_t w = w0;
-        uint64_t buf = 0;
-        int nb = (int)(b0 & 31);                   // leading zero bits of the first word
-        for (int j = 0; j < len; ++j) {
-            const uint32_t s = row[j];
-            int l = s < LC_ENC_TAB ? tlen[s] : P.lengths[s];
-            const unsigned long long cw = s < LC_ENC_TAB ? tcw[s] : P.cw[s];
-            while (l > 0) {
-                const int take = l > 32 ? l - 32 : l;      // high part first
-                const uint64_t piece = (cw >> (l - take)) & ((take == 64) ? ~0ULL : ((1ULL << take) - 1));
-                buf = (buf << take) | piece;
-                nb += take;
-                l -= take;
-                if (nb >= 32) {
-                    const uint32_t word = (uint32_t)(buf >> (nb - 32));
-                    lc_put_word(P.payload, w, word, w == w0 || w == wl);
-                    ++w;
-                    nb -= 32;
-                    buf &= (nb ? ((1ULL << nb) - 1) : 0ULL);
+        const unsigned lb = (unsigned)(B0 & 31) + (unsigned)(ex & 0xffffffffull);   // bit in the tile buffer
+        const unsigned nwt = (unsigned)(((B0 & 31) + abits + 31) >> 5);
+        if (fast && nwt <= LC_ENC_WBUF) {
+            for (unsigned i = tid; i < nwt; i += LC_TPB) wbuf[i] = 0;
+            __syncthreads();
+            if (bits) {
+                const unsigned wfirst = lb >> 5, wlast = (unsigned)((lb + bits - 1) >> 5);
+                unsigned w = wfirst;
+                unsigned long long acc = 0;
+                int nb = (int)(lb & 31);
+#pragma unroll
+                for (int j = 0; j < LC_L; ++j) {
+                    if (j < len) {
+                        const unsigned long long e = entry(C.get(j));
+                        const int l = (int)(e >> 32);
+                        acc = (acc << l) | (uint32_t)e;
+                        nb += l;
+                        if (nb >= 32) {
+                            nb -= 32;
+                            const uint32_t word = (uint32_t)(acc >> nb);
+                            if (w == wfirst || w == wlast) atomicOr(wbuf + w, word);
+                            else wbuf[w] = word;
+                            ++w;
+                        }
+                    }
+                }
+                if (nb > 0) atomicOr(wbuf + w, (uint32_t)(acc << (32 - nb)));
+            }
+            __syncthreads();
+            const unsigned long long gw0 = B0 >> 5;
+            for (unsigned i = tid; i < nwt; i += LC_TPB) {
+                const uint32_t v = __byte_perm(wbuf[i], 0, 0x0123);       // MSB-first bytes
+                if (i == 0 || i + 1 == nwt) atomicOr(P.payload + gw0 + i, v);
+                else P.payload[gw0 + i] = v;
+            }
+        } else if (bits) {
+            // long codes or a very long tile: pack straight into global words
+            const unsigned long long b0 = B0 + (ex & 0xffffffffull);
+            const unsigned long long b1 = b0 + bits;
+            const uint64_t w0 = b0 >> 5, wl = (b1 - 1) >> 5;
+            uint64_t w = w0;
+            uint64_t buf = 0;
+            int nb = (int)(b0 & 31);
+            for (int j = 0; j < len; ++j) {
+                const uint32_t s = (uint32_t)codes[p0 + j];
+                int l = P.lengths[s];
+                const unsigned long long cw = P.cw[s];
+                while (l > 0) {
+                    const int take = l > 32 ? l - 32 : l;      // high part first
+                    const uint64_t piece = (cw >> (l - take)) & ((take == 64) ? ~0ULL : ((1ULL << take) - 1));
+                    buf = (buf << take) | piece;
+                    nb += take;
+                    l -= take;
+                    if (nb >= 32) {
+                        const uint32_t word = (uint32_t)(buf >> (nb - 32));
+                        lc_put_word(P.payload, w, word, w == w0 || w == wl);
+                        ++w;
+                        nb -= 32;
+                        buf &= (nb ? ((1ULL << nb) - 1) : 0ULL);
+                    }
                 }
             }
-        }
-        if (nb > 0) {
-            const uint32_t word = (uint32_t)(buf << (32 - nb));
-            lc_put_word(P.payload, w, word, true);
+            if (nb > 0) lc_put_word(P.payload, w, (uint32_t)(buf << (32 - nb)), true);
         }
     }
 }
 
-size_t lc_codebook_smem_bytes() { return sizeof(unsigned long long) * LC_CB_SMEM_KEYS; }
+size_t lc_codebook_smem_bytes()
+{
+    return (2 * sizeof(unsigned long long) + 2 * sizeof(int) + sizeof(uint32_t) + 1) * LC_CB_SMEM_KEYS;
+}
 size_t lc_encode_smem_bytes()
 {
-    return sizeof(unsigned long long) * LC_ENC_TAB + sizeof(uint32_t) * LC_TPB * LC_ROW + LC_ENC_TAB;
+    return sizeof(unsigned long long) * LC_ENC_TAB + sizeof(uint32_t) * LC_ENC_WBUF;
 }
 
 template __global__ void lc_encode_kernel<uint16_t>(LcEncParams);

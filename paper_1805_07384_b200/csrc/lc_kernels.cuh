@@ -46,6 +46,7 @@ struct LcCodebookOut {
     int used;
     int status;              // 0 ok, 13 code length > 64
     int pad;
+    unsigned long long stamp[6];   // phase timestamps (globaltimer, diagnostics)
 };
 
 struct LcEncDesc {
@@ -67,6 +68,7 @@ struct LcEncParams {
     LcEncDesc *desc;
     unsigned int *tile_counter;
     uint64_t ntiles;
+    int max_len;             // longest code (<= 32: table path)
 };
 
 __global__ void lc_range_kernel(const double *__restrict__ x, uint64_t n, LcRangePart *__restrict__ parts);

@@ -382,22 +382,44 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_quant_b_kernel(LcQuantParams P, 
                 atomicMin(P.first_bad, (unsigned long long)(c + 1));
             }
         }
+        // histogram: runs of equal codes inside the thread's own chunk
+        if (P.count_hist && len > 0) {
+            const uint32_t *crow = reinterpret_cast<const uint32_t *>(xs + tid * LC_ROW);
+            uint32_t cur = crow[0], cnt = 0;
+            for (int j = 0; j < len; ++j) {
+                const uint32_t code = crow[j];
+                if (code != cur) {
+                    if (cur < hb) atomicAdd(&hs[cur], cnt);
+                    else atomicAdd(&P.hist[cur], cnt);
+                    cur = code;
+                    cnt = 0;
+                }
+                ++cnt;
+            }
+            if (cur < hb) atomicAdd(&hs[cur], cnt);
+            else atomicAdd(&P.hist[cur], cnt);
+        }
         __syncthreads();
-        // histogram (warp-aggregated) + coalesced code store
-#pragma unroll 4
-        for (int k = 0; k < LC_L; ++k) {
-            const int off = k * LC_TPB + tid;
-            const long long pos = pbeg + off;
-            const bool valid = pos < nel;
-            const uint32_t code = valid ? reinterpret_cast<const uint32_t *>(xs)[(off >> 5) * (2 * LC_ROW) + (off & 31)]
-                                        : 0xffffffffu;
-            if (valid) codes[pos] = (CodeT)code;
-            if (P.count_hist) {
-                const unsigned peers = __match_any_sync(0xffffffffu, code);
-                if (valid && (int)(__ffs(peers) - 1) == lane) {
-                    const unsigned cnt = __popc(peers);
-                    if (code < hb) atomicAdd(&hs[code], cnt);
-                    else atomicAdd(&P.hist[code], cnt);
+        // coalesced 16-byte code stores: 16 / sizeof(CodeT) consecutive codes per thread
+        {
+            constexpr int V = 16 / sizeof(CodeT);
+            const long long tile_n = min((long long)LC_TILE, nel - pbeg);
+            for (int g = tid; g * V < tile_n; g += LC_TPB) {
+                const int off = g * V;                       // first element of the group
+                const uint32_t *src = reinterpret_cast<const uint32_t *>(xs) + (off >> 5) * (2 * LC_ROW) + (off & 31);
+                if (off + V <= tile_n) {
+                    uint4 v;
+                    if (V == 8) {
+                        v.x = (src[0] & 0xffffu) | (src[1] << 16);
+                        v.y = (src[2] & 0xffffu) | (src[3] << 16);
+                        v.z = (src[4] & 0xffffu) | (src[5] << 16);
+                        v.w = (src[6] & 0xffffu) | (src[7] << 16);
+                    } else {
+                        v.x = src[0]; v.y = src[1]; v.z = src[2]; v.w = src[3];
+                    }
+                    *reinterpret_cast<uint4 *>(codes + pbeg + off) = v;
+                } else {
+                    for (int k = 0; off + k < tile_n; ++k) codes[pbeg + off + k] = (CodeT)src[k];
                 }
             }
         }
