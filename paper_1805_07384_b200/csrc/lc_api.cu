@@ -277,7 +277,7 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
         const double ms = ctx->rng_maxstep;
         P.use_anchors = ((ms * (1.0 - 0x1p-50)) - (eb_abs * (1.0 + 0x1p-50))) >= P.esc_thresh || !isfinite(ms);
     }
-    const int ga = 2 * ctx->sm_count, gb = 3 * ctx->sm_count;
+    const int ga = 3 * ctx->sm_count, gb = 3 * ctx->sm_count;
     for (;;) {
         P.ntiles = (nchunks - P.first_chunk + LC_TPB - 1) / LC_TPB;
         LC_CUDA_OK(cudaMemsetAsync(first_bad, 0xff, 8, st));

@@ -875,7 +875,7 @@ __global__ void __launch_bounds__(1024) lc_rec0_scan_kernel(LcRecSplit S, long l
     }
 }
 
-__global__ void __launch_bounds__(LC_TPB, 2) lc_rec_a_kernel(LcRecParams P, LcRecSplit S)
+__global__ void __launch_bounds__(LC_TPB, 3) lc_rec_a_kernel(LcRecParams P, LcRecSplit S)
 {
     extern __shared__ __align__(16) unsigned char lc_dyn_smem[];
     uint32_t *cs = reinterpret_cast<uint32_t *>(lc_dyn_smem);
@@ -934,9 +934,10 @@ __global__ void __launch_bounds__(LC_TPB, 2) lc_rec_a_kernel(LcRecParams P, LcRe
                 r = rn;
             }
             lc_events_step_if(E, pend, len - 1, pr, pc, prn);
-            if (!lc_events_finish(E, g0, H)) {          // events: replay, compose at flagged steps
-                double r2 = g0;
-                for (int j = 0; j < len; ++j) {
+            if (!lc_events_finish(E, g0, H)) {          // replay from the first flagged step
+                const int j0 = __ffs(E.mask) - 1, j1 = 31 - __clz(E.mask);
+                double r2 = E.r_first;
+                for (int j = j0; j <= j1; ++j) {
                     const int64_t m = lc_code_m(crow[j]);  // no escape here (E.esc would be set)
                     if (m != 0) {
                         const double inc_ = LC_MUL((double)m, P.delta);
@@ -1280,7 +1281,8 @@ int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_valu
         const int grid = (int)(R.ntiles < grid_cap ? R.ntiles : grid_cap);
         lc_rec0_kernel<<<(int)(R.ntiles < 3 * grid_cap ? R.ntiles : 3 * grid_cap), LC_TPB, 0, st>>>(R, RS);
         lc_rec0_scan_kernel<<<1, 1024, 0, st>>>(RS, R.ntiles, R.anchor_cnt);
-        lc_rec_a_kernel<<<grid, LC_TPB, lc_rec_a_smem_bytes(), st>>>(R, RS);
+        lc_rec_a_kernel<<<(int)(R.ntiles < 3 * lc_sm_count(ctx) ? R.ntiles : 3 * lc_sm_count(ctx)), LC_TPB,
+                          lc_rec_a_smem_bytes(), st>>>(R, RS);
         { int _rc = lc_debug_check(ctx, "lc_rec_a_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
         lc_map_scan_kernel<<<1, 1024, 0, st>>>(RS.tile_agg, RS.tile_D, R.ntiles);
         lc_rec_b_kernel<<<grid, LC_TPB, lc_rec_b_smem_bytes(), st>>>(R, RS);

@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(1024) lc_anchor_scan_kernel(const long long *_
     }
 }
 
-__global__ void __launch_bounds__(LC_TPB, 2) lc_quant_a_kernel(LcQuantParams P)
+__global__ void __launch_bounds__(LC_TPB, 3) lc_quant_a_kernel(LcQuantParams P)
 {
     typedef cub::BlockScan<long long, LC_TPB> ScanLL;
     extern __shared__ __align__(16) unsigned char lc_dyn_smem[];
@@ -240,9 +240,10 @@ __global__ void __launch_bounds__(LC_TPB, 2) lc_quant_a_kernel(LcQuantParams P)
                 r = rn;
             }
             lc_events_step_if(E, pend, len - 1, pr, pc, prn);
-            if (!lc_events_finish(E, g0, H)) {          // events: replay, compose at flagged steps
-                double r2 = g0;
-                for (int j = 0; j < len; ++j) {
+            if (!lc_events_finish(E, g0, H)) {          // replay from the first flagged step
+                const int j0 = __ffs(E.mask) - 1, j1 = 31 - __clz(E.mask);
+                double r2 = E.r_first;
+                for (int j = j0; j <= j1; ++j) {
                     int esc; double inc;
                     const double rn = lc_step_guess(P.Q, row[j], r2, &esc, &inc);
                     if ((E.mask >> j) & 1u) lc_map_step(H, r2, inc, rn);
@@ -322,7 +323,7 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_quant_b_kernel(LcQuantParams P, 
     uint32_t *hs = reinterpret_cast<uint32_t *>(xs + LC_TPB * LC_ROW);
     __shared__ double xhalo[LC_L + 1];
     __shared__ double starts[LC_TPB + 1];
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x;
     const long long nel = (long long)P.n - 1;
     const uint32_t hb = P.nbins < LC_HBINS_B ? P.nbins : LC_HBINS_B;
     for (uint32_t i = tid; i < LC_HBINS_B; i += LC_TPB) hs[i] = 0;

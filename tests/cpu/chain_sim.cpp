@@ -19,7 +19,7 @@ int64_t sim_predict(const double *x, int64_t n, double eb, int64_t nbh, int L,
     std::vector<double> guess(nc), rend(nc);
     std::vector<OffMap> maps(nc);
     const double x0 = x[0];
-    int64_t events = 0;
+    int64_t events = 0, flagged = 0;
     *n_events = 0;
     for (int64_t c = 0; c < nc; ++c) {
         const int64_t s = c * L;
@@ -55,15 +55,16 @@ int64_t sim_predict(const double *x, int64_t n, double eb, int64_t nbh, int L,
         }
         {   // the deferred tracker must reproduce the step-by-step map exactly
             OffMap H2;
-            if (!lc_events_finish(E, g0, H2)) {      // replay at flagged steps
-                double r2 = g0;
-                int j2 = 0;
-                for (int64_t i = s + 1; i <= e; ++i, ++j2) {
+            if (!lc_events_finish(E, g0, H2)) {      // replay from the first flagged step
+                const int j0 = __builtin_ctz(E.mask), j1 = 31 - __builtin_clz(E.mask);
+                double r2 = E.r_first;
+                for (int j2 = j0; j2 <= j1; ++j2) {
                     uint32_t code; double inc; int esc; double pe;
-                    const double rn = lc_step(Q, x[i], r2, &code, &esc, &inc, &pe);
+                    const double rn = lc_step(Q, x[s + 1 + j2], r2, &code, &esc, &inc, &pe);
                     if ((E.mask >> j2) & 1u) lc_map_step(H2, r2, inc, rn);
                     r2 = rn;
                 }
+                flagged += __builtin_popcount(E.mask);
             }
             {
                 if (H2.kind != H.kind || lc_bits(H2.y) != lc_bits(H.y) || lc_bits(H2.t0) != lc_bits(H.t0) ||
@@ -103,7 +104,7 @@ int64_t sim_predict(const double *x, int64_t n, double eb, int64_t nbh, int L,
             r = lc_step(Q, x[i], r, &code, &esc, &inc, &pe);
         }
     }
-    if (*n_events >= 0) *n_events = events;
+    if (*n_events >= 0) *n_events = events * 1000000 + flagged;   // true map changes, flagged steps
     return bad;
 }
 
