@@ -17,6 +17,8 @@
  *   lc_decompress_f64   huffman.decode + _decompress_kernel + checks
  *                                                      compressor.py:430-439,
  *                                                      huffman.py:110-132,153-172
+ *   lc_error_stats_f64  measured_psnr reductions + error_identity_check
+ *                                                      compressor.py:81-94,443-460
  *
  * Status codes (return values):
  *   0 ok
@@ -111,6 +113,26 @@ int lc_phase_ms(lc_ctx *ctx, double *ms, int cap);
 
 /* Kernels this context has launched since creation (diagnostic count).   */
 uint64_t lc_launch_count(lc_ctx *ctx);
+
+/* Distortion statistics of a reconstruction in one fused pass: the sum of
+ * squared errors sum((x - y)^2) (compensated; MSE = sum / n), max |x - y|,
+ * min/max of x (value range), a non-finite flag and, when pe / pe_rec (the
+ * n-1 compression traces) are given, the error-identity deviation
+ * max(|x_0 - y_0|, max_i |(x_i - y_i) - (pe_{i-1} - pe_rec_{i-1})|)
+ * (else -1).  Replaces the numpy reductions of measured_psnr
+ * (compressor.py:81-94) and error_identity_check (compressor.py:443-460).  */
+typedef struct lc_stats {
+    double sum_sq_err;
+    double max_abs_err;
+    double vmin;
+    double vmax;
+    double max_identity_dev;
+    int nonfinite;
+    int pad;
+} lc_stats;
+
+int lc_error_stats_f64(lc_ctx *ctx, const double *original, const double *recon, uint64_t n,
+                       int on_device, const double *pe, const double *pe_rec, lc_stats *out);
 
 #ifdef __cplusplus
 }

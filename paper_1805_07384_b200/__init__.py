@@ -31,4 +31,17 @@ from .errors import (  # noqa: F401
     UnrecoverableImageError,
 )
 
+from . import checkpoint  # noqa: F401
+from .checkpoint import (  # noqa: F401
+    AsyncCheckpointer,
+    CheckpointImage,
+    CkptCost,
+    RecCost,
+    StorageTarget,
+    checkpoint_lossy,
+    checkpoint_traditional,
+    decode_payload,
+    recover,
+)
+
 __version__ = "0.1.0"

@@ -31,6 +31,13 @@ class LcResult(ctypes.Structure):
                 ("used_symbols", ctypes.c_uint32), ("relaunches", ctypes.c_uint32)]
 
 
+class LcStats(ctypes.Structure):
+    _fields_ = [("sum_sq_err", ctypes.c_double), ("max_abs_err", ctypes.c_double),
+                ("vmin", ctypes.c_double), ("vmax", ctypes.c_double),
+                ("max_identity_dev", ctypes.c_double), ("nonfinite", ctypes.c_int),
+                ("pad", ctypes.c_int)]
+
+
 _vp = ctypes.c_void_p
 _lib = None
 _lib_lock = threading.Lock()
@@ -75,13 +82,16 @@ def library():
         L.lc_phase_ms.restype = ctypes.c_int
         L.lc_launch_count.argtypes = [_vp]
         L.lc_launch_count.restype = ctypes.c_uint64
+        L.lc_error_stats_f64.argtypes = [_vp, _vp, _vp, ctypes.c_uint64, ctypes.c_int, _vp, _vp,
+                                         ctypes.POINTER(LcStats)]
+        L.lc_error_stats_f64.restype = ctypes.c_int
         _lib = L
         return L
 
 
 EXPORTED = ["lc_ctx_create", "lc_ctx_destroy", "lc_last_error", "lc_range_f64", "lc_compress_f64",
             "lc_result_fetch", "lc_result_device", "lc_decompress_f64", "lc_last_device_ms",
-            "lc_phase_ms", "lc_launch_count"]
+            "lc_phase_ms", "lc_launch_count", "lc_error_stats_f64"]
 
 
 class Context:
@@ -111,6 +121,23 @@ class Context:
 
 
 _ctx_local = threading.local()
+
+
+def bind_stream(device, stream_ptr):
+    """Make this thread's context for `device` run on the given CUDA stream
+    (cudaStream_t as int); used by workers that must overlap with the caller."""
+    ctxs = getattr(_ctx_local, "ctxs", None)
+    if ctxs is None:
+        ctxs = _ctx_local.ctxs = {}
+    old = ctxs.get(device)
+    if old is not None and getattr(old, "stream", None) == stream_ptr:
+        return old
+    ctx = Context(device, stream=_vp(stream_ptr))
+    ctx.stream = stream_ptr
+    ctxs[device] = ctx
+    if old is not None:
+        old.close()
+    return ctx
 
 
 def context(device=0):

@@ -39,6 +39,7 @@ struct lc_ctx {
     // scratch
     LcBuf xbuf, codes, hist, desc, counters, bad_end, pe, pe_rec, lengths, cw, gkeys, ifreq,
         parent, cbout, payload, esc_idx, esc_val, encdesc, range_parts, small, pred, tiles;
+    LcBuf st_b, st_pe, st_pr, st_parts;
     // last lc_range_f64 on device data (lets compress skip the anchor pass)
     const void *rng_ptr = nullptr;
     uint64_t rng_n = 0;
@@ -136,7 +137,8 @@ void lc_ctx_destroy(lc_ctx *ctx)
                      &ctx->parent, &ctx->cbout, &ctx->payload, &ctx->esc_idx, &ctx->esc_val,
                      &ctx->encdesc, &ctx->range_parts, &ctx->small, &ctx->pred, &ctx->tiles, &ctx->dec[0], &ctx->dec[1],
                      &ctx->dec[2], &ctx->dec[3], &ctx->dec[4], &ctx->dec[5], &ctx->dec[6],
-                     &ctx->dec[7], &ctx->dec[8], &ctx->dec[9]};
+                     &ctx->dec[7], &ctx->dec[8], &ctx->dec[9], &ctx->st_b, &ctx->st_pe, &ctx->st_pr,
+                     &ctx->st_parts};
     for (LcBuf *b : bufs)
         if (b->p) cudaFree(b->p);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
@@ -191,6 +193,45 @@ int lc_range_f64(lc_ctx *ctx, const double *x, uint64_t n, int x_on_device, doub
     ctx->rng_ptr = x_on_device ? (const void *)x : nullptr;
     ctx->rng_n = n;
     ctx->rng_maxstep = h->maxstep;
+    return 0;
+}
+
+int lc_error_stats_f64(lc_ctx *ctx, const double *original, const double *recon, uint64_t n, int on_device,
+                       const double *pe, const double *pe_rec, lc_stats *out)
+{
+    if (!ctx || !out || n == 0) return 12;
+    cudaStream_t st = ctx->stream;
+    int rc;
+    const double *da = lc_device_input(ctx, original, n, on_device, &rc);
+    if (rc) return rc;
+    auto stage = [&](LcBuf &buf, const double *h, uint64_t cnt) -> const double * {
+        if (on_device || !h) return h;
+        if (lc_reserve(buf, cnt * sizeof(double)) != cudaSuccess) return nullptr;
+        if (cudaMemcpyAsync(buf.p, h, cnt * sizeof(double), cudaMemcpyHostToDevice, st) != cudaSuccess) return nullptr;
+        return (const double *)buf.p;
+    };
+    const double *db = stage(ctx->st_b, recon, n);
+    const bool with_pe = pe && pe_rec && n > 1;
+    const double *dpe = with_pe ? stage(ctx->st_pe, pe, n - 1) : nullptr;
+    const double *dpr = with_pe ? stage(ctx->st_pr, pe_rec, n - 1) : nullptr;
+    if (!db || (with_pe && (!dpe || !dpr))) return lc_fail(ctx, cudaErrorMemoryAllocation, "stats H2D", __FILE__, __LINE__);
+    int nb = (int)((n + 255) / 256);
+    if (nb > 4 * ctx->sm_count) nb = 4 * ctx->sm_count;
+    LC_CUDA_OK(lc_reserve(ctx->st_parts, sizeof(LcStatsPart) * (nb + 1)));
+    LcStatsPart *parts = (LcStatsPart *)ctx->st_parts.p;
+    lc_stats_kernel<<<nb, 256, 0, st>>>(da, db, n, dpe, dpr, parts);
+    lc_stats_final_kernel<<<1, 1, 0, st>>>(parts, nb, parts + nb);
+    ctx->launches += 2;
+    { int _rc = lc_debug_check(ctx, "lc_stats_final_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+    LcStatsPart *h = (LcStatsPart *)ctx->pinned;
+    LC_CUDA_OK(cudaMemcpyAsync(h, parts + nb, sizeof(LcStatsPart), cudaMemcpyDeviceToHost, st));
+    LC_CUDA_OK(cudaStreamSynchronize(st));
+    out->sum_sq_err = h->sum + h->comp;
+    out->max_abs_err = h->maxabs;
+    out->vmin = h->vmin;
+    out->vmax = h->vmax;
+    out->max_identity_dev = with_pe ? h->dev : -1.0;
+    out->nonfinite = h->nonfinite;
     return 0;
 }
 

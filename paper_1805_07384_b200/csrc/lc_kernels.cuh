@@ -49,6 +49,17 @@ struct LcCodebookOut {
     unsigned long long stamp[6];   // phase timestamps (globaltimer, diagnostics)
 };
 
+struct LcStatsPart {
+    double sum, comp;        // sum of squared errors (Neumaier: sum + comp)
+    double maxabs, vmin, vmax, dev;
+    int nonfinite;
+    int pad;
+};
+__global__ void lc_stats_kernel(const double *__restrict__ a, const double *__restrict__ b, uint64_t n,
+                                const double *__restrict__ pe, const double *__restrict__ pr,
+                                LcStatsPart *__restrict__ parts);
+__global__ void lc_stats_final_kernel(const LcStatsPart *__restrict__ parts, int np, LcStatsPart *__restrict__ out);
+
 struct LcEncDesc {
     int st;
     int pad;
