@@ -1,0 +1,191 @@
+"""Sharded checkpoints across ranks.
+
+Each rank compresses its own slab of the global vector as an independent
+LCKP0001 block with the reference semantics (per-shard value range), so the
+data path has no collective.  The only exchange is the block metadata:
+an all-gather of (n, payload_bits, n_esc, block_bytes) per rank (32 B), whose
+exclusive scan gives every rank its byte offset in a shared sharded image, so
+all ranks write their blocks concurrently (positional writes, no funnel
+through rank 0).
+
+Sharded image "LCKPSHD1" (little-endian):
+    magic 8 B | u32 version=1 | u32 world | world x (u64 offset, u64 bytes, u64 n)
+    | world concatenated CompressedBlock.to_bytes() blobs
+The blobs are exactly the reference's LCKP0001 bytes (compressor.py:251-266).
+
+Works with any torch.distributed backend: NCCL (CUDA tensors) on the GPU
+path, gloo (CPU tensors) in the CPU tests.
+"""
+
+from __future__ import annotations
+
+import os
+import struct
+from dataclasses import dataclass
+from typing import Optional, Tuple
+
+import numpy as np
+
+from .compressor import CompressedBlock
+from .errors import IntegrityError, ParameterError
+
+SHARD_MAGIC = b"LCKPSHD1"
+SHARD_VERSION = 1
+_SHD_HEAD = "<II"
+_SHD_ENTRY = "<QQQ"
+
+
+def shard_bounds(n_total: int, world: int, rank: int) -> Tuple[int, int]:
+    """[lo, hi) of rank's slab: contiguous, sizes differ by at most one element
+    (the first n_total % world ranks take one more)."""
+    if world < 1 or not 0 <= rank < world or n_total < 0:
+        raise ParameterError("invalid shard request")
+    base, extra = divmod(n_total, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+@dataclass(frozen=True)
+class ShardLayout:
+    """Per-rank block sizes and offsets inside the sharded image."""
+
+    n: Tuple[int, ...]
+    payload_bits: Tuple[int, ...]
+    n_esc: Tuple[int, ...]
+    nbytes: Tuple[int, ...]
+    offsets: Tuple[int, ...]            # absolute byte offsets of each rank's blob
+    total_bytes: int
+
+    @property
+    def world(self) -> int:
+        return len(self.n)
+
+
+def header_bytes(world: int) -> int:
+    return len(SHARD_MAGIC) + struct.calcsize(_SHD_HEAD) + world * struct.calcsize(_SHD_ENTRY)
+
+
+def layout_from_meta(meta: np.ndarray) -> ShardLayout:
+    """meta: [world, 4] int64 rows (n, payload_bits, n_esc, block_bytes) -> layout
+    (exclusive scan of block sizes after the header)."""
+    meta = np.asarray(meta, dtype=np.int64).reshape(-1, 4)
+    world = meta.shape[0]
+    sizes = meta[:, 3]
+    offs = header_bytes(world) + np.concatenate([[0], np.cumsum(sizes)[:-1]])
+    return ShardLayout(tuple(int(v) for v in meta[:, 0]), tuple(int(v) for v in meta[:, 1]),
+                       tuple(int(v) for v in meta[:, 2]), tuple(int(v) for v in sizes),
+                       tuple(int(v) for v in offs), int(header_bytes(world) + sizes.sum()))
+
+
+def block_meta(block: CompressedBlock, blob: Optional[bytes] = None) -> np.ndarray:
+    nbytes = len(blob) if blob is not None else block.nbytes
+    return np.array([block.n, block.payload_bits, len(block.escape_indices), nbytes], dtype=np.int64)
+
+
+def gather_layout(local_meta: np.ndarray, group=None, device=None) -> ShardLayout:
+    """All-gather every rank's (n, payload_bits, n_esc, block_bytes): the one
+    collective of the sharded path."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    dev = device if device is not None else ("cuda" if dist.get_backend(group) == "nccl" else "cpu")
+    t = torch.as_tensor(np.asarray(local_meta, dtype=np.int64), device=dev)
+    out = torch.empty(world * 4, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(out, t, group=group)
+    return layout_from_meta(out.cpu().numpy().reshape(world, 4))
+
+
+def max_over_ranks(value: float, group=None, device=None) -> float:
+    """Max of a per-rank scalar (timings are reported as the slowest rank)."""
+    import torch
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return float(value)
+    dev = device if device is not None else ("cuda" if dist.get_backend(group) == "nccl" else "cpu")
+    t = torch.tensor([float(value)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())
+
+
+def encode_header(layout: ShardLayout) -> bytes:
+    out = [SHARD_MAGIC, struct.pack(_SHD_HEAD, SHARD_VERSION, layout.world)]
+    for off, nb, n in zip(layout.offsets, layout.nbytes, layout.n):
+        out.append(struct.pack(_SHD_ENTRY, off, nb, n))
+    return b"".join(out)
+
+
+def decode_header(blob: bytes) -> ShardLayout:
+    head = len(SHARD_MAGIC) + struct.calcsize(_SHD_HEAD)
+    if len(blob) < head or blob[:8] != SHARD_MAGIC:
+        raise IntegrityError("not a sharded checkpoint image (bad magic)")
+    version, world = struct.unpack_from(_SHD_HEAD, blob, 8)
+    if version != SHARD_VERSION or world < 1:
+        raise IntegrityError(f"unsupported sharded image version {version} / world {world}")
+    need = header_bytes(world)
+    if len(blob) < need:
+        raise IntegrityError("truncated sharded image header")
+    ents = [struct.unpack_from(_SHD_ENTRY, blob, head + i * struct.calcsize(_SHD_ENTRY)) for i in range(world)]
+    offs = tuple(e[0] for e in ents)
+    sizes = tuple(e[1] for e in ents)
+    ns = tuple(e[2] for e in ents)
+    expect = need
+    for o, s in zip(offs, sizes):
+        if o != expect:
+            raise IntegrityError("sharded image offsets are not contiguous")
+        expect += s
+    return ShardLayout(ns, (0,) * world, (0,) * world, sizes, offs, expect)
+
+
+def write_shard(path, rank: int, blob: bytes, layout: ShardLayout) -> None:
+    """Positional write of this rank's blob (rank 0 also writes the header).
+    Every rank opens the same file; no data moves between ranks."""
+    if len(blob) != layout.nbytes[rank]:
+        raise ParameterError("blob size disagrees with the gathered layout")
+    fd = os.open(str(path), os.O_WRONLY | os.O_CREAT, 0o644)
+    try:
+        if rank == 0:
+            os.pwrite(fd, encode_header(layout), 0)
+        os.pwrite(fd, blob, layout.offsets[rank])
+    finally:
+        os.close(fd)
+
+
+def read_shard(path, rank: int) -> CompressedBlock:
+    with open(path, "rb") as f:
+        head = f.read(len(SHARD_MAGIC) + struct.calcsize(_SHD_HEAD))
+        if len(head) < len(SHARD_MAGIC) + 8:
+            raise IntegrityError("truncated sharded image")
+        world = struct.unpack_from(_SHD_HEAD, head, 8)[1]
+        f.seek(0)
+        layout = decode_header(f.read(header_bytes(world)))
+        if not 0 <= rank < layout.world:
+            raise ParameterError(f"rank {rank} not in image of {layout.world} shards")
+        f.seek(layout.offsets[rank])
+        blob = f.read(layout.nbytes[rank])
+    if len(blob) != layout.nbytes[rank]:
+        raise IntegrityError("sharded image truncated")
+    blk = CompressedBlock.from_bytes(blob)
+    if blk.n != layout.n[rank]:
+        raise IntegrityError("shard length disagrees with the header")
+    return blk
+
+
+def checkpoint_sharded(x_local, config, path, group=None) -> Tuple[CompressedBlock, ShardLayout]:
+    """Compress this rank's slab on its GPU, gather the layout, write the blob."""
+    import torch.distributed as dist
+    from .compressor import compress
+    rank = dist.get_rank(group)
+    block = compress(x_local, config)
+    blob = block.to_bytes()
+    layout = gather_layout(block_meta(block, blob), group=group)
+    write_shard(path, rank, blob, layout)
+    dist.barrier(group=group)
+    return block, layout
+
+
+def restore_sharded(path, group=None, device=None):
+    """Decompress this rank's slab from a sharded image (device tensor when `device`)."""
+    import torch.distributed as dist
+    from .compressor import decompress
+    return decompress(read_shard(path, dist.get_rank(group)), device=device)
+
