@@ -233,3 +233,21 @@ __device__ __forceinline__ void lc_mbar_wait(unsigned long long *bar, unsigned p
                      : "=r"(ok) : "r"(b), "r"(phase) : "memory");
     } while (!ok);
 }
+
+// Inclusive scan (in place) of nw <= 32 per-warp map aggregates by warp 0
+// (log2(nw) shuffle levels instead of a sequential loop); call from all
+// threads between two __syncthreads().
+__device__ __forceinline__ void lc_scan_warp_maps(OffMap *agg, int nw)
+{
+    if ((threadIdx.x >> 5) == 0) {
+        const int lane = threadIdx.x & 31;
+        OffMap v = lane < nw ? agg[lane] : lc_map_neutral();
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            if (o >= nw) break;
+            const OffMap up = lc_shfl_up_map(v, o);
+            if (lane >= o) v = lc_map_compose(v, up);
+        }
+        if (lane < nw) agg[lane] = v;
+    }
+}

@@ -760,19 +760,54 @@ struct LcRecSplit {
     LcChunkPred pred;         // RA -> RB
 };
 
+// This thread's chunk codes (32 consecutive) with 16-byte loads; the tail
+// chunk falls back to scalar loads.  v[j] = code j (0 past the end).
+__device__ __forceinline__ void lc_load_chunk_codes(const LcRecParams &P, long long p0, int len, uint32_t (&v)[LC_L])
+{
+    if (len == LC_L) {
+        if (P.code_bytes == 2) {
+            const uint4 *src = reinterpret_cast<const uint4 *>(reinterpret_cast<const uint16_t *>(P.codes) + p0);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint4 q = __ldg(src + k);
+                const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    v[8 * k + 2 * h] = w4[h] & 0xffffu;
+                    v[8 * k + 2 * h + 1] = w4[h] >> 16;
+                }
+            }
+        } else {
+            const uint4 *src = reinterpret_cast<const uint4 *>(reinterpret_cast<const uint32_t *>(P.codes) + p0);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint4 q = __ldg(src + k);
+                v[4 * k] = q.x; v[4 * k + 1] = q.y; v[4 * k + 2] = q.z; v[4 * k + 3] = q.w;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < LC_L; ++j) {
+            uint32_t c = 0;
+            if (j < len) c = P.code_bytes == 2 ? (uint32_t)reinterpret_cast<const uint16_t *>(P.codes)[p0 + j]
+                                               : reinterpret_cast<const uint32_t *>(P.codes)[p0 + j];
+            v[j] = c;
+        }
+    }
+}
+
+// Codes of the tile into padded smem rows (row = this thread's chunk).
 __device__ __forceinline__ void lc_load_codes_tile(const LcRecParams &P, long long pbeg, uint32_t *cs)
 {
     const int tid = threadIdx.x;
     const long long nel = (long long)P.n - 1;
-#pragma unroll 8
-    for (int k = 0; k < LC_L; ++k) {
-        const int off = k * LC_TPB + tid;
-        const long long pos = pbeg + off;
-        uint32_t v = 0;
-        if (pos < nel) v = P.code_bytes == 2 ? (uint32_t)reinterpret_cast<const uint16_t *>(P.codes)[pos]
-                                             : reinterpret_cast<const uint32_t *>(P.codes)[pos];
-        cs[(off >> 5) * LC_ROW + (off & 31)] = v;
-    }
+    const long long p0 = pbeg + (long long)tid * LC_L;
+    const int len = (int)max(0LL, min((long long)LC_L, nel - p0));
+    uint32_t v[LC_L];
+    lc_load_chunk_codes(P, p0, len, v);
+    uint32_t *row = cs + tid * LC_ROW;
+#pragma unroll
+    for (int j = 0; j < LC_L; ++j) row[j] = v[j];
 }
 
 __device__ __forceinline__ LcSegScan lc_chunk_segscan(const uint32_t *crow, int len)
@@ -823,7 +858,6 @@ __device__ __forceinline__ LcSegScan lc_block_segscan(const LcSegScan &mine, LcS
 
 __global__ void __launch_bounds__(LC_TPB) lc_rec0_kernel(LcRecParams P, LcRecSplit S)
 {
-    __shared__ uint32_t cs[LC_TPB * LC_ROW];
     __shared__ LcSegScan wseg[LC_TPB / 32];
     const int tid = threadIdx.x;
     const long long nel = (long long)P.n - 1;
@@ -831,10 +865,18 @@ __global__ void __launch_bounds__(LC_TPB) lc_rec0_kernel(LcRecParams P, LcRecSpl
         const long long cbeg = P.first_chunk + t * LC_TPB;
         const long long c = cbeg + tid;
         const int len = (c < P.nchunks) ? (int)min((long long)LC_L, nel - c * LC_L) : 0;
+        uint32_t v[LC_L];
+        lc_load_chunk_codes(P, c * LC_L, len, v);
+        LcSegScan mine; mine.sum = 0; mine.cnt = 0; mine.has = 0; mine.moved = 0;
+#pragma unroll
+        for (int j = 0; j < LC_L; ++j) {
+            if (j < len) {
+                const uint32_t code = v[j];
+                if (code == 0) { mine.sum = 0; mine.cnt += 1; mine.has = 1; mine.moved = 0; }
+                else { const int64_t mm = lc_code_m(code); mine.sum += mm; mine.moved |= (mm != 0); }
+            }
+        }
         __syncthreads();
-        lc_load_codes_tile(P, cbeg * LC_L, cs);
-        __syncthreads();
-        const LcSegScan mine = lc_chunk_segscan(cs + tid * LC_ROW, len);
         LcSegScan agg;
         lc_block_segscan(mine, wseg, &agg);
         if (tid == 0) S.tile_seg[t] = agg;
@@ -959,8 +1001,7 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_rec_a_kernel(LcRecParams P, LcRe
         }
         if (lane == 31) warp_agg[wid] = inc_map;
         __syncthreads();
-        if (tid == 0)
-            for (int w = 1; w < LC_TPB / 32; ++w) warp_agg[w] = lc_map_compose(warp_agg[w], warp_agg[w - 1]);
+        lc_scan_warp_maps(warp_agg, LC_TPB / 32);
         __syncthreads();
         if (wid > 0) inc_map = lc_map_compose(inc_map, warp_agg[wid - 1]);
         OffMap exc_map = lc_shfl_up_map(inc_map, 1);

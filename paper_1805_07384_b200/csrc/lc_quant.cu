@@ -264,8 +264,7 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_quant_a_kernel(LcQuantParams P)
         }
         if (lane == 31) warp_agg[wid] = inc_map;
         __syncthreads();
-        if (tid == 0)
-            for (int w = 1; w < LC_TPB / 32; ++w) warp_agg[w] = lc_map_compose(warp_agg[w], warp_agg[w - 1]);
+        lc_scan_warp_maps(warp_agg, LC_TPB / 32);
         __syncthreads();
         if (wid > 0) inc_map = lc_map_compose(inc_map, warp_agg[wid - 1]);
         OffMap exc_map = lc_shfl_up_map(inc_map, 1);
@@ -301,8 +300,7 @@ __global__ void __launch_bounds__(1024) lc_map_scan_kernel(const OffMap *__restr
     }
     if (lane == 31) wsum[wid] = inc;
     __syncthreads();
-    if (tid == 0)
-        for (int w = 1; w < 32; ++w) wsum[w] = lc_map_compose(wsum[w], wsum[w - 1]);
+    lc_scan_warp_maps(wsum, 32);
     __syncthreads();
     if (wid > 0) inc = lc_map_compose(inc, wsum[wid - 1]);
     OffMap exc = lc_shfl_up_map(inc, 1);
