@@ -494,6 +494,60 @@ __global__ void __launch_bounds__(LC_DEC_TPB) lc_dec_sync_kernel(LcDecParams P, 
     }
 }
 
+// Boundary fix after the first sync pass: CTA b's first segment was walked
+// from its own base, but the true entry is CTA b-1's exit.  One thread per
+// CTA boundary re-walks that segment from the entry (payload read through
+// L1/L2).  When the new walk reaches the same exit and status, only the
+// segment's start and count change and the CTA is final; otherwise the
+// exit moved, nothing is written and *changed asks the host for the general
+// propagation passes (lc_dec_sync_kernel).
+__global__ void __launch_bounds__(128) lc_dec_fix_kernel(LcDecParams P, LcSeg *__restrict__ seg,
+                                                         const LcBlkOut *__restrict__ bout, int *__restrict__ changed)
+{
+    const long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x + 1;
+    if (b >= P.nblk) return;
+    const unsigned long long t = (unsigned long long)b * LC_DEC_TPB;
+    if (t >= P.nseg) return;
+    const unsigned segb = (unsigned)P.seg_bits;
+    const unsigned long long sbit = t * segb;
+    const unsigned long long ex = bout[b - 1].exit;
+    LcSeg S = seg[t];
+    const unsigned long long cur = S.start == LC_SEG_DEAD ? ~0ull : sbit + S.start;
+    if (ex == cur) return;
+    if (ex == ~0ull) { atomicExch(changed, 1); return; }    // the path ended before this CTA
+    const LcDecTables &T = *P.T;
+    const unsigned bits_rel = lc_bits_rel(P.bits, sbit);
+    LcBitReader<LcGlobSrc> br;
+    br.src.w = P.payload + sbit / 32;
+    br.seek((unsigned)(ex - sbit));
+    int cnt = 0, term = 0;
+    while (br.pos < segb) {
+        if (br.pos >= bits_rel) { term = 4; break; }
+        const unsigned e2 = T.lut2[br.buf >> (64 - LC_LUT_BITS)];
+        int adv = (int)((e2 >> 12) & 15u);
+        unsigned sm = e2 & 0xfffu;
+        if (!e2 || br.pos + (unsigned)adv > bits_rel) {
+            adv = e2 ? 0 : lc_long_len(T, br.buf);
+            if (!adv || br.pos + (unsigned)adv > bits_rel) {
+                uint32_t sym;
+                adv = lc_next_symbol(T, P.sorted, br, bits_rel, &sym, &term);
+                if (!adv) break;
+            }
+            sm = 1u;
+        }
+        const unsigned lim = segb - br.pos;
+        const unsigned inside = lim >= LC_LUT_BITS ? sm : (sm & ((1u << lim) - 1u));
+        cnt += __popc(inside);
+        const unsigned beyond = sm ^ inside;
+        if (beyond) { br.consume(__ffs(beyond) - 1); break; }
+        br.consume(adv);
+    }
+    if (br.pos != S.exit || term != S.term) { atomicExch(changed, 1); return; }
+    S.start = (unsigned short)(ex - sbit);
+    S.count = (unsigned short)cnt;
+    seg[t] = S;
+}
+
 // Device-wide exclusive scan of segment counts (decoupled look-back) and the
 // first anomaly on the decode path.
 struct LcScanDesc { int st; int pad; unsigned long long agg, incl; };
@@ -883,37 +937,62 @@ __global__ void __launch_bounds__(LC_TPB) lc_rec0_kernel(LcRecParams P, LcRecSpl
     }
 }
 
-__global__ void __launch_bounds__(1024) lc_rec0_scan_kernel(LcRecSplit S, long long ntiles, long long anchor_cnt)
+__global__ void __launch_bounds__(512) lc_rec0_scan_kernel(LcRecSplit S, long long ntiles, long long anchor_cnt)
 {
-    // sequential runs per thread + block scan of the runs (LcSegScan is a monoid)
-    __shared__ LcSegScan wsum[32];
+    // rounds of 512 x 8 tiles: loads first (registers), per-thread runs, warp
+    // scan + warp-0 scan of warp sums; LcSegScan is a monoid.  The state
+    // entering each round is carried to the next.
+    constexpr int PER = 8;
+    __shared__ LcSegScan wsum[16];
+    __shared__ LcSegScan s_carry;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const long long per = (ntiles + 1023) / 1024;
-    const long long b0 = (long long)tid * per, b1 = min(ntiles, b0 + per);
-    LcSegScan run; run.sum = 0; run.cnt = 0; run.has = 0; run.moved = 0;
-    for (long long t = b0; t < b1; ++t) run = lc_segscan_op(run, S.tile_seg[t]);
-    LcSegScan inc = run;
+    LcSegScan carry; carry.sum = 0; carry.cnt = anchor_cnt; carry.has = 1; carry.moved = 0;   // launch anchor
+    for (long long r0 = 0; r0 < ntiles; r0 += 512LL * PER) {
+        const long long b0 = r0 + (long long)tid * PER;
+        LcSegScan v[PER];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const LcSegScan up = lc_shfl_up_seg(inc, o);
-        if (lane >= o) inc = lc_segscan_op(up, inc);
-    }
-    if (lane == 31) wsum[wid] = inc;
-    __syncthreads();
-    if (tid == 0)
-        for (int w = 1; w < 32; ++w) wsum[w] = lc_segscan_op(wsum[w - 1], wsum[w]);
-    __syncthreads();
-    if (wid > 0) inc = lc_segscan_op(wsum[wid - 1], inc);
-    LcSegScan exc = lc_shfl_up_seg(inc, 1);
-    if (lane == 0) {
-        if (wid > 0) exc = wsum[wid - 1];
-        else { exc.sum = 0; exc.cnt = 0; exc.has = 0; exc.moved = 0; }
-    }
-    LcSegScan st; st.sum = 0; st.cnt = anchor_cnt; st.has = 1; st.moved = 0;   // launch anchor
-    st = lc_segscan_op(st, exc);
-    for (long long t = b0; t < b1; ++t) {
-        S.tile_in[t] = st;
-        st = lc_segscan_op(st, S.tile_seg[t]);
+        for (int k = 0; k < PER; ++k) {
+            if (b0 + k < ntiles) v[k] = S.tile_seg[b0 + k];
+            else { v[k].sum = 0; v[k].cnt = 0; v[k].has = 0; v[k].moved = 0; }
+        }
+        LcSegScan inc = v[0];
+#pragma unroll
+        for (int k = 1; k < PER; ++k) inc = lc_segscan_op(inc, v[k]);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const LcSegScan up = lc_shfl_up_seg(inc, o);
+            if (lane >= o) inc = lc_segscan_op(up, inc);
+        }
+        if (lane == 31) wsum[wid] = inc;
+        __syncthreads();
+        if (wid == 0) {
+            LcSegScan w;
+            if (lane < 16) w = wsum[lane];
+            else { w.sum = 0; w.cnt = 0; w.has = 0; w.moved = 0; }
+#pragma unroll
+            for (int o = 1; o < 16; o <<= 1) {
+                const LcSegScan up = lc_shfl_up_seg(w, o);
+                if (lane >= o) w = lc_segscan_op(up, w);
+            }
+            if (lane < 16) wsum[lane] = w;
+        }
+        __syncthreads();
+        if (wid > 0) inc = lc_segscan_op(wsum[wid - 1], inc);
+        LcSegScan exc = lc_shfl_up_seg(inc, 1);
+        if (lane == 0) {
+            if (wid > 0) exc = wsum[wid - 1];
+            else { exc.sum = 0; exc.cnt = 0; exc.has = 0; exc.moved = 0; }
+        }
+        LcSegScan st = lc_segscan_op(carry, exc);
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            if (b0 + k < ntiles) S.tile_in[b0 + k] = st;
+            st = lc_segscan_op(st, v[k]);
+        }
+        if (tid == 511) s_carry = st;
+        __syncthreads();
+        carry = s_carry;
+        __syncthreads();
     }
 }
 
@@ -1210,7 +1289,17 @@ int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_valu
     { int _rc = lc_debug_check(ctx, "lc_dec_sync_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
     lc_count_launch(ctx, 1);
     LcBlkOut *bprev = bo_a, *bcur = bo_b;
-    for (int it = 0; nblk > 1 && it < 1000000; ++it) {
+    bool general = false;
+    if (nblk > 1) {                                     // boundary fix; general passes only on a cascade
+        LC_CUDA_OK(cudaMemsetAsync(changed, 0, 4, st));
+        lc_dec_fix_kernel<<<(int)((nblk - 1 + 127) / 128), 128, 0, st>>>(DP, segs, bo_a, changed);
+        { int _rc = lc_debug_check(ctx, "lc_dec_fix_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+        lc_count_launch(ctx, 1);
+        LC_CUDA_OK(cudaMemcpyAsync(hchanged, changed, 4, cudaMemcpyDeviceToHost, st));
+        LC_CUDA_OK(cudaStreamSynchronize(st));
+        general = *hchanged != 0;
+    }
+    for (int it = 0; general && it < 1000000; ++it) {
         LC_CUDA_OK(cudaMemsetAsync(changed, 0, 4, st));
         sync_launch(bprev, bcur, 0);
         { int _rc = lc_debug_check(ctx, "lc_dec_sync_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
@@ -1321,7 +1410,7 @@ int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_valu
         LC_CUDA_OK(cudaMemsetAsync(R.first_bad, 0xff, 8, st));
         const int grid = (int)(R.ntiles < grid_cap ? R.ntiles : grid_cap);
         lc_rec0_kernel<<<(int)(R.ntiles < 3 * grid_cap ? R.ntiles : 3 * grid_cap), LC_TPB, 0, st>>>(R, RS);
-        lc_rec0_scan_kernel<<<1, 1024, 0, st>>>(RS, R.ntiles, R.anchor_cnt);
+        lc_rec0_scan_kernel<<<1, 512, 0, st>>>(RS, R.ntiles, R.anchor_cnt);
         lc_rec_a_kernel<<<(int)(R.ntiles < 3 * lc_sm_count(ctx) ? R.ntiles : 3 * lc_sm_count(ctx)), LC_TPB,
                           lc_rec_a_smem_bytes(), st>>>(R, RS);
         { int _rc = lc_debug_check(ctx, "lc_rec_a_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
