@@ -624,17 +624,25 @@ __global__ void __launch_bounds__(LC_DEC_TPB) lc_dec_write_kernel(LcDecParams P,
                                                                  unsigned long long *__restrict__ end_pos, int cap)
 {
     __shared__ LcDecTables Ts;
+    __shared__ unsigned long long s_bar;
     extern __shared__ __align__(16) unsigned char s_dyn[];
-    lc_load_tables(Ts, P.T);
     constexpr int VEC = 16 / sizeof(CodeT);
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    CodeT *stage = reinterpret_cast<CodeT *>(s_dyn) + (size_t)wid * (cap + 2 * VEC + 16);
-    CodeT *gout = reinterpret_cast<CodeT *>(out);
-    const unsigned long long nwt = (P.nseg + 31) / 32;
-    const unsigned long long nwarps = (unsigned long long)gridDim.x * (blockDim.x >> 5);
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const unsigned segb = (unsigned)P.seg_bits;
-    for (unsigned long long wt = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + wid; wt < nwt; wt += nwarps) {
-        const unsigned long long t = wt * 32 + lane;
+    const int nw_stage = LC_DEC_TPB * (int)(segb / 32) + LC_DEC_STAGE_PAD;    // payload words per CTA range
+    uint32_t *s_words = reinterpret_cast<uint32_t *>(s_dyn);
+    CodeT *stage = reinterpret_cast<CodeT *>(s_dyn + (size_t)nw_stage * 4) + (size_t)wid * (cap + 2 * VEC + 16);
+    CodeT *gout = reinterpret_cast<CodeT *>(out);
+    if (tid == 0) lc_mbar_init(&s_bar, 1);
+    unsigned phase = 0;
+    lc_load_tables(Ts, P.T);
+    const int max_len = Ts.max_len;
+    LcSmemSrc src;
+    src.w = s_words;
+    for (long long b = blockIdx.x; b < P.nblk; b += gridDim.x) {
+        const unsigned long long cbit = (unsigned long long)b * LC_DEC_TPB * segb;
+        if (tid == 0) lc_bulk_load(s_words, P.payload + cbit / 32, (unsigned)(nw_stage * 4), &s_bar);
+        const unsigned long long t = (unsigned long long)b * LC_DEC_TPB + tid;
         unsigned long long o = 0;
         unsigned todo = 0;
         LcSeg S0;
@@ -646,91 +654,94 @@ __global__ void __launch_bounds__(LC_DEC_TPB) lc_dec_write_kernel(LcDecParams P,
         }
         if (o >= m) todo = 0;
         else if ((unsigned long long)todo > m - o) todo = (unsigned)(m - o);
+        const unsigned bits_rel = lc_bits_rel(P.bits, cbit);
+        lc_mbar_wait(&s_bar, phase);
+        phase ^= 1u;
         const unsigned long long wlo = __shfl_sync(0xffffffffu, o, 0);
         // warp-relative output slots (a warp covers <= 32 * 1024 symbols)
         unsigned orel = (unsigned)(o - wlo), whi = todo ? orel + todo : 0u;
         whi = __reduce_max_sync(0xffffffffu, whi);
-        if (!whi) continue;
-        const int a = (int)(wlo & (VEC - 1));
-        const bool last = todo && o + todo == m;
-        // segment-relative bit positions
-        const unsigned long long sbit = t * (unsigned long long)segb;
-        const unsigned bits_rel = lc_bits_rel(P.bits, sbit);
-        LcBitReader<LcGlobSrc> br;
-        br.src.w = P.payload + sbit / 32;
-        if (todo) br.seek(S0.start);
-        for (unsigned wb = 0; wb < whi; wb += (unsigned)cap) {
-            const unsigned wend = wb + (unsigned)cap;
-            CodeT *st0 = stage + a - wb;
-            while (todo && orel < wend) {
-                CodeT *dst = st0 + orel;
-                const unsigned w12 = (unsigned)(br.buf >> (64 - LC_LUT_BITS));
-                const unsigned e1 = Ts.lut[w12];
-                const unsigned e2 = Ts.lut2[w12];
-                const unsigned n2 = e2 >> 16;
-                const unsigned L2 = (e2 >> 12) & 15u;
-                const bool fits = br.pos + L2 <= bits_rel;
-                if (n2 >= 2 && n2 <= todo && fits) {
-                    // several codewords in the next 12 bits; the first is e1
-                    dst[0] = (CodeT)(e1 & 0xffffffu);
-                    unsigned sm = (e2 & 0xfffu) & ((e2 & 0xfffu) - 1u);
-                    int k = 1;
-                    do {
-                        const int i = __ffs(sm) - 1;
-                        sm &= sm - 1;
-                        dst[k++] = (CodeT)(Ts.lut[(w12 << i) & ((1u << LC_LUT_BITS) - 1)] & 0xffffffu);
-                    } while (sm);
-                    br.consume((int)L2);
-                    orel += n2;
-                    todo -= n2;
-                } else {
-                    uint32_t sym;
-                    int l;
-                    if (e2 && fits) {                        // one codeword of <= 12 bits
-                        sym = e1 & 0xffffffu;
-                        l = (int)(e1 >> 24);
+        if (whi) {
+            const int a = (int)(wlo & (VEC - 1));
+            const bool last = todo && o + todo == m;
+            LcBitReader<LcSmemSrc> br;
+            br.src = src;
+            if (todo) br.seek(tid * segb + S0.start);
+            for (unsigned wb = 0; wb < whi; wb += (unsigned)cap) {
+                const unsigned wend = wb + (unsigned)cap;
+                CodeT *st0 = stage + a - wb;
+                while (todo && orel < wend) {
+                    CodeT *dst = st0 + orel;
+                    const unsigned w12 = (unsigned)(br.buf >> (64 - LC_LUT_BITS));
+                    const unsigned e1 = Ts.lut[w12];
+                    const unsigned e2 = Ts.lut2[w12];
+                    const unsigned n2 = e2 >> 16;
+                    const unsigned L2 = (e2 >> 12) & 15u;
+                    const bool fits = br.pos + L2 <= bits_rel;
+                    if (n2 >= 2 && n2 <= todo && fits) {
+                        // several codewords in the next 12 bits; the first is e1
+                        dst[0] = (CodeT)(e1 & 0xffffffu);
+                        unsigned sm = (e2 & 0xfffu) & ((e2 & 0xfffu) - 1u);
+                        int k = 1;
+                        do {
+                            const int i = __ffs(sm) - 1;
+                            sm &= sm - 1;
+                            dst[k++] = (CodeT)(Ts.lut[(w12 << i) & ((1u << LC_LUT_BITS) - 1)] & 0xffffffu);
+                        } while (sm);
+                        br.consume((int)L2);
+                        orel += n2;
+                        todo -= n2;
                     } else {
-                        l = e2 ? 0 : lc_long_len(Ts, br.buf);
-                        if (l && br.pos + (unsigned)l <= bits_rel) {
-                            const unsigned long long v = (br.buf >> 32) >> (32 - l);
-                            sym = __ldg(P.sorted + Ts.offset[l] + (v - Ts.first_code[l]));
+                        uint32_t sym;
+                        int l;
+                        if (e2 && fits) {                        // one codeword of <= 12 bits
+                            sym = e1 & 0xffffffu;
+                            l = (int)(e1 >> 24);
                         } else {
-                            int term = 0;
-                            l = lc_next_symbol(Ts, P.sorted, br, bits_rel, &sym, &term);
-                            if (!l) { todo = 0; break; }     // cannot happen on the converged path
+                            l = e2 ? 0 : lc_long_len(Ts, br.buf);
+                            if (l && br.pos + (unsigned)l <= bits_rel) {
+                                const unsigned long long v = (br.buf >> 32) >> (32 - l);
+                                sym = __ldg(P.sorted + Ts.offset[l] + (v - Ts.first_code[l]));
+                            } else {
+                                int term = 0;
+                                l = lc_next_symbol(Ts, P.sorted, br, bits_rel, &sym, &term);
+                                if (!l) { todo = 0; break; }     // cannot happen on the converged path
+                            }
                         }
+                        dst[0] = (CodeT)sym;
+                        br.consume(l);
+                        ++orel;
+                        --todo;
                     }
-                    dst[0] = (CodeT)sym;
-                    br.consume(l);
-                    ++orel;
-                    --todo;
+                    if (last && !todo) *end_pos = cbit + br.pos;
                 }
-                if (last && !todo) *end_pos = sbit + br.pos;
-            }
-            __syncwarp();
-            const unsigned len = whi - wb < (unsigned)cap ? whi - wb : (unsigned)cap;
-            const int tot = a + (int)len;
-            CodeT *g = gout + (wlo + wb - a);
-            for (int i0 = lane * VEC; i0 < tot; i0 += 32 * VEC) {
-                if (i0 >= a && i0 + VEC <= tot) {
-                    *reinterpret_cast<uint4 *>(g + i0) = *reinterpret_cast<const uint4 *>(stage + i0);
-                } else {
+                __syncwarp();
+                const unsigned len = whi - wb < (unsigned)cap ? whi - wb : (unsigned)cap;
+                const int tot = a + (int)len;
+                CodeT *g = gout + (wlo + wb - a);
+                for (int i0 = lane * VEC; i0 < tot; i0 += 32 * VEC) {
+                    if (i0 >= a && i0 + VEC <= tot) {
+                        *reinterpret_cast<uint4 *>(g + i0) = *reinterpret_cast<const uint4 *>(stage + i0);
+                    } else {
 #pragma unroll
-                    for (int k = 0; k < VEC; ++k)
-                        if (i0 + k >= a && i0 + k < tot) g[i0 + k] = stage[i0 + k];
+                        for (int k = 0; k < VEC; ++k)
+                            if (i0 + k >= a && i0 + k < tot) g[i0 + k] = stage[i0 + k];
+                    }
                 }
+                __syncwarp();
+                if (len == (unsigned)cap && lane < 16) stage[a + lane] = stage[a + cap + lane];
+                __syncwarp();
             }
-            __syncwarp();
-            if (len == (unsigned)cap && lane < 16) stage[a + lane] = stage[a + cap + lane];
-            __syncwarp();
         }
+        __syncthreads();                                 // payload stage is reused by the next range
     }
 }
 
-static size_t lc_dec_write_smem(int cap, int code_bytes)
+static size_t lc_dec_write_smem(int cap, int code_bytes, int seg_bits)
 {
     const int vec = 16 / code_bytes;
-    return (size_t)(LC_DEC_TPB / 32) * (size_t)(cap + 2 * vec + 16) * code_bytes;
+    return sizeof(uint32_t) * (size_t)(LC_DEC_TPB * (seg_bits / 32) + LC_DEC_STAGE_PAD)
+         + (size_t)(LC_DEC_TPB / 32) * (size_t)(cap + 2 * vec + 16) * code_bytes;
 }
 
 // Resolve the reference status (huffman.py:114-132) from the segment walk.
@@ -1327,9 +1338,8 @@ int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_valu
         cap = (cap + 63) / 64 * 64;
         if (cap < 256) cap = 256;
         if (cap > 4096) cap = 4096;
-        const size_t wsm = lc_dec_write_smem((int)cap, code_bytes);
-        const unsigned long long wb = (nseg + LC_DEC_TPB - 1) / LC_DEC_TPB;
-        const int wgrid = (int)(wb < (unsigned long long)(4 * lc_sm_count(ctx)) ? wb : 4 * lc_sm_count(ctx));
+        const size_t wsm = lc_dec_write_smem((int)cap, code_bytes, seg_bits);
+        const int wgrid = (int)(nblk < (long long)(2 * lc_sm_count(ctx)) ? nblk : 2 * lc_sm_count(ctx));
         if (code_bytes == 2) {
             LC_CUDA_OK(cudaFuncSetAttribute(lc_dec_write_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
             lc_dec_write_kernel<uint16_t><<<wgrid, LC_DEC_TPB, wsm, st>>>(DP, segs, offs, bcodes.p, m, endpos, (int)cap);
