@@ -617,6 +617,15 @@ __global__ void __launch_bounds__(LC_TPB) lc_dec_scan_kernel(const LcSeg *__rest
 // window to global memory with 16-byte stores.  Ranges longer than the window
 // take several rounds (lanes pause at the window end; the <= 11 symbols a
 // step spills past it move to the front of the next window).
+// words of one warp's padded output window: cap + spill (16) + head (< 8)
+// codes, plus one padding word per 32
+__host__ __device__ inline int lc_dec_stage_words(int cap, int code_bytes)
+{
+    const int epw = 4 / code_bytes;
+    const int words = (cap + 16 + 8 + epw - 1) / epw + 4;
+    return words + words / 32 + 2;
+}
+
 template <typename CodeT>
 __global__ void __launch_bounds__(LC_DEC_TPB) lc_dec_write_kernel(LcDecParams P, const LcSeg *__restrict__ seg,
                                                                  const unsigned long long *__restrict__ off,
@@ -626,12 +635,17 @@ __global__ void __launch_bounds__(LC_DEC_TPB) lc_dec_write_kernel(LcDecParams P,
     __shared__ LcDecTables Ts;
     __shared__ unsigned long long s_bar;
     extern __shared__ __align__(16) unsigned char s_dyn[];
-    constexpr int VEC = 16 / sizeof(CodeT);
+    constexpr int EPW = 4 / sizeof(CodeT);              // codes per 32-bit word
+    constexpr int VEC = 16 / sizeof(CodeT);             // codes per 16-byte store
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const unsigned segb = (unsigned)P.seg_bits;
     const int nw_stage = LC_DEC_TPB * (int)(segb / 32) + LC_DEC_STAGE_PAD;    // payload words per CTA range
     uint32_t *s_words = reinterpret_cast<uint32_t *>(s_dyn);
-    CodeT *stage = reinterpret_cast<CodeT *>(s_dyn + (size_t)nw_stage * 4) + (size_t)wid * (cap + 2 * VEC + 16);
+    // per-warp window, one padding word after every 32 words: the lanes' write
+    // streams start ~segment-size apart, which without padding falls on few banks
+    const int stage_words = lc_dec_stage_words(cap, (int)sizeof(CodeT));
+    uint32_t *stagew = reinterpret_cast<uint32_t *>(s_dyn + (size_t)nw_stage * 4) + (size_t)wid * stage_words;
+    CodeT *stage = reinterpret_cast<CodeT *>(stagew);
     CodeT *gout = reinterpret_cast<CodeT *>(out);
     if (tid == 0) lc_mbar_init(&s_bar, 1);
     unsigned phase = 0;
@@ -669,9 +683,12 @@ __global__ void __launch_bounds__(LC_DEC_TPB) lc_dec_write_kernel(LcDecParams P,
             if (todo) br.seek(tid * segb + S0.start);
             for (unsigned wb = 0; wb < whi; wb += (unsigned)cap) {
                 const unsigned wend = wb + (unsigned)cap;
-                CodeT *st0 = stage + a - wb;
                 while (todo && orel < wend) {
-                    CodeT *dst = st0 + orel;
+                    const unsigned p0 = a + (orel - wb);         // logical window index
+                    auto put = [&](int k, uint32_t v) {
+                        const unsigned p = p0 + k;
+                        stage[p + EPW * (p / (32 * EPW))] = (CodeT)v;
+                    };
                     const unsigned w12 = (unsigned)(br.buf >> (64 - LC_LUT_BITS));
                     const unsigned e1 = Ts.lut[w12];
                     const unsigned e2 = Ts.lut2[w12];
@@ -679,15 +696,21 @@ __global__ void __launch_bounds__(LC_DEC_TPB) lc_dec_write_kernel(LcDecParams P,
                     const unsigned L2 = (e2 >> 12) & 15u;
                     const bool fits = br.pos + L2 <= bits_rel;
                     if (n2 >= 2 && n2 <= todo && fits) {
-                        // several codewords in the next 12 bits; the first is e1
-                        dst[0] = (CodeT)(e1 & 0xffffffu);
+                        // several codewords in the next 12 bits; the first is e1.  All
+                        // table reads are issued unconditionally (independent), only the
+                        // stores are predicated, so their latencies overlap.
+                        put(0, e1 & 0xffffffu);
                         unsigned sm = (e2 & 0xfffu) & ((e2 & 0xfffu) - 1u);
-                        int k = 1;
-                        do {
-                            const int i = __ffs(sm) - 1;
+                        uint32_t sy[LC_LUT_BITS - 1];
+#pragma unroll
+                        for (int k = 0; k < LC_LUT_BITS - 1; ++k) {
+                            const int i = __ffs(sm) - 1;           // -1 once exhausted
                             sm &= sm - 1;
-                            dst[k++] = (CodeT)(Ts.lut[(w12 << i) & ((1u << LC_LUT_BITS) - 1)] & 0xffffffu);
-                        } while (sm);
+                            sy[k] = Ts.lut[(w12 << (i & 15)) & ((1u << LC_LUT_BITS) - 1)];
+                        }
+#pragma unroll
+                        for (int k = 0; k < LC_LUT_BITS - 1; ++k)
+                            if (k + 1 < (int)n2) put(k + 1, sy[k] & 0xffffffu);
                         br.consume((int)L2);
                         orel += n2;
                         todo -= n2;
@@ -708,7 +731,7 @@ __global__ void __launch_bounds__(LC_DEC_TPB) lc_dec_write_kernel(LcDecParams P,
                                 if (!l) { todo = 0; break; }     // cannot happen on the converged path
                             }
                         }
-                        dst[0] = (CodeT)sym;
+                        put(0, sym);
                         br.consume(l);
                         ++orel;
                         --todo;
@@ -717,19 +740,33 @@ __global__ void __launch_bounds__(LC_DEC_TPB) lc_dec_write_kernel(LcDecParams P,
                 }
                 __syncwarp();
                 const unsigned len = whi - wb < (unsigned)cap ? whi - wb : (unsigned)cap;
-                const int tot = a + (int)len;
-                CodeT *g = gout + (wlo + wb - a);
-                for (int i0 = lane * VEC; i0 < tot; i0 += 32 * VEC) {
-                    if (i0 >= a && i0 + VEC <= tot) {
-                        *reinterpret_cast<uint4 *>(g + i0) = *reinterpret_cast<const uint4 *>(stage + i0);
+                const int tot = a + (int)len;                     // logical elements in the window
+                CodeT *g = gout + (wlo + wb - a);                 // word aligned
+                const int nchunks = (tot + VEC - 1) / VEC;        // 16-byte chunks of the window
+                for (int c = lane; c < nchunks; c += 32) {
+                    uint32_t v[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int w = 4 * c + k;
+                        v[k] = stagew[w + (w >> 5)];
+                    }
+                    if (c * VEC >= a && c * VEC + VEC <= tot) {
+                        *reinterpret_cast<uint4 *>(g + c * VEC) = make_uint4(v[0], v[1], v[2], v[3]);
                     } else {
 #pragma unroll
-                        for (int k = 0; k < VEC; ++k)
-                            if (i0 + k >= a && i0 + k < tot) g[i0 + k] = stage[i0 + k];
+                        for (int k = 0; k < VEC; ++k) {
+                            const int i = c * VEC + k;
+                            if (i >= a && i < tot) g[i] = (CodeT)(v[k / EPW] >> (8 * sizeof(CodeT) * (k % EPW)));
+                        }
                     }
                 }
                 __syncwarp();
-                if (len == (unsigned)cap && lane < 16) stage[a + lane] = stage[a + cap + lane];
+                if (len == (unsigned)cap) {                       // spill (< 12 codes) to the front
+                    for (int k = lane; k < 16; k += 32) {
+                        const unsigned ps = a + cap + k, pd = a + k;
+                        stage[pd + EPW * (pd / (32 * EPW))] = stage[ps + EPW * (ps / (32 * EPW))];
+                    }
+                }
                 __syncwarp();
             }
         }
@@ -739,9 +776,8 @@ __global__ void __launch_bounds__(LC_DEC_TPB) lc_dec_write_kernel(LcDecParams P,
 
 static size_t lc_dec_write_smem(int cap, int code_bytes, int seg_bits)
 {
-    const int vec = 16 / code_bytes;
     return sizeof(uint32_t) * (size_t)(LC_DEC_TPB * (seg_bits / 32) + LC_DEC_STAGE_PAD)
-         + (size_t)(LC_DEC_TPB / 32) * (size_t)(cap + 2 * vec + 16) * code_bytes;
+         + sizeof(uint32_t) * (size_t)(LC_DEC_TPB / 32) * lc_dec_stage_words(cap, code_bytes);
 }
 
 // Resolve the reference status (huffman.py:114-132) from the segment walk.
