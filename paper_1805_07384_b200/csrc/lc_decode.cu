@@ -1087,7 +1087,7 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_rec_a_kernel(LcRecParams P, LcRe
             LcEvents E;
             lc_events_init(E, g0);
             bool pend = false;
-            double pr = 0.0, pc = 0.0, prn = 0.0;
+            double pr = g0, pc = 0.0, prn = g0;        // first call is a no-op step at g0
             for (int j = 0; j < len; ++j) {
                 const uint32_t code = crow[j];
                 const bool esc = code == 0;

@@ -68,16 +68,24 @@ __device__ __forceinline__ void lc_codebook_body(const uint32_t *__restrict__ hi
     while (npow2 < k) npow2 <<= 1;
     // 1b. compaction in symbol order (warp ranges, ballot ranks)
     int wpos = wbase;
-    for (uint32_t s0 = wsb; s0 < wse; s0 += 32) {
-        const uint32_t sy = s0 + lane;
-        const uint32_t h = sy < wse ? __ldg(hist + sy) : 0u;
-        const unsigned bal = __ballot_sync(0xffffffffu, h != 0);
-        if (h) {
-            const int pp = wpos + __popc(bal & ((1u << lane) - 1u));
-            keys[pp] = ((unsigned long long)h << 32) | (uint32_t)pp;
-            syms[pp] = sy;
+    for (uint32_t s0 = wsb; s0 < wse; s0 += 256) {             // 8 independent loads per lane
+        uint32_t hv[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            const uint32_t sy = s0 + 32 * g + lane;
+            hv[g] = sy < wse ? __ldg(hist + sy) : 0u;
         }
-        wpos += __popc(bal);
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            const uint32_t sy = s0 + 32 * g + lane;
+            const unsigned bal = __ballot_sync(0xffffffffu, hv[g] != 0);
+            if (hv[g]) {
+                const int pp = wpos + __popc(bal & ((1u << lane) - 1u));
+                keys[pp] = ((unsigned long long)hv[g] << 32) | (uint32_t)pp;
+                syms[pp] = sy;
+            }
+            wpos += __popc(bal);
+        }
     }
     for (int i = k + tid; i < npow2; i += LC_CB_THREADS) keys[i] = ~0ULL;
     __syncthreads();
@@ -97,42 +105,90 @@ __device__ __forceinline__ void lc_codebook_body(const uint32_t *__restrict__ hi
     lc_bitonic_sort(keys, npow2);
     if (tid == 0) out->stamp[1] = lc_gtimer();
 
-    // 3. two-queue merge.  Leaves 0..k-1 in sorted order; internal node m
-    //    (0..k-2) has freq ifreq[m]; parent[leaf] at [0,k), parent[k + m] for
-    //    internal node m.  A leaf wins ties: heapq pops (freq, counter) and
-    //    leaves were pushed first (huffman.py:36-48).  The first warp runs it
-    //    (lane-varying start values keep it off the uniform datapath; lane 0
-    //    stores); queue heads and their successors stay in registers.
-    if (wid == 0) {
+    // 3. two-queue merge (huffman.py:36-48: heapq pops (freq, counter); leaves were
+    //    pushed first, so with leaves sorted by (freq, symbol) and internal nodes in
+    //    creation order a leaf wins ties).  Leaves 0..k-1; internal node m has
+    //    freq ifreq[m]; parent[leaf] at [0,k), parent[k + m] for internal node m.
+    //    Batched: with t the smallest head, every queued item of freq <= 2t is
+    //    picked before any node created from them (new nodes are >= 2t and lose
+    //    ties to older items), so the batch's picks are the merged order of the
+    //    two queues up to 2t and its pairs become new nodes in parallel (merge
+    //    path per pair).  t at least doubles per batch: O(log total) batches.
+    {
+        __shared__ int s_li, s_ii, s_m, s_na, s_nb, s_go;
+        if (tid == 0) { s_li = 0; s_ii = 0; s_m = 0; }
+        __syncthreads();
         const unsigned long long INF = ~0ULL;
-        int li = lane >> 5, ii = lane >> 5;          // 0, but not provably warp-uniform
-        unsigned long long lf0 = keys[0] >> 32, lf1 = keys[1] >> 32;   // k >= 2 here
-        unsigned long long if0 = INF, if1 = INF;
-        for (int m = 0; m < k - 1; ++m) {
-            int pk[2];
-            unsigned long long f[2];
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                const bool tl = lf0 <= if0;
-                f[q] = tl ? lf0 : if0;
-                pk[q] = tl ? li : k + ii;
-                li += tl;
-                ii += !tl;
-                const unsigned long long lnext = li + 1 < k ? (keys[min(li + 1, k - 1)] >> 32) : INF;
-                const unsigned long long inext = ii + 1 < m ? ifreq[min(ii + 1, k - 2)] : INF;
-                lf0 = tl ? lf1 : lf0;
-                lf1 = tl ? lnext : lf1;
-                if0 = tl ? if0 : if1;
-                if1 = tl ? if1 : inext;
+        for (;;) {
+            if (tid == 0) {
+                const int li = s_li, ii = s_ii, m = s_m;
+                s_go = m < k - 1;
+                if (s_go) {
+                    const unsigned long long lf = li < k ? keys[li] >> 32 : INF;
+                    const unsigned long long nf = ii < m ? ifreq[ii] : INF;
+                    const unsigned long long t = lf < nf ? lf : nf;
+                    const unsigned long long T = t > (INF >> 1) ? INF : 2 * t;
+                    int lo = li, hi = k;                          // leaves with freq <= T
+                    while (lo < hi) { const int md = (lo + hi) >> 1; if ((keys[md] >> 32) <= T) lo = md + 1; else hi = md; }
+                    const int la = lo;
+                    lo = ii; hi = m;                              // internal nodes with freq <= T
+                    while (lo < hi) { const int md = (lo + hi) >> 1; if (ifreq[md] <= T) lo = md + 1; else hi = md; }
+                    s_na = la - li;
+                    s_nb = lo - ii;
+                    if (s_na + s_nb < 2) {                        // one sequential step
+                        int pk[2];
+                        unsigned long long f[2];
+                        int l2 = li, i2 = ii;
+                        for (int q = 0; q < 2; ++q) {
+                            const unsigned long long a = l2 < k ? keys[l2] >> 32 : INF;
+                            const unsigned long long b = i2 < m ? ifreq[i2] : INF;
+                            if (a <= b) { pk[q] = l2; f[q] = a; ++l2; } else { pk[q] = k + i2; f[q] = b; ++i2; }
+                        }
+                        ifreq[m] = f[0] + f[1];
+                        parent[pk[0]] = m;
+                        parent[pk[1]] = m;
+                        s_li = l2; s_ii = i2; s_m = m + 1;
+                        s_na = -1;
+                    }
+                }
             }
-            const unsigned long long fm = f[0] + f[1];
-            if (lane == 0) {
-                ifreq[m] = fm;
-                parent[pk[0]] = m;
-                parent[pk[1]] = m;
+            __syncthreads();
+            if (!s_go) break;
+            const int li = s_li, ii = s_ii, m = s_m, na = s_na, nb = s_nb;
+            if (na >= 0) {
+                const int npairs = (na + nb) >> 1;
+                // merged position p -> (# leaves among the first p picks); leaf wins ties
+                auto split = [&](int p) -> int {
+                    int lo = max(0, p - nb), hi = min(p, na);
+                    while (lo < hi) {
+                        const int i = (lo + hi) >> 1, j = p - i;
+                        if ((keys[li + i] >> 32) <= ifreq[ii + j - 1]) lo = i + 1; else hi = i;
+                    }
+                    return lo;
+                };
+                auto item = [&](int p, unsigned long long *f) -> int {
+                    const int i = split(p), j = p - i;
+                    const bool leaf = i < na && (j >= nb || (keys[li + i] >> 32) <= ifreq[ii + j]);
+                    if (leaf) { *f = keys[li + i] >> 32; return li + i; }
+                    *f = ifreq[ii + j];
+                    return k + ii + j;
+                };
+                for (int q = tid; q < npairs; q += LC_CB_THREADS) {
+                    unsigned long long fa, fb;
+                    const int a = item(2 * q, &fa), b = item(2 * q + 1, &fb);
+                    ifreq[m + q] = fa + fb;                       // beyond the batch's read range
+                    parent[a] = m + q;
+                    parent[b] = m + q;
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    const int used = split(2 * npairs);
+                    s_li = li + used;
+                    s_ii = ii + 2 * npairs - used;
+                    s_m = m + npairs;
+                }
             }
-            if0 = ii == m ? fm : if0;
-            if1 = ii + 1 == m ? fm : if1;
+            __syncthreads();
         }
     }
     __syncthreads();
@@ -268,9 +324,15 @@ __global__ void __launch_bounds__(LC_CB_THREADS) lc_codebook_kernel(
     const uint32_t span = ((nbins + LC_CB_THREADS / 32 - 1) / (LC_CB_THREADS / 32) + 31) & ~31u;
     const uint32_t wsb = min(nbins, wid * span), wse = min(nbins, wsb + span);
     int cnt = 0;
-    for (uint32_t s0 = wsb; s0 < wse; s0 += 32) {
-        const uint32_t sy = s0 + lane;
-        cnt += __popc(__ballot_sync(0xffffffffu, sy < wse && __ldg(hist + sy) != 0));
+    for (uint32_t s0 = wsb; s0 < wse; s0 += 256) {             // 8 independent loads per lane
+        uint32_t hv[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            const uint32_t sy = s0 + 32 * g + lane;
+            hv[g] = sy < wse ? __ldg(hist + sy) : 0u;
+        }
+#pragma unroll
+        for (int g = 0; g < 8; ++g) cnt += __popc(__ballot_sync(0xffffffffu, hv[g] != 0));
     }
     for (uint32_t sy = tid; sy < nbins; sy += LC_CB_THREADS) lengths[sy] = 0;
     if (lane == 0) s_wcnt[wid][0] = cnt;
