@@ -22,22 +22,72 @@ __global__ void __launch_bounds__(256) lc_range_kernel(const double *__restrict_
                                                       LcRangePart *__restrict__ parts)
 {
     // min, max, non-finite flag and max |x_i - x_{i-1}| (decides whether definite
-    // escapes are possible, lc_compress_f64).  Grid-stride over warp-contiguous
-    // runs; the predecessor comes from the neighbouring lane.
+    // escapes are possible, lc_compress_f64).  Each lane owns 8 consecutive
+    // elements per group (four 16-byte loads, two groups in flight), so a warp
+    // covers 256 contiguous elements; the predecessor of a lane's first element
+    // is the previous lane's last one (lane 0 loads it).  An 8-byte aligned x
+    // starts the groups at x + 1 (x[0] is folded in by thread 0).
     double mn = INFINITY, mx = -INFINITY, ms = 0.0;
     int nf = 0;
     const int lane = threadIdx.x & 31;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n; base += stride) {
-        const uint64_t i = base + lane;
-        const double a = i < n ? __ldcs(x + i) : 0.0;
-        double prev = __shfl_up_sync(0xffffffffu, a, 1);
-        if (lane == 0) prev = base > 0 ? x[base - 1] : a;
-        if (i < n) {
+    const uint64_t off = (reinterpret_cast<uintptr_t>(x) & 15) ? 1 : 0;
+    const double *base = x + off;
+    const uint64_t nb = n > off ? n - off : 0;
+    const uint64_t ngroups = nb / 8;                      // full 8-element groups
+    const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
+    const double2 *x2 = reinterpret_cast<const double2 *>(base);
+    auto group = [&](uint64_t g, const double (&v)[8]) {
+        double prev = __shfl_up_sync(0xffffffffu, v[7], 1);
+        if (lane == 0) prev = g > 0 ? base[8 * g - 1] : (off ? x[0] : v[0]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const double a = v[k];
             nf |= !isfinite(a);
             mn = fmin(mn, a);
             mx = fmax(mx, a);
-            ms = fmax(ms, fabs(__dsub_rn(a, prev)));
+            ms = fmax(ms, fabs(__dsub_rn(a, k ? v[k - 1] : prev)));
+        }
+    };
+    // warp-uniform trip counts: the warp's first group decides
+    for (uint64_t wg = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); wg < ngroups; wg += 2 * gstride) {
+        const uint64_t g0 = wg + lane, g1 = wg + gstride + lane;
+        double v0[8], v1[8];
+        const bool ok0 = g0 < ngroups, ok1 = g1 < ngroups;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const double2 a = ok0 ? __ldcs(x2 + 4 * g0 + k) : make_double2(0.0, 0.0);
+            const double2 c = ok1 ? __ldcs(x2 + 4 * g1 + k) : make_double2(0.0, 0.0);
+            v0[2 * k] = a.x; v0[2 * k + 1] = a.y;
+            v1[2 * k] = c.x; v1[2 * k + 1] = c.y;
+        }
+        // lanes past the end repeat the last valid element of the warp's range
+        const unsigned m0 = __ballot_sync(0xffffffffu, ok0), m1 = __ballot_sync(0xffffffffu, ok1);
+        if (m0) {
+            if (!ok0) {
+                const double last = base[8 * (wg + (31 - __clz(m0))) + 7];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) v0[k] = last;
+            }
+            group(wg, v0);
+        }
+        if (m1) {
+            if (!ok1) {
+                const double last = base[8 * (wg + gstride + (31 - __clz(m1))) + 7];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) v1[k] = last;
+            }
+            group(wg + gstride, v1);
+        }
+    }
+    // x[0] when skipped for alignment, and the tail (< 8 elements): thread 0
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (off) { const double a = x[0]; nf |= !isfinite(a); mn = fmin(mn, a); mx = fmax(mx, a); }
+        for (uint64_t i = off + ngroups * 8; i < n; ++i) {
+            const double a = x[i];
+            nf |= !isfinite(a);
+            mn = fmin(mn, a);
+            mx = fmax(mx, a);
+            if (i > 0) ms = fmax(ms, fabs(__dsub_rn(a, x[i - 1])));
         }
     }
     for (int o = 16; o; o >>= 1) {
