@@ -19,6 +19,9 @@
  *                                                      huffman.py:110-132,153-172
  *   lc_error_stats_f64  measured_psnr reductions + error_identity_check
  *                                                      compressor.py:81-94,443-460
+ *   lc_stencil_apply_f64, lc_residual_f64, lc_jacobi_step_f64, lc_dot_f64,
+ *   lc_axpy_f64         solver harness: spmv / residual / Jacobi step /
+ *                       dot / axpy of solvers.py:92-241, sparse.py:150-157
  *
  * Status codes (return values):
  *   0 ok
@@ -133,6 +136,35 @@ typedef struct lc_stats {
 
 int lc_error_stats_f64(lc_ctx *ctx, const double *original, const double *recon, uint64_t n,
                        int on_device, const double *pe, const double *pe_rec, lc_stats *out);
+
+/* ---- solver harness (device pointers only) -------------------------------
+ * Constant-coefficient 7-point stencil on an nx x ny x nz grid, x fastest
+ * (k = (z*ny + y)*nx + x), Dirichlet: neighbours outside the grid are dropped.
+ * 2-D problems use nz = 1.  Replaces spmv (sparse.py:21-28,150-157) for the
+ * stencil matrices of the configs (generate_poisson2d, sparse.py:184-206);
+ * rows are accumulated in CSR column order (z-1, y-1, x-1, centre, x+1,
+ * y+1, z+1) with unfused multiply/add, bit-identical to the reference.
+ * Reductions are deterministic for a given n.  *_dev outputs stay on the
+ * device (NULL: scratch); *_host (optional) receives the value after a sync. */
+typedef struct lc_stencil {
+    int64_t nx, ny, nz;
+    double c, xm, xp, ym, yp, zm, zp;
+} lc_stencil;
+
+/* y = A x                                                                  */
+int lc_stencil_apply_f64(lc_ctx *ctx, const lc_stencil *s, const double *x, double *y);
+/* r = b - A x, sumsq = sum r^2                                              */
+int lc_residual_f64(lc_ctx *ctx, const lc_stencil *s, const double *x, const double *b, double *r,
+                    double *sumsq_dev, double *sumsq_host);
+/* one Jacobi step (solvers.py:104-110): x_out = x + inv*r, r_out = b - A x_out,
+ * sumsq = sum r_out^2 (one launch + the final sum)                          */
+int lc_jacobi_step_f64(lc_ctx *ctx, const lc_stencil *s, double inv_diag, const double *x, const double *r,
+                       const double *b, double *x_out, double *r_out, double *sumsq_dev, double *sumsq_host);
+/* dot = a . b                                                               */
+int lc_dot_f64(lc_ctx *ctx, const double *a, const double *b, uint64_t n, double *dot_dev, double *dot_host);
+/* y += alpha x, alpha = a_scale * (*a_dev) when a_dev is set, else a         */
+int lc_axpy_f64(lc_ctx *ctx, double a, const double *a_dev, double a_scale, const double *x, double *y,
+                uint64_t n);
 
 #ifdef __cplusplus
 }

@@ -85,13 +85,23 @@ def library():
         L.lc_error_stats_f64.argtypes = [_vp, _vp, _vp, ctypes.c_uint64, ctypes.c_int, _vp, _vp,
                                          ctypes.POINTER(LcStats)]
         L.lc_error_stats_f64.restype = ctypes.c_int
+        _d = ctypes.c_double
+        _dp = ctypes.POINTER(ctypes.c_double)
+        L.lc_stencil_apply_f64.argtypes = [_vp, _vp, _vp, _vp]
+        L.lc_residual_f64.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _dp]
+        L.lc_jacobi_step_f64.argtypes = [_vp, _vp, _d, _vp, _vp, _vp, _vp, _vp, _vp, _dp]
+        L.lc_dot_f64.argtypes = [_vp, _vp, _vp, ctypes.c_uint64, _vp, _dp]
+        L.lc_axpy_f64.argtypes = [_vp, _d, _vp, _d, _vp, _vp, ctypes.c_uint64]
+        for f in (L.lc_stencil_apply_f64, L.lc_residual_f64, L.lc_jacobi_step_f64, L.lc_dot_f64, L.lc_axpy_f64):
+            f.restype = ctypes.c_int
         _lib = L
         return L
 
 
 EXPORTED = ["lc_ctx_create", "lc_ctx_destroy", "lc_last_error", "lc_range_f64", "lc_compress_f64",
             "lc_result_fetch", "lc_result_device", "lc_decompress_f64", "lc_last_device_ms",
-            "lc_phase_ms", "lc_launch_count", "lc_error_stats_f64"]
+            "lc_phase_ms", "lc_launch_count", "lc_error_stats_f64", "lc_stencil_apply_f64",
+            "lc_residual_f64", "lc_jacobi_step_f64", "lc_dot_f64", "lc_axpy_f64"]
 
 
 class Context:

@@ -39,7 +39,7 @@ struct lc_ctx {
     // scratch
     LcBuf xbuf, codes, hist, desc, counters, bad_end, pe, pe_rec, lengths, cw, gkeys, ifreq,
         parent, cbout, payload, esc_idx, esc_val, encdesc, range_parts, small, pred, tiles;
-    LcBuf st_b, st_pe, st_pr, st_parts;
+    LcBuf st_b, st_pe, st_pr, st_parts, solver;
     // last lc_range_f64 on device data (lets compress skip the anchor pass)
     const void *rng_ptr = nullptr;
     uint64_t rng_n = 0;
@@ -78,6 +78,10 @@ cudaError_t lc_reserve(LcBuf &b, size_t bytes)
 cudaStream_t lc_stream(lc_ctx *ctx) { return ctx->stream; }
 int lc_sm_count(lc_ctx *ctx) { return ctx->sm_count; }
 void *lc_pinned(lc_ctx *ctx) { return ctx->pinned; }
+void *lc_solver_scratch(lc_ctx *ctx, size_t bytes)
+{
+    return lc_reserve(ctx->solver, bytes) == cudaSuccess ? ctx->solver.p : nullptr;
+}
 void lc_set_err(lc_ctx *ctx, const char *msg) { ctx->err = msg; }
 LcBuf *lc_dec_bufs(lc_ctx *ctx) { return ctx->dec; }
 cudaEvent_t lc_phase_ev(lc_ctx *ctx, int i) { return ctx->pev[i]; }
@@ -138,7 +142,7 @@ void lc_ctx_destroy(lc_ctx *ctx)
                      &ctx->encdesc, &ctx->range_parts, &ctx->small, &ctx->pred, &ctx->tiles, &ctx->dec[0], &ctx->dec[1],
                      &ctx->dec[2], &ctx->dec[3], &ctx->dec[4], &ctx->dec[5], &ctx->dec[6],
                      &ctx->dec[7], &ctx->dec[8], &ctx->dec[9], &ctx->st_b, &ctx->st_pe, &ctx->st_pr,
-                     &ctx->st_parts};
+                     &ctx->st_parts, &ctx->solver};
     for (LcBuf *b : bufs)
         if (b->p) cudaFree(b->p);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
