@@ -415,6 +415,10 @@ def run_b200(args, rank, world, local_rank):
                "sample": f"oracle C port, compress+decompress of the config-2 vector at n=2^{args.cpu_log2} "
                          f"for each of the 3 bounds, single thread ({dt:.1f} s)"}
 
+    solver = None
+    if rank == 0 and world == 1 and not args.no_solver:
+        solver = config1_harness(lc)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
@@ -424,8 +428,39 @@ def run_b200(args, rank, world, local_rank):
                        "l2": "inputs (512 MB/GPU) exceed L2; no flush"},
             "clocks": clk, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "per_bound": per,
+            "config1_solver_harness": solver,
         }
         print(json.dumps(line), flush=True)
+
+
+def config1_harness(lc):
+    """BASELINE.json config 1 on the GPU harness (outside the timed region): Jacobi on
+    poisson2d(256), b ~ U(-1,1) seed 0, x0 = 0, lossy checkpoint every 10 iterations at
+    rel eb 1e-4, failure at 200 -> restart from 190, run to ||r||/||b|| < 1e-6."""
+    import torch
+    from types import SimpleNamespace
+    from paper_1805_07384_b200 import checkpoint as ck, harness, solvers
+    a, _ = solvers.generate_poisson2d(256)
+    m = solvers.jacobi_preconditioner(a)
+    b = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, 65536)).cuda()
+    cfg = solvers.SolveConfig(tolerance=1e-6, max_iterations=10 ** 6, ckpt_intvl=10)
+    comp = lc.CompressorConfig.value_range_relative(1e-4)
+    t0 = time.perf_counter()
+    res = harness.measure_n_prime("jacobi", a, m, b, cfg, comp, [200])
+    t_np = time.perf_counter() - t0
+    s = solvers.init("jacobi", a, m, b, cfg)
+    while s.iteration < 190:
+        s.step()
+    img, cost = ck.checkpoint_lossy(s, comp, ck.StorageTarget())
+    blk = lc.CompressedBlock.from_bytes(img.payload)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    ck.decode_payload(img, device="cuda")
+    torch.cuda.synchronize()
+    return {"baseline_iterations": res.baseline_n, "n_prime": res.samples[0].n_prime,
+            "reference_n_prime": -61, "reference_baseline": 112797,
+            "ratio_x190": blk.compression_ratio, "reference_ratio_x190": 6.717, "compress_ms": 1e3 * cost.t_compress,
+            "decompress_ms": 1e3 * (time.perf_counter() - t1), "harness_seconds": t_np}
 
 
 def main():
@@ -438,6 +473,7 @@ def main():
     ap.add_argument("--cpu-log2", type=int, default=26)
     ap.add_argument("--ref-log2", type=int, default=24)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-solver", action="store_true")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
