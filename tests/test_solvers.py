@@ -147,3 +147,43 @@ def test_config1_n_prime(dev, sg):
                                   CompressorConfig.value_range_relative(eb), sg["config1/inject"])
     assert abs(res.baseline_n - int(sg["config1/baseline"][0])) <= 1
     np.testing.assert_allclose(res.values(), sg["config1/nprime"], atol=1)
+
+
+TG = os.path.join(ROOT, "tests", "golden", "trial_golden.json")
+
+
+def test_sim_config_validation():
+    from paper_1805_07384_b200 import harness
+    from paper_1805_07384_b200.errors import ParameterError
+    for bad in (dict(method="synthetic"), dict(policy="x"), dict(ckpt_intvl=0), dict(policy="lossy")):
+        with pytest.raises(ParameterError):
+            harness.SimConfig(**bad)
+    draw = harness.FailureProcess(0.5, 3).arrivals()
+    r = np.random.default_rng(3)
+    assert [draw() for _ in range(4)] == [float(r.exponential(2.0)) for _ in range(4)]
+
+
+@pytest.mark.gpu
+def test_run_trial_matches_reference(dev):
+    """Poisson-failure trials on the GPU workload against the reference's run_trial with
+    its CPU workload: identical event bookkeeping for Jacobi (bit-identical iterates);
+    CG/GMRES recoveries may shift the convergence step by one per recovery."""
+    import json
+    from paper_1805_07384_b200 import harness
+    from paper_1805_07384_b200.compressor import CompressorConfig
+    for case in json.load(open(TG)):
+        c = dict(case["config"])
+        eb = c.pop("eb_rel")
+        if eb is not None:
+            c["compressor_config"] = CompressorConfig.value_range_relative(eb)
+        rep = harness.run_trial(harness.SimConfig(**c), c["seed"])
+        ref = case["report"]
+        assert rep.converged == ref["converged"] and rep.diverged == ref["diverged"], c
+        if c["method"] == "jacobi":
+            for k, v in ref.items():
+                if isinstance(v, float):
+                    assert abs(getattr(rep, k) - v) <= 1e-9 * max(1.0, abs(v)), (k, c)
+                else:
+                    assert getattr(rep, k) == v, (k, c)
+        else:
+            assert abs(rep.iterations_final - ref["iterations_final"]) <= 1 + ref["n_recoveries"], c
