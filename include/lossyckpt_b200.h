@@ -30,6 +30,7 @@
  *   3 trailing bits              -> IntegrityError("... trailing bits after last symbol")
  *   4 escape count mismatch      -> IntegrityError("escape count mismatch: ...")
  *   5 escape positions mismatch  -> IntegrityError("escape positions disagree with escape codes")
+ *   6 v2 sync table mismatch     -> IntegrityError("sync table disagrees with the payload")
  *  10 non-finite input           -> ParameterError("input contains NaN or Inf")
  *  11 error bound overflow       -> ParameterError("error bound too large to quantize")
  *  12 bad argument               -> ParameterError
@@ -136,6 +137,19 @@ typedef struct lc_stats {
 
 int lc_error_stats_f64(lc_ctx *ctx, const double *original, const double *recon, uint64_t n,
                        int on_device, const double *pe, const double *pe_rec, lc_stats *out);
+
+/* ---- v2 blocks ------------------------------------
+ * A v2 block carries the bit offset of every LC_SYNC_K (= 1024)-th symbol, so
+ * decoding needs no segment synchronisation.  Every compress records them;
+ * lc_result_sync copies min(cap, count) offsets (count = ceil((n-1)/1024)).  */
+int lc_result_sync(lc_ctx *ctx, uint64_t *offsets, uint64_t cap, uint64_t *count);
+/* lc_decompress_f64 for a v2 block: sync[n_sync] bit offsets, sync_k = 1024. */
+int lc_decompress_v2_f64(lc_ctx *ctx, uint64_t n, double eb_abs, double first_value,
+                         const uint8_t *code_lengths, uint64_t n_lengths, const uint8_t *payload,
+                         uint64_t payload_bytes, uint64_t payload_bits, const uint64_t *sync,
+                         uint64_t n_sync, uint32_t sync_k, const uint64_t *esc_idx,
+                         const double *esc_val, uint64_t n_esc, int inputs_on_device, double *out,
+                         int out_on_device, int64_t *esc_used);
 
 /* ---- solver harness (device pointers only) -------------------------------
  * Constant-coefficient 7-point stencil on an nx x ny x nz grid, x fastest

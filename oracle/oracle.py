@@ -216,6 +216,18 @@ def compress(data, mode, param, n_bins_half=32768, record=False):
                 codes=codes, recon=recon, traces=(pe, pe_rec) if record else None)
 
 
+def sync_offsets(codes, lengths, k=1024):
+    """v2 block sync table (no reference counterpart):
+    bit offset in the payload of symbol 0, k, 2k, ... (prefix sums of the
+    code lengths encode() lays down, huffman.py:131-146)."""
+    codes = np.asarray(codes, dtype=np.int64)
+    if codes.size == 0:
+        return np.zeros(0, np.uint64)
+    bits = np.asarray(lengths, dtype=np.uint64)[codes]
+    start = np.concatenate([[0], np.cumsum(bits)[:-1]]).astype(np.uint64)
+    return start[::k].copy()
+
+
 def decompress(blk):
     """compressor.py:420-440."""
     n = blk["n"]

@@ -17,7 +17,8 @@ LIB_PATH = os.path.join(HERE, "_lib", "liblossyckpt_b200.so")
 STATUS_INTEGRITY = {1: "Huffman decode failed: invalid codeword",
                     2: "Huffman decode failed: payload exhausted mid-symbol",
                     3: "Huffman decode failed: trailing bits after last symbol",
-                    5: "escape positions disagree with escape codes"}
+                    5: "escape positions disagree with escape codes",
+                    6: "sync table disagrees with the payload"}
 STATUS_PARAMETER = {10: "input contains NaN or Inf",
                     11: "error bound too large to quantize",
                     12: "invalid argument",
@@ -94,6 +95,13 @@ def library():
         L.lc_axpy_f64.argtypes = [_vp, _d, _vp, _d, _vp, _vp, ctypes.c_uint64]
         for f in (L.lc_stencil_apply_f64, L.lc_residual_f64, L.lc_jacobi_step_f64, L.lc_dot_f64, L.lc_axpy_f64):
             f.restype = ctypes.c_int
+        L.lc_result_sync.argtypes = [_vp, _vp, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
+        L.lc_result_sync.restype = ctypes.c_int
+        L.lc_decompress_v2_f64.argtypes = [_vp, ctypes.c_uint64, ctypes.c_double, ctypes.c_double, _vp,
+                                           ctypes.c_uint64, _vp, ctypes.c_uint64, ctypes.c_uint64, _vp,
+                                           ctypes.c_uint64, ctypes.c_uint32, _vp, _vp, ctypes.c_uint64,
+                                           ctypes.c_int, _vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int64)]
+        L.lc_decompress_v2_f64.restype = ctypes.c_int
         _lib = L
         return L
 
@@ -101,7 +109,8 @@ def library():
 EXPORTED = ["lc_ctx_create", "lc_ctx_destroy", "lc_last_error", "lc_range_f64", "lc_compress_f64",
             "lc_result_fetch", "lc_result_device", "lc_decompress_f64", "lc_last_device_ms",
             "lc_phase_ms", "lc_launch_count", "lc_error_stats_f64", "lc_stencil_apply_f64",
-            "lc_residual_f64", "lc_jacobi_step_f64", "lc_dot_f64", "lc_axpy_f64"]
+            "lc_residual_f64", "lc_jacobi_step_f64", "lc_dot_f64", "lc_axpy_f64", "lc_result_sync",
+            "lc_decompress_v2_f64"]
 
 
 class Context:

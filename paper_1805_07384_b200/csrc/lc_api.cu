@@ -9,11 +9,11 @@
 
 #include "lc_kernels.cuh"
 
-int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_value,
-                       const uint8_t *code_lengths, uint64_t n_lengths, const uint8_t *payload,
-                       uint64_t payload_bytes, uint64_t payload_bits, const uint64_t *esc_idx,
-                       const double *esc_val, uint64_t n_esc, int inputs_on_device, double *out,
-                       int out_on_device, int64_t *esc_used);
+int lc_decompress_impl2(lc_ctx *ctx, uint64_t n, double eb_abs, double first_value,
+                        const uint8_t *code_lengths, uint64_t n_lengths, const uint8_t *payload,
+                        uint64_t payload_bytes, uint64_t payload_bits, const uint64_t *esc_idx,
+                        const double *esc_val, uint64_t n_esc, int inputs_on_device, double *out,
+                        int out_on_device, int64_t *esc_used, const uint64_t *sync, uint64_t n_sync);
 
 // ---------------------------------------------------------------------------
 
@@ -39,7 +39,8 @@ struct lc_ctx {
     // scratch
     LcBuf xbuf, codes, hist, desc, counters, bad_end, pe, pe_rec, lengths, cw, gkeys, ifreq,
         parent, cbout, payload, esc_idx, esc_val, encdesc, range_parts, small, pred, tiles;
-    LcBuf st_b, st_pe, st_pr, st_parts, solver;
+    LcBuf st_b, st_pe, st_pr, st_parts, solver, sync;
+    uint64_t nsync = 0;                 // v2 sync offsets of the last compress
     // last lc_range_f64 on device data (lets compress skip the anchor pass)
     const void *rng_ptr = nullptr;
     uint64_t rng_n = 0;
@@ -142,7 +143,7 @@ void lc_ctx_destroy(lc_ctx *ctx)
                      &ctx->encdesc, &ctx->range_parts, &ctx->small, &ctx->pred, &ctx->tiles, &ctx->dec[0], &ctx->dec[1],
                      &ctx->dec[2], &ctx->dec[3], &ctx->dec[4], &ctx->dec[5], &ctx->dec[6],
                      &ctx->dec[7], &ctx->dec[8], &ctx->dec[9], &ctx->st_b, &ctx->st_pe, &ctx->st_pr,
-                     &ctx->st_parts, &ctx->solver};
+                     &ctx->st_parts, &ctx->solver, &ctx->sync};
     for (LcBuf *b : bufs)
         if (b->p) cudaFree(b->p);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
@@ -407,6 +408,9 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     E.tile_counter = tile_counter;
     E.ntiles = etiles;
     E.max_len = ctx->cb.max_len;
+    ctx->nsync = (m + LC_SYNC_K - 1) / LC_SYNC_K;
+    LC_CUDA_OK(lc_reserve(ctx->sync, (ctx->nsync + 1) * 8));
+    E.sync = (unsigned long long *)ctx->sync.p;
     const int egrid = (int)(etiles < (uint64_t)(4 * ctx->sm_count) ? etiles : 4 * ctx->sm_count);
     lc_encode_kernel<CodeT><<<egrid, LC_TPB, lc_encode_smem_bytes(), st>>>(E);
     { int _rc = lc_debug_check(ctx, "lc_encode_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
@@ -508,9 +512,35 @@ int lc_decompress_f64(lc_ctx *ctx, uint64_t n, double eb_abs, double first_value
 {
     if (!ctx) return 12;
     LC_CUDA_OK(cudaSetDevice(ctx->device));
-    return lc_decompress_impl(ctx, n, eb_abs, first_value, code_lengths, n_lengths, payload, payload_bytes,
-                              payload_bits, esc_idx, esc_val, n_esc, inputs_on_device, out, out_on_device,
-                              esc_used);
+    return lc_decompress_impl2(ctx, n, eb_abs, first_value, code_lengths, n_lengths, payload, payload_bytes,
+                               payload_bits, esc_idx, esc_val, n_esc, inputs_on_device, out, out_on_device,
+                               esc_used, nullptr, 0);
+}
+
+int lc_result_sync(lc_ctx *ctx, uint64_t *offsets, uint64_t cap, uint64_t *count)
+{
+    if (!ctx) return 12;
+    if (count) *count = ctx->nsync;
+    if (offsets && cap) {
+        const uint64_t k = cap < ctx->nsync ? cap : ctx->nsync;
+        LC_CUDA_OK(cudaMemcpyAsync(offsets, ctx->sync.p, k * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        LC_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    }
+    return 0;
+}
+
+int lc_decompress_v2_f64(lc_ctx *ctx, uint64_t n, double eb_abs, double first_value, const uint8_t *code_lengths,
+                         uint64_t n_lengths, const uint8_t *payload, uint64_t payload_bytes, uint64_t payload_bits,
+                         const uint64_t *sync, uint64_t n_sync, uint32_t sync_k, const uint64_t *esc_idx,
+                         const double *esc_val, uint64_t n_esc, int inputs_on_device, double *out,
+                         int out_on_device, int64_t *esc_used)
+{
+    if (!ctx) return 12;
+    if (!sync || sync_k != LC_SYNC_K || n < 2 || n_sync != (n - 1 + LC_SYNC_K - 1) / LC_SYNC_K) return 12;
+    LC_CUDA_OK(cudaSetDevice(ctx->device));
+    return lc_decompress_impl2(ctx, n, eb_abs, first_value, code_lengths, n_lengths, payload, payload_bytes,
+                               payload_bits, esc_idx, esc_val, n_esc, inputs_on_device, out, out_on_device,
+                               esc_used, sync, n_sync);
 }
 
 // Debug/test hook: copy an intermediate of the last compress to host.

@@ -780,6 +780,95 @@ static size_t lc_dec_write_smem(int cap, int code_bytes, int seg_bits)
          + sizeof(uint32_t) * (size_t)(LC_DEC_TPB / 32) * lc_dec_stage_words(cap, code_bytes);
 }
 
+// v2 blocks: decode from the sync table, no segment synchronisation.  Thread
+// j decodes the LC_SYNC_K symbols starting at bit sync[j] (the last group:
+// the rest) straight into codes[j*LC_SYNC_K ...] with 16-byte stores, and
+// checks that it stops exactly at the next sync point (status 6 otherwise;
+// 1/2 for an invalid codeword / exhausted payload).
+template <typename CodeT>
+__global__ void __launch_bounds__(256) lc_dec_v2_kernel(LcDecParams P, const unsigned long long *__restrict__ sync,
+                                                       unsigned long long nsync, void *out_, unsigned long long m,
+                                                       int *__restrict__ status)
+{
+    __shared__ LcDecTables Ts;
+    lc_load_tables(Ts, P.T);
+    constexpr int VEC = 16 / sizeof(CodeT), HALF = VEC / 2, SH = 8 * sizeof(CodeT);
+    CodeT *out = reinterpret_cast<CodeT *>(out_);
+    const int max_len = Ts.max_len;
+    for (unsigned long long j = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; j < nsync;
+         j += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long s0 = sync[j], s1 = j + 1 < nsync ? sync[j + 1] : P.bits;
+        const unsigned long long o0 = j * LC_SYNC_K;
+        if (s0 > s1 || s1 > P.bits || o0 >= m || (j == 0 && s0 != 0)) { atomicExch(status, 6); continue; }
+        unsigned todo = (unsigned)(m - o0 < LC_SYNC_K ? m - o0 : LC_SYNC_K);
+        const unsigned long long wbase = s0 & ~31ull;
+        const unsigned bits_rel = lc_bits_rel(P.bits, wbase);
+        LcBitReader<LcGlobSrc> br;
+        br.src.w = P.payload + wbase / 32;
+        br.seek((unsigned)(s0 - wbase));
+        unsigned long long lo = 0, hi = 0, o = o0;
+        int cnt = 0, bad = 0;
+        auto put = [&](uint32_t sym) {
+            const unsigned long long v = (unsigned long long)(CodeT)sym;
+            if (cnt < HALF) lo |= v << (SH * cnt);
+            else hi |= v << (SH * (cnt - HALF));
+            if (++cnt == VEC) {
+                *reinterpret_cast<uint4 *>(out + o) = make_uint4((uint32_t)lo, (uint32_t)(lo >> 32),
+                                                                (uint32_t)hi, (uint32_t)(hi >> 32));
+                o += VEC;
+                lo = hi = 0;
+                cnt = 0;
+            }
+        };
+        while (todo) {
+            const unsigned w12 = (unsigned)(br.buf >> (64 - LC_LUT_BITS));
+            const unsigned e1 = Ts.lut[w12];
+            const unsigned e2 = Ts.lut2[w12];
+            const unsigned n2 = e2 >> 16;
+            const unsigned L2 = (e2 >> 12) & 15u;
+            const bool fits = br.pos + L2 <= bits_rel;
+            if (n2 >= 2 && n2 <= todo && fits) {
+                put(e1 & 0xffffffu);
+                unsigned sm = (e2 & 0xfffu) & ((e2 & 0xfffu) - 1u);
+#pragma unroll
+                for (int k = 1; k < LC_LUT_BITS; ++k) {
+                    if ((unsigned)k < n2) {
+                        const int i = __ffs(sm) - 1;
+                        sm &= sm - 1;
+                        put(Ts.lut[(w12 << i) & ((1u << LC_LUT_BITS) - 1)] & 0xffffffu);
+                    }
+                }
+                br.consume((int)L2);
+                todo -= n2;
+            } else {
+                uint32_t sym;
+                int l;
+                if (e2 && fits) {
+                    sym = e1 & 0xffffffu;
+                    l = (int)(e1 >> 24);
+                } else {
+                    l = e2 ? 0 : lc_long_len(Ts, br.buf);
+                    if (l && br.pos + (unsigned)l <= bits_rel) {
+                        const unsigned long long v = (br.buf >> 32) >> (32 - l);
+                        sym = __ldg(P.sorted + Ts.offset[l] + (v - Ts.first_code[l]));
+                    } else {
+                        int term = 0;
+                        l = lc_next_symbol(Ts, P.sorted, br, bits_rel, &sym, &term);
+                        if (!l) { bad = term == 4 ? 2 : term; break; }
+                    }
+                }
+                put(sym);
+                br.consume(l);
+                --todo;
+            }
+        }
+        for (int k = 0; k < cnt; ++k)                   // partial last group
+            out[o + k] = (CodeT)((k < HALF ? lo >> (SH * k) : hi >> (SH * (k - HALF))));
+        if (bad) atomicExch(status, bad);
+        else if (wbase + br.pos != s1) atomicExch(status, 6);
+    }
+}
+
 // Resolve the reference status (huffman.py:114-132) from the segment walk.
 __global__ void lc_dec_status_kernel(const LcSeg *__restrict__ seg, const unsigned long long *__restrict__ off,
                                      const unsigned long long *__restrict__ total_and_term,
@@ -1233,11 +1322,15 @@ void lc_count_launch(lc_ctx *ctx, int k);
 void lc_set_kind(lc_ctx *ctx, int k);
 int lc_debug_check(lc_ctx *ctx, const char *what, const char *file, int line);
 
-int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_value,
-                       const uint8_t *code_lengths, uint64_t n_lengths, const uint8_t *payload,
-                       uint64_t payload_bytes, uint64_t payload_bits, const uint64_t *esc_idx,
-                       const double *esc_val, uint64_t n_esc, int inputs_on_device, double *out,
-                       int out_on_device, int64_t *esc_used)
+static int lc_reconstruct(lc_ctx *ctx, uint64_t n, double eb_abs, double first_value, const double *esc_val_in,
+                          uint64_t n_esc, double *out, int out_on_device, int64_t *esc_used, void *codes,
+                          int code_bytes);
+
+int lc_decompress_impl2(lc_ctx *ctx, uint64_t n, double eb_abs, double first_value,
+                        const uint8_t *code_lengths, uint64_t n_lengths, const uint8_t *payload,
+                        uint64_t payload_bytes, uint64_t payload_bits, const uint64_t *esc_idx,
+                        const double *esc_val, uint64_t n_esc, int inputs_on_device, double *out,
+                        int out_on_device, int64_t *esc_used, const uint64_t *sync, uint64_t n_sync)
 {
     if (n < 2 || n_lengths == 0 || payload_bits > 8 * payload_bytes) return 12;
     cudaStream_t st = lc_stream(ctx);
@@ -1280,6 +1373,38 @@ int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_valu
     // Huffman decode
     const int code_bytes = n_lengths <= 65536 ? 2 : 4;
     LC_CUDA_OK(lc_reserve(bcodes, m * code_bytes + 16));
+    if (sync) {                                         // v2: decode straight from the sync table
+        LC_CUDA_OK(lc_reserve(baux, 256));
+        int *status = (int *)((char *)baux.p + 64);
+        int *esc_flags_v2 = (int *)((char *)baux.p + 80);
+        (void)esc_flags_v2;
+        LC_CUDA_OK(lc_reserve(bsync, n_sync * 8 + 64));
+        LC_CUDA_OK(cudaMemcpyAsync(bsync.p, sync, n_sync * 8,
+                                   inputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+        LC_CUDA_OK(cudaMemsetAsync(status, 0, 4, st));
+        LcDecParams DP;
+        DP.payload = (const uint32_t *)bpay.p;
+        DP.bits = payload_bits;
+        DP.T = T;
+        DP.sorted = sorted;
+        DP.nseg = 0; DP.nblk = 0; DP.seg_bits = 0; DP.nwords = words;
+        LC_CUDA_OK(cudaEventRecord(lc_phase_ev(ctx, 8), st));
+        LC_CUDA_OK(cudaEventRecord(lc_phase_ev(ctx, 9), st));
+        const int g = (int)((n_sync + 255) / 256 < (uint64_t)(8 * lc_sm_count(ctx)) ? (n_sync + 255) / 256
+                                                                                    : 8 * lc_sm_count(ctx));
+        if (code_bytes == 2)
+            lc_dec_v2_kernel<uint16_t><<<g, 256, 0, st>>>(DP, (const unsigned long long *)bsync.p, n_sync, bcodes.p, m, status);
+        else
+            lc_dec_v2_kernel<uint32_t><<<g, 256, 0, st>>>(DP, (const unsigned long long *)bsync.p, n_sync, bcodes.p, m, status);
+        { int _rc = lc_debug_check(ctx, "lc_dec_v2_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+        lc_count_launch(ctx, 1);
+        int *hstat = (int *)lc_pinned(ctx);
+        LC_CUDA_OK(cudaMemcpyAsync(hstat, status, 4, cudaMemcpyDeviceToHost, st));
+        LC_CUDA_OK(cudaStreamSynchronize(st));
+        if (*hstat) return *hstat;
+        return lc_reconstruct(ctx, n, eb_abs, first_value, esc_val, n_esc, out, out_on_device, esc_used,
+                              bcodes.p, code_bytes);
+    }
     // segment size: ~40 average codewords (canonical codes resynchronise
     // within a few codewords), 128..1024 bits, while keeping >= 2 waves of CTAs
     int sub = 2;                                         // 64-bit sub-segments
@@ -1391,8 +1516,22 @@ int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_valu
     LC_CUDA_OK(cudaMemcpyAsync(hstat, status, 4, cudaMemcpyDeviceToHost, st));
     LC_CUDA_OK(cudaStreamSynchronize(st));
     if (*hstat) return *hstat;
+    return lc_reconstruct(ctx, n, eb_abs, first_value, esc_val, n_esc, out, out_on_device, esc_used, bcodes.p,
+                          code_bytes);
+}
 
-    // reconstruction
+// Reconstruction from decoded codes (compressor.py:358-376, 430-439): exact
+// chunked chain + escape checks; inputs already staged in the context.
+static int lc_reconstruct(lc_ctx *ctx, uint64_t n, double eb_abs, double first_value, const double *esc_val_in,
+                          uint64_t n_esc, double *out, int out_on_device, int64_t *esc_used, void *codes,
+                          int code_bytes)
+{
+    (void)esc_val_in;
+    cudaStream_t st = lc_stream(ctx);
+    LcBuf *B = lc_dec_bufs(ctx);
+    LcBuf &beidx = B[2], &beval = B[3], &bout = B[4], &baux = B[8], &baux2 = B[9];
+    const uint64_t m = n - 1;
+    int *esc_flags = (int *)((char *)baux.p + 80);
     LC_CUDA_OK(cudaEventRecord(lc_phase_ev(ctx, 6), st));
     double *dout = out;
     if (!out_on_device) {
@@ -1404,7 +1543,7 @@ int lc_decompress_impl(lc_ctx *ctx, uint64_t n, double eb_abs, double first_valu
     LC_CUDA_OK(lc_reserve(baux2, (size_t)(ntiles + 1) * (2 * sizeof(LcSegScan) + sizeof(OffMap) + sizeof(double))
                                  + (size_t)nchunks * (16 + sizeof(int) + 5 * sizeof(double)) + 256));
     LcRecParams R;
-    R.codes = bcodes.p;
+    R.codes = codes;
     R.code_bytes = code_bytes;
     R.n = n;
     R.delta = 2.0 * eb_abs;

@@ -490,6 +490,9 @@ __global__ void __launch_bounds__(LC_TPB) lc_encode_kernel(LcEncParams P)
         }
         __syncthreads();
         const unsigned long long B0 = sh_in_bits;
+        // v2 sync table: bit offset of every LC_SYNC_K-th symbol
+        if (P.sync && len > 0 && (p0 & (LC_SYNC_K - 1)) == 0)
+            P.sync[p0 / LC_SYNC_K] = B0 + (ex & 0xffffffffull);
         // escapes (compressor.py:409-410): code index i-1 <-> element i
         if (nesc) {
             unsigned long long e = sh_in_esc + (ex >> 32);

@@ -39,6 +39,9 @@ struct LcQuantParams {
     double *tile_D;              // [ntiles + 1] scan -> pass B (offset at each tile start)
 };
 
+// v2 blocks: a bit offset for every LC_SYNC_K-th symbol (a multiple of LC_L)
+#define LC_SYNC_K 1024
+
 struct LcCodebookOut {
     unsigned long long total_bits;
     unsigned long long n_esc;
@@ -80,6 +83,7 @@ struct LcEncParams {
     unsigned int *tile_counter;
     uint64_t ntiles;
     int max_len;             // longest code (<= 32: table path)
+    unsigned long long *sync; // v2 sync table [ceil(m / LC_SYNC_K)] (bit offsets), may be null
 };
 
 __global__ void lc_range_kernel(const double *__restrict__ x, uint64_t n, LcRangePart *__restrict__ parts);

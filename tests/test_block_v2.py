@@ -1,0 +1,117 @@
+"""Block format v2: LCKP0001 version 2 adds a table
+of payload bit offsets every SYNC_K = 1024 symbols, so the decoder starts
+every thread at a known codeword boundary (no segment synchronisation).
+
+Bars: the sync table equals the oracle's prefix sums of code lengths; a v2
+block's codes, payload and escapes are the v1 block's (bit-exact to the
+reference); v2 reconstruction is bit-identical to v1/the oracle; a sync table
+that disagrees with the payload raises IntegrityError (status 6)."""
+
+import dataclasses
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+
+
+def _blk(lc, x, eb_rel, version):
+    return lc.compress(x, lc.CompressorConfig.value_range_relative(eb_rel, block_version=version))
+
+
+def test_v2_wire_format_roundtrip_cpu():
+    """to_bytes/from_bytes of a v2 block assembled from the oracle (no GPU)."""
+    import paper_1805_07384_b200 as lc
+    x = np.random.default_rng(2).normal(size=5000).cumsum()
+    ref = orc.compress(x, "value_range_relative", 1e-5)
+    sync = orc.sync_offsets(ref["codes"], ref["code_lengths"])
+    assert sync.size == -(-(x.size - 1) // 1024)
+    blk = lc.CompressedBlock(n=ref["n"], eb_abs=ref["eb_abs"], value_range=ref["value_range"],
+                             first_value=ref["first_value"], code_lengths=ref["code_lengths"],
+                             payload=ref["payload"], payload_bits=ref["payload_bits"],
+                             escape_indices=ref["escape_indices"], escape_values=ref["escape_values"],
+                             version=2, sync_offsets=sync)
+    raw = blk.to_bytes()
+    v1 = orc.to_bytes(ref)
+    assert len(raw) == len(v1) + 12 + 8 * sync.size
+    back = lc.CompressedBlock.from_bytes(raw)
+    assert back.version == 2 and np.array_equal(back.sync_offsets, sync)
+    assert back.payload == ref["payload"] and back.to_bytes() == raw
+    bad = bytearray(raw)
+    off = len(v1) - len(ref["payload"])             # sync_k field follows payload_bits
+    bad[off:off + 4] = (512).to_bytes(4, "little")
+    with pytest.raises(lc.IntegrityError):
+        lc.CompressedBlock.from_bytes(bytes(bad))
+    with pytest.raises(lc.IntegrityError):
+        lc.CompressedBlock.from_bytes(raw[:off + 20])
+    with pytest.raises(lc.ParameterError):
+        lc.CompressorConfig.absolute(1.0, block_version=3)
+
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def lc():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1805_07384_b200 as lc
+    return lc
+
+
+def _sine(n, seed=0):
+    r = np.random.default_rng(seed)
+    t = np.arange(n) / n
+    out = sum(r.uniform(0, 1) * np.sin(2 * np.pi * r.uniform(1, 64) * t + r.uniform(0, 6)) for _ in range(8))
+    return out + r.normal(0, 1e-3, n)
+
+
+@pytest.mark.gpu
+def test_v2_matches_v1_and_oracle(lc):
+    rng = np.random.default_rng(77)
+    cases = [(_sine(200_001, 1), 1e-4), (rng.normal(size=70_000).cumsum(), 1e-7),
+             (rng.normal(size=1025), 1e-2), (rng.normal(size=1024), 1e-3), (rng.normal(size=2), 1e-3)]
+    spiky = rng.normal(size=30_000).cumsum()
+    spiky[rng.integers(0, spiky.size, 5)] += 1e9
+    cases.append((spiky, 1e-9))
+    for x, eb in cases:
+        b1 = _blk(lc, x, eb, 1)
+        b2 = _blk(lc, x, eb, 2)
+        ref = orc.compress(x, "value_range_relative", eb)
+        assert b2.payload == b1.payload and np.array_equal(b2.escape_indices, b1.escape_indices)
+        assert np.array_equal(b2.sync_offsets, orc.sync_offsets(ref["codes"], ref["code_lengths"]))
+        b2 = lc.CompressedBlock.from_bytes(b2.to_bytes())
+        r2 = lc.decompress(b2)
+        assert np.array_equal(r2.view(np.int64), ref["recon"].view(np.int64)), (x.size, eb)
+        assert np.array_equal(r2.view(np.int64), lc.decompress(b1).view(np.int64))
+
+
+@pytest.mark.gpu
+def test_v2_full_size(lc):
+    n = 1 << 26
+    x = _sine(n, 5)
+    b2 = _blk(lc, x, 1e-6, 2)
+    b1 = _blk(lc, x, 1e-6, 1)
+    assert b2.sync_offsets.size == -(-(n - 1) // 1024)
+    assert np.all(np.diff(b2.sync_offsets.astype(np.int64)) > 0)
+    d2 = lc.decompress(b2, device="cuda")
+    d1 = lc.decompress(b1, device="cuda")
+    assert torch.equal(d1.view(torch.int64), d2.view(torch.int64))
+    assert float((d2 - torch.from_numpy(x).cuda()).abs().max()) <= b2.eb_abs
+
+
+@pytest.mark.gpu
+def test_v2_corrupted_sync_table(lc):
+    x = np.random.default_rng(4).normal(size=50_000).cumsum()
+    b2 = _blk(lc, x, 1e-6, 2)
+    for j, delta in ((1, 1), (3, -1), (b2.sync_offsets.size - 1, 5), (0, 1)):
+        s = b2.sync_offsets.copy()
+        s[j] = np.uint64(int(s[j]) + delta)
+        with pytest.raises(lc.IntegrityError):
+            lc.decompress(dataclasses.replace(b2, sync_offsets=s))
+    s = b2.sync_offsets.copy()
+    s[2] = np.uint64(b2.payload_bits + 100)
+    with pytest.raises(lc.IntegrityError):
+        lc.decompress(dataclasses.replace(b2, sync_offsets=s))
+    with pytest.raises(lc.IntegrityError):
+        lc.decompress(dataclasses.replace(b2, sync_offsets=b2.sync_offsets[:-1]))
