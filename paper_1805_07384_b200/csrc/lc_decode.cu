@@ -936,7 +936,7 @@ struct LcRecParams {
     int *esc_flags;             // [0] more escape codes than values, [1] position mismatch
 };
 
-__device__ __forceinline__ int64_t lc_code_m(uint32_t code) { return lc_unzigzag(code); }
+__device__ __forceinline__ int lc_code_m(uint32_t code) { return lc_unzigzag(code); }
 
 // ---------------------------------------------------------------------------
 // Split reconstruction (no inter-tile waiting): R0 segmented m-prefix per tile,
@@ -1006,7 +1006,7 @@ __device__ __forceinline__ LcSegScan lc_chunk_segscan(const uint32_t *crow, int 
     for (int j = 0; j < len; ++j) {
         const uint32_t code = crow[j];
         if (code == 0) { mine.sum = 0; mine.cnt += 1; mine.has = 1; mine.moved = 0; }
-        else { const int64_t mm = lc_code_m(code); mine.sum += mm; mine.moved |= (mm != 0); }
+        else { const int mm = lc_code_m(code); mine.sum += mm; mine.moved |= (mm != 0); }
     }
     return mine;
 }
@@ -1063,7 +1063,7 @@ __global__ void __launch_bounds__(LC_TPB) lc_rec0_kernel(LcRecParams P, LcRecSpl
             if (j < len) {
                 const uint32_t code = v[j];
                 if (code == 0) { mine.sum = 0; mine.cnt += 1; mine.has = 1; mine.moved = 0; }
-                else { const int64_t mm = lc_code_m(code); mine.sum += mm; mine.moved |= (mm != 0); }
+                else { const int mm = lc_code_m(code); mine.sum += mm; mine.moved |= (mm != 0); }
             }
         }
         __syncthreads();
@@ -1180,7 +1180,7 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_rec_a_kernel(LcRecParams P, LcRe
             for (int j = 0; j < len; ++j) {
                 const uint32_t code = crow[j];
                 const bool esc = code == 0;
-                const int64_t m = lc_code_m(code);
+                const int m = lc_code_m(code);
                 const double inc_ = LC_MUL((double)m, P.delta);
                 double rn = m != 0 ? LC_ADD(r, inc_) : r;
                 if (esc) { rn = e < (long long)P.n_esc ? P.esc_val[e] : 0.0; ++e; }
@@ -1195,7 +1195,7 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_rec_a_kernel(LcRecParams P, LcRe
                 const int j0 = __ffs(E.mask) - 1, j1 = 31 - __clz(E.mask);
                 double r2 = E.r_first;
                 for (int j = j0; j <= j1; ++j) {
-                    const int64_t m = lc_code_m(crow[j]);  // no escape here (E.esc would be set)
+                    const int m = lc_code_m(crow[j]);  // no escape here (E.esc would be set)
                     if (m != 0) {
                         const double inc_ = LC_MUL((double)m, P.delta);
                         const double rn = LC_ADD(r2, inc_);
@@ -1233,11 +1233,14 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_rec_a_kernel(LcRecParams P, LcRe
     }
 }
 
-__global__ void __launch_bounds__(LC_TPB, 2) lc_rec_b_kernel(LcRecParams P, LcRecSplit S)
+// Exact chain (compressor.py:360-375): codes straight into registers (no smem
+// staging), all per-chunk loads issued together, results transposed through
+// padded smem rows and written with 16-byte streaming stores.
+template <int CB>
+__global__ void __launch_bounds__(LC_TPB, 3) lc_rec_b_kernel(LcRecParams P, LcRecSplit S)
 {
     extern __shared__ __align__(16) unsigned char lc_dyn_smem[];
     double *ys = reinterpret_cast<double *>(lc_dyn_smem);
-    uint32_t *cs = reinterpret_cast<uint32_t *>(ys + LC_TPB * LC_ROW);
     __shared__ double starts[LC_TPB + 1];
     const int tid = threadIdx.x;
     const long long nel = (long long)P.n - 1;
@@ -1247,32 +1250,57 @@ __global__ void __launch_bounds__(LC_TPB, 2) lc_rec_b_kernel(LcRecParams P, LcRe
         const long long c = cbeg + tid;
         const long long p0 = c * LC_L;
         const int len = (c < P.nchunks) ? (int)min((long long)LC_L, nel - p0) : 0;
-        __syncthreads();
-        lc_load_codes_tile(P, pbeg, cs);
-        const double Dt = S.tile_D[t];
+        uint32_t v[LC_L];
+        if (len == LC_L) {
+            if (CB == 2) {
+                const uint4 *src = reinterpret_cast<const uint4 *>(reinterpret_cast<const uint16_t *>(P.codes) + p0);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint4 q = __ldcs(src + k);
+                    const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) { v[8 * k + 2 * h] = w4[h] & 0xffffu; v[8 * k + 2 * h + 1] = w4[h] >> 16; }
+                }
+            } else {
+                const uint4 *src = reinterpret_cast<const uint4 *>(reinterpret_cast<const uint32_t *>(P.codes) + p0);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const uint4 q = __ldcs(src + k);
+                    v[4 * k] = q.x; v[4 * k + 1] = q.y; v[4 * k + 2] = q.z; v[4 * k + 3] = q.w;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < LC_L; ++j)
+                v[j] = j < len ? (CB == 2 ? (uint32_t)reinterpret_cast<const uint16_t *>(P.codes)[p0 + j]
+                                          : reinterpret_cast<const uint32_t *>(P.codes)[p0 + j]) : 1u;
+        }
         double start = 0.0;
+        long long e = 0;
         if (len > 0) {
             OffMap m;
             m.kind = S.pred.kind[c]; m.B = S.pred.B[c]; m.t0 = S.pred.t0[c]; m.t1 = S.pred.t1[c]; m.y = S.pred.y[c];
             m.v = 0.0; m.og = 0.0;
-            start = lc_apply_offset(S.pred.g0[c], lc_map_eval(m, Dt));
+            const double g0 = S.pred.g0[c];
+            e = P.chunk_esc[c];
+            start = lc_apply_offset(g0, lc_map_eval(m, S.tile_D[t]));
         }
+        __syncthreads();                                 // previous tile's ys/starts reads are done
         starts[tid] = start;
         if (tid == LC_TPB - 1) {
             const long long cn = cbeg + LC_TPB;
             starts[LC_TPB] = (cn < P.nchunks) ? lc_apply_offset(S.pred.g0[cn], S.tile_D[t + 1]) : 0.0;
         }
         __syncthreads();
-        const uint32_t *crow = cs + tid * LC_ROW;
         double *yrow = ys + tid * LC_ROW;
         if (len > 0) {
             double r = start;
-            long long e = P.chunk_esc[c];
-            for (int j = 0; j < len; ++j) {
-                const uint32_t code = crow[j];
-                const int64_t m = lc_code_m(code);
-                double rn = m != 0 ? LC_ADD(r, LC_MUL((double)m, P.delta)) : r;   // compressor.py:371-374
-                if (code == 0) {                                                   // :365-369
+#pragma unroll
+            for (int j = 0; j < LC_L; ++j) {
+                const uint32_t code = v[j];
+                const int mm = lc_code_m(code);
+                double rn = mm != 0 ? LC_ADD(r, LC_MUL((double)mm, P.delta)) : r;   // compressor.py:371-374
+                if (code == 0) {                                                     // :365-369
                     if (e < (long long)P.n_esc) {
                         rn = P.esc_val[e];
                         if (P.esc_idx[e] != (unsigned long long)(p0 + j + 1)) atomicExch(&P.esc_flags[1], 1);
@@ -1283,6 +1311,7 @@ __global__ void __launch_bounds__(LC_TPB, 2) lc_rec_b_kernel(LcRecParams P, LcRe
                 }
                 yrow[j] = rn;
                 r = rn;
+                if (j + 1 == len) break;
             }
             if (c + 1 < P.nchunks && lc_bits(r) != lc_bits(starts[tid + 1])) {
                 P.bad_end[c] = r;
@@ -1290,17 +1319,29 @@ __global__ void __launch_bounds__(LC_TPB, 2) lc_rec_b_kernel(LcRecParams P, LcRe
             }
         }
         __syncthreads();
-#pragma unroll 8
-        for (int k = 0; k < LC_L; ++k) {
-            const int off = k * LC_TPB + tid;
-            const long long pos = pbeg + 1 + off;
-            if (pos <= nel) __stcs(P.out + pos, ys[(off >> 5) * LC_ROW + (off & 31)]);
+        // out[pbeg + 1 + off], off = 0..8191: pairs (off, off+1) from smem, 16-byte
+        // stores at even out positions (out + pbeg + 1 is 16-byte aligned iff out is
+        // 8 mod 16, so the pairing phase follows the base address).
+        const long long q0 = pbeg + 1;
+        const int ph = (int)(((reinterpret_cast<uintptr_t>(P.out + q0)) >> 3) & 1);   // 1: first element alone
+        const long long tile_n = min((long long)LC_TILE, nel - pbeg);
+        if (ph && tid == 0) __stcs(P.out + q0, ys[0]);
+#pragma unroll 4
+        for (int k = 0; k < LC_L / 2; ++k) {
+            const int off = ph + 2 * (k * LC_TPB + tid);
+            if (off + 1 < tile_n) {
+                const double a = ys[(off >> 5) * LC_ROW + (off & 31)];
+                const double b = ys[((off + 1) >> 5) * LC_ROW + ((off + 1) & 31)];
+                __stcs(reinterpret_cast<double2 *>(P.out + q0 + off), make_double2(a, b));
+            } else if (off < tile_n) {
+                __stcs(P.out + q0 + off, ys[(off >> 5) * LC_ROW + (off & 31)]);
+            }
         }
     }
 }
 
 size_t lc_rec_a_smem_bytes() { return sizeof(uint32_t) * LC_TPB * LC_ROW; }
-size_t lc_rec_b_smem_bytes() { return sizeof(double) * LC_TPB * LC_ROW + sizeof(uint32_t) * LC_TPB * LC_ROW; }
+size_t lc_rec_b_smem_bytes() { return sizeof(double) * LC_TPB * LC_ROW; }
 
 
 __global__ void lc_set_first_kernel(double *out, double v) { out[0] = v; }
@@ -1332,7 +1373,7 @@ int lc_decompress_impl2(lc_ctx *ctx, uint64_t n, double eb_abs, double first_val
                         const double *esc_val, uint64_t n_esc, int inputs_on_device, double *out,
                         int out_on_device, int64_t *esc_used, const uint64_t *sync, uint64_t n_sync)
 {
-    if (n < 2 || n_lengths == 0 || payload_bits > 8 * payload_bytes) return 12;
+    if (n < 2 || n_lengths == 0 || n_lengths > (1ull << 31) + 2 || payload_bits > 8 * payload_bytes) return 12;
     cudaStream_t st = lc_stream(ctx);
     LcBuf *B = lc_dec_bufs(ctx);      // ctx->dec[10]
     LcBuf &bpay = B[0], &blen = B[1], &beidx = B[2], &beval = B[3], &bout = B[4], &bcodes = B[5], &btab = B[6],
@@ -1580,7 +1621,9 @@ static int lc_reconstruct(lc_ctx *ctx, uint64_t n, double eb_abs, double first_v
     if (!attr_b) {
         LC_CUDA_OK(cudaFuncSetAttribute(lc_rec_a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)lc_rec_a_smem_bytes()));
-        LC_CUDA_OK(cudaFuncSetAttribute(lc_rec_b_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        LC_CUDA_OK(cudaFuncSetAttribute(lc_rec_b_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)lc_rec_b_smem_bytes()));
+        LC_CUDA_OK(cudaFuncSetAttribute(lc_rec_b_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)lc_rec_b_smem_bytes()));
         attr_b = true;
     }
@@ -1593,14 +1636,15 @@ static int lc_reconstruct(lc_ctx *ctx, uint64_t n, double eb_abs, double first_v
     for (;;) {
         R.ntiles = (nchunks - R.first_chunk + LC_TPB - 1) / LC_TPB;
         LC_CUDA_OK(cudaMemsetAsync(R.first_bad, 0xff, 8, st));
-        const int grid = (int)(R.ntiles < grid_cap ? R.ntiles : grid_cap);
         lc_rec0_kernel<<<(int)(R.ntiles < 3 * grid_cap ? R.ntiles : 3 * grid_cap), LC_TPB, 0, st>>>(R, RS);
         lc_rec0_scan_kernel<<<1, 512, 0, st>>>(RS, R.ntiles, R.anchor_cnt);
         lc_rec_a_kernel<<<(int)(R.ntiles < 3 * lc_sm_count(ctx) ? R.ntiles : 3 * lc_sm_count(ctx)), LC_TPB,
                           lc_rec_a_smem_bytes(), st>>>(R, RS);
         { int _rc = lc_debug_check(ctx, "lc_rec_a_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
         lc_map_scan_kernel<<<1, 1024, 0, st>>>(RS.tile_agg, RS.tile_D, R.ntiles);
-        lc_rec_b_kernel<<<grid, LC_TPB, lc_rec_b_smem_bytes(), st>>>(R, RS);
+        const int grid_b = (int)(R.ntiles < 3 * lc_sm_count(ctx) ? R.ntiles : 3 * lc_sm_count(ctx));
+        if (code_bytes == 2) lc_rec_b_kernel<2><<<grid_b, LC_TPB, lc_rec_b_smem_bytes(), st>>>(R, RS);
+        else lc_rec_b_kernel<4><<<grid_b, LC_TPB, lc_rec_b_smem_bytes(), st>>>(R, RS);
         { int _rc = lc_debug_check(ctx, "lc_rec_b_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
         lc_count_launch(ctx, 5);
         LC_CUDA_OK(cudaMemcpyAsync(hbad, R.first_bad, 8, cudaMemcpyDeviceToHost, st));
