@@ -293,11 +293,10 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     }
     CodeT *codes = (CodeT *)ctx->codes.p;
 
-    LC_CUDA_OK(cudaMemcpyAsync(&P.anchor_val, dx, sizeof(double), cudaMemcpyDeviceToHost, st));
-    LC_CUDA_OK(cudaStreamSynchronize(st));
     LC_CUDA_OK(cudaMemsetAsync(P.hist, 0, nbins * sizeof(uint32_t), st));
 
     unsigned long long *hbad = (unsigned long long *)ctx->pinned;
+    LcCodebookOut *hcb = (LcCodebookOut *)((char *)ctx->pinned + 64);
     uint32_t relaunches = 0;
     LC_CUDA_OK(cudaEventRecord(ctx->pev[1], st));
     // split-pass buffers
@@ -324,7 +323,7 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
         P.use_anchors = ((ms * (1.0 - 0x1p-50)) - (eb_abs * (1.0 + 0x1p-50))) >= P.esc_thresh || !isfinite(ms);
     }
     const int ga = 3 * ctx->sm_count, gb = 3 * ctx->sm_count;
-    for (;;) {
+    auto quant_launch = [&]() -> int {
         P.ntiles = (nchunks - P.first_chunk + LC_TPB - 1) / LC_TPB;
         LC_CUDA_OK(cudaMemsetAsync(first_bad, 0xff, 8, st));
         if (P.use_anchors) {
@@ -338,32 +337,19 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
         lc_quant_b_kernel<CodeT><<<(int)(P.ntiles < gb ? P.ntiles : gb), LC_TPB, lc_quant_b_smem_bytes(), st>>>(P, codes);
         { int _rc = lc_debug_check(ctx, "lc_quant_b_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
         ctx->launches += 3;
-        LC_CUDA_OK(cudaMemcpyAsync(hbad, first_bad, 8, cudaMemcpyDeviceToHost, st));
-        LC_CUDA_OK(cudaStreamSynchronize(st));
-        const unsigned long long fb = *hbad;
-        if (fb == ~0ULL) break;
-        ++relaunches;
-        double anchor;
-        LC_CUDA_OK(cudaMemcpy(&anchor, P.bad_end + (fb - 1), sizeof(double), cudaMemcpyDeviceToHost));
-        P.first_chunk = (int64_t)fb;
-        P.anchor_val = anchor;
-        P.count_hist = 0;
-        if (relaunches > 64) {                      // pathological input: exact serial chain
-            lc_quant_serial_kernel<CodeT><<<1, 32, 0, st>>>(P, codes);
-            { int _rc = lc_debug_check(ctx, "lc_quant_serial_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
-            ctx->launches += 1;
-            break;
-        }
-    }
-    if (relaunches) {
-        LC_CUDA_OK(cudaMemsetAsync(P.hist, 0, nbins * sizeof(uint32_t), st));
-        lc_hist_kernel<CodeT><<<4 * ctx->sm_count, 256, 0, st>>>(codes, m, P.hist, nbins);
-        { int _rc = lc_debug_check(ctx, "lc_hist_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
-        ctx->launches += 1;
-    }
-    LC_CUDA_OK(cudaEventRecord(ctx->pev[2], st));
+        return 0;
+    };
 
-    // codebook
+    // codebook + encoder buffers: the payload is at most ceil(log2(nbins)) bits per
+    // symbol (a fixed-length code is never shorter than the Huffman code), so it is
+    // sized before the codebook is known; escapes use the capacity of the last call
+    // and are re-gathered when short (the host sees the count after the one sync).
+    int lg = 1;
+    while ((1ull << lg) < nbins) ++lg;
+    const uint64_t words_cap = (m * (uint64_t)lg + 31) / 32 + 2;
+    LC_CUDA_OK(lc_reserve(ctx->payload, words_cap * 4));
+    LC_CUDA_OK(lc_reserve(ctx->esc_idx, 64 * 8));
+    LC_CUDA_OK(lc_reserve(ctx->esc_val, 64 * 8));
     LC_CUDA_OK(lc_reserve(ctx->lengths, nbins));
     LC_CUDA_OK(lc_reserve(ctx->cw, nbins * sizeof(unsigned long long)));
     LC_CUDA_OK(lc_reserve(ctx->gkeys, 3 * (size_t)nbins * sizeof(unsigned long long)));
@@ -371,29 +357,10 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     LC_CUDA_OK(lc_reserve(ctx->parent, 2 * (size_t)nbins * sizeof(int)));
     LC_CUDA_OK(lc_reserve(ctx->cbout, sizeof(LcCodebookOut)));
     LcCodebookOut *cbo = (LcCodebookOut *)ctx->cbout.p;
-    lc_codebook_kernel<<<1, 1024, lc_codebook_smem_bytes(), st>>>(
-        P.hist, nbins, (uint8_t *)ctx->lengths.p, (unsigned long long *)ctx->cw.p,
-        (unsigned long long *)ctx->gkeys.p, (unsigned long long *)ctx->ifreq.p, (int *)ctx->parent.p, cbo);
-    { int _rc = lc_debug_check(ctx, "lc_codebook_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
-    LC_CUDA_OK(cudaEventRecord(ctx->pev[3], st));
-    ctx->launches += 1;
-    LcCodebookOut *hcb = (LcCodebookOut *)ctx->pinned;
-    LC_CUDA_OK(cudaMemcpyAsync(hcb, cbo, sizeof(LcCodebookOut), cudaMemcpyDeviceToHost, st));
-    LC_CUDA_OK(cudaStreamSynchronize(st));
-    ctx->cb = *hcb;
-    if (ctx->cb.status) {
-        ctx->err = "code length exceeds 64 bits";
-        return ctx->cb.status;
-    }
-    const uint64_t words = (ctx->cb.total_bits + 31) / 32;
-    LC_CUDA_OK(lc_reserve(ctx->payload, (words + 1) * 4));
-    LC_CUDA_OK(lc_reserve(ctx->esc_idx, (ctx->cb.n_esc + 1) * 8));
-    LC_CUDA_OK(lc_reserve(ctx->esc_val, (ctx->cb.n_esc + 1) * 8));
-    lc_zero_words_kernel<<<2 * ctx->sm_count, 256, 0, st>>>((uint32_t *)ctx->payload.p, cbo);
     const uint64_t etiles = (m + LC_TILE - 1) / LC_TILE;
     LC_CUDA_OK(lc_reserve(ctx->encdesc, etiles * sizeof(LcEncDesc)));
-    LC_CUDA_OK(cudaMemsetAsync(ctx->encdesc.p, 0, etiles * sizeof(LcEncDesc), st));
-    LC_CUDA_OK(cudaMemsetAsync(ctx->counters.p, 0, 16, st));
+    ctx->nsync = (m + LC_SYNC_K - 1) / LC_SYNC_K;
+    LC_CUDA_OK(lc_reserve(ctx->sync, (ctx->nsync + 1) * 8));
     LcEncParams E;
     E.codes = codes;
     E.m = m;
@@ -402,23 +369,90 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     E.nbins = nbins;
     E.payload = (uint32_t *)ctx->payload.p;
     E.x = dx;
-    E.esc_idx = (unsigned long long *)ctx->esc_idx.p;
-    E.esc_val = (double *)ctx->esc_val.p;
     E.desc = (LcEncDesc *)ctx->encdesc.p;
     E.tile_counter = tile_counter;
     E.ntiles = etiles;
-    E.max_len = ctx->cb.max_len;
-    ctx->nsync = (m + LC_SYNC_K - 1) / LC_SYNC_K;
-    LC_CUDA_OK(lc_reserve(ctx->sync, (ctx->nsync + 1) * 8));
+    E.cb = cbo;
     E.sync = (unsigned long long *)ctx->sync.p;
     const int egrid = (int)(etiles < (uint64_t)(4 * ctx->sm_count) ? etiles : 4 * ctx->sm_count);
-    lc_encode_kernel<CodeT><<<egrid, LC_TPB, lc_encode_smem_bytes(), st>>>(E);
-    { int _rc = lc_debug_check(ctx, "lc_encode_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
-    ctx->launches += 2;
-    LC_CUDA_OK(cudaEventRecord(ctx->pev[4], st));
+    auto codebook_launch = [&]() -> int {
+        LC_CUDA_OK(cudaEventRecord(ctx->pev[2], st));
+        lc_codebook_kernel<<<1, 1024, lc_codebook_smem_bytes(), st>>>(
+            P.hist, nbins, (uint8_t *)ctx->lengths.p, (unsigned long long *)ctx->cw.p,
+            (unsigned long long *)ctx->gkeys.p, (unsigned long long *)ctx->ifreq.p, (int *)ctx->parent.p, cbo);
+        { int _rc = lc_debug_check(ctx, "lc_codebook_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+        LC_CUDA_OK(cudaEventRecord(ctx->pev[3], st));
+        ctx->launches += 1;
+        return 0;
+    };
+    auto encode_launch = [&]() -> int {
+        E.esc_idx = (unsigned long long *)ctx->esc_idx.p;
+        E.esc_val = (double *)ctx->esc_val.p;
+        E.esc_cap = ctx->esc_idx.cap / 8;
+        lc_zero_words_kernel<<<2 * ctx->sm_count, 256, 0, st>>>((uint32_t *)ctx->payload.p, cbo);
+        LC_CUDA_OK(cudaMemsetAsync(ctx->encdesc.p, 0, etiles * sizeof(LcEncDesc), st));
+        LC_CUDA_OK(cudaMemsetAsync(ctx->counters.p, 0, 16, st));
+        lc_encode_kernel<CodeT><<<egrid, LC_TPB, lc_encode_smem_bytes(), st>>>(E);
+        { int _rc = lc_debug_check(ctx, "lc_encode_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+        ctx->launches += 2;
+        LC_CUDA_OK(cudaEventRecord(ctx->pev[4], st));
+        return 0;
+    };
+    auto readback = [&]() -> int {                       // the one host round trip
+        LC_CUDA_OK(cudaMemcpyAsync(hbad, first_bad, 8, cudaMemcpyDeviceToHost, st));
+        LC_CUDA_OK(cudaMemcpyAsync(hcb, cbo, sizeof(LcCodebookOut), cudaMemcpyDeviceToHost, st));
+        LC_CUDA_OK(cudaStreamSynchronize(st));
+        return 0;
+    };
+
+    // common path: quantize, codebook and encode back to back, one sync
+    { int _rc = quant_launch(); if (_rc) return _rc; }
+    { int _rc = codebook_launch(); if (_rc) return _rc; }
+    { int _rc = encode_launch(); if (_rc) return _rc; }
+    { int _rc = readback(); if (_rc) return _rc; }
+    if (*hbad != ~0ULL) {
+        // a chunk prediction failed: relaunch from the first bad chunk (anchor =
+        // the exact end of its predecessor) until every check passes
+        for (;;) {
+            const unsigned long long fb = *hbad;
+            if (fb == ~0ULL) break;
+            ++relaunches;
+            double anchor;
+            LC_CUDA_OK(cudaMemcpy(&anchor, P.bad_end + (fb - 1), sizeof(double), cudaMemcpyDeviceToHost));
+            P.first_chunk = (int64_t)fb;
+            P.anchor_val = anchor;
+            P.count_hist = 0;
+            if (relaunches > 64) {                      // pathological input: exact serial chain
+                lc_quant_serial_kernel<CodeT><<<1, 32, 0, st>>>(P, codes);
+                { int _rc = lc_debug_check(ctx, "lc_quant_serial_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+                ctx->launches += 1;
+                break;
+            }
+            { int _rc = quant_launch(); if (_rc) return _rc; }
+            LC_CUDA_OK(cudaMemcpyAsync(hbad, first_bad, 8, cudaMemcpyDeviceToHost, st));
+            LC_CUDA_OK(cudaStreamSynchronize(st));
+        }
+        LC_CUDA_OK(cudaMemsetAsync(P.hist, 0, nbins * sizeof(uint32_t), st));
+        lc_hist_kernel<CodeT><<<4 * ctx->sm_count, 256, 0, st>>>(codes, m, P.hist, nbins);
+        { int _rc = lc_debug_check(ctx, "lc_hist_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+        ctx->launches += 1;
+        { int _rc = codebook_launch(); if (_rc) return _rc; }
+        { int _rc = encode_launch(); if (_rc) return _rc; }
+        { int _rc = readback(); if (_rc) return _rc; }
+    }
+    ctx->cb = *hcb;
+    if (ctx->cb.status) {
+        ctx->err = "code length exceeds 64 bits";
+        return ctx->cb.status;
+    }
+    if (ctx->cb.n_esc > ctx->esc_idx.cap / 8) {          // more escapes than the last call: re-gather
+        LC_CUDA_OK(lc_reserve(ctx->esc_idx, (ctx->cb.n_esc + 1) * 8));
+        LC_CUDA_OK(lc_reserve(ctx->esc_val, (ctx->cb.n_esc + 1) * 8));
+        { int _rc = encode_launch(); if (_rc) return _rc; }
+        { int _rc = readback(); if (_rc) return _rc; }
+    }
     LC_CUDA_OK(cudaEventRecord(ctx->ev1, st));
     ctx->last_kind = 1;
-    LC_CUDA_OK(cudaStreamSynchronize(st));
 
     ctx->n = n;
     ctx->nbins = nbins;

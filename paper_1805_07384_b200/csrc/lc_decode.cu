@@ -420,8 +420,9 @@ template <int NS>
 __global__ void __launch_bounds__(LC_DEC_TPB) lc_dec_sync_kernel(LcDecParams P, LcSeg *__restrict__ seg,
                                                                 const LcBlkOut *__restrict__ bprev,
                                                                 LcBlkOut *__restrict__ bcur, int first_pass,
-                                                                int *__restrict__ changed)
+                                                                int *__restrict__ changed, const int *need)
 {
+    if (need && *(volatile const int *)need == 0) return;   // speculative general pass not needed
     __shared__ LcDecTables Ts;
     __shared__ unsigned s_exit[LC_DEC_TPB];
     __shared__ int s_skip;
@@ -934,7 +935,13 @@ struct LcRecParams {
     double *bad_end;
     long long *chunk_esc;       // escapes up to each chunk's start (inclusive of position cL)
     int *esc_flags;             // [0] more escape codes than values, [1] position mismatch
+    const int *abort_a, *abort_b;   // decode status / cascade flag: non-zero -> kernels exit (no host sync before)
 };
+
+__device__ __forceinline__ bool lc_rec_aborted(const LcRecParams &P)
+{
+    return (P.abort_a && *(volatile const int *)P.abort_a) || (P.abort_b && *(volatile const int *)P.abort_b);
+}
 
 __device__ __forceinline__ int lc_code_m(uint32_t code) { return lc_unzigzag(code); }
 
@@ -1049,6 +1056,7 @@ __device__ __forceinline__ LcSegScan lc_block_segscan(const LcSegScan &mine, LcS
 __global__ void __launch_bounds__(LC_TPB) lc_rec0_kernel(LcRecParams P, LcRecSplit S)
 {
     __shared__ LcSegScan wseg[LC_TPB / 32];
+    if (lc_rec_aborted(P)) return;
     const int tid = threadIdx.x;
     const long long nel = (long long)P.n - 1;
     for (long long t = blockIdx.x; t < P.ntiles; t += gridDim.x) {
@@ -1140,6 +1148,7 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_rec_a_kernel(LcRecParams P, LcRe
     __shared__ OffMap warp_agg[LC_TPB / 32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const long long nel = (long long)P.n - 1;
+    if (lc_rec_aborted(P)) return;
     for (long long t = blockIdx.x; t < P.ntiles; t += gridDim.x) {
         const long long cbeg = P.first_chunk + t * LC_TPB;
         const long long c = cbeg + tid;
@@ -1244,6 +1253,7 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_rec_b_kernel(LcRecParams P, LcRe
     __shared__ double starts[LC_TPB + 1];
     const int tid = threadIdx.x;
     const long long nel = (long long)P.n - 1;
+    if (lc_rec_aborted(P)) return;
     for (long long t = blockIdx.x; t < P.ntiles; t += gridDim.x) {
         const long long cbeg = P.first_chunk + t * LC_TPB;
         const long long pbeg = cbeg * LC_L;
@@ -1365,7 +1375,8 @@ int lc_debug_check(lc_ctx *ctx, const char *what, const char *file, int line);
 
 static int lc_reconstruct(lc_ctx *ctx, uint64_t n, double eb_abs, double first_value, const double *esc_val_in,
                           uint64_t n_esc, double *out, int out_on_device, int64_t *esc_used, void *codes,
-                          int code_bytes);
+                          int code_bytes, const int *abort_a, const int *abort_b, int *abort_hit);
+#define LC_RC_CASCADE (-100)   // lc_reconstruct: the decode needs general sync passes, redo
 
 int lc_decompress_impl2(lc_ctx *ctx, uint64_t n, double eb_abs, double first_value,
                         const uint8_t *code_lengths, uint64_t n_lengths, const uint8_t *payload,
@@ -1439,12 +1450,9 @@ int lc_decompress_impl2(lc_ctx *ctx, uint64_t n, double eb_abs, double first_val
             lc_dec_v2_kernel<uint32_t><<<g, 256, 0, st>>>(DP, (const unsigned long long *)bsync.p, n_sync, bcodes.p, m, status);
         { int _rc = lc_debug_check(ctx, "lc_dec_v2_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
         lc_count_launch(ctx, 1);
-        int *hstat = (int *)lc_pinned(ctx);
-        LC_CUDA_OK(cudaMemcpyAsync(hstat, status, 4, cudaMemcpyDeviceToHost, st));
-        LC_CUDA_OK(cudaStreamSynchronize(st));
-        if (*hstat) return *hstat;
+        int hit;                                         // the status is checked with the final readback
         return lc_reconstruct(ctx, n, eb_abs, first_value, esc_val, n_esc, out, out_on_device, esc_used,
-                              bcodes.p, code_bytes);
+                              bcodes.p, code_bytes, status, nullptr, &hit);
     }
     // segment size: ~40 average codewords (canonical codes resynchronise
     // within a few codewords), 128..1024 bits, while keeping >= 2 waves of CTAs
@@ -1489,32 +1497,78 @@ int lc_decompress_impl2(lc_ctx *ctx, uint64_t n, double eb_abs, double first_val
     case 8: LC_CUDA_OK(cudaFuncSetAttribute(lc_dec_sync_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm)); break;
     default: LC_CUDA_OK(cudaFuncSetAttribute(lc_dec_sync_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm)); break;
     }
-    auto sync_launch = [&](LcBlkOut *bp, LcBlkOut *bc, int first) {
+    auto sync_launch = [&](LcBlkOut *bp, LcBlkOut *bc, int first, int *chg, const int *need) {
         switch (sub) {
-        case 2: lc_dec_sync_kernel<2><<<pgrid_, LC_DEC_TPB, ssm, st>>>(DP, segs, bp, bc, first, changed); break;
-        case 4: lc_dec_sync_kernel<4><<<pgrid_, LC_DEC_TPB, ssm, st>>>(DP, segs, bp, bc, first, changed); break;
-        case 8: lc_dec_sync_kernel<8><<<pgrid_, LC_DEC_TPB, ssm, st>>>(DP, segs, bp, bc, first, changed); break;
-        default: lc_dec_sync_kernel<16><<<pgrid_, LC_DEC_TPB, ssm, st>>>(DP, segs, bp, bc, first, changed); break;
+        case 2: lc_dec_sync_kernel<2><<<pgrid_, LC_DEC_TPB, ssm, st>>>(DP, segs, bp, bc, first, chg, need); break;
+        case 4: lc_dec_sync_kernel<4><<<pgrid_, LC_DEC_TPB, ssm, st>>>(DP, segs, bp, bc, first, chg, need); break;
+        case 8: lc_dec_sync_kernel<8><<<pgrid_, LC_DEC_TPB, ssm, st>>>(DP, segs, bp, bc, first, chg, need); break;
+        default: lc_dec_sync_kernel<16><<<pgrid_, LC_DEC_TPB, ssm, st>>>(DP, segs, bp, bc, first, chg, need); break;
         }
     };
     int *hchanged = (int *)lc_pinned(ctx);
-    sync_launch(bo_b, bo_a, 1);
+    sync_launch(bo_b, bo_a, 1, changed, nullptr);
     { int _rc = lc_debug_check(ctx, "lc_dec_sync_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
     lc_count_launch(ctx, 1);
     LcBlkOut *bprev = bo_a, *bcur = bo_b;
-    bool general = false;
-    if (nblk > 1) {                                     // boundary fix; general passes only on a cascade
-        LC_CUDA_OK(cudaMemsetAsync(changed, 0, 4, st));
+    int *changed2 = changed + 1;
+    // CTA-boundary fix; a cascade (a CTA's own exit moved) needs general passes.
+    // That is rare, so the rest of the decode and the reconstruction are queued
+    // right behind the fix and the flag is read with their final readback; on a
+    // cascade the reconstruction kernels exit at once and the host redoes them.
+    // One general pass is queued speculatively: it returns at once unless the
+    // fix flagged a cascade (common at high bits per symbol); a second cascade
+    // (its own flag) is left to the host.
+    LC_CUDA_OK(cudaMemsetAsync(changed, 0, 8, st));
+    if (nblk > 1) {
         lc_dec_fix_kernel<<<(int)((nblk - 1 + 127) / 128), 128, 0, st>>>(DP, segs, bo_a, changed);
         { int _rc = lc_debug_check(ctx, "lc_dec_fix_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
-        lc_count_launch(ctx, 1);
-        LC_CUDA_OK(cudaMemcpyAsync(hchanged, changed, 4, cudaMemcpyDeviceToHost, st));
-        LC_CUDA_OK(cudaStreamSynchronize(st));
-        general = *hchanged != 0;
+        sync_launch(bprev, bcur, 0, changed2, changed);
+        { int _rc = lc_debug_check(ctx, "lc_dec_sync_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+        lc_count_launch(ctx, 2);
+        LcBlkOut *tmp = bprev; bprev = bcur; bcur = tmp;
     }
-    for (int it = 0; general && it < 1000000; ++it) {
+    auto tail = [&]() -> int {                           // count scan, write, status
+        LC_CUDA_OK(cudaEventRecord(lc_phase_ev(ctx, 8), st));
+        LC_CUDA_OK(cudaMemsetAsync(sdesc, 0, scan_tiles * sizeof(LcScanDesc), st));
+        LC_CUDA_OK(cudaMemsetAsync(scan_counter, 0, 4, st));
+        LC_CUDA_OK(cudaMemsetAsync(tot + 1, 0xff, 8, st));
+        {
+            const int g = (int)(scan_tiles < (unsigned long long)(2 * lc_sm_count(ctx)) ? scan_tiles : 2 * lc_sm_count(ctx));
+            lc_dec_scan_kernel<<<g, LC_TPB, 0, st>>>(segs, nseg, offs, sdesc, scan_counter, tot);
+            { int _rc = lc_debug_check(ctx, "lc_dec_scan_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+        }
+        LC_CUDA_OK(cudaEventRecord(lc_phase_ev(ctx, 9), st));
+        LC_CUDA_OK(cudaMemsetAsync(endpos, 0xff, 8, st));
+        {
+            // output window per warp: the typical 32-segment range (+25%), <= 4096 symbols
+            const double syms_per_seg = (double)m * seg_bits / (double)(payload_bits ? payload_bits : 1);
+            long long cap = (long long)(1.25 * 32.0 * syms_per_seg);
+            cap = (cap + 63) / 64 * 64;
+            if (cap < 256) cap = 256;
+            if (cap > 4096) cap = 4096;
+            const size_t wsm = lc_dec_write_smem((int)cap, code_bytes, seg_bits);
+            const int wgrid = (int)(nblk < (long long)(2 * lc_sm_count(ctx)) ? nblk : 2 * lc_sm_count(ctx));
+            if (code_bytes == 2) {
+                LC_CUDA_OK(cudaFuncSetAttribute(lc_dec_write_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+                lc_dec_write_kernel<uint16_t><<<wgrid, LC_DEC_TPB, wsm, st>>>(DP, segs, offs, bcodes.p, m, endpos, (int)cap);
+            } else {
+                LC_CUDA_OK(cudaFuncSetAttribute(lc_dec_write_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+                lc_dec_write_kernel<uint32_t><<<wgrid, LC_DEC_TPB, wsm, st>>>(DP, segs, offs, bcodes.p, m, endpos, (int)cap);
+            }
+        }
+        lc_dec_status_kernel<<<1, 1, 0, st>>>(segs, offs, tot, endpos, m, payload_bits, status);
+        { int _rc = lc_debug_check(ctx, "lc_dec_status_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+        lc_count_launch(ctx, 3);
+        return 0;
+    };
+    { int _rc = tail(); if (_rc) return _rc; }
+    int hit = 0;
+    int rc = lc_reconstruct(ctx, n, eb_abs, first_value, esc_val, n_esc, out, out_on_device, esc_used, bcodes.p,
+                            code_bytes, status, nblk > 1 ? changed2 : nullptr, &hit);
+    if (rc != LC_RC_CASCADE) return rc;
+    for (int it = 0; it < 1000000; ++it) {              // general passes until no CTA exit moves
         LC_CUDA_OK(cudaMemsetAsync(changed, 0, 4, st));
-        sync_launch(bprev, bcur, 0);
+        sync_launch(bprev, bcur, 0, changed, nullptr);
         { int _rc = lc_debug_check(ctx, "lc_dec_sync_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
         lc_count_launch(ctx, 1);
         LcBlkOut *tmp = bprev; bprev = bcur; bcur = tmp;
@@ -1522,50 +1576,36 @@ int lc_decompress_impl2(lc_ctx *ctx, uint64_t n, double eb_abs, double first_val
         LC_CUDA_OK(cudaStreamSynchronize(st));
         if (!*hchanged) break;
     }
-    LC_CUDA_OK(cudaEventRecord(lc_phase_ev(ctx, 8), st));
-    LC_CUDA_OK(cudaMemsetAsync(sdesc, 0, scan_tiles * sizeof(LcScanDesc), st));
-    LC_CUDA_OK(cudaMemsetAsync(scan_counter, 0, 4, st));
-    LC_CUDA_OK(cudaMemsetAsync(tot + 1, 0xff, 8, st));
-    {
-        const int g = (int)(scan_tiles < (unsigned long long)(2 * lc_sm_count(ctx)) ? scan_tiles : 2 * lc_sm_count(ctx));
-        lc_dec_scan_kernel<<<g, LC_TPB, 0, st>>>(segs, nseg, offs, sdesc, scan_counter, tot);
-        { int _rc = lc_debug_check(ctx, "lc_dec_scan_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
-    }
-    LC_CUDA_OK(cudaEventRecord(lc_phase_ev(ctx, 9), st));
-    LC_CUDA_OK(cudaMemsetAsync(endpos, 0xff, 8, st));
-    {
-        // output window per warp: the typical 32-segment range (+25%), <= 4096 symbols
-        const double syms_per_seg = (double)m * seg_bits / (double)(payload_bits ? payload_bits : 1);
-        long long cap = (long long)(1.25 * 32.0 * syms_per_seg);
-        cap = (cap + 63) / 64 * 64;
-        if (cap < 256) cap = 256;
-        if (cap > 4096) cap = 4096;
-        const size_t wsm = lc_dec_write_smem((int)cap, code_bytes, seg_bits);
-        const int wgrid = (int)(nblk < (long long)(2 * lc_sm_count(ctx)) ? nblk : 2 * lc_sm_count(ctx));
-        if (code_bytes == 2) {
-            LC_CUDA_OK(cudaFuncSetAttribute(lc_dec_write_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
-            lc_dec_write_kernel<uint16_t><<<wgrid, LC_DEC_TPB, wsm, st>>>(DP, segs, offs, bcodes.p, m, endpos, (int)cap);
-        } else {
-            LC_CUDA_OK(cudaFuncSetAttribute(lc_dec_write_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
-            lc_dec_write_kernel<uint32_t><<<wgrid, LC_DEC_TPB, wsm, st>>>(DP, segs, offs, bcodes.p, m, endpos, (int)cap);
-        }
-    }
-    lc_dec_status_kernel<<<1, 1, 0, st>>>(segs, offs, tot, endpos, m, payload_bits, status);
-    { int _rc = lc_debug_check(ctx, "lc_dec_status_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
-    lc_count_launch(ctx, 3);
-    int *hstat = (int *)lc_pinned(ctx);
-    LC_CUDA_OK(cudaMemcpyAsync(hstat, status, 4, cudaMemcpyDeviceToHost, st));
-    LC_CUDA_OK(cudaStreamSynchronize(st));
-    if (*hstat) return *hstat;
+    { int _rc = tail(); if (_rc) return _rc; }
     return lc_reconstruct(ctx, n, eb_abs, first_value, esc_val, n_esc, out, out_on_device, esc_used, bcodes.p,
-                          code_bytes);
+                          code_bytes, status, nullptr, &hit);
 }
 
 // Reconstruction from decoded codes (compressor.py:358-376, 430-439): exact
 // chunked chain + escape checks; inputs already staged in the context.
+// Everything the host needs after the reconstruction, packed by one thread so a
+// single copy + sync ends the call.
+struct LcRecFinal {
+    unsigned long long first_bad;
+    int esc_flags[2];
+    long long cnt_a, cnt_b;     // escapes: state at the last tile start + that tile's aggregate
+    int abort_a, abort_b;
+};
+
+__global__ void lc_rec_final_kernel(LcRecParams P, LcRecSplit S, long long last, LcRecFinal *f)
+{
+    f->first_bad = *P.first_bad;
+    f->esc_flags[0] = P.esc_flags[0];
+    f->esc_flags[1] = P.esc_flags[1];
+    f->cnt_a = S.tile_in[last].cnt;
+    f->cnt_b = S.tile_seg[last].cnt;
+    f->abort_a = P.abort_a ? *P.abort_a : 0;
+    f->abort_b = P.abort_b ? *P.abort_b : 0;
+}
+
 static int lc_reconstruct(lc_ctx *ctx, uint64_t n, double eb_abs, double first_value, const double *esc_val_in,
                           uint64_t n_esc, double *out, int out_on_device, int64_t *esc_used, void *codes,
-                          int code_bytes)
+                          int code_bytes, const int *abort_a, const int *abort_b, int *abort_hit)
 {
     (void)esc_val_in;
     cudaStream_t st = lc_stream(ctx);
@@ -1601,6 +1641,11 @@ static int lc_reconstruct(lc_ctx *ctx, uint64_t n, double eb_abs, double first_v
     R.out = dout;
     R.first_bad = (unsigned long long *)((char *)baux.p + 112);
     R.esc_flags = esc_flags;
+    R.abort_a = abort_a;
+    R.abort_b = abort_b;
+    LcRecFinal *dfin = (LcRecFinal *)((char *)baux.p + 160);
+    LcRecFinal *hfin = (LcRecFinal *)((char *)lc_pinned(ctx) + 256);
+    *abort_hit = 0;
     LcRecSplit RS;
     {
         char *pp = (char *)baux2.p;
@@ -1631,7 +1676,6 @@ static int lc_reconstruct(lc_ctx *ctx, uint64_t n, double eb_abs, double first_v
     lc_set_first_kernel<<<1, 1, 0, st>>>(dout, first_value);
     lc_count_launch(ctx, 1);
     const int grid_cap = 2 * lc_sm_count(ctx);
-    unsigned long long *hbad = (unsigned long long *)lc_pinned(ctx);
     int relaunches = 0;
     for (;;) {
         R.ntiles = (nchunks - R.first_chunk + LC_TPB - 1) / LC_TPB;
@@ -1646,11 +1690,16 @@ static int lc_reconstruct(lc_ctx *ctx, uint64_t n, double eb_abs, double first_v
         if (code_bytes == 2) lc_rec_b_kernel<2><<<grid_b, LC_TPB, lc_rec_b_smem_bytes(), st>>>(R, RS);
         else lc_rec_b_kernel<4><<<grid_b, LC_TPB, lc_rec_b_smem_bytes(), st>>>(R, RS);
         { int _rc = lc_debug_check(ctx, "lc_rec_b_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
-        lc_count_launch(ctx, 5);
-        LC_CUDA_OK(cudaMemcpyAsync(hbad, R.first_bad, 8, cudaMemcpyDeviceToHost, st));
+        lc_rec_final_kernel<<<1, 1, 0, st>>>(R, RS, R.ntiles - 1, dfin);
+        lc_count_launch(ctx, 6);
+        LC_CUDA_OK(cudaMemcpyAsync(hfin, dfin, sizeof(LcRecFinal), cudaMemcpyDeviceToHost, st));
         LC_CUDA_OK(cudaStreamSynchronize(st));
-        if (*hbad == ~0ULL) break;
-        const unsigned long long fb = *hbad;
+        if (hfin->abort_a || hfin->abort_b) {            // the decode failed or needs another pass
+            *abort_hit = hfin->abort_b ? LC_RC_CASCADE : hfin->abort_a;   // a cascade voids the status
+            return *abort_hit;
+        }
+        if (hfin->first_bad == ~0ULL) break;
+        const unsigned long long fb = hfin->first_bad;
         ++relaunches;
         double anchor;
         long long acnt;
@@ -1662,16 +1711,8 @@ static int lc_reconstruct(lc_ctx *ctx, uint64_t n, double eb_abs, double first_v
         if (relaunches > 100000) { lc_set_err(ctx, "reconstruction did not converge"); return 20; }
     }
     // escape checks (compressor.py:435-439)
-    int hflags[2];
-    long long total_esc;
-    LC_CUDA_OK(cudaMemcpy(hflags, esc_flags, 8, cudaMemcpyDeviceToHost));
-    {
-        // total escape codes = state at the last tile start + that tile's aggregate
-        LcSegScan a, b;
-        LC_CUDA_OK(cudaMemcpy(&a, RS.tile_in + (R.ntiles - 1), sizeof(LcSegScan), cudaMemcpyDeviceToHost));
-        LC_CUDA_OK(cudaMemcpy(&b, RS.tile_seg + (R.ntiles - 1), sizeof(LcSegScan), cudaMemcpyDeviceToHost));
-        total_esc = a.cnt + b.cnt;
-    }
+    const int hflags[2] = {hfin->esc_flags[0], hfin->esc_flags[1]};
+    const long long total_esc = hfin->cnt_a + hfin->cnt_b;
     LC_CUDA_OK(cudaEventRecord(lc_phase_ev(ctx, 7), st));
     lc_set_kind(ctx, 2);
     int64_t used = hflags[0] ? -1 : total_esc;

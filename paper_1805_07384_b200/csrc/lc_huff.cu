@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(LC_TPB) lc_encode_kernel(LcEncParams P)
     __shared__ int sh_j;
     const int tid = threadIdx.x;
     const CodeT *codes = reinterpret_cast<const CodeT *>(P.codes);
-    const bool fast = P.max_len <= 32;
+    const bool fast = P.cb->max_len <= 32;
     const uint32_t tab = P.nbins < LC_ENC_TAB ? P.nbins : LC_ENC_TAB;
     for (uint32_t s = tid; s < tab; s += LC_TPB)
         tpk[s] = ((unsigned long long)P.lengths[s] << 32) | (fast ? (uint32_t)P.cw[s] : 0u);
@@ -500,8 +500,10 @@ __global__ void __launch_bounds__(LC_TPB) lc_encode_kernel(LcEncParams P)
             for (int j = 0; j < LC_L; ++j)
                 if (j < len && C.get(j) == 0) {
                     const unsigned long long el = (unsigned long long)(p0 + j + 1);
-                    P.esc_idx[e] = el;
-                    P.esc_val[e] = P.x ? P.x[el] : 0.0;
+                    if (e < P.esc_cap) {
+                        P.esc_idx[e] = el;
+                        P.esc_val[e] = P.x ? P.x[el] : 0.0;
+                    }
                     ++e;
                 }
         }

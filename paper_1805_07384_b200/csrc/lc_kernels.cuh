@@ -18,7 +18,7 @@ struct LcQuantParams {
     LcQuant Q;
     double esc_thresh;       // |x_i - x_{i-1}| test for definite escapes
     int64_t first_chunk;     // relaunch start chunk (0 for a fresh run)
-    double anchor_val;       // exact chain value at position first_chunk*L
+    double anchor_val;       // exact chain value at position first_chunk*L (x[0] read on device when 0)
     int64_t nchunks;         // total chunks ceil((n-1)/L)
     int64_t ntiles;          // tiles in this launch
     LcTileDesc *desc;
@@ -82,7 +82,8 @@ struct LcEncParams {
     LcEncDesc *desc;
     unsigned int *tile_counter;
     uint64_t ntiles;
-    int max_len;             // longest code (<= 32: table path)
+    const LcCodebookOut *cb; // device codebook summary (max_len <= 32: table path)
+    unsigned long long esc_cap;   // capacity of esc_idx / esc_val (host re-runs when short)
     unsigned long long *sync; // v2 sync table [ceil(m / LC_SYNC_K)] (bit offsets), may be null
 };
 

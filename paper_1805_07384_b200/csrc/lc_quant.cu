@@ -266,8 +266,10 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_quant_a_kernel(LcQuantParams P)
         } else {
             apos = apos_next = launch_apos;
         }
-        const double aval = (apos == launch_apos) ? P.anchor_val : P.x[apos];
-        const double aval_next = (apos_next == launch_apos) ? P.anchor_val : P.x[apos_next];
+        // the launch anchor is x[0] itself on a fresh run (first_chunk 0)
+        const bool relaunch = P.first_chunk != 0;
+        const double aval = (relaunch && apos == launch_apos) ? P.anchor_val : P.x[apos];
+        const double aval_next = (relaunch && apos_next == launch_apos) ? P.anchor_val : P.x[apos_next];
         const double xend = len > 0 ? row[len - 1] : xstart;
         const double g0 = lc_guess(P, xstart, p0, apos, aval);
         const double g1 = lc_guess(P, xend, p0 + len, apos_next, aval_next);
