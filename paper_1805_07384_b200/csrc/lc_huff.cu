@@ -445,15 +445,31 @@ __global__ void __launch_bounds__(LC_TPB) lc_encode_kernel(LcEncParams P)
                 }
             }
         }
-        unsigned long long bits = 0, nesc = 0;
+        // full chunk with every symbol in the smem table: no per-symbol guards
+        uint32_t cmax = 0;
 #pragma unroll
-        for (int j = 0; j < LC_L; ++j) {
-            if (j < len) {
-                const uint32_t s = C.get(j);
-                bits += (uint32_t)(entry(s) >> 32);
-                nesc += (s == 0);
+        for (int k = 0; k < LcCodeRegs<CodeT>::NW; ++k) cmax = sizeof(CodeT) == 2 ? __vmaxu2(cmax, C.w[k]) : max(cmax, C.w[k]);
+        if (sizeof(CodeT) == 2) cmax = max(cmax & 0xffffu, cmax >> 16);
+        const bool tabled = len == LC_L && cmax < LC_ENC_TAB;
+        const uint32_t *tlen = reinterpret_cast<const uint32_t *>(tpk) + 1;   // high words: lengths
+        uint32_t bits32 = 0, nesc32 = 0;
+        if (tabled) {
+#pragma unroll
+            for (int j = 0; j < LC_L; ++j) bits32 += tlen[2 * C.get(j)];
+#pragma unroll
+            for (int k = 0; k < LcCodeRegs<CodeT>::NW; ++k)
+                nesc32 += sizeof(CodeT) == 2 ? __popc(__vcmpeq2(C.w[k], 0u)) >> 4 : (C.w[k] == 0u);
+        } else {
+#pragma unroll
+            for (int j = 0; j < LC_L; ++j) {
+                if (j < len) {
+                    const uint32_t s = C.get(j);
+                    bits32 += (uint32_t)(entry(s) >> 32);
+                    nesc32 += (s == 0);
+                }
             }
         }
+        const unsigned long long bits = bits32, nesc = nesc32;
         // per-tile bits < 2^20 and escapes < 2^14: one scan of (esc << 32 | bits)
         unsigned long long ex, agg;
         ScanU(scan_tmp).ExclusiveSum(bits | (nesc << 32), ex, agg);
@@ -517,21 +533,25 @@ __global__ void __launch_bounds__(LC_TPB) lc_encode_kernel(LcEncParams P)
                 unsigned w = wfirst;
                 unsigned long long acc = 0;
                 int nb = (int)(lb & 31);
-#pragma unroll
-                for (int j = 0; j < LC_L; ++j) {
-                    if (j < len) {
-                        const unsigned long long e = entry(C.get(j));
-                        const int l = (int)(e >> 32);
-                        acc = (acc << l) | (uint32_t)e;
-                        nb += l;
-                        if (nb >= 32) {
-                            nb -= 32;
-                            const uint32_t word = (uint32_t)(acc >> nb);
-                            if (w == wfirst || w == wlast) atomicOr(wbuf + w, word);
-                            else wbuf[w] = word;
-                            ++w;
-                        }
+                auto put = [&](unsigned long long e) {
+                    const int l = (int)(e >> 32);
+                    acc = (acc << l) | (uint32_t)e;
+                    nb += l;
+                    if (nb >= 32) {
+                        nb -= 32;
+                        const uint32_t word = (uint32_t)(acc >> nb);
+                        if (w == wfirst || w == wlast) atomicOr(wbuf + w, word);
+                        else wbuf[w] = word;
+                        ++w;
                     }
+                };
+                if (tabled) {
+#pragma unroll
+                    for (int j = 0; j < LC_L; ++j) put(tpk[C.get(j)]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < LC_L; ++j)
+                        if (j < len) put(entry(C.get(j)));
                 }
                 if (nb > 0) atomicOr(wbuf + w, (uint32_t)(acc << (32 - nb)));
             }
