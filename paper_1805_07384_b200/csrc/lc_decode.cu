@@ -949,7 +949,14 @@ __device__ __forceinline__ int lc_code_m(uint32_t code) { return lc_unzigzag(cod
 // Split reconstruction (no inter-tile waiting): R0 segmented m-prefix per tile,
 // R0 scan, RA guess chains + maps, map scan (lc_map_scan_kernel), RB exact chain.
 
+struct LcSegPk {               // in-tile exclusive LcSegScan of one chunk (R0 -> RA)
+    long long sum;
+    int cnt;                    // <= LC_TILE
+    int flags;                  // has | moved << 1
+};
+
 struct LcRecSplit {
+    LcSegPk *chunk_excl;      // [nchunks] R0 output (state at each chunk start within its tile)
     LcSegScan *tile_seg;      // [ntiles] R0 output (tile aggregate)
     LcSegScan *tile_in;       // [ntiles] R0 scan output (state at each tile start)
     OffMap *tile_agg;         // [ntiles] RA output
@@ -1005,17 +1012,6 @@ __device__ __forceinline__ void lc_load_codes_tile(const LcRecParams &P, long lo
     uint32_t *row = cs + tid * LC_ROW;
 #pragma unroll
     for (int j = 0; j < LC_L; ++j) row[j] = v[j];
-}
-
-__device__ __forceinline__ LcSegScan lc_chunk_segscan(const uint32_t *crow, int len)
-{
-    LcSegScan mine; mine.sum = 0; mine.cnt = 0; mine.has = 0; mine.moved = 0;
-    for (int j = 0; j < len; ++j) {
-        const uint32_t code = crow[j];
-        if (code == 0) { mine.sum = 0; mine.cnt += 1; mine.has = 1; mine.moved = 0; }
-        else { const int mm = lc_code_m(code); mine.sum += mm; mine.moved |= (mm != 0); }
-    }
-    return mine;
 }
 
 __device__ __forceinline__ LcSegScan lc_shfl_up_seg(const LcSegScan &v, int o)
@@ -1076,7 +1072,12 @@ __global__ void __launch_bounds__(LC_TPB) lc_rec0_kernel(LcRecParams P, LcRecSpl
         }
         __syncthreads();
         LcSegScan agg;
-        lc_block_segscan(mine, wseg, &agg);
+        const LcSegScan exc = lc_block_segscan(mine, wseg, &agg);
+        if (len > 0) {
+            LcSegPk pk;
+            pk.sum = exc.sum; pk.cnt = (int)exc.cnt; pk.flags = exc.has | (exc.moved << 1);
+            S.chunk_excl[c] = pk;
+        }
         if (tid == 0) S.tile_seg[t] = agg;
     }
 }
@@ -1144,7 +1145,6 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_rec_a_kernel(LcRecParams P, LcRe
 {
     extern __shared__ __align__(16) unsigned char lc_dyn_smem[];
     uint32_t *cs = reinterpret_cast<uint32_t *>(lc_dyn_smem);
-    __shared__ LcSegScan wseg[LC_TPB / 32];
     __shared__ OffMap warp_agg[LC_TPB / 32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const long long nel = (long long)P.n - 1;
@@ -1157,11 +1157,18 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_rec_a_kernel(LcRecParams P, LcRe
         lc_load_codes_tile(P, cbeg * LC_L, cs);
         __syncthreads();
         const uint32_t *crow = cs + tid * LC_ROW;
-        const LcSegScan mine = lc_chunk_segscan(crow, len);
-        LcSegScan agg;
-        const LcSegScan exc = lc_block_segscan(mine, wseg, &agg);
-        const LcSegScan before = lc_segscan_op(S.tile_in[t], exc);
-        const LcSegScan after = lc_segscan_op(before, mine);
+        // chunk start states from R0 (in-tile exclusive) + the tile's incoming state
+        auto unpk = [](const LcSegPk &p) {
+            LcSegScan v; v.sum = p.sum; v.cnt = p.cnt; v.has = p.flags & 1; v.moved = p.flags >> 1;
+            return v;
+        };
+        const LcSegScan tin = S.tile_in[t];
+        LcSegScan before = tin, after = tin;
+        if (len > 0) {
+            before = lc_segscan_op(tin, unpk(S.chunk_excl[c]));
+            if (c + 1 < P.nchunks)
+                after = tid + 1 < LC_TPB ? lc_segscan_op(tin, unpk(S.chunk_excl[c + 1])) : S.tile_in[t + 1];
+        }
         auto anchor_of = [&](const LcSegScan &s) -> double {
             if (s.cnt > P.anchor_cnt) {
                 const long long e = s.cnt - 1;
@@ -1622,7 +1629,7 @@ static int lc_reconstruct(lc_ctx *ctx, uint64_t n, double eb_abs, double first_v
     const int64_t nchunks = (int64_t)((m + LC_L - 1) / LC_L);
     const int64_t ntiles = (nchunks + LC_TPB - 1) / LC_TPB;
     LC_CUDA_OK(lc_reserve(baux2, (size_t)(ntiles + 1) * (2 * sizeof(LcSegScan) + sizeof(OffMap) + sizeof(double))
-                                 + (size_t)nchunks * (16 + sizeof(int) + 5 * sizeof(double)) + 256));
+                                 + (size_t)nchunks * (16 + sizeof(int) + 5 * sizeof(double) + sizeof(LcSegPk)) + 256));
     LcRecParams R;
     R.codes = codes;
     R.code_bytes = code_bytes;
@@ -1649,6 +1656,7 @@ static int lc_reconstruct(lc_ctx *ctx, uint64_t n, double eb_abs, double first_v
     LcRecSplit RS;
     {
         char *pp = (char *)baux2.p;
+        RS.chunk_excl = (LcSegPk *)pp;           pp += nchunks * sizeof(LcSegPk);
         RS.tile_seg = (LcSegScan *)pp;           pp += (ntiles + 1) * sizeof(LcSegScan);
         RS.tile_in = (LcSegScan *)pp;            pp += (ntiles + 1) * sizeof(LcSegScan);
         RS.tile_agg = (OffMap *)pp;              pp += (ntiles + 1) * sizeof(OffMap);
