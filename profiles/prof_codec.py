@@ -1,0 +1,26 @@
+"""Profiling driver: one warm-up + one measured compress/decompress of the config-2 vector
+(n = 2^26) at one bound through the public API.  Used under ncu (profiles/README in DESIGN.md):
+
+    python profiles/prof_codec.py [eb_rel] [log2n]
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1805_07384_b200 as lc  # noqa: E402
+from bench import make_vector  # noqa: E402
+
+eb = float(sys.argv[1]) if len(sys.argv) > 1 else 1e-4
+n = 1 << (int(sys.argv[2]) if len(sys.argv) > 2 else 26)
+xd = torch.from_numpy(make_vector(n)).cuda()
+cfg = lc.CompressorConfig.value_range_relative(eb)
+for _ in range(2):
+    blk = lc.compress(xd, cfg)
+    rec = lc.decompress(blk, device="cuda")
+torch.cuda.synchronize()
+err = float((rec - xd).abs().max())
+assert err <= blk.eb_abs, (err, blk.eb_abs)
+print("ok", n, eb, blk.payload_bits, err / blk.eb_abs)
