@@ -251,3 +251,76 @@ __device__ __forceinline__ void lc_scan_warp_maps(OffMap *agg, int nw)
         if (lane < nw) agg[lane] = v;
     }
 }
+
+// ---- compacted replay of flagged chunks -------------------------------------
+// Chunks whose hot loop flagged possible map events are queued in shared memory
+// and replayed by consecutive threads (full warps) instead of by their owners
+// (one divergent lane per warp).  Entry = chunk index in the tile, its flag
+// mask and its guess start.  replay(q) computes the chunk's map and stores it
+// where the owner reads it after this call.  Call from all threads.
+struct LcReplayItem {
+    int ch;
+    unsigned mask;
+    double g0;
+};
+
+template <typename Replay>
+__device__ __forceinline__ void lc_tile_replay(bool need, unsigned mask, double g0, LcReplayItem *q,
+                                               int *s_cnt, Replay replay)
+{
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const unsigned b = __ballot_sync(0xffffffffu, need);
+    if (lane == 0) s_cnt[wid] = __popc(b);
+    __syncthreads();
+    int base = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < LC_TPB / 32; ++w) {
+        const int cw = s_cnt[w];
+        base += w < wid ? cw : 0;
+        tot += cw;
+    }
+    if (need) {
+        LcReplayItem it;
+        it.ch = tid; it.mask = mask; it.g0 = g0;
+        q[base + __popc(b & ((1u << lane) - 1u))] = it;
+    }
+    __syncthreads();
+    for (int k = tid; k < tot; k += LC_TPB) replay(q[k]);
+    __syncthreads();
+}
+
+// OffMap <-> 14 shared-memory words (rows of 32-bit codes are only 4-byte aligned)
+__device__ __forceinline__ void lc_map_to_words(uint32_t *w, const OffMap &m)
+{
+    const double f[6] = {m.v, m.B, m.t0, m.t1, m.y, m.og};
+    w[0] = (uint32_t)m.kind;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+        w[1 + 2 * i] = (uint32_t)__double2loint(f[i]);
+        w[2 + 2 * i] = (uint32_t)__double2hiint(f[i]);
+    }
+}
+
+__device__ __forceinline__ OffMap lc_map_from_words(const uint32_t *w)
+{
+    double f[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) f[i] = __hiloint2double((int)w[2 + 2 * i], (int)w[1 + 2 * i]);
+    OffMap m;
+    m.kind = (int)w[0];
+    m.v = f[0]; m.B = f[1]; m.t0 = f[2]; m.t1 = f[3]; m.y = f[4]; m.og = f[5];
+    return m;
+}
+
+// ---- asynchronous global -> shared copies (LDGSTS) and L2 prefetch ----------
+__device__ __forceinline__ void lc_cp_async8(void *smem_dst, const void *gsrc)
+{
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void lc_cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void lc_cp_async_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void lc_prefetch_l2(const void *p)
+{
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}

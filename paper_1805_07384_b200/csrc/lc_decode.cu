@@ -1146,6 +1146,8 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_rec_a_kernel(LcRecParams P, LcRe
     extern __shared__ __align__(16) unsigned char lc_dyn_smem[];
     uint32_t *cs = reinterpret_cast<uint32_t *>(lc_dyn_smem);
     __shared__ OffMap warp_agg[LC_TPB / 32];
+    __shared__ LcReplayItem s_rq[LC_TPB];
+    __shared__ int s_rcnt[LC_TPB / 32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const long long nel = (long long)P.n - 1;
     if (lc_rec_aborted(P)) return;
@@ -1184,46 +1186,54 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_rec_a_kernel(LcRecParams P, LcRe
         };
         const double g0 = guess_of(before);
         const double g1 = guess_of(after);
+        // guess chain with superset event flags; flagged chunks are replayed below
+        // by a compacted queue of threads
         OffMap H;
+        bool need = false;
+        unsigned mask = 0u;
+        double r = g0;
         if (len > 0) {
             P.chunk_esc[c] = before.cnt;
-            double r = g0;
             long long e = before.cnt;
-            LcEvents E;
-            lc_events_init(E, g0);
-            bool pend = false;
-            double pr = g0, pc = 0.0, prn = g0;        // first call is a no-op step at g0
+            LcFlags F;
+            lc_flags_init(F, g0);
+            int anyesc = 0;
             for (int j = 0; j < len; ++j) {
                 const uint32_t code = crow[j];
-                const bool esc = code == 0;
                 const int m = lc_code_m(code);
                 const double inc_ = LC_MUL((double)m, P.delta);
                 double rn = m != 0 ? LC_ADD(r, inc_) : r;
-                if (esc) { rn = e < (long long)P.n_esc ? P.esc_val[e] : 0.0; ++e; }
-                lc_events_step_if(E, pend, j - 1, pr, pc, prn);
-                lc_events_escape_if(E, esc);
-                pend = !esc && m != 0;
-                pr = r; pc = inc_; prn = rn;
+                if (code == 0) { rn = e < (long long)P.n_esc ? P.esc_val[e] : 0.0; ++e; anyesc = 1; }
+                lc_flags_step(F, j, r, inc_, rn);
                 r = rn;
             }
-            lc_events_step_if(E, pend, len - 1, pr, pc, prn);
-            if (!lc_events_finish(E, g0, H)) {          // replay from the first flagged step
-                const int j0 = __ffs(E.mask) - 1, j1 = 31 - __clz(E.mask);
-                double r2 = E.r_first;
-                for (int j = j0; j <= j1; ++j) {
-                    const int m = lc_code_m(crow[j]);  // no escape here (E.esc would be set)
-                    if (m != 0) {
-                        const double inc_ = LC_MUL((double)m, P.delta);
-                        const double rn = LC_ADD(r2, inc_);
-                        if ((E.mask >> j) & 1u) lc_map_step(H, r2, inc_, rn);
-                        r2 = rn;
-                    }
-                }
+            if (anyesc) H = lc_map_const(0.0);
+            else {
+                H = lc_map_identity(lc_ulp(g0));
+                mask = F.mask;
+                need = mask != 0u;
             }
-            if (c + 1 < P.nchunks) lc_map_shift_out(H, LC_SUB(r, g1));
         } else {
             H = lc_map_neutral();
         }
+        lc_tile_replay(need, mask, g0, s_rq, s_rcnt, [&](const LcReplayItem &it) {
+            uint32_t *rw = cs + it.ch * LC_ROW;
+            const int j1 = 31 - __clz(it.mask);
+            OffMap Hr = lc_map_identity(lc_ulp(it.g0));
+            double r2 = it.g0;
+            for (int j = 0; j <= j1; ++j) {
+                const int m = lc_code_m(rw[j]);              // no escapes in replayed chunks
+                if (m != 0) {
+                    const double inc_ = LC_MUL((double)m, P.delta);
+                    const double rn = LC_ADD(r2, inc_);
+                    if ((it.mask >> j) & 1u) lc_map_step(Hr, r2, inc_, rn);
+                    r2 = rn;
+                }
+            }
+            lc_map_to_words(rw, Hr);
+        });
+        if (need) H = lc_map_from_words(crow);
+        if (len > 0 && c + 1 < P.nchunks) lc_map_shift_out(H, LC_SUB(r, g1));
         OffMap inc_map = H;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {

@@ -160,19 +160,37 @@ __device__ __forceinline__ double lc_guess(const LcQuantParams &P, double xpos, 
 // chain).  No tile ever waits for another tile.
 
 // Load one tile of x into padded smem rows; xhalo[LC_L] = x[tile start].
+// Coalesced 8-byte cp.async copies (no register staging: all 32 per thread are
+// in flight at once); the caller publishes the tile with lc_cp_async_wait()
+// + __syncthreads().  lc_prefetch_x_tile warms L2 with the tile a CTA
+// processes next while it computes the current one.
 __device__ __forceinline__ void lc_load_x_tile(const LcQuantParams &P, long long pbeg, double *xs, double *xhalo)
 {
     const int tid = threadIdx.x;
     const long long nel = (long long)P.n - 1;
-#pragma unroll 8
+#pragma unroll
     for (int k = 0; k < LC_L; ++k) {
         const int off = k * LC_TPB + tid;
         const long long pos = pbeg + 1 + off;
-        if (pos <= nel) xs[(off >> 5) * LC_ROW + (off & 31)] = __ldcs(P.x + pos);
+        if (pos <= nel) lc_cp_async8(xs + (off >> 5) * LC_ROW + (off & 31), P.x + pos);
     }
+    lc_cp_async_commit();
     if (tid <= LC_L) {
         const long long pos = pbeg - LC_L + tid;
         xhalo[tid] = pos >= 0 ? P.x[pos] : 0.0;
+    }
+}
+
+__device__ __forceinline__ void lc_prefetch_x_tile(const LcQuantParams &P, long long t_next)
+{
+    if (t_next >= P.ntiles) return;
+    const long long pbeg = (P.first_chunk + t_next * LC_TPB) * LC_L;
+    const long long nel = (long long)P.n - 1;
+    // LC_TILE doubles = 512 lines of 128 B: two per thread
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const long long pos = pbeg + 1 + (long long)(k * LC_TPB + threadIdx.x) * 16;
+        if (pos <= nel) lc_prefetch_l2(P.x + pos);
     }
 }
 
@@ -231,6 +249,8 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_quant_a_kernel(LcQuantParams P)
     __shared__ double xhalo[LC_L + 1];
     __shared__ typename ScanLL::TempStorage scan_tmp;
     __shared__ OffMap warp_agg[LC_TPB / 32];
+    __shared__ LcReplayItem s_rq[LC_TPB];
+    __shared__ int s_rcnt[LC_TPB / 32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const long long nel = (long long)P.n - 1;
     const long long launch_apos = P.first_chunk * LC_L;
@@ -243,7 +263,9 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_quant_a_kernel(LcQuantParams P)
         const int len = (c < P.nchunks) ? (int)min((long long)LC_L, nel - p0) : 0;
         __syncthreads();
         lc_load_x_tile(P, pbeg, xs, xhalo);
+        lc_cp_async_wait();
         __syncthreads();
+        lc_prefetch_x_tile(P, t + gridDim.x);
         const double *row = xs + tid * LC_ROW;
         const double xstart = tid == 0 ? xhalo[LC_L] : xs[(tid - 1) * LC_ROW + LC_L - 1];
 
@@ -274,38 +296,47 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_quant_a_kernel(LcQuantParams P)
         const double g0 = lc_guess(P, xstart, p0, apos, aval);
         const double g1 = lc_guess(P, xend, p0 + len, apos_next, aval_next);
 
-        // guess chain -> chunk map (software-pipelined event detection)
+        // guess chain with superset event flags (lc_flags_*); flagged chunks are
+        // replayed below by a compacted queue of threads
         OffMap H;
+        bool need = false;
+        unsigned mask = 0u;
+        double r = g0;
         if (len > 0) {
-            double r = g0;
-            LcEvents E;
-            lc_events_init(E, g0);
-            bool pend = false;
-            double pr = g0, pc = 0.0, prn = g0;        // first call is a no-op step at g0
+            LcFlags F;
+            lc_flags_init(F, g0);
+            int anyesc = 0;
             for (int j = 0; j < len; ++j) {
                 int esc; double inc;
                 const double rn = lc_step_guess(P.Q, row[j], r, &esc, &inc);
-                lc_events_step_if(E, pend, j - 1, pr, pc, prn);
-                lc_events_escape_if(E, esc);
-                pend = !esc && inc != 0.0;
-                pr = r; pc = inc; prn = rn;
+                anyesc |= esc;
+                lc_flags_step(F, j, r, inc, rn);
                 r = rn;
             }
-            lc_events_step_if(E, pend, len - 1, pr, pc, prn);
-            if (!lc_events_finish(E, g0, H)) {          // replay from the first flagged step
-                const int j0 = __ffs(E.mask) - 1, j1 = 31 - __clz(E.mask);
-                double r2 = E.r_first;
-                for (int j = j0; j <= j1; ++j) {
-                    int esc; double inc;
-                    const double rn = lc_step_guess(P.Q, row[j], r2, &esc, &inc);
-                    if ((E.mask >> j) & 1u) lc_map_step(H, r2, inc, rn);
-                    r2 = rn;
-                }
+            if (anyesc) H = lc_map_const(0.0);
+            else {
+                H = lc_map_identity(lc_ulp(g0));
+                mask = F.mask;
+                need = mask != 0u;
             }
-            if (c + 1 < P.nchunks) lc_map_shift_out(H, LC_SUB(r, g1));
         } else {
             H = lc_map_neutral();
         }
+        lc_tile_replay(need, mask, g0, s_rq, s_rcnt, [&](const LcReplayItem &it) {
+            double *rw = xs + it.ch * LC_ROW;
+            const int j1 = 31 - __clz(it.mask);
+            OffMap Hr = lc_map_identity(lc_ulp(it.g0));
+            double r2 = it.g0;
+            for (int j = 0; j <= j1; ++j) {
+                int esc; double inc;
+                const double rn = lc_step_guess(P.Q, rw[j], r2, &esc, &inc);
+                if (((it.mask >> j) & 1u) && inc != 0.0) lc_map_step(Hr, r2, inc, rn);
+                r2 = rn;
+            }
+            lc_map_to_words(reinterpret_cast<uint32_t *>(rw), Hr);
+        });
+        if (need) H = lc_map_from_words(reinterpret_cast<const uint32_t *>(row));
+        if (len > 0 && c + 1 < P.nchunks) lc_map_shift_out(H, LC_SUB(r, g1));
 
         // in-tile inclusive scan of maps
         OffMap inc_map = H;
@@ -399,7 +430,9 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_quant_b_kernel(LcQuantParams P, 
             const long long cn = cbeg + LC_TPB;          // first chunk of the next tile
             starts[LC_TPB] = (cn < P.nchunks) ? lc_apply_offset(P.pred.g0[cn], P.tile_D[t + 1]) : 0.0;
         }
+        lc_cp_async_wait();
         __syncthreads();
+        lc_prefetch_x_tile(P, t + gridDim.x);
         const double *row = xs + tid * LC_ROW;
         {
             double r = start;

@@ -36,35 +36,38 @@ int64_t sim_predict(const double *x, int64_t n, double eb, int64_t nbh, int L,
         const int64_t e = (s + L < n - 1) ? s + L : n - 1;
         double r = guess[c];
         OffMap H = lc_map_identity(lc_ulp(r));
-        LcEvents E; lc_events_init(E, r);
+        LcFlags F; lc_flags_init(F, r);
+        int anyesc = 0;
         const double g0 = r;
         int jj = 0;
         for (int64_t i = s + 1; i <= e; ++i) {
             uint32_t code; double inc; int esc; double pe;
             const double rn = lc_step(Q, x[i], r, &code, &esc, &inc, &pe);
-            if (esc) { H = lc_map_const(0.0); lc_events_escape(E); }
-            else if (inc != 0.0) {
-                const int kb = H.kind;
-                const double Bb = H.B;
-                lc_map_step(H, r, inc, rn);
-                lc_events_step_if(E, true, jj, r, inc, rn);
-                if (H.kind != kb || H.B != Bb) ++events;
+            if (esc) { H = lc_map_const(0.0); anyesc = 1; }
+            else {
+                lc_flags_step(F, jj, r, inc, rn);           // every step, as the kernels do
+                if (inc != 0.0) {
+                    const int kb = H.kind;
+                    const double Bb = H.B;
+                    lc_map_step(H, r, inc, rn);
+                    if (H.kind != kb || H.B != Bb) ++events;
+                }
             }
             r = rn;
             ++jj;
         }
-        {   // the deferred tracker must reproduce the step-by-step map exactly
-            OffMap H2;
-            if (!lc_events_finish(E, g0, H2)) {      // replay from the first flagged step
-                const int j0 = __builtin_ctz(E.mask), j1 = 31 - __builtin_clz(E.mask);
-                double r2 = E.r_first;
-                for (int j2 = j0; j2 <= j1; ++j2) {
+        {   // the flag tracker + replay must reproduce the step-by-step map exactly
+            OffMap H2 = anyesc ? lc_map_const(0.0) : lc_map_identity(lc_ulp(g0));
+            if (!anyesc && F.mask) {                 // replay up to the last flagged step
+                const int j1 = 31 - __builtin_clz(F.mask);
+                double r2 = g0;
+                for (int j2 = 0; j2 <= j1; ++j2) {
                     uint32_t code; double inc; int esc; double pe;
                     const double rn = lc_step(Q, x[s + 1 + j2], r2, &code, &esc, &inc, &pe);
-                    if ((E.mask >> j2) & 1u) lc_map_step(H2, r2, inc, rn);
+                    if (((F.mask >> j2) & 1u) && inc != 0.0) lc_map_step(H2, r2, inc, rn);
                     r2 = rn;
                 }
-                flagged += __builtin_popcount(E.mask);
+                flagged += __builtin_popcount(F.mask);
             }
             {
                 if (H2.kind != H.kind || lc_bits(H2.y) != lc_bits(H.y) || lc_bits(H2.t0) != lc_bits(H.t0) ||
@@ -305,15 +308,15 @@ void sim_event_hist(const double *x, int64_t n, double eb, int L, int64_t *hist)
     for (int64_t c = 0; c < nc; ++c) {
         const int64_t s = c * L, e = (s + L < n - 1) ? s + L : n - 1;
         double r = c == 0 ? x0 : x0 + floor((x[s] - x0) / Q.delta + 0.5) * Q.delta;
-        LcEvents E; lc_events_init(E, r);
-        int jj = 0;
+        LcFlags F; lc_flags_init(F, r);
+        int jj = 0, anyesc = 0;
         for (int64_t i = s + 1; i <= e; ++i, ++jj) {
             uint32_t code; double inc; int esc; double pe;
             const double rn = lc_step(Q, x[i], r, &code, &esc, &inc, &pe);
-            if (esc) lc_events_escape(E); else if (inc != 0.0) lc_events_step_if(E, true, jj, r, inc, rn);
+            if (esc) anyesc = 1; else lc_flags_step(F, jj, r, inc, rn);
             r = rn;
         }
-        const int ne = __builtin_popcount(E.mask);
+        const int ne = anyesc ? 0 : __builtin_popcount(F.mask);
         hist[ne < 15 ? ne : 15]++;
     }
 }

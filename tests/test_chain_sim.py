@@ -1,5 +1,5 @@
 """Host simulation of the chunked exact chain (product header lc_chain.cuh
-compiled with g++): the deferred event tracker reproduces the step-by-step
+compiled with g++): the superset flag tracker + replay reproduces the step-by-step
 offset map of every chunk, and the composed maps predict every chunk start of
 the sequential reference chain (compressor.py:319-355) -- sequential and
 tree-ordered composition (the GPU's in-tile scan + tile scan order)."""
