@@ -271,6 +271,11 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     P.Q.max_m = (double)(nbh - 1);
     P.Q.max_m1 = P.Q.max_m + 1.0;
     P.Q.inv = 1.0 / P.Q.delta;
+    {   // decision margin of lc_step_nb: T = 2^e >= 2^-50 (max_m + 2)
+        int e2;
+        frexp(P.Q.max_m + 2.0, &e2);
+        P.Q.cert = 0.5 - ldexp(1.0, e2 - 50);
+    }
     P.esc_thresh = (double)nbh * P.Q.delta * (1.0 + 0x1p-40);
     P.first_chunk = 0;
     P.anchor_val = 0.0;

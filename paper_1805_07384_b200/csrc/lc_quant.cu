@@ -466,22 +466,40 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_quant_b_kernel(LcQuantParams P, 
                 atomicMin(P.first_bad, (unsigned long long)(c + 1));
             }
         }
-        // histogram: runs of equal codes inside the thread's own chunk
-        if (P.count_hist && len > 0) {
+        // histogram: codes 1..16 (the small |m| that dominate smooth data) in
+        // packed per-thread byte counters (a chunk adds at most 32 to a code),
+        // summed per warp with redux.sync; every other code atomically
+        if (P.count_hist) {
             const uint32_t *crow = reinterpret_cast<const uint32_t *>(xs + tid * LC_ROW);
-            uint32_t cur = crow[0], cnt = 0;
+            unsigned long long A = 0ull, B = 0ull;
             for (int j = 0; j < len; ++j) {
                 const uint32_t code = crow[j];
-                if (code != cur) {
-                    if (cur < hb) atomicAdd(&hs[cur], cnt);
-                    else atomicAdd(&P.hist[cur], cnt);
-                    cur = code;
-                    cnt = 0;
+                const uint32_t idx = code - 1u;                   // escape (code 0) -> 2^32 - 1
+                const unsigned long long one = 1ull << ((idx & 7u) * 8u);
+                A += idx < 8u ? one : 0ull;
+                B += idx - 8u < 8u ? one : 0ull;
+                if (idx >= 16u) {
+                    if (code < hb) atomicAdd(&hs[code], 1u);
+                    else atomicAdd(&P.hist[code], 1u);
                 }
-                ++cnt;
             }
-            if (cur < hb) atomicAdd(&hs[cur], cnt);
-            else atomicAdd(&P.hist[cur], cnt);
+            uint32_t w[8];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                w[k] = (uint32_t)((A >> (16 * k)) & 0xffull) | ((uint32_t)((A >> (16 * k + 8)) & 0xffull) << 16);
+                w[4 + k] = (uint32_t)((B >> (16 * k)) & 0xffull) | ((uint32_t)((B >> (16 * k + 8)) & 0xffull) << 16);
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) w[k] = __reduce_add_sync(0xffffffffu, w[k]);   // halves <= 1024
+            if ((tid & 31) == 0) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const uint32_t lo = w[k] & 0xffffu, hi = w[k] >> 16;
+                    const uint32_t c0 = 2u * k + 1u, c1 = 2u * k + 2u;
+                    if (lo) { if (c0 < hb) atomicAdd(&hs[c0], lo); else atomicAdd(&P.hist[c0], lo); }
+                    if (hi) { if (c1 < hb) atomicAdd(&hs[c1], hi); else atomicAdd(&P.hist[c1], hi); }
+                }
+            }
         }
         __syncthreads();
         // coalesced 16-byte code stores: 16 / sizeof(CodeT) consecutive codes per thread
