@@ -315,10 +315,12 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
         P.pred.g0 = P.pred.y + nchunks;
         P.pred.kind = (int *)(P.pred.g0 + nchunks);
     }
-    LC_CUDA_OK(lc_reserve(ctx->tiles, (size_t)(ntiles + 1) * (sizeof(OffMap) + sizeof(double) + 2 * sizeof(long long))));
+    LC_CUDA_OK(lc_reserve(ctx->tiles, (size_t)(ntiles + 1) * (sizeof(OffMap) + sizeof(double) + 2 * sizeof(long long))
+                                          + LC_MAPSCAN_SCRATCH));
     P.tile_agg = (OffMap *)ctx->tiles.p;
     P.tile_D = (double *)(P.tile_agg + ntiles + 1);
     P.tile_last_esc = (long long *)(P.tile_D + ntiles + 1);
+    void *mapscan_scratch = (void *)(P.tile_last_esc + 2 * (ntiles + 1));
     P.anc_in = (const long long *)(P.tile_last_esc + ntiles + 1);
     long long *anc_in = (long long *)(P.tile_last_esc + ntiles + 1);
     // definite escapes possible?  Same test as lc_definite_escape on the largest step.
@@ -338,7 +340,7 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
         }
         lc_quant_a_kernel<<<(int)(P.ntiles < ga ? P.ntiles : ga), LC_TPB, lc_quant_a_smem_bytes(), st>>>(P);
         { int _rc = lc_debug_check(ctx, "lc_quant_a_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
-        lc_map_scan_kernel<<<1, 1024, 0, st>>>(P.tile_agg, P.tile_D, P.ntiles);
+        LC_CUDA_OK((cudaError_t)lc_launch_map_scan(P.tile_agg, P.tile_D, P.ntiles, mapscan_scratch, ctx->sm_count, st));
         lc_quant_b_kernel<CodeT><<<(int)(P.ntiles < gb ? P.ntiles : gb), LC_TPB, lc_quant_b_smem_bytes(), st>>>(P, codes);
         { int _rc = lc_debug_check(ctx, "lc_quant_b_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
         ctx->launches += 3;

@@ -1638,7 +1638,7 @@ static int lc_reconstruct(lc_ctx *ctx, uint64_t n, double eb_abs, double first_v
     }
     const int64_t nchunks = (int64_t)((m + LC_L - 1) / LC_L);
     const int64_t ntiles = (nchunks + LC_TPB - 1) / LC_TPB;
-    LC_CUDA_OK(lc_reserve(baux2, (size_t)(ntiles + 1) * (2 * sizeof(LcSegScan) + sizeof(OffMap) + sizeof(double))
+    LC_CUDA_OK(lc_reserve(baux2, LC_MAPSCAN_SCRATCH + (size_t)(ntiles + 1) * (2 * sizeof(LcSegScan) + sizeof(OffMap) + sizeof(double))
                                  + (size_t)nchunks * (16 + sizeof(int) + 5 * sizeof(double) + sizeof(LcSegPk)) + 256));
     LcRecParams R;
     R.codes = codes;
@@ -1664,12 +1664,14 @@ static int lc_reconstruct(lc_ctx *ctx, uint64_t n, double eb_abs, double first_v
     LcRecFinal *hfin = (LcRecFinal *)((char *)lc_pinned(ctx) + 256);
     *abort_hit = 0;
     LcRecSplit RS;
+    void *mapscan_scratch;
     {
         char *pp = (char *)baux2.p;
         RS.chunk_excl = (LcSegPk *)pp;           pp += nchunks * sizeof(LcSegPk);
         RS.tile_seg = (LcSegScan *)pp;           pp += (ntiles + 1) * sizeof(LcSegScan);
         RS.tile_in = (LcSegScan *)pp;            pp += (ntiles + 1) * sizeof(LcSegScan);
         RS.tile_agg = (OffMap *)pp;              pp += (ntiles + 1) * sizeof(OffMap);
+        mapscan_scratch = (void *)pp;            pp += LC_MAPSCAN_SCRATCH;
         RS.tile_D = (double *)pp;                pp += (ntiles + 1) * sizeof(double);
         R.bad_end = (double *)pp;                pp += nchunks * sizeof(double);
         R.chunk_esc = (long long *)pp;           pp += nchunks * sizeof(long long);
@@ -1703,7 +1705,7 @@ static int lc_reconstruct(lc_ctx *ctx, uint64_t n, double eb_abs, double first_v
         lc_rec_a_kernel<<<(int)(R.ntiles < 3 * lc_sm_count(ctx) ? R.ntiles : 3 * lc_sm_count(ctx)), LC_TPB,
                           lc_rec_a_smem_bytes(), st>>>(R, RS);
         { int _rc = lc_debug_check(ctx, "lc_rec_a_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
-        lc_map_scan_kernel<<<1, 1024, 0, st>>>(RS.tile_agg, RS.tile_D, R.ntiles);
+        LC_CUDA_OK((cudaError_t)lc_launch_map_scan(RS.tile_agg, RS.tile_D, R.ntiles, mapscan_scratch, lc_sm_count(ctx), st));
         const int grid_b = (int)(R.ntiles < 3 * lc_sm_count(ctx) ? R.ntiles : 3 * lc_sm_count(ctx));
         if (code_bytes == 2) lc_rec_b_kernel<2><<<grid_b, LC_TPB, lc_rec_b_smem_bytes(), st>>>(R, RS);
         else lc_rec_b_kernel<4><<<grid_b, LC_TPB, lc_rec_b_smem_bytes(), st>>>(R, RS);

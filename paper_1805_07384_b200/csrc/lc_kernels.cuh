@@ -93,7 +93,14 @@ __global__ void lc_anchor_tiles_kernel(LcQuantParams P);
 __global__ void lc_anchor_scan_kernel(const long long *__restrict__ last, long long *__restrict__ incoming,
                                       long long ntiles, long long launch_pos);
 __global__ void lc_quant_a_kernel(LcQuantParams P);
-__global__ void lc_map_scan_kernel(const OffMap *__restrict__ agg, double *__restrict__ tileD, long long ntiles);
+__global__ void lc_map_scan_kernel(const OffMap *__restrict__ agg, double *__restrict__ tileD, long long ntiles,
+                                   long long per, OffMap *gagg, int *gflag);
+// map scan launch: G co-resident CTAs of 1024 threads, `per` tiles per thread;
+// scratch = LC_MAPSCAN_SCRATCH bytes (group aggregates + flags)
+#define LC_MAPSCAN_MAXG 1024
+#define LC_MAPSCAN_SCRATCH (LC_MAPSCAN_MAXG * (sizeof(OffMap) + sizeof(int)))
+int lc_launch_map_scan(const OffMap *agg, double *tileD, long long ntiles, void *scratch, int sm_count,
+                       cudaStream_t st);
 template <typename CodeT> __global__ void lc_quant_b_kernel(LcQuantParams P, CodeT *__restrict__ codes);
 size_t lc_quant_a_smem_bytes();
 size_t lc_quant_b_smem_bytes();

@@ -364,15 +364,19 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_quant_a_kernel(LcQuantParams P)
     }
 }
 
-// Offsets at every tile start: D_0 = 0, D_{t+1} = agg_t(D_t).  One CTA: each
-// thread composes a run of tiles, a block scan composes the runs.
+// Offsets at every tile start: D_0 = 0, D_{t+1} = agg_t(D_t).  G co-resident
+// CTAs of 1024 threads (G <= SM count); thread i composes `per` consecutive tile
+// maps, a block scan gives each thread's in-group exclusive map and the group
+// aggregate, which is published (release flag).  Thread 0 folds the aggregates
+// of all earlier groups (acquire; they never wait on later groups) into the
+// offset at the group start; every thread then evaluates its tiles.
 __global__ void __launch_bounds__(1024) lc_map_scan_kernel(const OffMap *__restrict__ agg, double *__restrict__ tileD,
-                                                          long long ntiles)
+                                                          long long ntiles, long long per, OffMap *gagg, int *gflag)
 {
     __shared__ OffMap wsum[32];
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const long long per = (ntiles + 1023) / 1024;
-    const long long b0 = (long long)tid * per, b1 = min(ntiles, b0 + per);
+    __shared__ double s_D;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, g = blockIdx.x;
+    const long long b0 = min(ntiles, ((long long)g * 1024 + tid) * per), b1 = min(ntiles, b0 + per);
     OffMap run = lc_map_neutral();
     for (long long t = b0; t < b1; ++t) run = lc_map_compose(agg[t], run);
     OffMap inc = run;
@@ -388,12 +392,40 @@ __global__ void __launch_bounds__(1024) lc_map_scan_kernel(const OffMap *__restr
     if (wid > 0) inc = lc_map_compose(inc, wsum[wid - 1]);
     OffMap exc = lc_shfl_up_map(inc, 1);
     if (lane == 0) exc = wid > 0 ? wsum[wid - 1] : lc_map_neutral();
-    double D = lc_map_eval(exc, 0.0);
+    if (tid == 0) {
+        gagg[g] = wsum[31];
+        __threadfence();
+        st_release(gflag + g, 1);
+        double D = 0.0;
+        for (int j = 0; j < g; ++j) {
+            while (ld_acquire(gflag + j) != 1) { }
+            D = lc_map_eval(gagg[j], D);
+        }
+        s_D = D;
+    }
+    __syncthreads();
+    double D = lc_map_eval(exc, s_D);
     for (long long t = b0; t < b1; ++t) {
         tileD[t] = D;
         D = lc_map_eval(agg[t], D);
     }
-    if (b1 == ntiles && b0 < b1) tileD[ntiles] = D;
+    if (b0 < b1 && b1 == ntiles) tileD[ntiles] = D;
+}
+
+int lc_launch_map_scan(const OffMap *agg, double *tileD, long long ntiles, void *scratch, int sm_count,
+                       cudaStream_t st)
+{
+    long long G = (ntiles + 1023) / 1024;
+    if (G > sm_count) G = sm_count;
+    if (G > LC_MAPSCAN_MAXG) G = LC_MAPSCAN_MAXG;
+    if (G < 1) G = 1;
+    const long long per = (ntiles + 1024 * G - 1) / (1024 * G);
+    OffMap *gagg = (OffMap *)scratch;
+    int *gflag = (int *)(gagg + LC_MAPSCAN_MAXG);
+    cudaError_t e = cudaMemsetAsync(gflag, 0, G * sizeof(int), st);
+    if (e != cudaSuccess) return (int)e;
+    lc_map_scan_kernel<<<(int)G, 1024, 0, st>>>(agg, tileD, ntiles, per, gagg, gflag);
+    return (int)cudaGetLastError();
 }
 
 template <typename CodeT>
