@@ -324,3 +324,12 @@ __device__ __forceinline__ void lc_prefetch_l2(const void *p)
 {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
+
+// L2 prefetch of [p, p + bytes) by the whole CTA (one 128-byte line per thread
+// and round); used to warm the next tile's inputs while the current one runs.
+__device__ __forceinline__ void lc_prefetch_bytes(const void *p, size_t bytes)
+{
+    const char *c = reinterpret_cast<const char *>(reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)127);
+    const char *e = reinterpret_cast<const char *>(p) + bytes;
+    for (const char *q = c + 128 * threadIdx.x; q < e; q += 128 * blockDim.x) lc_prefetch_l2(q);
+}

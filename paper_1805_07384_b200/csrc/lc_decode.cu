@@ -1014,6 +1014,16 @@ __device__ __forceinline__ void lc_load_codes_tile(const LcRecParams &P, long lo
     for (int j = 0; j < LC_L; ++j) row[j] = v[j];
 }
 
+// L2 prefetch of tile t's codes (rec kernels run tiles t, t + gridDim.x, ...)
+__device__ __forceinline__ void lc_prefetch_codes_tile(const LcRecParams &P, long long t)
+{
+    if (t >= P.ntiles) return;
+    const long long p0 = (P.first_chunk + t * LC_TPB) * LC_L;
+    const long long nel = (long long)P.n - 1;
+    const long long cnt = min((long long)LC_TILE, nel - p0);
+    if (cnt > 0) lc_prefetch_bytes(reinterpret_cast<const char *>(P.codes) + p0 * P.code_bytes, cnt * P.code_bytes);
+}
+
 __device__ __forceinline__ LcSegScan lc_shfl_up_seg(const LcSegScan &v, int o)
 {
     LcSegScan r;
@@ -1061,6 +1071,7 @@ __global__ void __launch_bounds__(LC_TPB) lc_rec0_kernel(LcRecParams P, LcRecSpl
         const int len = (c < P.nchunks) ? (int)min((long long)LC_L, nel - c * LC_L) : 0;
         uint32_t v[LC_L];
         lc_load_chunk_codes(P, c * LC_L, len, v);
+        lc_prefetch_codes_tile(P, t + gridDim.x);
         LcSegScan mine; mine.sum = 0; mine.cnt = 0; mine.has = 0; mine.moved = 0;
 #pragma unroll
         for (int j = 0; j < LC_L; ++j) {
@@ -1158,6 +1169,9 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_rec_a_kernel(LcRecParams P, LcRe
         __syncthreads();
         lc_load_codes_tile(P, cbeg * LC_L, cs);
         __syncthreads();
+        lc_prefetch_codes_tile(P, t + gridDim.x);
+        if (t + gridDim.x < P.ntiles)
+            lc_prefetch_bytes(S.chunk_excl + P.first_chunk + (t + gridDim.x) * LC_TPB, (LC_TPB + 1) * sizeof(LcSegPk));
         const uint32_t *crow = cs + tid * LC_ROW;
         // chunk start states from R0 (in-tile exclusive) + the tile's incoming state
         auto unpk = [](const LcSegPk &p) {
@@ -1301,6 +1315,17 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_rec_b_kernel(LcRecParams P, LcRe
             for (int j = 0; j < LC_L; ++j)
                 v[j] = j < len ? (CB == 2 ? (uint32_t)reinterpret_cast<const uint16_t *>(P.codes)[p0 + j]
                                           : reinterpret_cast<const uint32_t *>(P.codes)[p0 + j]) : 1u;
+        }
+        if (t + gridDim.x < P.ntiles) {                      // next tile's inputs
+            const long long cn = P.first_chunk + (t + gridDim.x) * LC_TPB;
+            lc_prefetch_codes_tile(P, t + gridDim.x);
+            lc_prefetch_bytes(S.pred.kind + cn, LC_TPB * sizeof(int));
+            lc_prefetch_bytes(S.pred.B + cn, LC_TPB * sizeof(double));
+            lc_prefetch_bytes(S.pred.t0 + cn, LC_TPB * sizeof(double));
+            lc_prefetch_bytes(S.pred.t1 + cn, LC_TPB * sizeof(double));
+            lc_prefetch_bytes(S.pred.y + cn, LC_TPB * sizeof(double));
+            lc_prefetch_bytes(S.pred.g0 + cn, LC_TPB * sizeof(double));
+            lc_prefetch_bytes(P.chunk_esc + cn, LC_TPB * sizeof(long long));
         }
         double start = 0.0;
         long long e = 0;

@@ -465,6 +465,15 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_quant_b_kernel(LcQuantParams P, 
         lc_cp_async_wait();
         __syncthreads();
         lc_prefetch_x_tile(P, t + gridDim.x);
+        if (t + gridDim.x < P.ntiles) {                      // next tile's chunk predictions
+            const long long cn = P.first_chunk + (t + gridDim.x) * LC_TPB;
+            lc_prefetch_bytes(P.pred.kind + cn, LC_TPB * sizeof(int));
+            lc_prefetch_bytes(P.pred.B + cn, LC_TPB * sizeof(double));
+            lc_prefetch_bytes(P.pred.t0 + cn, LC_TPB * sizeof(double));
+            lc_prefetch_bytes(P.pred.t1 + cn, LC_TPB * sizeof(double));
+            lc_prefetch_bytes(P.pred.y + cn, LC_TPB * sizeof(double));
+            lc_prefetch_bytes(P.pred.g0 + cn, LC_TPB * sizeof(double));
+        }
         const double *row = xs + tid * LC_ROW;
         {
             double r = start;
