@@ -29,6 +29,7 @@
 #define LC_LUT_BITS 12
 #define LC_DEC_TPB 256
 #define LC_SEG_DEAD 0xffffu
+#define LC_L16 4096                  // second-level length table (16-bit prefixes of long codes)
 
 struct LcDecTables {
     int max_len;
@@ -42,7 +43,9 @@ struct LcDecTables {
     unsigned int lut2[1 << LC_LUT_BITS];  // codewords inside the 12 bits: (n << 16) | (bits << 12) | start mask
     unsigned long long lim[34];      // left-justified 32-bit code limits per length (canonical codes, l <= 32)
     int canon;                       // Kraft <= 1 and max_len <= 32: lengths follow from lim[]
-    int pad2[3];
+    unsigned s16;                    // first 16-bit prefix of the codes longer than LC_LUT_BITS (canonical)
+    int pad2[2];
+    unsigned char len16[LC_L16];     // length (13..16) of the code under 16-bit prefix s16 + i; 0: longer / none
 };
 
 // lengths[nl] -> tables + sorted symbols (canonical order).  SM: the lengths
@@ -123,8 +126,27 @@ __global__ void __launch_bounds__(1024) lc_dec_tables_kernel(const uint8_t *__re
             T->lim[l] = v;
         }
         T->canon = canon;
+        // long canonical codes occupy the 12-bit prefixes from lim[12] upwards
+        T->s16 = (canon && ml > LC_LUT_BITS) ? (unsigned)(T->lim[LC_LUT_BITS] >> 16) : 0x10000u;
     }
     __syncthreads();
+    {
+        // lengths 13..16 depend on the top 16 bits only (lim[l] is a multiple
+        // of 2^16 for l <= 16); same rule as lc_long_len
+        const unsigned s16 = T->s16;
+        const int ml = s_max;
+        for (int i = tid; i < LC_L16; i += blockDim.x) {
+            const unsigned w16 = s16 + (unsigned)i;
+            int len = 0;
+            if (w16 < 0x10000u) {
+                const unsigned long long w = (unsigned long long)w16 << 16;
+                if (w < T->lim[ml <= 32 ? ml : 32])
+                    for (int l = LC_LUT_BITS + 1; l <= 16 && l <= ml; ++l)
+                        if (w < T->lim[l]) { len = l; break; }
+            }
+            T->len16[i] = (unsigned char)len;
+        }
+    }
     if (tid >= 1 && tid <= 64 && s_cnt[tid]) {
         int acc = 0;
         for (int w = 0; w < nw; ++w) {
@@ -326,6 +348,15 @@ __device__ __forceinline__ int lc_long_len(const LcDecTables &T, unsigned long l
     return l;
 }
 
+// lc_long_len through the 16-bit second-level table (codes of 13..16 bits),
+// the limit walk for longer ones
+__device__ __forceinline__ int lc_long_len_fast(const LcDecTables &T, unsigned long long buf)
+{
+    const unsigned i = (unsigned)(buf >> 48) - T.s16;
+    const int l = i < (unsigned)LC_L16 ? (int)T.len16[i] : 0;
+    return l ? l : lc_long_len(T, buf);
+}
+
 __device__ __forceinline__ void lc_seg_dead(LcSeg &S)
 {
     S.start = S.exit = LC_SEG_DEAD;
@@ -361,7 +392,7 @@ __device__ void lc_seg_walk(const LcDecTables &T, const uint32_t *__restrict__ s
             int adv = (int)((e2 >> 12) & 15u);
             unsigned sm = e2 & 0xfffu;
             if (!e2 || br.pos + (unsigned)adv > bits_rel) {
-                adv = e2 ? 0 : lc_long_len(T, br.buf);
+                adv = e2 ? 0 : lc_long_len_fast(T, br.buf);
                 if (!adv || br.pos + (unsigned)adv > bits_rel) {
                     uint32_t sym;
                     adv = lc_next_symbol(T, sorted, br, bits_rel, &sym, &term);
@@ -528,7 +559,7 @@ __global__ void __launch_bounds__(128) lc_dec_fix_kernel(LcDecParams P, LcSeg *_
         int adv = (int)((e2 >> 12) & 15u);
         unsigned sm = e2 & 0xfffu;
         if (!e2 || br.pos + (unsigned)adv > bits_rel) {
-            adv = e2 ? 0 : lc_long_len(T, br.buf);
+            adv = e2 ? 0 : lc_long_len_fast(T, br.buf);
             if (!adv || br.pos + (unsigned)adv > bits_rel) {
                 uint32_t sym;
                 adv = lc_next_symbol(T, P.sorted, br, bits_rel, &sym, &term);
@@ -722,7 +753,7 @@ __global__ void __launch_bounds__(LC_DEC_TPB) lc_dec_write_kernel(LcDecParams P,
                             sym = e1 & 0xffffffu;
                             l = (int)(e1 >> 24);
                         } else {
-                            l = e2 ? 0 : lc_long_len(Ts, br.buf);
+                            l = e2 ? 0 : lc_long_len_fast(Ts, br.buf);
                             if (l && br.pos + (unsigned)l <= bits_rel) {
                                 const unsigned long long v = (br.buf >> 32) >> (32 - l);
                                 sym = __ldg(P.sorted + Ts.offset[l] + (v - Ts.first_code[l]));
@@ -848,7 +879,7 @@ __global__ void __launch_bounds__(256) lc_dec_v2_kernel(LcDecParams P, const uns
                     sym = e1 & 0xffffffu;
                     l = (int)(e1 >> 24);
                 } else {
-                    l = e2 ? 0 : lc_long_len(Ts, br.buf);
+                    l = e2 ? 0 : lc_long_len_fast(Ts, br.buf);
                     if (l && br.pos + (unsigned)l <= bits_rel) {
                         const unsigned long long v = (br.buf >> 32) >> (32 - l);
                         sym = __ldg(P.sorted + Ts.offset[l] + (v - Ts.first_code[l]));
