@@ -86,9 +86,10 @@ __device__ __forceinline__ OffMap lc_map_neutral() { return lc_map_trans(0.0, 0.
 // stops at the nearest inclusive one and folds the aggregates in between
 // with a shuffle tree.  op(a, b) means "a then b" (a is the earlier tile).
 // st_of(k) must be an acquire load; val_of(k, st) the matching value.
+// `first` is the value before tile 0 (the launch state; ident by default).
 template <typename T, typename Op, typename Shfl, typename StOf, typename ValOf>
 __device__ __forceinline__ T lc_lookback_warp(long long t, T ident, Op op, Shfl shfl_down,
-                                             StOf st_of, ValOf val_of)
+                                             StOf st_of, ValOf val_of, const T *first = nullptr)
 {
     const int lane = threadIdx.x & 31;
     T acc = ident;                                // prefix of tiles already folded (later ones)
@@ -96,7 +97,7 @@ __device__ __forceinline__ T lc_lookback_warp(long long t, T ident, Op op, Shfl 
     for (;;) {
         const long long idx = k - lane;
         int st = 2;
-        T v = ident;
+        T v = (idx == -1 && first) ? *first : ident;
         if (idx >= 0) {
             while ((st = st_of(idx)) == 0) { }
             v = val_of(idx, st);

@@ -937,14 +937,23 @@ __device__ __forceinline__ LcSegScan lc_segscan_op(const LcSegScan &a, const LcS
     return r;
 }
 
-struct LcRecDesc {
-    int st_seg, st_map;
-    long long seg_agg_sum, seg_agg_cnt, seg_inc_sum, seg_inc_cnt;
-    int seg_agg_has, seg_inc_has;
-    int map_kind, pad;
-    double mv, mB, mt0, mt1, my, mog;
-    double incl_D;
+// look-back descriptor of one reconstruction tile: status 1 = aggregate, 2 = inclusive
+struct LcSegDesc {
+    int st;
+    int pad;
+    LcSegScan agg, incl;
 };
+
+__device__ __forceinline__ LcSegScan lc_shfl_down_seg(const LcSegScan &v, int o)
+{
+    LcSegScan r;
+    r.sum = __shfl_down_sync(0xffffffffu, v.sum, o);
+    r.cnt = __shfl_down_sync(0xffffffffu, v.cnt, o);
+    r.has = __shfl_down_sync(0xffffffffu, v.has, o);
+    r.moved = __shfl_down_sync(0xffffffffu, v.moved, o);
+    return r;
+}
+
 
 struct LcRecParams {
     const void *codes;
@@ -959,8 +968,6 @@ struct LcRecParams {
     double anchor_val;          // exact value at position first_chunk*L
     long long anchor_cnt;       // escapes before position first_chunk*L (inclusive)
     int64_t nchunks, ntiles;
-    LcRecDesc *desc;
-    unsigned int *tile_counter;
     double *out;
     unsigned long long *first_bad;
     double *bad_end;
@@ -977,19 +984,15 @@ __device__ __forceinline__ bool lc_rec_aborted(const LcRecParams &P)
 __device__ __forceinline__ int lc_code_m(uint32_t code) { return lc_unzigzag(code); }
 
 // ---------------------------------------------------------------------------
-// Split reconstruction (no inter-tile waiting): R0 segmented m-prefix per tile,
-// R0 scan, RA guess chains + maps, map scan (lc_map_scan_kernel), RB exact chain.
+// Split reconstruction: RA (segmented m-prefix by block scan + look-back, guess
+// chains + maps), map scan (lc_map_scan_kernel), RB exact chain.
 
-struct LcSegPk {               // in-tile exclusive LcSegScan of one chunk (R0 -> RA)
-    long long sum;
-    int cnt;                    // <= LC_TILE
-    int flags;                  // has | moved << 1
-};
 
 struct LcRecSplit {
-    LcSegPk *chunk_excl;      // [nchunks] R0 output (state at each chunk start within its tile)
-    LcSegScan *tile_seg;      // [ntiles] R0 output (tile aggregate)
-    LcSegScan *tile_in;       // [ntiles] R0 scan output (state at each tile start)
+    LcSegScan *tile_seg;      // [ntiles] RA: tile aggregate of the segmented m-prefix
+    LcSegScan *tile_in;       // [ntiles] RA: state at each tile start
+    LcSegDesc *seg_desc;      // [ntiles] RA look-back descriptors (status zeroed per launch)
+    unsigned long long *tile_ctr;   // RA dynamic tile counter (zeroed per launch)
     OffMap *tile_agg;         // [ntiles] RA output
     double *tile_D;           // [ntiles + 1] map scan output
     LcChunkPred pred;         // RA -> RB
@@ -1090,99 +1093,11 @@ __device__ __forceinline__ LcSegScan lc_block_segscan(const LcSegScan &mine, LcS
     return exc;
 }
 
-__global__ void __launch_bounds__(LC_TPB) lc_rec0_kernel(LcRecParams P, LcRecSplit S)
-{
-    __shared__ LcSegScan wseg[LC_TPB / 32];
-    if (lc_rec_aborted(P)) return;
-    const int tid = threadIdx.x;
-    const long long nel = (long long)P.n - 1;
-    for (long long t = blockIdx.x; t < P.ntiles; t += gridDim.x) {
-        const long long cbeg = P.first_chunk + t * LC_TPB;
-        const long long c = cbeg + tid;
-        const int len = (c < P.nchunks) ? (int)min((long long)LC_L, nel - c * LC_L) : 0;
-        uint32_t v[LC_L];
-        lc_load_chunk_codes(P, c * LC_L, len, v);
-        lc_prefetch_codes_tile(P, t + gridDim.x);
-        LcSegScan mine; mine.sum = 0; mine.cnt = 0; mine.has = 0; mine.moved = 0;
-#pragma unroll
-        for (int j = 0; j < LC_L; ++j) {
-            if (j < len) {
-                const uint32_t code = v[j];
-                if (code == 0) { mine.sum = 0; mine.cnt += 1; mine.has = 1; mine.moved = 0; }
-                else { const int mm = lc_code_m(code); mine.sum += mm; mine.moved |= (mm != 0); }
-            }
-        }
-        __syncthreads();
-        LcSegScan agg;
-        const LcSegScan exc = lc_block_segscan(mine, wseg, &agg);
-        if (len > 0) {
-            LcSegPk pk;
-            pk.sum = exc.sum; pk.cnt = (int)exc.cnt; pk.flags = exc.has | (exc.moved << 1);
-            S.chunk_excl[c] = pk;
-        }
-        if (tid == 0) S.tile_seg[t] = agg;
-    }
-}
-
-__global__ void __launch_bounds__(512) lc_rec0_scan_kernel(LcRecSplit S, long long ntiles, long long anchor_cnt)
-{
-    // rounds of 512 x 8 tiles: loads first (registers), per-thread runs, warp
-    // scan + warp-0 scan of warp sums; LcSegScan is a monoid.  The state
-    // entering each round is carried to the next.
-    constexpr int PER = 8;
-    __shared__ LcSegScan wsum[16];
-    __shared__ LcSegScan s_carry;
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    LcSegScan carry; carry.sum = 0; carry.cnt = anchor_cnt; carry.has = 1; carry.moved = 0;   // launch anchor
-    for (long long r0 = 0; r0 < ntiles; r0 += 512LL * PER) {
-        const long long b0 = r0 + (long long)tid * PER;
-        LcSegScan v[PER];
-#pragma unroll
-        for (int k = 0; k < PER; ++k) {
-            if (b0 + k < ntiles) v[k] = S.tile_seg[b0 + k];
-            else { v[k].sum = 0; v[k].cnt = 0; v[k].has = 0; v[k].moved = 0; }
-        }
-        LcSegScan inc = v[0];
-#pragma unroll
-        for (int k = 1; k < PER; ++k) inc = lc_segscan_op(inc, v[k]);
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const LcSegScan up = lc_shfl_up_seg(inc, o);
-            if (lane >= o) inc = lc_segscan_op(up, inc);
-        }
-        if (lane == 31) wsum[wid] = inc;
-        __syncthreads();
-        if (wid == 0) {
-            LcSegScan w;
-            if (lane < 16) w = wsum[lane];
-            else { w.sum = 0; w.cnt = 0; w.has = 0; w.moved = 0; }
-#pragma unroll
-            for (int o = 1; o < 16; o <<= 1) {
-                const LcSegScan up = lc_shfl_up_seg(w, o);
-                if (lane >= o) w = lc_segscan_op(up, w);
-            }
-            if (lane < 16) wsum[lane] = w;
-        }
-        __syncthreads();
-        if (wid > 0) inc = lc_segscan_op(wsum[wid - 1], inc);
-        LcSegScan exc = lc_shfl_up_seg(inc, 1);
-        if (lane == 0) {
-            if (wid > 0) exc = wsum[wid - 1];
-            else { exc.sum = 0; exc.cnt = 0; exc.has = 0; exc.moved = 0; }
-        }
-        LcSegScan st = lc_segscan_op(carry, exc);
-#pragma unroll
-        for (int k = 0; k < PER; ++k) {
-            if (b0 + k < ntiles) S.tile_in[b0 + k] = st;
-            st = lc_segscan_op(st, v[k]);
-        }
-        if (tid == 511) s_carry = st;
-        __syncthreads();
-        carry = s_carry;
-        __syncthreads();
-    }
-}
-
+// RA: tiles in claim order (dynamic counter, so every tile a CTA waits for
+// was claimed earlier by a running CTA).  Each tile derives the escape-
+// segmented m-prefix of its chunks from its codes (block scan) and the state at
+// the tile start by a decoupled look-back over the tiles' aggregates; then
+// guess chains, flags, compacted replays and the in-tile map scan.
 __global__ void __launch_bounds__(LC_TPB, 3) lc_rec_a_kernel(LcRecParams P, LcRecSplit S)
 {
     extern __shared__ __align__(16) unsigned char lc_dyn_smem[];
@@ -1190,31 +1105,76 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_rec_a_kernel(LcRecParams P, LcRe
     __shared__ OffMap warp_agg[LC_TPB / 32];
     __shared__ LcReplayItem s_rq[LC_TPB];
     __shared__ int s_rcnt[LC_TPB / 32];
+    __shared__ LcSegScan wseg[LC_TPB / 32];
+    __shared__ LcSegScan s_tin;
+    __shared__ long long s_tile;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const long long nel = (long long)P.n - 1;
     if (lc_rec_aborted(P)) return;
-    for (long long t = blockIdx.x; t < P.ntiles; t += gridDim.x) {
+    for (;;) {
+        __syncthreads();                                 // the previous tile is done with smem
+        if (tid == 0) s_tile = (long long)atomicAdd(S.tile_ctr, 1ull);
+        __syncthreads();
+        const long long t = s_tile;
+        if (t >= P.ntiles) break;
         const long long cbeg = P.first_chunk + t * LC_TPB;
         const long long c = cbeg + tid;
         const int len = (c < P.nchunks) ? (int)min((long long)LC_L, nel - c * LC_L) : 0;
+        LcSegScan mine; mine.sum = 0; mine.cnt = 0; mine.has = 0; mine.moved = 0;
+        {
+            uint32_t v[LC_L];
+            lc_load_chunk_codes(P, c * LC_L, len, v);
+            uint32_t *row = cs + tid * LC_ROW;
+#pragma unroll
+            for (int j = 0; j < LC_L; ++j) {
+                row[j] = v[j];
+                if (j < len) {
+                    const uint32_t code = v[j];
+                    if (code == 0) { mine.sum = 0; mine.cnt += 1; mine.has = 1; mine.moved = 0; }
+                    else { const int mm = lc_code_m(code); mine.sum += mm; mine.moved |= (mm != 0); }
+                }
+            }
+        }
+        lc_prefetch_codes_tile(P, t + 1);
+        LcSegScan agg;
+        const LcSegScan exc = lc_block_segscan(mine, wseg, &agg);      // barriers inside
+        if (wid == 0) {
+            LcSegDesc *d = S.seg_desc + t;
+            if (lane == 0) {
+                d->agg = agg;
+                __threadfence();
+                st_release(&d->st, 1);
+            }
+            LcSegScan ident; ident.sum = 0; ident.cnt = 0; ident.has = 0; ident.moved = 0;
+            LcSegScan first; first.sum = 0; first.cnt = P.anchor_cnt; first.has = 1; first.moved = 0;   // launch anchor
+            const LcSegScan pre = lc_lookback_warp<LcSegScan>(
+                t, ident, [](const LcSegScan &x, const LcSegScan &y) { return lc_segscan_op(x, y); },
+                [](const LcSegScan &v, int o) { return lc_shfl_down_seg(v, o); },
+                [&](long long k) { return ld_acquire(&S.seg_desc[k].st); },
+                [&](long long k, int st) {
+                    const LcSegDesc *q = S.seg_desc + k;
+                    LcSegScan r;
+                    const LcSegScan *src = st == 2 ? &q->incl : &q->agg;
+                    r.sum = __ldcg(&src->sum); r.cnt = __ldcg(&src->cnt);
+                    r.has = __ldcg(&src->has); r.moved = __ldcg(&src->moved);
+                    return r;
+                }, &first);
+            if (lane == 0) {
+                d->incl = lc_segscan_op(pre, agg);
+                __threadfence();
+                st_release(&d->st, 2);
+                s_tin = pre;
+                S.tile_in[t] = pre;
+                S.tile_seg[t] = agg;
+            }
+        }
         __syncthreads();
-        lc_load_codes_tile(P, cbeg * LC_L, cs);
-        __syncthreads();
-        lc_prefetch_codes_tile(P, t + gridDim.x);
-        if (t + gridDim.x < P.ntiles)
-            lc_prefetch_bytes(S.chunk_excl + P.first_chunk + (t + gridDim.x) * LC_TPB, (LC_TPB + 1) * sizeof(LcSegPk));
         const uint32_t *crow = cs + tid * LC_ROW;
-        // chunk start states from R0 (in-tile exclusive) + the tile's incoming state
-        auto unpk = [](const LcSegPk &p) {
-            LcSegScan v; v.sum = p.sum; v.cnt = p.cnt; v.has = p.flags & 1; v.moved = p.flags >> 1;
-            return v;
-        };
-        const LcSegScan tin = S.tile_in[t];
+        const LcSegScan tin = s_tin;
         LcSegScan before = tin, after = tin;
         if (len > 0) {
-            before = lc_segscan_op(tin, unpk(S.chunk_excl[c]));
-            if (c + 1 < P.nchunks)
-                after = tid + 1 < LC_TPB ? lc_segscan_op(tin, unpk(S.chunk_excl[c + 1])) : S.tile_in[t + 1];
+            before = lc_segscan_op(tin, exc);
+            if (c + 1 < P.nchunks) after = lc_segscan_op(before, mine);
         }
         auto anchor_of = [&](const LcSegScan &s) -> double {
             if (s.cnt > P.anchor_cnt) {
@@ -1694,8 +1654,8 @@ static int lc_reconstruct(lc_ctx *ctx, uint64_t n, double eb_abs, double first_v
     }
     const int64_t nchunks = (int64_t)((m + LC_L - 1) / LC_L);
     const int64_t ntiles = (nchunks + LC_TPB - 1) / LC_TPB;
-    LC_CUDA_OK(lc_reserve(baux2, LC_MAPSCAN_SCRATCH + (size_t)(ntiles + 1) * (2 * sizeof(LcSegScan) + sizeof(OffMap) + sizeof(double))
-                                 + (size_t)nchunks * (16 + sizeof(int) + 5 * sizeof(double) + sizeof(LcSegPk)) + 256));
+    LC_CUDA_OK(lc_reserve(baux2, LC_MAPSCAN_SCRATCH + 16 + (size_t)(ntiles + 1) * (2 * sizeof(LcSegScan) + sizeof(LcSegDesc) + sizeof(OffMap) + sizeof(double))
+                                 + (size_t)nchunks * (16 + sizeof(int) + 5 * sizeof(double)) + 256));
     LcRecParams R;
     R.codes = codes;
     R.code_bytes = code_bytes;
@@ -1709,8 +1669,6 @@ static int lc_reconstruct(lc_ctx *ctx, uint64_t n, double eb_abs, double first_v
     R.anchor_val = first_value;
     R.anchor_cnt = 0;
     R.nchunks = nchunks;
-    R.desc = nullptr;
-    R.tile_counter = nullptr;
     R.out = dout;
     R.first_bad = (unsigned long long *)((char *)baux.p + 112);
     R.esc_flags = esc_flags;
@@ -1723,9 +1681,10 @@ static int lc_reconstruct(lc_ctx *ctx, uint64_t n, double eb_abs, double first_v
     void *mapscan_scratch;
     {
         char *pp = (char *)baux2.p;
-        RS.chunk_excl = (LcSegPk *)pp;           pp += nchunks * sizeof(LcSegPk);
         RS.tile_seg = (LcSegScan *)pp;           pp += (ntiles + 1) * sizeof(LcSegScan);
         RS.tile_in = (LcSegScan *)pp;            pp += (ntiles + 1) * sizeof(LcSegScan);
+        RS.tile_ctr = (unsigned long long *)pp;  pp += 16;
+        RS.seg_desc = (LcSegDesc *)pp;           pp += (ntiles + 1) * sizeof(LcSegDesc);
         RS.tile_agg = (OffMap *)pp;              pp += (ntiles + 1) * sizeof(OffMap);
         mapscan_scratch = (void *)pp;            pp += LC_MAPSCAN_SCRATCH;
         RS.tile_D = (double *)pp;                pp += (ntiles + 1) * sizeof(double);
@@ -1751,13 +1710,12 @@ static int lc_reconstruct(lc_ctx *ctx, uint64_t n, double eb_abs, double first_v
     LC_CUDA_OK(cudaMemsetAsync(esc_flags, 0, 8, st));
     lc_set_first_kernel<<<1, 1, 0, st>>>(dout, first_value);
     lc_count_launch(ctx, 1);
-    const int grid_cap = 2 * lc_sm_count(ctx);
     int relaunches = 0;
     for (;;) {
         R.ntiles = (nchunks - R.first_chunk + LC_TPB - 1) / LC_TPB;
         LC_CUDA_OK(cudaMemsetAsync(R.first_bad, 0xff, 8, st));
-        lc_rec0_kernel<<<(int)(R.ntiles < 3 * grid_cap ? R.ntiles : 3 * grid_cap), LC_TPB, 0, st>>>(R, RS);
-        lc_rec0_scan_kernel<<<1, 512, 0, st>>>(RS, R.ntiles, R.anchor_cnt);
+        // RA look-back state: tile counter and descriptor statuses (contiguous)
+        LC_CUDA_OK(cudaMemsetAsync(RS.tile_ctr, 0, 16 + (size_t)R.ntiles * sizeof(LcSegDesc), st));
         lc_rec_a_kernel<<<(int)(R.ntiles < 3 * lc_sm_count(ctx) ? R.ntiles : 3 * lc_sm_count(ctx)), LC_TPB,
                           lc_rec_a_smem_bytes(), st>>>(R, RS);
         { int _rc = lc_debug_check(ctx, "lc_rec_a_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
@@ -1767,7 +1725,7 @@ static int lc_reconstruct(lc_ctx *ctx, uint64_t n, double eb_abs, double first_v
         else lc_rec_b_kernel<4><<<grid_b, LC_TPB, lc_rec_b_smem_bytes(), st>>>(R, RS);
         { int _rc = lc_debug_check(ctx, "lc_rec_b_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
         lc_rec_final_kernel<<<1, 1, 0, st>>>(R, RS, R.ntiles - 1, dfin);
-        lc_count_launch(ctx, 6);
+        lc_count_launch(ctx, 4);
         LC_CUDA_OK(cudaMemcpyAsync(hfin, dfin, sizeof(LcRecFinal), cudaMemcpyDeviceToHost, st));
         LC_CUDA_OK(cudaStreamSynchronize(st));
         if (hfin->abort_a || hfin->abort_b) {            // the decode failed or needs another pass
