@@ -1,9 +1,20 @@
-"""Summarise an ncu metrics CSV (dram bytes + duration per launch) into
-profiles/ncu_summary.json keyed by the bench's kernel groups."""
-import csv, json, sys, collections
+"""Summarise an ncu launch list of `bench.py --steps 1 --warmup 1 --no-cpu --no-solver`
+(metrics gpu__time_duration.sum, dram__bytes_read.sum, dram__bytes_write.sum) into
+profiles/ncu_summary.json keyed by the bench's kernel groups.
+
+    python profiles/make_ncu_summary.py launches.csv profiles/ncu_summary.json
+
+Every compress+decompress round trip starts with lc_range_kernel; the second
+step's three round trips (bounds 1e-3, 1e-4, 1e-6) are summarised."""
+import collections
+import csv
+import json
+import sys
+
 rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 10]
 h = rows[0]
-ki, mi, vi, ui, ii = h.index('Kernel Name'), h.index('Metric Name'), h.index('Metric Value'), h.index('Metric Unit'), h.index('ID')
+ki, mi, vi, ui, ii = (h.index('Kernel Name'), h.index('Metric Name'), h.index('Metric Value'),
+                      h.index('Metric Unit'), h.index('ID'))
 launch = collections.OrderedDict()
 for r in rows[1:]:
     d = launch.setdefault(r[ii], {'kernel': r[ki].split('(')[0].replace('void ', '').split('<')[0]})
@@ -14,30 +25,32 @@ for r in rows[1:]:
         d['dram'] = d.get('dram', 0) + v
     elif r[mi] == 'gpu__time_duration.sum':
         d['us'] = v / 1000 if u in ('ns', 'nsecond') else (v if u in ('us', 'usecond') else v * 1000)
-seq = list(launch.values())
-# split into the 6 iterations (2 per bound) at lc_anchor_tiles_kernel; keep the second of each bound
 its, cur = [], None
-for d in seq:
-    if d['kernel'] == 'lc_anchor_tiles_kernel':
-        cur = []; its.append(cur)
-    cur.append(d)
-groups = {'quantizer': ['lc_quant_a_kernel', 'lc_map_scan_kernel', 'lc_quant_b_kernel'],
+for d in launch.values():
+    if d['kernel'] == 'lc_range_kernel':
+        cur = []
+        its.append(cur)
+    if cur is not None:
+        cur.append(d)
+timed = its[3:6]
+groups = {'quantizer': ['lc_anchor_tiles_kernel', 'lc_anchor_scan_kernel', 'lc_quant_a_kernel', 'lc_map_scan_kernel',
+                        'lc_quant_b_kernel'],
           'encoder': ['lc_codebook_kernel', 'lc_zero_words_kernel', 'lc_encode_kernel'],
           'huffman_decode': ['lc_dec_tables_kernel', 'lc_dec_sync_kernel', 'lc_dec_fix_kernel', 'lc_dec_scan_kernel',
                              'lc_dec_write_kernel', 'lc_dec_status_kernel'],
-          'reconstruction': ['lc_rec0_kernel', 'lc_rec0_scan_kernel', 'lc_rec_a_kernel', 'lc_map_scan_kernel', 'lc_rec_b_kernel']}
+          'reconstruction': ['lc_rec_a_kernel', 'lc_map_scan_kernel', 'lc_rec_b_kernel', 'lc_rec_final_kernel']}
 out = {}
 bounds = ['1e-3', '1e-4', '1e-6']
 for g, ks in groups.items():
     per = {}
-    for bi, it in enumerate(its[1::2]):
-        # reconstruction's map_scan is the second one in the iteration
+    for bi, it in enumerate(timed):
+        names = [d['kernel'] for d in it]
         if g == 'reconstruction':
-            idx = [i for i, d in enumerate(it) if d['kernel'] == 'lc_rec0_kernel'][0]
-            sel = [d for d in it[idx:] if d['kernel'] in ks]
+            lo = names.index('lc_rec_a_kernel')
+            sel = [d for d in it[lo:] if d['kernel'] in ks]
         elif g == 'quantizer':
-            idx = [i for i, d in enumerate(it) if d['kernel'] == 'lc_quant_a_kernel'][0]
-            sel = [d for d in it[idx:idx + 3] if d['kernel'] in ks]
+            hi = names.index('lc_quant_b_kernel') + 1
+            sel = [d for d in it[:hi] if d['kernel'] in ks]
         else:
             sel = [d for d in it if d['kernel'] in ks]
         per[bounds[bi]] = {'dram_bytes': sum(d.get('dram', 0) for d in sel), 'us': sum(d.get('us', 0) for d in sel),
@@ -45,7 +58,14 @@ for g, ks in groups.items():
     out[g] = {'dram_bytes_per_launch': sum(p['dram_bytes'] for p in per.values()) / len(per),
               'ncu_us_per_launch': sum(p['us'] for p in per.values()) / len(per), 'per_bound': per,
               'source': 'ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum '
-                        '--clock-control none, scratch/prof_pipe.py 1e-3 1e-4 1e-6 (n=2^26), second call per bound'}
+                        '--clock-control none, bench.py --steps 1 --warmup 1 --no-cpu --no-solver (n=2^26), '
+                        'timed step'}
+other = collections.defaultdict(float)
+for it in timed:
+    for d in it:
+        if d['kernel'] == 'lc_range_kernel' or d['kernel'] == 'lc_range_final_kernel':
+            other[d['kernel']] += d.get('us', 0) / 3
+out['range'] = {'ncu_us_per_launch': sum(other.values()), 'kernels': dict(other)}
 json.dump(out, open(sys.argv[2], 'w'), indent=1)
 for g, d in out.items():
-    print(g, 'dram MB/launch %.1f' % (d['dram_bytes_per_launch'] / 1e6), 'ncu us %.0f' % d['ncu_us_per_launch'])
+    print(g, 'dram MB/launch %.1f' % (d.get('dram_bytes_per_launch', 0) / 1e6), 'ncu us %.0f' % d['ncu_us_per_launch'])
