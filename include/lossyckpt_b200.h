@@ -118,6 +118,15 @@ int lc_phase_ms(lc_ctx *ctx, double *ms, int cap);
 /* Kernels this context has launched since creation (diagnostic count).   */
 uint64_t lc_launch_count(lc_ctx *ctx);
 
+/* Launch timeline (diagnostics; contexts created with LC_TRACE=1 in the
+ * environment): lc_trace_mark_api adds a named mark, every launch adds one
+ * with the kernel name; lc_trace_read syncs the stream, writes one line
+ * "name host_us gpu_us" per mark (host enqueue time and device completion
+ * time, both relative to the first mark) and clears the trace.  Returns the
+ * bytes written (0 when tracing is off).                                    */
+int lc_trace_mark_api(lc_ctx *ctx, const char *what);
+int lc_trace_read(lc_ctx *ctx, char *out, int cap);
+
 /* Distortion statistics of a reconstruction in one fused pass: the sum of
  * squared errors sum((x - y)^2) (compensated; MSE = sum / n), max |x - y|,
  * min/max of x (value range), a non-finite flag and, when pe / pe_rec (the

@@ -83,6 +83,10 @@ def library():
         L.lc_phase_ms.restype = ctypes.c_int
         L.lc_launch_count.argtypes = [_vp]
         L.lc_launch_count.restype = ctypes.c_uint64
+        L.lc_trace_mark_api.argtypes = [_vp, ctypes.c_char_p]
+        L.lc_trace_mark_api.restype = ctypes.c_int
+        L.lc_trace_read.argtypes = [_vp, ctypes.c_char_p, ctypes.c_int]
+        L.lc_trace_read.restype = ctypes.c_int
         L.lc_error_stats_f64.argtypes = [_vp, _vp, _vp, ctypes.c_uint64, ctypes.c_int, _vp, _vp,
                                          ctypes.POINTER(LcStats)]
         L.lc_error_stats_f64.restype = ctypes.c_int
@@ -110,7 +114,7 @@ EXPORTED = ["lc_ctx_create", "lc_ctx_destroy", "lc_last_error", "lc_range_f64", 
             "lc_result_fetch", "lc_result_device", "lc_decompress_f64", "lc_last_device_ms",
             "lc_phase_ms", "lc_launch_count", "lc_error_stats_f64", "lc_stencil_apply_f64",
             "lc_residual_f64", "lc_jacobi_step_f64", "lc_dot_f64", "lc_axpy_f64", "lc_result_sync",
-            "lc_decompress_v2_f64"]
+            "lc_decompress_v2_f64", "lc_trace_mark_api", "lc_trace_read"]
 
 
 class Context:

@@ -1,5 +1,6 @@
 // lc_api.cu -- C ABI (include/lossyckpt_b200.h): contexts, compress and
 // decompress drivers over the sm_100a kernels.
+#include <chrono>
 #include <cuda_runtime.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -33,6 +34,11 @@ struct lc_ctx {
     int last_kind = 0;              // 1 compress, 2 decompress
     bool debug_sync = false;        // LC_DEBUG_SYNC=1: sync + check after every launch
     bool timeline_on = false;       // LC_TIMELINE=1: per-tile phase stamps of the quantizer
+    bool trace_on = false;          // LC_TRACE=1: an event + host timestamp after every launch
+    cudaEvent_t tev[256] = {};
+    const char *tname[256] = {};
+    double thost[256] = {};
+    int tn = 0;
     LcBuf timeline;
     int64_t timeline_tiles = 0;
     uint64_t launches = 0;
@@ -88,8 +94,24 @@ LcBuf *lc_dec_bufs(lc_ctx *ctx) { return ctx->dec; }
 cudaEvent_t lc_phase_ev(lc_ctx *ctx, int i) { return ctx->pev[i]; }
 void lc_count_launch(lc_ctx *ctx, int k) { ctx->launches += k; }
 void lc_set_kind(lc_ctx *ctx, int k) { ctx->last_kind = k; }
+static double lc_host_us()
+{
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+void lc_trace_mark(lc_ctx *ctx, const char *what)
+{
+    if (!ctx->trace_on || ctx->tn >= 256) return;
+    if (!ctx->tev[ctx->tn]) cudaEventCreate(&ctx->tev[ctx->tn]);
+    ctx->thost[ctx->tn] = lc_host_us();
+    ctx->tname[ctx->tn] = what;
+    cudaEventRecord(ctx->tev[ctx->tn], ctx->stream);
+    ++ctx->tn;
+}
+
 int lc_debug_check(lc_ctx *ctx, const char *what, const char *file, int line)
 {
+    lc_trace_mark(ctx, what);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess && ctx->debug_sync) e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) return lc_fail(ctx, e, what, file, line);
@@ -107,6 +129,8 @@ int lc_ctx_create(lc_ctx **out, int device, void *stream)
     ctx->debug_sync = dbg && dbg[0] == '1';
     const char *tlv = getenv("LC_TIMELINE");
     ctx->timeline_on = tlv && tlv[0] == '1';
+    const char *trv = getenv("LC_TRACE");
+    ctx->trace_on = trv && trv[0] == '1';
     LC_CUDA_OK(cudaSetDevice(device));
     cudaDeviceProp prop;
     LC_CUDA_OK(cudaGetDeviceProperties(&prop, device));
@@ -183,12 +207,13 @@ int lc_range_f64(lc_ctx *ctx, const double *x, uint64_t n, int x_on_device, doub
     if (rc) return rc;
     int nb = (int)((n + 255) / 256);
     if (nb > 4 * ctx->sm_count) nb = 4 * ctx->sm_count;
-    LC_CUDA_OK(lc_reserve(ctx->range_parts, sizeof(LcRangePart) * (nb + 1)));
+    LC_CUDA_OK(lc_reserve(ctx->range_parts, sizeof(LcRangePart) * (nb + 1) + 16));
     LcRangePart *parts = (LcRangePart *)ctx->range_parts.p;
-    lc_range_kernel<<<nb, 256, 0, ctx->stream>>>(dx, n, parts);
-    lc_range_final_kernel<<<1, 32, 0, ctx->stream>>>(parts, nb, parts + nb);
-    ctx->launches += 2;
-    { int _rc = lc_debug_check(ctx, "lc_range_final_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+    unsigned *done = (unsigned *)(parts + nb + 1);
+    LC_CUDA_OK(cudaMemsetAsync(done, 0, sizeof(unsigned), ctx->stream));
+    lc_range_kernel<<<nb, 256, 0, ctx->stream>>>(dx, n, parts, done);
+    ctx->launches += 1;
+    { int _rc = lc_debug_check(ctx, "lc_range_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
     LcRangePart *h = (LcRangePart *)ctx->pinned;
     LC_CUDA_OK(cudaMemcpyAsync(h, parts + nb, sizeof(LcRangePart), cudaMemcpyDeviceToHost, ctx->stream));
     LC_CUDA_OK(cudaStreamSynchronize(ctx->stream));
@@ -521,6 +546,30 @@ int lc_result_device(lc_ctx *ctx, const uint8_t **payload, const uint8_t **code_
     if (code_lengths) *code_lengths = (const uint8_t *)ctx->lengths.p;
     if (esc_idx) *esc_idx = (const uint64_t *)ctx->esc_idx.p;
     if (esc_val) *esc_val = (const double *)ctx->esc_val.p;
+    return 0;
+}
+
+// LC_TRACE=1 diagnostics: "name host_us gpu_us" per mark since the last read
+// (times relative to the first mark); clears the trace.  Returns bytes written.
+int lc_trace_read(lc_ctx *ctx, char *out, int cap)
+{
+    if (!ctx || !out || cap <= 0) return 0;
+    cudaStreamSynchronize(ctx->stream);
+    int w = 0;
+    out[0] = 0;
+    for (int i = 0; i < ctx->tn && w < cap - 96; ++i) {
+        float ms = 0.0f;
+        if (i > 0) cudaEventElapsedTime(&ms, ctx->tev[0], ctx->tev[i]);
+        w += snprintf(out + w, cap - w, "%s %.1f %.1f\n", ctx->tname[i], ctx->thost[i] - ctx->thost[0], 1e3 * ms);
+    }
+    ctx->tn = 0;
+    return w;
+}
+
+int lc_trace_mark_api(lc_ctx *ctx, const char *what)
+{
+    if (!ctx) return 12;
+    lc_trace_mark(ctx, what);
     return 0;
 }
 

@@ -87,8 +87,8 @@ struct LcEncParams {
     unsigned long long *sync; // v2 sync table [ceil(m / LC_SYNC_K)] (bit offsets), may be null
 };
 
-__global__ void lc_range_kernel(const double *__restrict__ x, uint64_t n, LcRangePart *__restrict__ parts);
-__global__ void lc_range_final_kernel(const LcRangePart *__restrict__ parts, int np, LcRangePart *__restrict__ out);
+__global__ void lc_range_kernel(const double *__restrict__ x, uint64_t n, LcRangePart *__restrict__ parts,
+                                unsigned *__restrict__ done);
 __global__ void lc_anchor_tiles_kernel(LcQuantParams P);
 __global__ void lc_anchor_scan_kernel(const long long *__restrict__ last, long long *__restrict__ incoming,
                                       long long ntiles, long long launch_pos);

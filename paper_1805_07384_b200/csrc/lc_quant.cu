@@ -19,7 +19,7 @@
 
 
 __global__ void __launch_bounds__(256) lc_range_kernel(const double *__restrict__ x, uint64_t n,
-                                                      LcRangePart *__restrict__ parts)
+                                                      LcRangePart *__restrict__ parts, unsigned *__restrict__ done)
 {
     // min, max, non-finite flag and max |x_i - x_{i-1}| (decides whether definite
     // escapes are possible, lc_compress_f64).  Each lane owns 8 consecutive
@@ -110,17 +110,20 @@ __global__ void __launch_bounds__(256) lc_range_kernel(const double *__restrict_
         parts[blockIdx.x].maxstep = ms;
         parts[blockIdx.x].nonfinite = nf;
     }
-}
-
-// launch with a single warp
-__global__ void lc_range_final_kernel(const LcRangePart *__restrict__ parts, int np,
-                                      LcRangePart *__restrict__ out)
-{
-    double mn = INFINITY, mx = -INFINITY, ms = 0.0;
-    int nf = 0;
-    for (int i = threadIdx.x; i < np; i += blockDim.x) {
-        mn = fmin(mn, parts[i].vmin); mx = fmax(mx, parts[i].vmax); ms = fmax(ms, parts[i].maxstep);
-        nf |= parts[i].nonfinite;
+    // the last block to finish folds every block's part into parts[gridDim.x]
+    // (and re-arms the counter for the next call)
+    __shared__ bool s_last;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last || threadIdx.x >= 32) return;
+    __threadfence();
+    mn = INFINITY; mx = -INFINITY; ms = 0.0; nf = 0;
+    for (unsigned i = threadIdx.x; i < gridDim.x; i += 32) {
+        mn = fmin(mn, __ldcg(&parts[i].vmin)); mx = fmax(mx, __ldcg(&parts[i].vmax));
+        ms = fmax(ms, __ldcg(&parts[i].maxstep)); nf |= __ldcg(&parts[i].nonfinite);
     }
     for (int o = 16; o; o >>= 1) {
         mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
@@ -128,7 +131,11 @@ __global__ void lc_range_final_kernel(const LcRangePart *__restrict__ parts, int
         ms = fmax(ms, __shfl_xor_sync(0xffffffffu, ms, o));
         nf |= __shfl_xor_sync(0xffffffffu, nf, o);
     }
-    if (threadIdx.x == 0) { out->vmin = mn; out->vmax = mx; out->maxstep = ms; out->nonfinite = nf; }
+    if (threadIdx.x == 0) {
+        LcRangePart *out = parts + gridDim.x;
+        out->vmin = mn; out->vmax = mx; out->maxstep = ms; out->nonfinite = nf;
+        *done = 0u;
+    }
 }
 
 // ---------------------------------------------------------------------------
