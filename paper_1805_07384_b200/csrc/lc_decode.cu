@@ -1098,7 +1098,7 @@ __device__ __forceinline__ LcSegScan lc_block_segscan(const LcSegScan &mine, LcS
 // segmented m-prefix of its chunks from its codes (block scan) and the state at
 // the tile start by a decoupled look-back over the tiles' aggregates; then
 // guess chains, flags, compacted replays and the in-tile map scan.
-__global__ void __launch_bounds__(LC_TPB, 3) lc_rec_a_kernel(LcRecParams P, LcRecSplit S)
+__global__ void __launch_bounds__(LC_TPB, 4) lc_rec_a_kernel(LcRecParams P, LcRecSplit S)
 {
     extern __shared__ __align__(16) unsigned char lc_dyn_smem[];
     uint32_t *cs = reinterpret_cast<uint32_t *>(lc_dyn_smem);
@@ -1716,7 +1716,7 @@ static int lc_reconstruct(lc_ctx *ctx, uint64_t n, double eb_abs, double first_v
         LC_CUDA_OK(cudaMemsetAsync(R.first_bad, 0xff, 8, st));
         // RA look-back state: tile counter and descriptor statuses (contiguous)
         LC_CUDA_OK(cudaMemsetAsync(RS.tile_ctr, 0, 16 + (size_t)R.ntiles * sizeof(LcSegDesc), st));
-        lc_rec_a_kernel<<<(int)(R.ntiles < 3 * lc_sm_count(ctx) ? R.ntiles : 3 * lc_sm_count(ctx)), LC_TPB,
+        lc_rec_a_kernel<<<(int)(R.ntiles < 4 * lc_sm_count(ctx) ? R.ntiles : 4 * lc_sm_count(ctx)), LC_TPB,
                           lc_rec_a_smem_bytes(), st>>>(R, RS);
         { int _rc = lc_debug_check(ctx, "lc_rec_a_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
         LC_CUDA_OK((cudaError_t)lc_launch_map_scan(RS.tile_agg, RS.tile_D, R.ntiles, mapscan_scratch, lc_sm_count(ctx), st));
