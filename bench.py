@@ -249,13 +249,13 @@ def run_b200(args, rank, world, local_rank):
     vp = ctypes.c_void_p
 
     def rt(eb_rel, stats=None):
-        vmin, vmax, nf = ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
-        rc = L.lc_range_f64(ctx.h, xd.data_ptr(), n, 1, ctypes.byref(vmin), ctypes.byref(vmax), ctypes.byref(nf))
-        assert rc == 0, ctx.error()
-        eb_abs = eb_rel * float(vmax.value - vmin.value)
-        res = _native.LcResult()
-        rc = L.lc_compress_f64(ctx.h, xd.data_ptr(), n, 1, eb_abs, 32768, 0, ctypes.byref(res))
-        assert rc == 0, ctx.error()
+        # value range + device-resolved bounds + quantizer + codebook + encoder (one host
+        # round trip, the path paper_1805_07384_b200.compress takes), then the decoder
+        res, bnd = _native.LcResult(), _native.LcBounds()
+        rc = L.lc_compress_auto_f64(ctx.h, xd.data_ptr(), n, 1, 1, eb_rel, 32768, 0, ctypes.byref(res),
+                                    ctypes.byref(bnd))
+        assert rc == 0, (rc, ctx.error())
+        eb_abs = bnd.eb_abs
         if stats is not None:
             ph = (ctypes.c_double * 8)()
             k = L.lc_phase_ms(ctx.h, ph, 8)

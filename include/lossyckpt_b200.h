@@ -81,6 +81,30 @@ int lc_compress_f64(lc_ctx *ctx, const double *x, uint64_t n, int x_on_device,
                     double eb_abs, uint32_t n_bins_half, int record_traces,
                     lc_result *res);
 
+/* Bounds of an lc_compress_auto_f64 call, resolved on the device.         */
+typedef struct {
+    double vmin, vmax;     /* compressor.py:386 x.min(), x.max()           */
+    double value_range;    /* vmax - vmin (+0.0 when equal)                */
+    double eb_abs;         /* resolve_bounds (compressor.py:138-148)       */
+    double first_value;    /* x[0]                                         */
+    int nonfinite;         /* x holds NaN or Inf                           */
+    int status;            /* 0, 10, 11, 12 or 15 (= the return value)     */
+} lc_bounds;
+
+/* compressor.py:381-413 in one host round trip: value range (non-finite
+ * check), bounds (eb_abs = eb_param * value_range when eb_relative, else
+ * eb_param), the 2*eb check and, for a non-constant vector, the whole
+ * compression of lc_compress_f64 -- the quantizer reads the bounds the
+ * device derived, so nothing waits for the host between the range pass and
+ * the encoder.  Returns 0 with results, 10 (non-finite input), 11 (2*eb not
+ * finite), 12 (bad argument / eb_abs <= 0) or 15 (constant vector: the
+ * caller writes the reference's constant block from *bounds); *bounds is
+ * filled whenever the passes ran.  Replaces compressor.py:381-413 (range,
+ * resolve_bounds call, checks, _compress_kernel, bincount, encode).      */
+int lc_compress_auto_f64(lc_ctx *ctx, const double *x, uint64_t n, int x_on_device,
+                         int eb_relative, double eb_param, uint32_t n_bins_half,
+                         int record_traces, lc_result *res, lc_bounds *bounds);
+
 /* Copy the last compress result to host buffers (any may be NULL):
  * code_lengths[n_symbols], payload[payload_bytes], esc_idx/esc_val[n_esc],
  * pe/pe_rec[n-1] (only when record_traces was set).                       */

@@ -32,6 +32,15 @@ class LcResult(ctypes.Structure):
                 ("used_symbols", ctypes.c_uint32), ("relaunches", ctypes.c_uint32)]
 
 
+class LcBounds(ctypes.Structure):
+    _fields_ = [("vmin", ctypes.c_double), ("vmax", ctypes.c_double), ("value_range", ctypes.c_double),
+                ("eb_abs", ctypes.c_double), ("first_value", ctypes.c_double), ("nonfinite", ctypes.c_int),
+                ("status", ctypes.c_int)]
+
+
+STATUS_CONSTANT = 15        # lc_compress_auto_f64: constant vector (reference constant block)
+
+
 class LcStats(ctypes.Structure):
     _fields_ = [("sum_sq_err", ctypes.c_double), ("max_abs_err", ctypes.c_double),
                 ("vmin", ctypes.c_double), ("vmax", ctypes.c_double),
@@ -67,6 +76,10 @@ def library():
         L.lc_compress_f64.argtypes = [_vp, _vp, ctypes.c_uint64, ctypes.c_int, ctypes.c_double,
                                       ctypes.c_uint32, ctypes.c_int, ctypes.POINTER(LcResult)]
         L.lc_compress_f64.restype = ctypes.c_int
+        L.lc_compress_auto_f64.argtypes = [_vp, _vp, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                           ctypes.c_uint32, ctypes.c_int, ctypes.POINTER(LcResult),
+                                           ctypes.POINTER(LcBounds)]
+        L.lc_compress_auto_f64.restype = ctypes.c_int
         L.lc_result_fetch.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp]
         L.lc_result_fetch.restype = ctypes.c_int
         L.lc_result_device.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
@@ -114,7 +127,7 @@ EXPORTED = ["lc_ctx_create", "lc_ctx_destroy", "lc_last_error", "lc_range_f64", 
             "lc_result_fetch", "lc_result_device", "lc_decompress_f64", "lc_last_device_ms",
             "lc_phase_ms", "lc_launch_count", "lc_error_stats_f64", "lc_stencil_apply_f64",
             "lc_residual_f64", "lc_jacobi_step_f64", "lc_dot_f64", "lc_axpy_f64", "lc_result_sync",
-            "lc_decompress_v2_f64", "lc_trace_mark_api", "lc_trace_read"]
+            "lc_decompress_v2_f64", "lc_trace_mark_api", "lc_trace_read", "lc_compress_auto_f64"]
 
 
 class Context:

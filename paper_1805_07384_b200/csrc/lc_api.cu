@@ -1,6 +1,7 @@
 // lc_api.cu -- C ABI (include/lossyckpt_b200.h): contexts, compress and
 // decompress drivers over the sm_100a kernels.
 #include <chrono>
+#include <mutex>
 #include <cuda_runtime.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -39,6 +40,7 @@ struct lc_ctx {
     const char *tname[256] = {};
     double thost[256] = {};
     int tn = 0;
+    int qslot = -1;                 // __constant__ bounds slot (lc_compress_auto_f64), -1: none free
     LcBuf timeline;
     int64_t timeline_tiles = 0;
     uint64_t launches = 0;
@@ -94,6 +96,24 @@ LcBuf *lc_dec_bufs(lc_ctx *ctx) { return ctx->dec; }
 cudaEvent_t lc_phase_ev(lc_ctx *ctx, int i) { return ctx->pev[i]; }
 void lc_count_launch(lc_ctx *ctx, int k) { ctx->launches += k; }
 void lc_set_kind(lc_ctx *ctx, int k) { ctx->last_kind = k; }
+static std::mutex g_qslot_mu;
+static uint32_t g_qslot_used = 0;
+
+static int lc_qslot_acquire()
+{
+    std::lock_guard<std::mutex> g(g_qslot_mu);
+    for (int i = 0; i < LC_QDYN_SLOTS; ++i)
+        if (!(g_qslot_used & (1u << i))) { g_qslot_used |= 1u << i; return i; }
+    return -1;
+}
+
+static void lc_qslot_release(int i)
+{
+    if (i < 0) return;
+    std::lock_guard<std::mutex> g(g_qslot_mu);
+    g_qslot_used &= ~(1u << i);
+}
+
 static double lc_host_us()
 {
     return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -131,6 +151,7 @@ int lc_ctx_create(lc_ctx **out, int device, void *stream)
     ctx->timeline_on = tlv && tlv[0] == '1';
     const char *trv = getenv("LC_TRACE");
     ctx->trace_on = trv && trv[0] == '1';
+    ctx->qslot = lc_qslot_acquire();
     LC_CUDA_OK(cudaSetDevice(device));
     cudaDeviceProp prop;
     LC_CUDA_OK(cudaGetDeviceProperties(&prop, device));
@@ -161,6 +182,7 @@ void lc_ctx_destroy(lc_ctx *ctx)
 {
     if (!ctx) return;
     cudaStreamSynchronize(ctx->stream);
+    lc_qslot_release(ctx->qslot);
     LcBuf *bufs[] = {&ctx->xbuf, &ctx->codes, &ctx->hist, &ctx->desc, &ctx->counters, &ctx->bad_end,
                      &ctx->pe, &ctx->pe_rec, &ctx->lengths, &ctx->cw, &ctx->gkeys, &ctx->ifreq,
                      &ctx->parent, &ctx->cbout, &ctx->payload, &ctx->esc_idx, &ctx->esc_val,
@@ -267,9 +289,12 @@ int lc_error_stats_f64(lc_ctx *ctx, const double *original, const double *recon,
 
 }  // extern "C"
 
+// dyn (device) non-null: the bounds were resolved on the device by
+// lc_quant_setup_kernel (eb_abs is unused); *hdyn receives them with the one
+// readback and a non-zero hdyn->status is returned without results.
 template <typename CodeT>
 static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_abs, uint32_t nbh, int record,
-                         lc_result *res)
+                         lc_result *res, const LcQuantDyn *dyn = nullptr, LcQuantDyn *hdyn = nullptr)
 {
     cudaStream_t st = ctx->stream;
     const uint32_t nbins = 2u * nbh;
@@ -289,6 +314,8 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     unsigned long long *first_bad = (unsigned long long *)((char *)ctx->counters.p + 16);
 
     LcQuantParams P;
+    P.dyn = dyn;
+    P.dyn_slot = dyn ? ctx->qslot : -1;
     P.x = dx;
     P.n = n;
     P.Q.delta = 2.0 * eb_abs;
@@ -349,8 +376,8 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     P.anc_in = (const long long *)(P.tile_last_esc + ntiles + 1);
     long long *anc_in = (long long *)(P.tile_last_esc + ntiles + 1);
     // definite escapes possible?  Same test as lc_definite_escape on the largest step.
-    P.use_anchors = 1;
-    if (ctx->rng_ptr == (const void *)dx && ctx->rng_n == n) {
+    P.use_anchors = 1;                                   // with dyn: the device decides
+    if (!dyn && ctx->rng_ptr == (const void *)dx && ctx->rng_n == n) {
         const double ms = ctx->rng_maxstep;
         P.use_anchors = ((ms * (1.0 - 0x1p-50)) - (eb_abs * (1.0 + 0x1p-50))) >= P.esc_thresh || !isfinite(ms);
     }
@@ -360,7 +387,7 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
         LC_CUDA_OK(cudaMemsetAsync(first_bad, 0xff, 8, st));
         if (P.use_anchors) {
             lc_anchor_tiles_kernel<<<(int)(P.ntiles < ga ? P.ntiles : ga), LC_TPB, 0, st>>>(P);
-            lc_anchor_scan_kernel<<<1, 1024, 0, st>>>(P.tile_last_esc, anc_in, P.ntiles, P.first_chunk * LC_L);
+            lc_anchor_scan_kernel<<<1, 1024, 0, st>>>(P.tile_last_esc, anc_in, P.ntiles, P.first_chunk * LC_L, dyn);
             ctx->launches += 2;
         }
         lc_quant_a_kernel<<<(int)(P.ntiles < ga ? P.ntiles : ga), LC_TPB, lc_quant_a_smem_bytes(), st>>>(P);
@@ -406,12 +433,13 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     E.ntiles = etiles;
     E.cb = cbo;
     E.sync = (unsigned long long *)ctx->sync.p;
+    E.dyn = dyn;
     const int egrid = (int)(etiles < (uint64_t)(4 * ctx->sm_count) ? etiles : 4 * ctx->sm_count);
     auto codebook_launch = [&]() -> int {
         LC_CUDA_OK(cudaEventRecord(ctx->pev[2], st));
         lc_codebook_kernel<<<1, 1024, lc_codebook_smem_bytes(), st>>>(
             P.hist, nbins, (uint8_t *)ctx->lengths.p, (unsigned long long *)ctx->cw.p,
-            (unsigned long long *)ctx->gkeys.p, (unsigned long long *)ctx->ifreq.p, (int *)ctx->parent.p, cbo);
+            (unsigned long long *)ctx->gkeys.p, (unsigned long long *)ctx->ifreq.p, (int *)ctx->parent.p, cbo, dyn);
         { int _rc = lc_debug_check(ctx, "lc_codebook_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
         LC_CUDA_OK(cudaEventRecord(ctx->pev[3], st));
         ctx->launches += 1;
@@ -433,6 +461,7 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     auto readback = [&]() -> int {                       // the one host round trip
         LC_CUDA_OK(cudaMemcpyAsync(hbad, first_bad, 8, cudaMemcpyDeviceToHost, st));
         LC_CUDA_OK(cudaMemcpyAsync(hcb, cbo, sizeof(LcCodebookOut), cudaMemcpyDeviceToHost, st));
+        if (dyn) LC_CUDA_OK(cudaMemcpyAsync(hdyn, dyn, sizeof(LcQuantDyn), cudaMemcpyDeviceToHost, st));
         LC_CUDA_OK(cudaStreamSynchronize(st));
         return 0;
     };
@@ -442,6 +471,7 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     { int _rc = codebook_launch(); if (_rc) return _rc; }
     { int _rc = encode_launch(); if (_rc) return _rc; }
     { int _rc = readback(); if (_rc) return _rc; }
+    if (dyn && hdyn->status) return hdyn->status;        // non-finite / constant / bad bound: no results
     if (*hbad != ~0ULL) {
         // a chunk prediction failed: relaunch from the first bad chunk (anchor =
         // the exact end of its predecessor) until every check passes
@@ -517,6 +547,56 @@ int lc_compress_f64(lc_ctx *ctx, const double *x, uint64_t n, int x_on_device, d
     if (rc) return rc;
     if (2ull * n_bins_half <= 65536ull) return lc_compress_t<uint16_t>(ctx, dx, n, eb_abs, n_bins_half, record_traces, res);
     return lc_compress_t<uint32_t>(ctx, dx, n, eb_abs, n_bins_half, record_traces, res);
+}
+
+int lc_compress_auto_f64(lc_ctx *ctx, const double *x, uint64_t n, int x_on_device, int eb_relative,
+                         double eb_param, uint32_t n_bins_half, int record_traces, lc_result *res, lc_bounds *bounds)
+{
+    if (!ctx || !res || !bounds || n < 2 || n_bins_half < 1 || !(eb_param > 0.0) || !isfinite(eb_param)) return 12;
+    if (n_bins_half > (1u << 30)) return 12;
+    LC_CUDA_OK(cudaSetDevice(ctx->device));
+    LC_CUDA_OK(cudaEventRecord(ctx->ev0, ctx->stream));
+    LC_CUDA_OK(cudaEventRecord(ctx->pev[0], ctx->stream));
+    int rc;
+    const double *dx = lc_device_input(ctx, x, n, x_on_device, &rc);
+    if (rc) return rc;
+    // range pass and device-side bounds: no host round trip before the quantizer
+    int nb = (int)((n + 255) / 256);
+    if (nb > 4 * ctx->sm_count) nb = 4 * ctx->sm_count;
+    LC_CUDA_OK(lc_reserve(ctx->range_parts, sizeof(LcRangePart) * (nb + 1) + 16 + sizeof(LcQuantDyn) + 64));
+    LcRangePart *parts = (LcRangePart *)ctx->range_parts.p;
+    unsigned *done = (unsigned *)(parts + nb + 1);
+    LcQuantDyn *dyn = (LcQuantDyn *)(((uintptr_t)(done + 4) + 63) & ~(uintptr_t)63);
+    LC_CUDA_OK(cudaMemsetAsync(done, 0, sizeof(unsigned), ctx->stream));
+    lc_range_kernel<<<nb, 256, 0, ctx->stream>>>(dx, n, parts, done);
+    lc_quant_setup_kernel<<<1, 32, 0, ctx->stream>>>(parts + nb, dx, n, eb_relative, eb_param, n_bins_half, dyn);
+    ctx->launches += 2;
+    { int _rc = lc_debug_check(ctx, "lc_quant_setup_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+    ctx->rng_ptr = nullptr;
+    LcQuantDyn *hdyn = (LcQuantDyn *)((char *)ctx->pinned + 512);
+    if (ctx->qslot < 0) {
+        // no __constant__ slot left (more than LC_QDYN_SLOTS live contexts): read the
+        // bounds back and take the host path
+        LC_CUDA_OK(cudaMemcpyAsync(hdyn, dyn, sizeof(LcQuantDyn), cudaMemcpyDeviceToHost, ctx->stream));
+        LC_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+        rc = hdyn->status;
+        if (!rc) {
+            if (2ull * n_bins_half <= 65536ull) rc = lc_compress_t<uint16_t>(ctx, dx, n, hdyn->eb_abs, n_bins_half, record_traces, res);
+            else rc = lc_compress_t<uint32_t>(ctx, dx, n, hdyn->eb_abs, n_bins_half, record_traces, res);
+        }
+    } else {
+        LC_CUDA_OK(lc_qdyn_to_slot(dyn, ctx->qslot, ctx->stream));
+        if (2ull * n_bins_half <= 65536ull) rc = lc_compress_t<uint16_t>(ctx, dx, n, 0.0, n_bins_half, record_traces, res, dyn, hdyn);
+        else rc = lc_compress_t<uint32_t>(ctx, dx, n, 0.0, n_bins_half, record_traces, res, dyn, hdyn);
+    }
+    bounds->vmin = hdyn->vmin;
+    bounds->vmax = hdyn->vmax;
+    bounds->value_range = hdyn->value_range;
+    bounds->eb_abs = hdyn->eb_abs;
+    bounds->first_value = hdyn->first_value;
+    bounds->nonfinite = hdyn->nonfinite;
+    bounds->status = hdyn->status;
+    return rc;
 }
 
 int lc_result_fetch(lc_ctx *ctx, uint8_t *code_lengths, uint8_t *payload, uint64_t *esc_idx, double *esc_val,

@@ -314,8 +314,12 @@ __device__ __forceinline__ void lc_codebook_body(const uint32_t *__restrict__ hi
 __global__ void __launch_bounds__(LC_CB_THREADS) lc_codebook_kernel(
     const uint32_t *__restrict__ hist, uint32_t nbins, uint8_t *__restrict__ lengths,
     unsigned long long *__restrict__ codes, unsigned long long *__restrict__ gkeys,
-    unsigned long long *__restrict__ ifreq_g, int *__restrict__ parent_g, LcCodebookOut *out)
+    unsigned long long *__restrict__ ifreq_g, int *__restrict__ parent_g, LcCodebookOut *out, const LcQuantDyn *dyn)
 {
+    if (dyn && dyn->skip) {                          // nothing was quantized (lc_compress_auto_f64)
+        if (threadIdx.x == 0) { out->total_bits = 0; out->n_esc = 0; out->max_len = 0; out->used = 0; out->status = 0; }
+        return;
+    }
     __shared__ int s_wcnt[LC_CB_THREADS / 32][65], s_len_count[66], s_len_start[66], s_wmax[32];
     __shared__ unsigned long long s_first[66], s_bits[32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -398,6 +402,7 @@ struct LcCodeRegs {
 template <typename CodeT>
 __global__ void __launch_bounds__(LC_TPB) lc_encode_kernel(LcEncParams P)
 {
+    if (P.dyn && P.dyn->skip) return;
     typedef cub::BlockScan<unsigned long long, LC_TPB> ScanU;
     extern __shared__ __align__(16) unsigned char lc_dyn_smem[];
     unsigned long long *tpk = reinterpret_cast<unsigned long long *>(lc_dyn_smem);   // (len << 32) | code

@@ -12,7 +12,25 @@ struct LcChunkPred {
     double *g0;              // guess of the chain value at the chunk start
 };
 
+// Bounds resolved on the device (lc_compress_auto_f64): the quantizer setup
+// derived from the range pass without a host round trip.  skip != 0: nothing
+// to quantize (status 10 non-finite, 11 2*eb overflow, 12 eb <= 0, 15 constant)
+// and every later kernel of the call returns at once.
+struct LcQuantDyn {
+    LcQuant Q;
+    double esc_thresh;
+    double eb_abs, value_range, vmin, vmax, first_value;
+    int use_anchors;
+    int skip;
+    int status;
+    int nonfinite;
+};
+
+#define LC_QDYN_SLOTS 32      // __constant__ copies of device-resolved bounds (one per context slot)
+
 struct LcQuantParams {
+    const LcQuantDyn *dyn;   // non-null: Q / esc_thresh / use_anchors come from the device ...
+    int dyn_slot;            // ... through the context's __constant__ slot c_qdyn[dyn_slot]
     const double *x;
     uint64_t n;              // elements; codes cover positions 1..n-1
     LcQuant Q;
@@ -83,6 +101,7 @@ struct LcEncParams {
     unsigned int *tile_counter;
     uint64_t ntiles;
     const LcCodebookOut *cb; // device codebook summary (max_len <= 32: table path)
+    const LcQuantDyn *dyn;   // device-resolved bounds (skip flag), may be null
     unsigned long long esc_cap;   // capacity of esc_idx / esc_val (host re-runs when short)
     unsigned long long *sync; // v2 sync table [ceil(m / LC_SYNC_K)] (bit offsets), may be null
 };
@@ -91,7 +110,12 @@ __global__ void lc_range_kernel(const double *__restrict__ x, uint64_t n, LcRang
                                 unsigned *__restrict__ done);
 __global__ void lc_anchor_tiles_kernel(LcQuantParams P);
 __global__ void lc_anchor_scan_kernel(const long long *__restrict__ last, long long *__restrict__ incoming,
-                                      long long ntiles, long long launch_pos);
+                                      long long ntiles, long long launch_pos, const LcQuantDyn *dyn);
+__global__ void lc_quant_setup_kernel(const LcRangePart *__restrict__ r, const double *__restrict__ x, uint64_t n,
+                                      int eb_relative, double eb_param, uint32_t nbh, LcQuantDyn *d);
+// copy a call's device-resolved bounds into the context's __constant__ slot
+// (in-stream device-to-device copy; lc_quant.cu)
+cudaError_t lc_qdyn_to_slot(const LcQuantDyn *dyn, int slot, cudaStream_t st);
 __global__ void lc_quant_a_kernel(LcQuantParams P);
 __global__ void lc_map_scan_kernel(const OffMap *__restrict__ agg, double *__restrict__ tileD, long long ntiles,
                                    long long per, OffMap *gagg, int *gflag);
@@ -109,7 +133,8 @@ template <typename CodeT>
 __global__ void lc_hist_kernel(const CodeT *__restrict__ codes, uint64_t m, uint32_t *__restrict__ hist, uint32_t nbins);
 __global__ void lc_codebook_kernel(const uint32_t *__restrict__ hist, uint32_t nbins, uint8_t *__restrict__ lengths,
                                    unsigned long long *__restrict__ codes, unsigned long long *__restrict__ gkeys,
-                                   unsigned long long *__restrict__ ifreq, int *__restrict__ parent, LcCodebookOut *out);
+                                   unsigned long long *__restrict__ ifreq, int *__restrict__ parent, LcCodebookOut *out,
+                                   const LcQuantDyn *dyn);
 __global__ void lc_zero_words_kernel(uint32_t *__restrict__ p, const LcCodebookOut *__restrict__ cb);
 template <typename CodeT> __global__ void lc_encode_kernel(LcEncParams P);
 size_t lc_codebook_smem_bytes();

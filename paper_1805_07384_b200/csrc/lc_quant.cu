@@ -14,6 +14,26 @@
 #include <cub/block/block_scan.cuh>
 #include "lc_kernels.cuh"
 
+__constant__ LcQuantDyn c_qdyn[LC_QDYN_SLOTS];
+
+// the slots live in lc_quant.cu (the quantizer kernels read them); the host
+// copies a call's LcQuantDyn into its context's slot with an in-stream
+// device-to-device cudaMemcpyToSymbolAsync, so the kernels see the bounds as
+// constant-bank operands like kernel parameters
+
+// kernel entry: take the device-resolved bounds; false = nothing to do
+__device__ __forceinline__ bool lc_quant_dyn(LcQuantParams &P)
+{
+    if (P.dyn_slot < 0) return true;
+    const LcQuantDyn &d = c_qdyn[P.dyn_slot];
+    if (d.skip) return false;
+    P.Q = d.Q;
+    P.esc_thresh = d.esc_thresh;
+    P.use_anchors = d.use_anchors;
+    return true;
+}
+
+
 // ---------------------------------------------------------------------------
 // range: min, max, non-finite flag
 
@@ -138,6 +158,49 @@ __global__ void __launch_bounds__(256) lc_range_kernel(const double *__restrict_
     }
 }
 
+cudaError_t lc_qdyn_to_slot(const LcQuantDyn *dyn, int slot, cudaStream_t st)
+{
+    return cudaMemcpyToSymbolAsync(c_qdyn, dyn, sizeof(LcQuantDyn), (size_t)slot * sizeof(LcQuantDyn),
+                                   cudaMemcpyDeviceToDevice, st);
+}
+
+// Quantizer setup on the device from the range pass (same IEEE operations as
+// the host path: compressor.py resolve_bounds eb_abs = eb_rel * vr, then the
+// lc_compress_f64 derivations), so relative-mode compression needs no host
+// round trip before the quantizer.
+__global__ void lc_quant_setup_kernel(const LcRangePart *__restrict__ r, const double *__restrict__ x, uint64_t n,
+                                      int eb_relative, double eb_param, uint32_t nbh, LcQuantDyn *d)
+{
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const double vmin = r->vmin, vmax = r->vmax;
+    double vr = __dsub_rn(vmax, vmin);
+    if (vr == 0.0) vr = 0.0;
+    const double eb = eb_relative ? __dmul_rn(eb_param, vr) : eb_param;
+    int st = 0;
+    if (r->nonfinite) st = 10;
+    else if (vr == 0.0 || n < 2) st = 15;
+    else if (!isfinite(__dmul_rn(2.0, eb))) st = 11;
+    else if (!(eb > 0.0)) st = 12;
+    LcQuantDyn o;
+    o.vmin = vmin; o.vmax = vmax; o.value_range = vr; o.eb_abs = eb; o.first_value = x[0];
+    o.nonfinite = r->nonfinite;
+    o.status = st;
+    o.skip = st != 0;
+    o.Q.delta = __dmul_rn(2.0, eb);
+    o.Q.eb = eb;
+    o.Q.max_m = (double)(nbh - 1);
+    o.Q.max_m1 = __dadd_rn(o.Q.max_m, 1.0);
+    o.Q.inv = __ddiv_rn(1.0, o.Q.delta);
+    int e2;
+    frexp(__dadd_rn(o.Q.max_m, 2.0), &e2);
+    o.Q.cert = __dsub_rn(0.5, ldexp(1.0, e2 - 50));
+    o.esc_thresh = __dmul_rn(__dmul_rn((double)nbh, o.Q.delta), 1.0 + 0x1p-40);
+    const double ms = r->maxstep;
+    o.use_anchors = (__dsub_rn(__dmul_rn(ms, 1.0 - 0x1p-50), __dmul_rn(eb, 1.0 + 0x1p-50)) >= o.esc_thresh) ||
+                    !isfinite(ms);
+    *d = o;
+}
+
 // ---------------------------------------------------------------------------
 // fused quantizer
 
@@ -203,6 +266,7 @@ __device__ __forceinline__ void lc_prefetch_x_tile(const LcQuantParams &P, long 
 
 __global__ void __launch_bounds__(LC_TPB) lc_anchor_tiles_kernel(LcQuantParams P)
 {
+    if (!lc_quant_dyn(P) || !P.use_anchors) return;
     // last definite escape position of every tile (escapes certain from the data)
     __shared__ long long wmax[LC_TPB / 32];
     const int tid = threadIdx.x;
@@ -227,8 +291,9 @@ __global__ void __launch_bounds__(LC_TPB) lc_anchor_tiles_kernel(LcQuantParams P
 
 __global__ void __launch_bounds__(1024) lc_anchor_scan_kernel(const long long *__restrict__ last,
                                                              long long *__restrict__ incoming, long long ntiles,
-                                                             long long launch_pos)
+                                                             long long launch_pos, const LcQuantDyn *dyn)
 {
+    if (dyn && (dyn->skip || !dyn->use_anchors)) return;
     typedef cub::BlockScan<long long, 1024> Scan;
     __shared__ typename Scan::TempStorage tmp;
     __shared__ long long carry;
@@ -250,6 +315,7 @@ __global__ void __launch_bounds__(1024) lc_anchor_scan_kernel(const long long *_
 
 __global__ void __launch_bounds__(LC_TPB, 3) lc_quant_a_kernel(LcQuantParams P)
 {
+    if (!lc_quant_dyn(P)) return;
     typedef cub::BlockScan<long long, LC_TPB> ScanLL;
     extern __shared__ __align__(16) unsigned char lc_dyn_smem[];
     double *xs = reinterpret_cast<double *>(lc_dyn_smem);
@@ -438,6 +504,7 @@ int lc_launch_map_scan(const OffMap *agg, double *tileD, long long ntiles, void 
 template <typename CodeT>
 __global__ void __launch_bounds__(LC_TPB, 3) lc_quant_b_kernel(LcQuantParams P, CodeT *__restrict__ codes)
 {
+    if (!lc_quant_dyn(P)) return;
     extern __shared__ __align__(16) unsigned char lc_dyn_smem[];
     double *xs = reinterpret_cast<double *>(lc_dyn_smem);
     uint32_t *hs = reinterpret_cast<uint32_t *>(xs + LC_TPB * LC_ROW);
@@ -591,6 +658,7 @@ template __global__ void lc_quant_b_kernel<uint32_t>(LcQuantParams, uint32_t *);
 template <typename CodeT>
 __global__ void lc_quant_serial_kernel(LcQuantParams P, CodeT *__restrict__ codes)
 {
+    if (!lc_quant_dyn(P)) return;
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     double r = P.anchor_val;
     for (uint64_t i = (uint64_t)P.first_chunk * LC_L + 1; i < P.n; ++i) {
