@@ -238,11 +238,17 @@ __device__ __forceinline__ void lc_load_x_tile(const LcQuantParams &P, long long
 {
     const int tid = threadIdx.x;
     const long long nel = (long long)P.n - 1;
+    // element off = k * LC_TPB + tid goes to row off / 32, column off % 32: both
+    // addresses advance by a constant per k (immediate offsets, no per-copy math)
+    double *dst = xs + (tid >> 5) * LC_ROW + (tid & 31);
+    const double *src = P.x + pbeg + 1 + tid;
+    if (pbeg + LC_TILE <= nel) {                         // full tile
 #pragma unroll
-    for (int k = 0; k < LC_L; ++k) {
-        const int off = k * LC_TPB + tid;
-        const long long pos = pbeg + 1 + off;
-        if (pos <= nel) lc_cp_async8(xs + (off >> 5) * LC_ROW + (off & 31), P.x + pos);
+        for (int k = 0; k < LC_L; ++k) lc_cp_async8(dst + k * (LC_TPB / 32) * LC_ROW, src + k * LC_TPB);
+    } else {
+#pragma unroll
+        for (int k = 0; k < LC_L; ++k)
+            if (pbeg + 1 + k * LC_TPB + tid <= nel) lc_cp_async8(dst + k * (LC_TPB / 32) * LC_ROW, src + k * LC_TPB);
     }
     lc_cp_async_commit();
     if (tid <= LC_L) {

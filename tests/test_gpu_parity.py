@@ -208,3 +208,20 @@ def test_integrity_errors(lc):
         lc.decompress(moved)
     with pytest.raises(lc.IntegrityError):
         lc.decompress(dataclasses.replace(blk, payload=blk.payload[: len(blk.payload) // 2]))
+
+
+def test_device_resolved_bounds_all_modes(lc):
+    """lc_compress_auto_f64 derives eb_abs on the device (compressor.py:138-148): every mode,
+    including a constant vector, gives the oracle's block byte for byte."""
+    x = _sine(20_000)
+    for mode, param, cfg in (("absolute", 1e-3, lc.CompressorConfig.absolute(1e-3)),
+                             ("value_range_relative", 1e-5, lc.CompressorConfig.value_range_relative(1e-5)),
+                             ("fixed_psnr", 80.0, lc.CompressorConfig.fixed_psnr(80.0))):
+        blk = lc.compress(x, cfg)
+        ref = orc.compress(x, mode, param)
+        assert blk.eb_abs == ref["eb_abs"] and blk.value_range == ref["value_range"], mode
+        assert blk.to_bytes() == orc.to_bytes(ref), mode
+        c = np.full(777, -2.5)
+        blk = lc.compress(c, cfg)
+        ref = orc.compress(c, mode, param)
+        assert blk.to_bytes() == orc.to_bytes(ref), mode
