@@ -334,3 +334,33 @@ __device__ __forceinline__ void lc_prefetch_bytes(const void *p, size_t bytes)
     const char *e = reinterpret_cast<const char *>(p) + bytes;
     for (const char *q = c + 128 * threadIdx.x; q < e; q += 128 * blockDim.x) lc_prefetch_l2(q);
 }
+
+// Inclusive warp scan of chunk maps (lane 0 earliest), in place.  When every
+// lane holds a translation with a non-zero grid (the common case: chunks
+// without events), compose(H2, H1) = H1 with y = H1.y + H2.y, so the scan is a
+// prefix sum of y in the same tree order (same roundings) and every lane ends
+// with lane 0's grid fields; otherwise the general composition.
+__device__ __forceinline__ void lc_warp_scan_maps(OffMap &inc)
+{
+    const int lane = threadIdx.x & 31;
+    if (__all_sync(0xffffffffu, inc.kind == LC_MAP_TRANS && inc.v != 0.0)) {
+        double y = inc.y;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double up = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= o) y = up + y;
+        }
+        inc.y = y;
+        inc.v = __shfl_sync(0xffffffffu, inc.v, 0);
+        inc.B = __shfl_sync(0xffffffffu, inc.B, 0);
+        inc.t0 = __shfl_sync(0xffffffffu, inc.t0, 0);
+        inc.t1 = __shfl_sync(0xffffffffu, inc.t1, 0);
+        inc.og = __shfl_sync(0xffffffffu, inc.og, 0);
+        return;
+    }
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const OffMap up = lc_shfl_up_map(inc, o);
+        if (lane >= o) inc = lc_map_compose(inc, up);
+    }
+}

@@ -1240,11 +1240,7 @@ __global__ void __launch_bounds__(LC_TPB, 4) lc_rec_a_kernel(LcRecParams P, LcRe
         if (need) H = lc_map_from_words(crow);
         if (len > 0 && c + 1 < P.nchunks) lc_map_shift_out(H, LC_SUB(r, g1));
         OffMap inc_map = H;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const OffMap up = lc_shfl_up_map(inc_map, o);
-            if (lane >= o) inc_map = lc_map_compose(inc_map, up);
-        }
+        lc_warp_scan_maps(inc_map);
         if (lane == 31) warp_agg[wid] = inc_map;
         __syncthreads();
         lc_scan_warp_maps(warp_agg, LC_TPB / 32);

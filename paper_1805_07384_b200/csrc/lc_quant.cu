@@ -419,11 +419,7 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_quant_a_kernel(LcQuantParams P)
 
         // in-tile inclusive scan of maps
         OffMap inc_map = H;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const OffMap up = lc_shfl_up_map(inc_map, o);
-            if (lane >= o) inc_map = lc_map_compose(inc_map, up);
-        }
+        lc_warp_scan_maps(inc_map);
         if (lane == 31) warp_agg[wid] = inc_map;
         __syncthreads();
         lc_scan_warp_maps(warp_agg, LC_TPB / 32);
