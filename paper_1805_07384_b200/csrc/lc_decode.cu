@@ -48,6 +48,19 @@ struct LcDecTables {
     unsigned char len16[LC_L16];     // length (13..16) of the code under 16-bit prefix s16 + i; 0: longer / none
 };
 
+// The part of LcDecTables the segment sync walk reads (multi-codeword LUT and
+// long-code lengths): ~21 KB of shared memory instead of ~39 KB, so more sync
+// CTAs fit per SM.  Rare slow paths read the full table from global memory.
+struct LcDecSyncTables {
+    int max_len;
+    int canon;
+    unsigned s16;
+    int pad;
+    unsigned long long lim[34];
+    unsigned int lut2[1 << LC_LUT_BITS];
+    unsigned char len16[LC_L16];
+};
+
 // lengths[nl] -> tables + sorted symbols (canonical order).  SM: the lengths
 // are first staged in shared memory with 16-byte loads (nl <= LC_DEC_LEN_SMEM).
 #define LC_DEC_LEN_SMEM 98304
@@ -338,7 +351,8 @@ __device__ __forceinline__ int lc_next_symbol(const LcDecTables &T, const uint32
 // Length of a codeword longer than LC_LUT_BITS for canonical codes (T.canon):
 // the first length whose left-justified limit exceeds the window.  Returns 0
 // when the window is past every code (the exact path then decides).
-__device__ __forceinline__ int lc_long_len(const LcDecTables &T, unsigned long long buf)
+template <class TT>
+__device__ __forceinline__ int lc_long_len(const TT &T, unsigned long long buf)
 {
     const unsigned long long w = buf >> 32;
     if (!T.canon || w >= T.lim[T.max_len]) return 0;
@@ -350,7 +364,8 @@ __device__ __forceinline__ int lc_long_len(const LcDecTables &T, unsigned long l
 
 // lc_long_len through the 16-bit second-level table (codes of 13..16 bits),
 // the limit walk for longer ones
-__device__ __forceinline__ int lc_long_len_fast(const LcDecTables &T, unsigned long long buf)
+template <class TT>
+__device__ __forceinline__ int lc_long_len_fast(const TT &T, unsigned long long buf)
 {
     const unsigned i = (unsigned)(buf >> 48) - T.s16;
     const int l = i < (unsigned)LC_L16 ? (int)T.len16[i] : 0;
@@ -372,7 +387,8 @@ __device__ __forceinline__ void lc_seg_dead(LcSeg &S)
 // walk stops at the first start both walks share: from there on they
 // coincide (count, exit and status carry over).
 template <int NS>
-__device__ void lc_seg_walk(const LcDecTables &T, const uint32_t *__restrict__ sorted, const LcSmemSrc &src,
+__device__ void lc_seg_walk(const LcDecSyncTables &T, const LcDecTables &Tg, const uint32_t *__restrict__ sorted,
+                            const LcSmemSrc &src,
                             unsigned bits_rel, unsigned seg_rel, unsigned start, bool resync, LcSeg &S,
                             unsigned long long *Ms)
 {
@@ -395,7 +411,7 @@ __device__ void lc_seg_walk(const LcDecTables &T, const uint32_t *__restrict__ s
                 adv = e2 ? 0 : lc_long_len_fast(T, br.buf);
                 if (!adv || br.pos + (unsigned)adv > bits_rel) {
                     uint32_t sym;
-                    adv = lc_next_symbol(T, sorted, br, bits_rel, &sym, &term);
+                    adv = lc_next_symbol(Tg, sorted, br, bits_rel, &sym, &term);
                     if (!adv) { stopped = true; break; }
                 }
                 sm = 1u;
@@ -432,6 +448,17 @@ __device__ void lc_seg_walk(const LcDecTables &T, const uint32_t *__restrict__ s
     }
 }
 
+__device__ __forceinline__ void lc_load_sync_tables(LcDecSyncTables &Ts, const LcDecTables *T)
+{
+    if (threadIdx.x == 0) { Ts.max_len = T->max_len; Ts.canon = T->canon; Ts.s16 = T->s16; }
+    for (int i = threadIdx.x; i < 34; i += blockDim.x) Ts.lim[i] = T->lim[i];
+    for (int i = threadIdx.x; i < (1 << LC_LUT_BITS) / 4; i += blockDim.x)
+        reinterpret_cast<uint4 *>(Ts.lut2)[i] = __ldg(reinterpret_cast<const uint4 *>(T->lut2) + i);
+    for (int i = threadIdx.x; i < LC_L16 / 16; i += blockDim.x)
+        reinterpret_cast<uint4 *>(Ts.len16)[i] = __ldg(reinterpret_cast<const uint4 *>(T->len16) + i);
+    __syncthreads();
+}
+
 __device__ __forceinline__ void lc_load_tables(LcDecTables &Ts, const LcDecTables *T)
 {
     for (int i = threadIdx.x; i < (int)(sizeof(LcDecTables) / 16); i += blockDim.x)
@@ -454,7 +481,7 @@ __global__ void __launch_bounds__(LC_DEC_TPB) lc_dec_sync_kernel(LcDecParams P, 
                                                                 int *__restrict__ changed, const int *need)
 {
     if (need && *(volatile const int *)need == 0) return;   // speculative general pass not needed
-    __shared__ LcDecTables Ts;
+    __shared__ LcDecSyncTables Ts;
     __shared__ unsigned s_exit[LC_DEC_TPB];
     __shared__ int s_skip;
     __shared__ unsigned long long s_bar;
@@ -463,7 +490,7 @@ __global__ void __launch_bounds__(LC_DEC_TPB) lc_dec_sync_kernel(LcDecParams P, 
     constexpr unsigned SEGB = 64u * NS;
     if (threadIdx.x == 0) lc_mbar_init(&s_bar, 1);
     unsigned phase = 0;
-    lc_load_tables(Ts, P.T);
+    lc_load_sync_tables(Ts, P.T);
     const int tid = threadIdx.x;
     unsigned long long *M = reinterpret_cast<unsigned long long *>(s_words + NW) + tid;
     LcSmemSrc src;
@@ -501,7 +528,7 @@ __global__ void __launch_bounds__(LC_DEC_TPB) lc_dec_sync_kernel(LcDecParams P, 
         lc_mbar_wait(&s_bar, phase);
         phase ^= 1u;
         if (first_pass && live) {
-            lc_seg_walk<NS>(Ts, P.sorted, src, bits_rel, seg_rel, seg_rel, false, S, M);
+            lc_seg_walk<NS>(Ts, *P.T, P.sorted, src, bits_rel, seg_rel, seg_rel, false, S, M);
             have_mask = true;
         }
         for (;;) {
@@ -511,7 +538,7 @@ __global__ void __launch_bounds__(LC_DEC_TPB) lc_dec_sync_kernel(LcDecParams P, 
             bool ch = false;
             if (live && want != my_start) {
                 if (want == LC_DEAD32) { lc_seg_dead(S); have_mask = false; }
-                else { lc_seg_walk<NS>(Ts, P.sorted, src, bits_rel, seg_rel, want, have_mask, S, M); have_mask = true; }
+                else { lc_seg_walk<NS>(Ts, *P.T, P.sorted, src, bits_rel, seg_rel, want, have_mask, S, M); have_mask = true; }
                 my_start = want;
                 ch = true;
             }
