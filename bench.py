@@ -9,7 +9,11 @@ decompressed at value-range-relative bounds 1e-3, 1e-4 and 1e-6.
 
 One step = for each bound: compress (value range + exact-chain quantizer +
 on-device Huffman codebook + encoder) then decompress (Huffman decode +
-exact-chain reconstruction), i.e. 3 round trips of the 512 MB vector.
+exact-chain reconstruction), i.e. 3 round trips of the 512 MB vector.  The
+three round trips are independent and run concurrently, each on its own codec
+context and CUDA stream (--streams 3, the default; a checkpoint of several state
+vectors uses the GPU the same way); the JSON line also reports the same step
+with the round trips one after the other ("sequential").
 metric value = raw fp64 bytes round-tripped per second over all GPUs
 (3 * 8n * N / step time).  Inputs (512 MB) exceed the 126 MB L2, so no L2
 flush is needed between steps.
@@ -49,7 +53,8 @@ sys.path.insert(0, ROOT)
 BOUNDS = (1e-3, 1e-4, 1e-6)
 METRIC = "checkpoint compress+decompress round-trip GB/s (raw fp64, all GPUs)"
 WORKLOAD = ("config2: fp64 n=2^26 per GPU, sum of 8 seeded sinusoids + N(0,1e-3), "
-            "eb_rel in {1e-3,1e-4,1e-6}; step = compress+decompress at each bound")
+            "eb_rel in {1e-3,1e-4,1e-6}; step = compress+decompress at each bound "
+            "(the three round trips on three streams)")
 
 
 def make_vector(n, seed=0):
@@ -247,8 +252,14 @@ def run_b200(args, rank, world, local_rank):
     L = ctx.lib
     out = torch.empty(n, dtype=torch.float64, device="cuda")
     vp = ctypes.c_void_p
+    # the timed step runs the three bounds' round trips concurrently, each on its own
+    # codec context bound to its own CUDA stream (--streams 1: one after the other)
+    nstr = max(1, min(args.streams, len(BOUNDS)))
+    wstreams = [torch.cuda.Stream() for _ in range(nstr)]
+    wctx = [_native.Context(local_rank, ctypes.c_void_p(st.cuda_stream)) for st in wstreams]
+    wout = [torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(nstr)]
 
-    def rt(eb_rel, stats=None):
+    def rt(eb_rel, stats=None, ctx=ctx, out=out):
         # value range + device-resolved bounds + quantizer + codebook + encoder (one host
         # round trip, the path paper_1805_07384_b200.compress takes), then the decoder
         res, bnd = _native.LcResult(), _native.LcBounds()
@@ -278,13 +289,24 @@ def run_b200(args, rank, world, local_rank):
     meta = torch.zeros(4 * len(BOUNDS), dtype=torch.float64, device="cuda")
     gathered = torch.zeros(world * meta.numel(), dtype=torch.float64, device="cuda") if world > 1 else None
 
+    from concurrent.futures import ThreadPoolExecutor
+    pool = ThreadPoolExecutor(nstr)                  # ctypes calls release the GIL
+    hmeta = np.zeros(4 * len(BOUNDS))
+
+    def lane(k):                                     # bounds k, k + nstr, ... on stream k
+        for i in range(k, len(BOUNDS), nstr):
+            res = rt(BOUNDS[i], ctx=wctx[k], out=wout[k])
+            hmeta[4 * i:4 * i + 4] = (n, res.payload_bits, res.n_esc, res.relaunches)
+
     def step():
-        for i, eb in enumerate(BOUNDS):
-            res = rt(eb)
-            meta[4 * i:4 * i + 4] = torch.tensor([n, res.payload_bits, res.n_esc, res.relaunches],
-                                                 dtype=torch.float64)
+        list(pool.map(lane, range(nstr)))
         if dist is not None:                     # per-rank block metadata -> file offsets
+            meta.copy_(torch.from_numpy(hmeta))
             dist.all_gather_into_tensor(gathered, meta)
+
+    def step_sequential():
+        for eb in BOUNDS:
+            rt(eb)
 
     def barrier():
         if dist is not None:
@@ -297,18 +319,30 @@ def run_b200(args, rank, world, local_rank):
     clocks = Clocks(local_rank)
     barrier()
     clocks.start()
-    launches0 = L.lc_launch_count(ctx.h)
+    launches0 = sum(L.lc_launch_count(c.h) for c in wctx)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record()
+    ev0.record()                                     # device idle: marks the start
     for _ in range(args.steps):
-        step()
+        step()                                       # every call ends with its stream synchronised
     ev1.record()
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
-    launches = int(L.lc_launch_count(ctx.h) - launches0)
+    launches = int(sum(L.lc_launch_count(c.h) for c in wctx) - launches0)
     ms = ev0.elapsed_time(ev1) / args.steps
+    # the same step with the bounds one after the other on one context (reported beside)
+    for _ in range(2):
+        step_sequential()
+    barrier()
+    ev2 = torch.cuda.Event(enable_timing=True)
+    ev3 = torch.cuda.Event(enable_timing=True)
+    ev2.record()
+    for _ in range(args.steps):
+        step_sequential()
+    ev3.record()
+    torch.cuda.synchronize()
+    ms_seq = ev2.elapsed_time(ev3) / args.steps
     if dist is not None:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -425,7 +459,9 @@ def run_b200(args, rank, world, local_rank):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOAD, "n": n, "eb_rel": list(BOUNDS), "parallelism": f"shard{world}",
-                       "l2": "inputs (512 MB/GPU) exceed L2; no flush"},
+                       "streams": nstr, "l2": "inputs (512 MB/GPU) exceed L2; no flush"},
+            "sequential": {"value": 8 * n * len(BOUNDS) * world / (ms_seq / 1e3) / 1e9, "ms_per_step": ms_seq,
+                           "note": "same step, the three round trips one after the other on one stream"},
             "clocks": clk, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "per_bound": per,
             "config1_solver_harness": solver,
@@ -474,6 +510,8 @@ def main():
     ap.add_argument("--ref-log2", type=int, default=24)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-solver", action="store_true")
+    ap.add_argument("--streams", type=int, default=3,
+                    help="concurrent round trips per step (each bound on its own stream and context)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
