@@ -225,3 +225,61 @@ def test_device_resolved_bounds_all_modes(lc):
         blk = lc.compress(c, cfg)
         ref = orc.compress(c, mode, param)
         assert blk.to_bytes() == orc.to_bytes(ref), mode
+
+
+def test_concurrent_streams_match_oracle(lc):
+    """Independent round trips on three host threads, each with its own CUDA stream and
+    bound codec context (the bench's concurrent step): every block and reconstruction is
+    the oracle's.  Exercises the per-context __constant__ bounds slots under overlap."""
+    import threading
+    import torch
+    from paper_1805_07384_b200 import _native
+    xs = [_sine(300_000, seed=s) for s in range(3)]
+    cfgs = [lc.CompressorConfig.value_range_relative(eb) for eb in (1e-3, 1e-5, 1e-7)]
+    out = [None] * 3
+
+    def work(k):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            _native.bind_stream(0, s.cuda_stream)
+            for _ in range(3):
+                blk = lc.compress(torch.from_numpy(xs[k]).cuda(), cfgs[k])
+                rec = lc.decompress(blk, device="cuda").cpu().numpy()
+            out[k] = (blk.to_bytes(), rec)
+
+    ts = [threading.Thread(target=work, args=(k,)) for k in range(3)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for k, eb in enumerate((1e-3, 1e-5, 1e-7)):
+        ref = orc.compress(xs[k], "value_range_relative", eb)
+        assert out[k][0] == orc.to_bytes(ref), k
+        assert np.array_equal(out[k][1].view(np.int64), ref["recon"].view(np.int64)), k
+
+
+def test_bounds_slot_exhaustion_falls_back(lc):
+    """More live contexts than __constant__ bounds slots: the extra context takes the host
+    path (range readback) and still writes the oracle's bytes."""
+    import ctypes
+    import torch
+    from paper_1805_07384_b200 import _native
+    x = _sine(100_000, seed=11)
+    xd = torch.from_numpy(x).cuda()
+    extra = [_native.Context(0) for _ in range(40)]          # > LC_QDYN_SLOTS live contexts
+    try:
+        ctx = extra[-1]
+        res, bnd = _native.LcResult(), _native.LcBounds()
+        rc = ctx.lib.lc_compress_auto_f64(ctx.h, xd.data_ptr(), x.size, 1, 1, 1e-4, 32768, 0,
+                                          ctypes.byref(res), ctypes.byref(bnd))
+        assert rc == 0, ctx.error()
+        ref = orc.compress(x, "value_range_relative", 1e-4)
+        assert bnd.eb_abs == ref["eb_abs"]
+        lengths = np.zeros(res.n_symbols, np.uint8)
+        payload = np.zeros(max(res.payload_bytes, 1), np.uint8)
+        ctx.lib.lc_result_fetch(ctx.h, lengths.ctypes.data, payload.ctypes.data, None, None, None, None)
+        assert np.array_equal(lengths, ref["code_lengths"])
+        assert payload[:res.payload_bytes].tobytes() == ref["payload"]
+    finally:
+        for c in extra:
+            c.close()
