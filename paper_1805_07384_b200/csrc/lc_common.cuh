@@ -256,17 +256,27 @@ __device__ __forceinline__ void lc_scan_warp_maps(OffMap *agg, int nw)
 // ---- compacted replay of flagged chunks -------------------------------------
 // Chunks whose hot loop flagged possible map events are queued in shared memory
 // and replayed by consecutive threads (full warps) instead of by their owners
-// (one divergent lane per warp).  Entry = chunk index in the tile, its flag
-// mask and its guess start.  replay(q) computes the chunk's map and stores it
-// where the owner reads it after this call.  Call from all threads.
+// (one divergent lane per warp).  replay(q) computes the chunk's map and stores
+// it where the owner reads it after this call.  Call from all threads.
+// Entry = chunk index in the tile with the binade of its guess start (the
+// identity map's grid), its flag mask and the chain value before its first
+// flagged step (the replay starts there: earlier steps are not events).
 struct LcReplayItem {
-    int ch;
+    int chg;            // chunk | g0 biased exponent << 8 | (g0 == 0) << 19
     unsigned mask;
-    double g0;
+    double rs;
 };
+__device__ __forceinline__ int lc_replay_ch(const LcReplayItem &it) { return it.chg & 0xff; }
+// ulp(g0) from the packed binade (lc_ulp only reads the exponent and zero-ness)
+__device__ __forceinline__ double lc_replay_ulp(const LcReplayItem &it)
+{
+    const int be = (it.chg >> 8) & 0x7ff;
+    if (it.chg >> 19) return 0.0;
+    return lc_ulp(be ? lc_from_bits((int64_t)be << 52) : lc_from_bits(1));
+}
 
 template <typename Replay>
-__device__ __forceinline__ void lc_tile_replay(bool need, unsigned mask, double g0, LcReplayItem *q,
+__device__ __forceinline__ void lc_tile_replay(bool need, unsigned mask, double g0, double rs, LcReplayItem *q,
                                                int *s_cnt, Replay replay)
 {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -282,7 +292,8 @@ __device__ __forceinline__ void lc_tile_replay(bool need, unsigned mask, double 
     }
     if (need) {
         LcReplayItem it;
-        it.ch = tid; it.mask = mask; it.g0 = g0;
+        it.chg = tid | (int)(((lc_bits(g0) >> 52) & 0x7ff) << 8) | ((g0 == 0.0) << 19);
+        it.mask = mask; it.rs = rs;
         q[base + __popc(b & ((1u << lane) - 1u))] = it;
     }
     __syncthreads();

@@ -1223,7 +1223,7 @@ __global__ void __launch_bounds__(LC_TPB, 4) lc_rec_a_kernel(LcRecParams P, LcRe
         OffMap H;
         bool need = false;
         unsigned mask = 0u;
-        double r = g0;
+        double r = g0, rs = g0;                      // rs: chain value before the first flagged step
         if (len > 0) {
             P.chunk_esc[c] = before.cnt;
             long long e = before.cnt;
@@ -1236,7 +1236,9 @@ __global__ void __launch_bounds__(LC_TPB, 4) lc_rec_a_kernel(LcRecParams P, LcRe
                 const double inc_ = LC_MUL((double)m, P.delta);
                 double rn = m != 0 ? LC_ADD(r, inc_) : r;
                 if (code == 0) { rn = e < (long long)P.n_esc ? P.esc_val[e] : 0.0; ++e; anyesc = 1; }
-                lc_flags_step(F, j, r, inc_, rn);
+                const bool f = lc_flag_test(F, r, inc_, rn);
+                rs = (f && F.mask == 0u) ? r : rs;
+                F.mask |= (unsigned)f << (j & 31);
                 r = rn;
             }
             if (anyesc) H = lc_map_const(0.0);
@@ -1248,12 +1250,12 @@ __global__ void __launch_bounds__(LC_TPB, 4) lc_rec_a_kernel(LcRecParams P, LcRe
         } else {
             H = lc_map_neutral();
         }
-        lc_tile_replay(need, mask, g0, s_rq, s_rcnt, [&](const LcReplayItem &it) {
-            uint32_t *rw = cs + it.ch * LC_ROW;
-            const int j1 = 31 - __clz(it.mask);
-            OffMap Hr = lc_map_identity(lc_ulp(it.g0));
-            double r2 = it.g0;
-            for (int j = 0; j <= j1; ++j) {
+        lc_tile_replay(need, mask, g0, rs, s_rq, s_rcnt, [&](const LcReplayItem &it) {
+            uint32_t *rw = cs + lc_replay_ch(it) * LC_ROW;
+            const int j0 = __ffs(it.mask) - 1, j1 = 31 - __clz(it.mask);
+            OffMap Hr = lc_map_identity(lc_replay_ulp(it));
+            double r2 = it.rs;
+            for (int j = j0; j <= j1; ++j) {
                 const int m = lc_code_m(rw[j]);              // no escapes in replayed chunks
                 if (m != 0) {
                     const double inc_ = LC_MUL((double)m, P.delta);

@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_quant_a_kernel(LcQuantParams P)
         OffMap H;
         bool need = false;
         unsigned mask = 0u;
-        double r = g0;
+        double r = g0, rs = g0;                      // rs: chain value before the first flagged step
         if (len > 0) {
             LcFlags F;
             lc_flags_init(F, g0);
@@ -389,7 +389,9 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_quant_a_kernel(LcQuantParams P)
                 int esc; double inc;
                 const double rn = lc_step_guess(P.Q, row[j], r, &esc, &inc);
                 anyesc |= esc;
-                lc_flags_step(F, j, r, inc, rn);
+                const bool f = lc_flag_test(F, r, inc, rn);
+                rs = (f && F.mask == 0u) ? r : rs;
+                F.mask |= (unsigned)f << (j & 31);
                 r = rn;
             }
             if (anyesc) H = lc_map_const(0.0);
@@ -401,12 +403,12 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_quant_a_kernel(LcQuantParams P)
         } else {
             H = lc_map_neutral();
         }
-        lc_tile_replay(need, mask, g0, s_rq, s_rcnt, [&](const LcReplayItem &it) {
-            double *rw = xs + it.ch * LC_ROW;
-            const int j1 = 31 - __clz(it.mask);
-            OffMap Hr = lc_map_identity(lc_ulp(it.g0));
-            double r2 = it.g0;
-            for (int j = 0; j <= j1; ++j) {
+        lc_tile_replay(need, mask, g0, rs, s_rq, s_rcnt, [&](const LcReplayItem &it) {
+            double *rw = xs + lc_replay_ch(it) * LC_ROW;
+            const int j0 = __ffs(it.mask) - 1, j1 = 31 - __clz(it.mask);
+            OffMap Hr = lc_map_identity(lc_replay_ulp(it));
+            double r2 = it.rs;
+            for (int j = j0; j <= j1; ++j) {
                 int esc; double inc;
                 const double rn = lc_step_guess(P.Q, rw[j], r2, &esc, &inc);
                 if (((it.mask >> j) & 1u) && inc != 0.0) lc_map_step(Hr, r2, inc, rn);

@@ -39,13 +39,16 @@ int64_t sim_predict(const double *x, int64_t n, double eb, int64_t nbh, int L,
         LcFlags F; lc_flags_init(F, r);
         int anyesc = 0;
         const double g0 = r;
+        double rs = r;                               // chain value before the first flagged step
         int jj = 0;
         for (int64_t i = s + 1; i <= e; ++i) {
             uint32_t code; double inc; int esc; double pe;
             const double rn = lc_step(Q, x[i], r, &code, &esc, &inc, &pe);
             if (esc) { H = lc_map_const(0.0); anyesc = 1; }
             else {
-                lc_flags_step(F, jj, r, inc, rn);           // every step, as the kernels do
+                const bool f = lc_flag_test(F, r, inc, rn);  // every step, as the kernels do
+                rs = (f && F.mask == 0u) ? r : rs;
+                F.mask |= (unsigned)f << (jj & 31);
                 if (inc != 0.0) {
                     const int kb = H.kind;
                     const double Bb = H.B;
@@ -58,10 +61,10 @@ int64_t sim_predict(const double *x, int64_t n, double eb, int64_t nbh, int L,
         }
         {   // the flag tracker + replay must reproduce the step-by-step map exactly
             OffMap H2 = anyesc ? lc_map_const(0.0) : lc_map_identity(lc_ulp(g0));
-            if (!anyesc && F.mask) {                 // replay up to the last flagged step
-                const int j1 = 31 - __builtin_clz(F.mask);
-                double r2 = g0;
-                for (int j2 = 0; j2 <= j1; ++j2) {
+            if (!anyesc && F.mask) {                 // replay the first to the last flagged step
+                const int j0 = __builtin_ctz(F.mask), j1 = 31 - __builtin_clz(F.mask);
+                double r2 = rs;
+                for (int j2 = j0; j2 <= j1; ++j2) {
                     uint32_t code; double inc; int esc; double pe;
                     const double rn = lc_step(Q, x[s + 1 + j2], r2, &code, &esc, &inc, &pe);
                     if (((F.mask >> j2) & 1u) && inc != 0.0) lc_map_step(H2, r2, inc, rn);
