@@ -468,6 +468,9 @@ def run_b200(args, rank, world, local_rank):
     e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
     for k in range(nstr):
         jobs[k].put(None)
+    for w in workers:
+        w.join()
+    pool.shutdown(wait=True)
     h2d = sum(b[0] for b in lane_bytes)
     d2h = sum(b[1] for b in lane_bytes)
     if dist is not None:
@@ -504,6 +507,9 @@ def run_b200(args, rank, world, local_rank):
             "config1_solver_harness": solver,
         }
         print(json.dumps(line), flush=True)
+    torch.cuda.synchronize()
+    for c in wctx:                                   # release the lane contexts before interpreter exit
+        c.close()
 
 
 def config1_harness(lc):
