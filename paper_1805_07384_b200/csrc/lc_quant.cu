@@ -610,14 +610,16 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_quant_b_kernel(LcQuantParams P, 
             }
 #pragma unroll
             for (int k = 0; k < 8; ++k) w[k] = __reduce_add_sync(0xffffffffu, w[k]);   // halves <= 1024
-            if ((tid & 31) == 0) {
+            // lane L < 16 adds the warp's count of code L + 1 (one atomic per lane, in parallel)
+            const int lane = tid & 31;
+            uint32_t mine = 0;
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const uint32_t lo = w[k] & 0xffffu, hi = w[k] >> 16;
-                    const uint32_t c0 = 2u * k + 1u, c1 = 2u * k + 2u;
-                    if (lo) { if (c0 < hb) atomicAdd(&hs[c0], lo); else atomicAdd(&P.hist[c0], lo); }
-                    if (hi) { if (c1 < hb) atomicAdd(&hs[c1], hi); else atomicAdd(&P.hist[c1], hi); }
-                }
+            for (int k = 0; k < 8; ++k)
+                if ((lane >> 1) == k) mine = (lane & 1) ? (w[k] >> 16) : (w[k] & 0xffffu);
+            if (lane < 16 && mine) {
+                const uint32_t code = (uint32_t)lane + 1u;
+                if (code < hb) atomicAdd(&hs[code], mine);
+                else atomicAdd(&P.hist[code], mine);
             }
         }
         __syncthreads();
