@@ -410,8 +410,6 @@ __global__ void __launch_bounds__(LC_TPB) lc_encode_kernel(LcEncParams P)
     __shared__ typename ScanU::TempStorage scan_tmp;
     __shared__ long long sh_tile;
     __shared__ unsigned long long sh_in_bits, sh_in_esc;
-    __shared__ ulonglong2 lb_u2[LC_TPB / 32], lb_u2_res;
-    __shared__ int sh_j;
     const int tid = threadIdx.x;
     const CodeT *codes = reinterpret_cast<const CodeT *>(P.codes);
     const bool fast = P.cb->max_len <= 32;
@@ -479,61 +477,45 @@ __global__ void __launch_bounds__(LC_TPB) lc_encode_kernel(LcEncParams P)
         unsigned long long ex, agg;
         ScanU(scan_tmp).ExclusiveSum(bits | (nesc << 32), ex, agg);
         const unsigned long long abits = agg & 0xffffffffull, aesc = agg >> 32;
-        {
-            LcEncDesc *d = P.desc + t;
+        const unsigned nwt0 = (unsigned)((abits + 31) >> 5);       // tile words at bit alignment 0
+        const bool fast_tile = fast && nwt0 + 1 <= LC_ENC_WBUF;
+        LcEncDesc *d = P.desc + t;
+        if (tid == 0 && t > 0) {                                     // publish the aggregate first
+            __stcg(&d->agg_bits, abits);
+            __stcg(&d->agg_esc, aesc);
+            st_release(&d->st, 1);
+        }
+        // Tile offsets by a decoupled look-back run by warp 0 while the other warps
+        // pack the tile's bits at alignment 0 (the shift by B0 % 32 happens on the
+        // way out), so the look-back latency overlaps the packing.
+        auto lookback = [&]() {
             ulonglong2 in = make_ulonglong2(0, 0);
-            if (t > 0) {
-                if (tid == 0) {
-                    __stcg(&d->agg_bits, abits);
-                    __stcg(&d->agg_esc, aesc);
-                    st_release(&d->st, 1);
-                }
-                in = lc_lookback_block<ulonglong2>(
+            if (t > 0)
+                in = lc_lookback_warp<ulonglong2>(
                     t, make_ulonglong2(0, 0),
                     [](const ulonglong2 &a, const ulonglong2 &b) { return make_ulonglong2(a.x + b.x, a.y + b.y); },
                     [](const ulonglong2 &v, int o) {
                         return make_ulonglong2(__shfl_down_sync(0xffffffffu, v.x, o),
                                                __shfl_down_sync(0xffffffffu, v.y, o));
                     },
-                    [&](long long k) { return &P.desc[k].st; },
+                    [&](long long k) { return ld_acquire(&P.desc[k].st); },
                     [&](long long k, int st) {
                         return st == 2 ? make_ulonglong2(__ldcg(&P.desc[k].incl_bits), __ldcg(&P.desc[k].incl_esc))
                                        : make_ulonglong2(__ldcg(&P.desc[k].agg_bits), __ldcg(&P.desc[k].agg_esc));
-                    },
-                    lb_u2, &sh_j, &lb_u2_res);
-            }
+                    });
             if (tid == 0) {
                 __stcg(&d->incl_bits, in.x + abits);
                 __stcg(&d->incl_esc, in.y + aesc);
                 st_release(&d->st, 2);
                 sh_in_bits = in.x; sh_in_esc = in.y;
             }
-        }
-        __syncthreads();
-        const unsigned long long B0 = sh_in_bits;
-        // v2 sync table: bit offset of every LC_SYNC_K-th symbol
-        if (P.sync && len > 0 && (p0 & (LC_SYNC_K - 1)) == 0)
-            P.sync[p0 / LC_SYNC_K] = B0 + (ex & 0xffffffffull);
-        // escapes (compressor.py:409-410): code index i-1 <-> element i
-        if (nesc) {
-            unsigned long long e = sh_in_esc + (ex >> 32);
-#pragma unroll
-            for (int j = 0; j < LC_L; ++j)
-                if (j < len && C.get(j) == 0) {
-                    const unsigned long long el = (unsigned long long)(p0 + j + 1);
-                    if (e < P.esc_cap) {
-                        P.esc_idx[e] = el;
-                        P.esc_val[e] = P.x ? P.x[el] : 0.0;
-                    }
-                    ++e;
-                }
-        }
-        const unsigned lb = (unsigned)(B0 & 31) + (unsigned)(ex & 0xffffffffull);   // bit in the tile buffer
-        const unsigned nwt = (unsigned)(((B0 & 31) + abits + 31) >> 5);
-        if (fast && nwt <= LC_ENC_WBUF) {
-            for (unsigned i = tid; i < nwt; i += LC_TPB) wbuf[i] = 0;
+        };
+        if (fast_tile) {
+            for (unsigned i = tid; i <= nwt0; i += LC_TPB) wbuf[i] = 0;
             __syncthreads();
+            if (tid < 32) lookback();
             if (bits) {
+                const unsigned lb = (unsigned)(ex & 0xffffffffull);            // bit in the tile buffer
                 const unsigned wfirst = lb >> 5, wlast = (unsigned)((lb + bits - 1) >> 5);
                 unsigned w = wfirst;
                 unsigned long long acc = 0;
@@ -561,10 +543,39 @@ __global__ void __launch_bounds__(LC_TPB) lc_encode_kernel(LcEncParams P)
                 if (nb > 0) atomicOr(wbuf + w, (uint32_t)(acc << (32 - nb)));
             }
             __syncthreads();
+        } else {
+            if (tid < 32) lookback();
+            __syncthreads();
+        }
+        const unsigned long long B0 = sh_in_bits;
+        // v2 sync table: bit offset of every LC_SYNC_K-th symbol
+        if (P.sync && len > 0 && (p0 & (LC_SYNC_K - 1)) == 0)
+            P.sync[p0 / LC_SYNC_K] = B0 + (ex & 0xffffffffull);
+        // escapes (compressor.py:409-410): code index i-1 <-> element i
+        if (nesc) {
+            unsigned long long e = sh_in_esc + (ex >> 32);
+#pragma unroll
+            for (int j = 0; j < LC_L; ++j)
+                if (j < len && C.get(j) == 0) {
+                    const unsigned long long el = (unsigned long long)(p0 + j + 1);
+                    if (e < P.esc_cap) {
+                        P.esc_idx[e] = el;
+                        P.esc_val[e] = P.x ? P.x[el] : 0.0;
+                    }
+                    ++e;
+                }
+        }
+        if (fast_tile) {
+            // out word i of the tile = the alignment-0 stream shifted right by s = B0 % 32
+            const unsigned sft = (unsigned)(B0 & 31);
+            const unsigned nout = (unsigned)((sft + abits + 31) >> 5);
             const unsigned long long gw0 = B0 >> 5;
-            for (unsigned i = tid; i < nwt; i += LC_TPB) {
-                const uint32_t v = __byte_perm(wbuf[i], 0, 0x0123);       // MSB-first bytes
-                if (i == 0 || i + 1 == nwt) atomicOr(P.payload + gw0 + i, v);
+            for (unsigned i = tid; i < nout; i += LC_TPB) {
+                const uint32_t cur = i < nwt0 ? wbuf[i] : 0u;
+                const uint32_t prev = (i > 0 && sft) ? wbuf[i - 1] : 0u;
+                const uint32_t word = sft ? ((cur >> sft) | (prev << (32 - sft))) : cur;
+                const uint32_t v = __byte_perm(word, 0, 0x0123);       // MSB-first bytes
+                if (i == 0 || i + 1 == nout) atomicOr(P.payload + gw0 + i, v);
                 else P.payload[gw0 + i] = v;
             }
         } else if (bits) {
