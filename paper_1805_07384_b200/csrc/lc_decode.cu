@@ -1453,7 +1453,8 @@ int lc_decompress_impl2(lc_ctx *ctx, uint64_t n, double eb_abs, double first_val
     // padded to whole sync-CTA ranges (bulk copies of up to 256 * 32 + 8 words)
     const uint64_t words_alloc = words + LC_DEC_TPB * 32 + LC_DEC_STAGE_PAD + 64;
     LC_CUDA_OK(lc_reserve(bpay, words_alloc * 4));
-    LC_CUDA_OK(cudaMemsetAsync(bpay.p, 0, words_alloc * 4, st));
+    // zero only the padding behind the payload (the copy writes the rest)
+    LC_CUDA_OK(cudaMemsetAsync((char *)bpay.p + payload_bytes, 0, words_alloc * 4 - payload_bytes, st));
     LC_CUDA_OK(cudaMemcpyAsync(bpay.p, payload, payload_bytes,
                                inputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
     LC_CUDA_OK(lc_reserve(blen, n_lengths));

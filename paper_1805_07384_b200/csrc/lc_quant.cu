@@ -218,7 +218,10 @@ __device__ __forceinline__ double lc_guess(const LcQuantParams &P, double xpos, 
                                            long long apos, double aval)
 {
     if (apos == pos) return aval;
-    const double k = floor(LC_ADD(LC_DIV(LC_SUB(xpos, aval), P.Q.delta), 0.5));
+    // a guess only has to be near the chain (the offset maps carry the rest), and chunk
+    // c's end guess and chunk c+1's start guess come from identical inputs: RN(1/delta)
+    // instead of a division
+    const double k = floor(LC_ADD(LC_MUL(LC_SUB(xpos, aval), P.Q.inv), 0.5));
     if (k == 0.0) return aval;
     const double g = LC_ADD(aval, LC_MUL(k, P.Q.delta));
     return isfinite(g) ? g : xpos;
