@@ -336,7 +336,7 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     P.tile_counter = tile_counter;
     P.hist = (uint32_t *)ctx->hist.p;
     P.nbins = nbins;
-    P.count_hist = 1;
+    P.count_hist = sizeof(CodeT) == 2 ? 0 : 1;           // u16 codes: lc_hist16_kernel after pass B
     P.first_bad = first_bad;
     P.bad_end = (double *)ctx->bad_end.p;
     P.pe = record ? (double *)ctx->pe.p : nullptr;
@@ -396,6 +396,11 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
         lc_quant_b_kernel<CodeT><<<(int)(P.ntiles < gb ? P.ntiles : gb), LC_TPB, lc_quant_b_smem_bytes(), st>>>(P, codes);
         { int _rc = lc_debug_check(ctx, "lc_quant_b_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
         ctx->launches += 3;
+        if (sizeof(CodeT) == 2 && P.first_chunk == 0) {
+            lc_hist16_kernel<<<4 * ctx->sm_count, 256, 0, st>>>((const uint16_t *)codes, m, P.hist, nbins, dyn);
+            { int _rc = lc_debug_check(ctx, "lc_hist16_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+            ctx->launches += 1;
+        }
         return 0;
     };
 

@@ -131,6 +131,8 @@ size_t lc_quant_b_smem_bytes();
 template <typename CodeT> __global__ void lc_quant_serial_kernel(LcQuantParams P, CodeT *__restrict__ codes);
 template <typename CodeT>
 __global__ void lc_hist_kernel(const CodeT *__restrict__ codes, uint64_t m, uint32_t *__restrict__ hist, uint32_t nbins);
+__global__ void lc_hist16_kernel(const uint16_t *__restrict__ codes, uint64_t m, uint32_t *__restrict__ hist,
+                                 uint32_t nbins, const LcQuantDyn *dyn);
 __global__ void lc_codebook_kernel(const uint32_t *__restrict__ hist, uint32_t nbins, uint8_t *__restrict__ lengths,
                                    unsigned long long *__restrict__ codes, unsigned long long *__restrict__ gkeys,
                                    unsigned long long *__restrict__ ifreq, int *__restrict__ parent, LcCodebookOut *out,

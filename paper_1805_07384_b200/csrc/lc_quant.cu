@@ -699,6 +699,80 @@ __global__ void __launch_bounds__(256) lc_hist_kernel(const CodeT *__restrict__ 
         if (hs[i]) atomicAdd(&hist[i], hs[i]);
 }
 
+// Histogram of u16 codes (np.bincount, compressor.py:411) as its own streaming
+// pass: 16-byte loads, codes 1..16 (the small |m| of smooth data) in packed
+// per-thread byte counters flushed every 128 codes into 16 register totals,
+// every other code by shared/global atomics; warp sums by redux.sync, one
+// atomic per lane and code.  m codes, hist pre-zeroed.
+__global__ void __launch_bounds__(256) lc_hist16_kernel(const uint16_t *__restrict__ codes, uint64_t m,
+                                                      uint32_t *__restrict__ hist, uint32_t nbins,
+                                                      const LcQuantDyn *dyn)
+{
+    if (dyn && dyn->skip) return;
+    __shared__ uint32_t hs[LC_HBINS];
+    for (int i = threadIdx.x; i < LC_HBINS; i += blockDim.x) hs[i] = 0;
+    __syncthreads();
+    const uint32_t hb = nbins < LC_HBINS ? nbins : LC_HBINS;
+    uint32_t tot[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) tot[k] = 0;
+    auto count = [&](uint32_t code, unsigned long long &A, unsigned long long &B) {
+        const uint32_t idx = code - 1u;
+        const unsigned long long one = 1ull << ((idx & 7u) * 8u);
+        A += idx < 8u ? one : 0ull;
+        B += idx - 8u < 8u ? one : 0ull;
+        if (idx >= 16u) {
+            if (code < hb) atomicAdd(&hs[code], 1u);
+            else atomicAdd(&hist[code], 1u);
+        }
+    };
+    auto flush = [&](unsigned long long A, unsigned long long B) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            tot[k] += (uint32_t)((A >> (8 * k)) & 0xffull);
+            tot[8 + k] += (uint32_t)((B >> (8 * k)) & 0xffull);
+        }
+    };
+    const uint64_t nv = m / 8;                                    // whole 16-byte vectors
+    const uint4 *v4 = reinterpret_cast<const uint4 *>(codes);    // codes buffer is 16-byte aligned
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    while (i < nv) {
+        unsigned long long A = 0ull, B = 0ull;
+        for (int r = 0; r < 16 && i < nv; ++r, i += stride) {     // <= 128 codes per byte counter
+            const uint4 q = __ldcs(v4 + i);
+            const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                count(w[h] & 0xffffu, A, B);
+                count(w[h] >> 16, A, B);
+            }
+        }
+        flush(A, B);
+    }
+    if (blockIdx.x == 0 && threadIdx.x < (unsigned)(m - nv * 8)) {   // tail codes
+        unsigned long long A = 0ull, B = 0ull;
+        count(codes[nv * 8 + threadIdx.x], A, B);
+        flush(A, B);
+    }
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) tot[k] = __reduce_add_sync(0xffffffffu, tot[k]);
+    uint32_t mine = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+        if (lane == k) mine = tot[k];
+    __syncthreads();
+    if (lane < 16 && mine) {
+        const uint32_t code = (uint32_t)lane + 1u;
+        if (code < hb) atomicAdd(&hs[code], mine);
+        else atomicAdd(&hist[code], mine);
+    }
+    __syncthreads();
+    for (uint32_t k = threadIdx.x; k < hb; k += blockDim.x)
+        if (hs[k]) atomicAdd(&hist[k], hs[k]);
+}
+
 template __global__ void lc_quant_serial_kernel<uint16_t>(LcQuantParams, uint16_t *);
 template __global__ void lc_quant_serial_kernel<uint32_t>(LcQuantParams, uint32_t *);
 template __global__ void lc_hist_kernel<uint16_t>(const uint16_t *, uint64_t, uint32_t *, uint32_t);
