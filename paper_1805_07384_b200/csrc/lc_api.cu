@@ -164,9 +164,13 @@ int lc_ctx_create(lc_ctx **out, int device, void *stream)
     LC_CUDA_OK(cudaMallocHost(&ctx->pinned, 4096));
     LC_CUDA_OK(cudaFuncSetAttribute(lc_quant_a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)lc_quant_a_smem_bytes()));
-    LC_CUDA_OK(cudaFuncSetAttribute(lc_quant_b_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    LC_CUDA_OK(cudaFuncSetAttribute(lc_quant_b_kernel<uint16_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)lc_quant_b_smem_bytes()));
-    LC_CUDA_OK(cudaFuncSetAttribute(lc_quant_b_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    LC_CUDA_OK(cudaFuncSetAttribute(lc_quant_b_kernel<uint32_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)lc_quant_b_smem_bytes()));
+    LC_CUDA_OK(cudaFuncSetAttribute(lc_quant_b_kernel<uint16_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)lc_quant_b_smem_bytes()));
+    LC_CUDA_OK(cudaFuncSetAttribute(lc_quant_b_kernel<uint32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)lc_quant_b_smem_bytes()));
     LC_CUDA_OK(cudaFuncSetAttribute(lc_codebook_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)lc_codebook_smem_bytes()));
@@ -393,7 +397,8 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
         lc_quant_a_kernel<<<(int)(P.ntiles < ga ? P.ntiles : ga), LC_TPB, lc_quant_a_smem_bytes(), st>>>(P);
         { int _rc = lc_debug_check(ctx, "lc_quant_a_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
         LC_CUDA_OK((cudaError_t)lc_launch_map_scan(P.tile_agg, P.tile_D, P.ntiles, mapscan_scratch, ctx->sm_count, st));
-        lc_quant_b_kernel<CodeT><<<(int)(P.ntiles < gb ? P.ntiles : gb), LC_TPB, lc_quant_b_smem_bytes(), st>>>(P, codes);
+        if (P.pe) lc_quant_b_kernel<CodeT, true><<<(int)(P.ntiles < gb ? P.ntiles : gb), LC_TPB, lc_quant_b_smem_bytes(), st>>>(P, codes);
+        else lc_quant_b_kernel<CodeT, false><<<(int)(P.ntiles < gb ? P.ntiles : gb), LC_TPB, lc_quant_b_smem_bytes(), st>>>(P, codes);
         { int _rc = lc_debug_check(ctx, "lc_quant_b_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
         ctx->launches += 3;
         if (sizeof(CodeT) == 2 && P.first_chunk == 0) {

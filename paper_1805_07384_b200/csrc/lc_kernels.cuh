@@ -125,7 +125,7 @@ __global__ void lc_map_scan_kernel(const OffMap *__restrict__ agg, double *__res
 #define LC_MAPSCAN_SCRATCH (LC_MAPSCAN_MAXG * (sizeof(OffMap) + sizeof(int)))
 int lc_launch_map_scan(const OffMap *agg, double *tileD, long long ntiles, void *scratch, int sm_count,
                        cudaStream_t st);
-template <typename CodeT> __global__ void lc_quant_b_kernel(LcQuantParams P, CodeT *__restrict__ codes);
+template <typename CodeT, bool REC> __global__ void lc_quant_b_kernel(LcQuantParams P, CodeT *__restrict__ codes);
 size_t lc_quant_a_smem_bytes();
 size_t lc_quant_b_smem_bytes();
 template <typename CodeT> __global__ void lc_quant_serial_kernel(LcQuantParams P, CodeT *__restrict__ codes);

@@ -508,7 +508,7 @@ int lc_launch_map_scan(const OffMap *agg, double *tileD, long long ntiles, void 
     return (int)cudaGetLastError();
 }
 
-template <typename CodeT>
+template <typename CodeT, bool REC>
 __global__ void __launch_bounds__(LC_TPB, 3) lc_quant_b_kernel(LcQuantParams P, CodeT *__restrict__ codes)
 {
     if (!lc_quant_dyn(P)) return;
@@ -564,7 +564,7 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_quant_b_kernel(LcQuantParams P, 
                 uint32_t code; int esc; double inc, pe;
                 const double rn = lc_step_nb(P.Q, row[j], r, &code, &inc, &esc, &pe, ok);
                 crow[j] = code;
-                if (P.pe) {
+                if (REC) {
                     P.pe[p0 + j] = pe;
                     P.pe_rec[p0 + j] = LC_SUB(rn, r);
                 }
@@ -576,7 +576,7 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_quant_b_kernel(LcQuantParams P, 
                     uint32_t code; int esc; double inc, pe;
                     const double rn = lc_step(P.Q, P.x[p0 + 1 + j], r, &code, &esc, &inc, &pe);
                     crow[j] = code;
-                    if (P.pe) {
+                    if (REC) {
                         P.pe[p0 + j] = pe;
                         P.pe_rec[p0 + j] = LC_SUB(rn, r);
                     }
@@ -659,8 +659,10 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_quant_b_kernel(LcQuantParams P, 
 size_t lc_quant_a_smem_bytes() { return sizeof(double) * LC_TPB * LC_ROW; }
 size_t lc_quant_b_smem_bytes() { return sizeof(double) * LC_TPB * LC_ROW + sizeof(uint32_t) * LC_HBINS_B; }
 
-template __global__ void lc_quant_b_kernel<uint16_t>(LcQuantParams, uint16_t *);
-template __global__ void lc_quant_b_kernel<uint32_t>(LcQuantParams, uint32_t *);
+template __global__ void lc_quant_b_kernel<uint16_t, false>(LcQuantParams, uint16_t *);
+template __global__ void lc_quant_b_kernel<uint32_t, false>(LcQuantParams, uint32_t *);
+template __global__ void lc_quant_b_kernel<uint16_t, true>(LcQuantParams, uint16_t *);
+template __global__ void lc_quant_b_kernel<uint32_t, true>(LcQuantParams, uint32_t *);
 
 // Sequential exact chain from chunk `first_chunk` (fallback for inputs whose
 // chunk predictions keep failing).  One thread; correct for every input.
