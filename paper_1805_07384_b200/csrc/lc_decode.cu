@@ -1363,8 +1363,7 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_rec_b_kernel(LcRecParams P, LcRe
         double *yrow = ys + tid * LC_ROW;
         if (len > 0) {
             double r = start;
-#pragma unroll
-            for (int j = 0; j < LC_L; ++j) {
+            auto step = [&](int j) {
                 const uint32_t code = v[j];
                 const int mm = lc_code_m(code);
                 double rn = mm != 0 ? LC_ADD(r, LC_MUL((double)mm, P.delta)) : r;   // compressor.py:371-374
@@ -1379,7 +1378,16 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_rec_b_kernel(LcRecParams P, LcRe
                 }
                 yrow[j] = rn;
                 r = rn;
-                if (j + 1 == len) break;
+            };
+            if (len == LC_L) {                               // full chunk: no per-step length test
+#pragma unroll
+                for (int j = 0; j < LC_L; ++j) step(j);
+            } else {
+#pragma unroll
+                for (int j = 0; j < LC_L; ++j) {
+                    step(j);
+                    if (j + 1 == len) break;
+                }
             }
             if (c + 1 < P.nchunks && lc_bits(r) != lc_bits(starts[tid + 1])) {
                 P.bad_end[c] = r;
