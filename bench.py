@@ -386,8 +386,8 @@ def run_b200(args, rank, world, local_rank):
     # encoder / read by the decoder); codes are an internal intermediate.
     peak, peak_src = measured_peak()
     groups = {
-        "quantizer[lc_quant_a+lc_map_scan+lc_quant_b]": lambda d: d["compress_phase_ms"]["quantize"],
-        "reconstruction[lc_rec0+lc_rec0_scan+lc_rec_a+lc_map_scan+lc_rec_b]":
+        "quantizer[lc_quant_a+lc_map_scan+lc_quant_b+lc_hist16]": lambda d: d["compress_phase_ms"]["quantize"],
+        "reconstruction[lc_rec_a+lc_map_scan+lc_rec_b]":
             lambda d: d["decompress_phase_ms"]["reconstruct"],
         "huffman_decode[lc_dec_tables+lc_dec_sync+lc_dec_scan+lc_dec_write]":
             lambda d: d["decompress_phase_ms"]["huffman_sync"] + d["decompress_phase_ms"]["huffman_scan"]

@@ -34,7 +34,7 @@ for d in launch.values():
         cur.append(d)
 timed = its[3:6]
 groups = {'quantizer': ['lc_anchor_tiles_kernel', 'lc_anchor_scan_kernel', 'lc_quant_a_kernel', 'lc_map_scan_kernel',
-                        'lc_quant_b_kernel'],
+                        'lc_quant_b_kernel', 'lc_hist16_kernel'],
           'encoder': ['lc_codebook_kernel', 'lc_zero_words_kernel', 'lc_encode_kernel'],
           'huffman_decode': ['lc_dec_tables_kernel', 'lc_dec_sync_kernel', 'lc_dec_fix_kernel', 'lc_dec_scan_kernel',
                              'lc_dec_write_kernel', 'lc_dec_status_kernel'],
@@ -50,6 +50,8 @@ for g, ks in groups.items():
             sel = [d for d in it[lo:] if d['kernel'] in ks]
         elif g == 'quantizer':
             hi = names.index('lc_quant_b_kernel') + 1
+            if hi < len(names) and names[hi] == 'lc_hist16_kernel':
+                hi += 1
             sel = [d for d in it[:hi] if d['kernel'] in ks]
         else:
             sel = [d for d in it if d['kernel'] in ks]
