@@ -381,11 +381,12 @@ __device__ __forceinline__ void lc_put_word(uint32_t *payload, uint64_t w, uint3
 
 // Encoder.  A tile of LC_TILE symbols per CTA iteration, 32 consecutive
 // symbols per thread held in registers.  Tile bit offsets come from a
-// decoupled look-back over (bits, escapes); the tile's bit string is
-// assembled in a shared-memory word buffer (thread-boundary words merged with
-// shared atomics) and written out with coalesced word stores, merging only
-// the tile's first and last words with the neighbouring tiles (the payload
-// is zeroed first).  huffman.encode (huffman.py:52-72) packs MSB-first.
+// decoupled look-back over (bits, escapes) run by warp 0 while the other warps
+// assemble the tile's bit string at bit alignment 0 in a shared-memory word
+// buffer (thread-boundary words merged with shared atomics); the string is
+// written out shifted by (tile offset % 32) with coalesced word stores, merging
+// only the tile's first and last words with the neighbouring tiles (the
+// payload is zeroed first).  huffman.encode (huffman.py:52-72) packs MSB-first.
 #define LC_ENC_WBUF 4096                 // tile buffer words (16 bits per symbol on average)
 
 template <typename CodeT>
