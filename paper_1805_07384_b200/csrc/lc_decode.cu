@@ -1009,6 +1009,12 @@ __device__ __forceinline__ bool lc_rec_aborted(const LcRecParams &P)
 }
 
 __device__ __forceinline__ int lc_code_m(uint32_t code) { return lc_unzigzag(code); }
+// the same for a non-escape code (code 0 gives garbage; callers replace that step's value)
+__device__ __forceinline__ int lc_code_m_nz(uint32_t code)
+{
+    const uint32_t zz = code - 1u;
+    return (int)(zz >> 1) ^ -(int)(zz & 1u);
+}
 
 // ---------------------------------------------------------------------------
 // Split reconstruction: RA (segmented m-prefix by block scan + look-back, guess
@@ -1232,7 +1238,7 @@ __global__ void __launch_bounds__(LC_TPB, 4) lc_rec_a_kernel(LcRecParams P, LcRe
             int anyesc = 0;
             for (int j = 0; j < len; ++j) {
                 const uint32_t code = crow[j];
-                const int m = lc_code_m(code);
+                const int m = lc_code_m_nz(code);            // escapes (code 0) are replaced below
                 const double inc_ = LC_MUL((double)m, P.delta);
                 double rn = m != 0 ? LC_ADD(r, inc_) : r;
                 if (code == 0) { rn = e < (long long)P.n_esc ? P.esc_val[e] : 0.0; ++e; anyesc = 1; }
@@ -1365,7 +1371,7 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_rec_b_kernel(LcRecParams P, LcRe
             double r = start;
             auto step = [&](int j) {
                 const uint32_t code = v[j];
-                const int mm = lc_code_m(code);
+                const int mm = lc_code_m_nz(code);                                   // code 0: replaced below
                 double rn = mm != 0 ? LC_ADD(r, LC_MUL((double)mm, P.delta)) : r;   // compressor.py:371-374
                 if (code == 0) {                                                     // :365-369
                     if (e < (long long)P.n_esc) {
