@@ -431,7 +431,9 @@ def run_b200(args, rank, world, local_rank):
                 for i in range(k, len(BOUNDS), nstr):
                     blk = lc.compress(xh, cfgs[i])             # H2D x, D2H block
                     rec = lc.decompress(blk, device="cuda")   # H2D block
-                    ohs[k].copy_(rec)                          # D2H reconstruction
+                    for off in range(0, n, 4 << 20):           # D2H reconstruction, 32 MB copies
+                        ohs[k][off:off + (4 << 20)].copy_(rec[off:off + (4 << 20)], non_blocking=True)
+                    torch.cuda.current_stream().synchronize()
                     meta_b = len(blk.payload) + blk.code_lengths.size + 16 * len(blk.escape_indices)
                     lane_bytes[k][0] += 8 * n + meta_b
                     lane_bytes[k][1] += meta_b + 8 * n

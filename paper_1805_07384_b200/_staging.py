@@ -85,6 +85,21 @@ def to_device(host_u8, device):
     return out
 
 
+def pinned_to_device(t, chunk=CHUNK):
+    """Host tensor -> new CUDA tensor on the current stream.  Large pinned sources move
+    in `chunk`-byte copies so transfers of other streams (a concurrent checkpoint's
+    small payload copies) are not queued behind one long DMA."""
+    import torch
+    if not t.is_pinned() or t.numel() * t.element_size() <= 2 * chunk:
+        return t.to("cuda", non_blocking=False)
+    out = torch.empty(t.shape, dtype=t.dtype, device="cuda")
+    step = max(1, chunk // t.element_size())
+    for off in range(0, t.numel(), step):
+        out[off:off + step].copy_(t[off:off + step], non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return out
+
+
 def to_host_into(dev_u8, host_u8):
     """Device uint8 tensor -> existing writable host uint8 tensor (chunked, pinned)."""
     n = dev_u8.numel()
