@@ -1560,7 +1560,6 @@ int lc_decompress_impl2(lc_ctx *ctx, uint64_t n, double eb_abs, double first_val
     DP.sorted = sorted;
     DP.nseg = nseg;
     DP.nblk = nblk;
-    const int pgrid_ = (int)(nblk < (long long)(6 * lc_sm_count(ctx)) ? nblk : 6 * lc_sm_count(ctx));
     DP.seg_bits = seg_bits;
     DP.nwords = words;
     const size_t ssm = lc_dec_stage_bytes(sub);
@@ -1570,6 +1569,21 @@ int lc_decompress_impl2(lc_ctx *ctx, uint64_t n, double eb_abs, double first_val
     case 8: LC_CUDA_OK(cudaFuncSetAttribute(lc_dec_sync_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm)); break;
     default: LC_CUDA_OK(cudaFuncSetAttribute(lc_dec_sync_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm)); break;
     }
+    // one resident wave: the CTAs stride over the payload ranges, so a grid
+    // larger than what fits leaves its late CTAs running at partial occupancy
+    static int s_occ[17] = {0};
+    if (!s_occ[sub]) {
+        int occ = 0;
+        switch (sub) {
+        case 2: LC_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lc_dec_sync_kernel<2>, LC_DEC_TPB, ssm)); break;
+        case 4: LC_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lc_dec_sync_kernel<4>, LC_DEC_TPB, ssm)); break;
+        case 8: LC_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lc_dec_sync_kernel<8>, LC_DEC_TPB, ssm)); break;
+        default: LC_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lc_dec_sync_kernel<16>, LC_DEC_TPB, ssm)); break;
+        }
+        s_occ[sub] = occ > 0 ? occ : 1;
+    }
+    const long long pmax = (long long)s_occ[sub] * lc_sm_count(ctx);
+    const int pgrid_ = (int)(nblk < pmax ? nblk : pmax);
     auto sync_launch = [&](LcBlkOut *bp, LcBlkOut *bc, int first, int *chg, const int *need) {
         switch (sub) {
         case 2: lc_dec_sync_kernel<2><<<pgrid_, LC_DEC_TPB, ssm, st>>>(DP, segs, bp, bc, first, chg, need); break;
