@@ -142,6 +142,29 @@ int lc_phase_ms(lc_ctx *ctx, double *ms, int cap);
 /* Kernels this context has launched since creation (diagnostic count).   */
 uint64_t lc_launch_count(lc_ctx *ctx);
 
+/* Context options (tests and diagnostics; no reference counterpart):
+ *   0 LC_OPT_MAX_QUANT     quantizer relaunches before the sequential exact
+ *                          chain finishes the vector (default 64)
+ *   1 LC_OPT_MAX_REC       the same for the decoder's reconstruction (64)
+ *   2 LC_OPT_INJECT_QUANT  perturb the predicted start of this chunk on the
+ *                          first launch (forces a relaunch; -1 off)
+ *   3 LC_OPT_INJECT_REC    the same in the decoder (-1 off)
+ *   4 LC_OPT_VERIFY        1: the quantizer re-runs every chunk with the exact
+ *                          reference step and checks every chunk end (no
+ *                          certified skip); 0 default
+ * lc_ctx_get_stat: 0 quantizer relaunches and 1 sequential-fallback flag of the
+ * last compress, 2 / 3 the same for the last decompress, 4 chunks the last
+ * compress re-ran exactly (uncertified).  Returns -1 for unknown keys.     */
+int lc_ctx_set_option(lc_ctx *ctx, int key, long long value);
+/* Test hook: run the device codebook build (the replacement of
+ * huffman.code_lengths + canonical_codes, huffman.py:21-72) on a host
+ * histogram of nbins u32 counts; lengths_out[nbins] / codes_out[nbins]
+ * (host, optional) receive the code lengths and canonical codewords, and
+ * *max_len_out the longest length.  Returns 0, or 13 for lengths > 64.    */
+int lc_debug_codebook(lc_ctx *ctx, const uint32_t *hist, uint32_t nbins, uint8_t *lengths_out,
+                      uint64_t *codes_out, int *max_len_out);
+long long lc_ctx_get_stat(lc_ctx *ctx, int key);
+
 /* Launch timeline (diagnostics; contexts created with LC_TRACE=1 in the
  * environment): lc_trace_mark_api adds a named mark, every launch adds one
  * with the kernel name; lc_trace_read syncs the stream, writes one line

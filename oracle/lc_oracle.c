@@ -247,3 +247,35 @@ int lco_decode_kernel(const uint8_t *payload, uint64_t bit_length, const uint8_t
     free(sorted);
     return bitpos != bit_length ? 3 : 0;             /* :130-132 */
 }
+
+/* Test-input generator (not a reference routine): the adversarial bin-edge
+ * corpus of SURVEY.md 8.P.  Advances the reference chain (compressor.py:
+ * 329-351, same operations as lco_compress_kernel) and places every x_i at
+ * prev + (m_i - 0.5) * delta moved by k_i ulps (|k_i| <= 3), i.e. within a few
+ * ulps of a bin edge of the reference's own prediction.  m and k are drawn by
+ * numpy (tests/stress_inputs.py) so the corpus is reproducible everywhere.  */
+void lco_edge_corpus(const int64_t *m, const int64_t *k, int64_t n, double x0, double eb,
+                     int64_t n_bins_half, double *out)
+{
+    const double delta = 2.0 * eb;
+    const double max_m = (double)(n_bins_half - 1);
+    double prev = x0;
+    out[0] = x0;
+    for (int64_t i = 1; i < n; ++i) {
+        const double edge = prev + ((double)m[i - 1] - 0.5) * delta;
+        double v = edge;
+        const int64_t kk = k[i - 1];
+        for (int64_t j = 0; j < (kk < 0 ? -kk : kk); ++j) v = nextafter(v, kk > 0 ? INFINITY : -INFINITY);
+        out[i] = v;
+        const double pe = v - prev;
+        const double q = pe / delta + 0.5;
+        int esc = 1;
+        double cand = prev;
+        if (q >= -max_m && q < max_m + 1.0) {
+            const double mm = floor(q);
+            cand = mm == 0.0 ? prev : prev + mm * delta;
+            if (fabs(v - cand) <= eb) esc = 0;
+        }
+        prev = esc ? v : cand;
+    }
+}

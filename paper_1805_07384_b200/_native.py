@@ -112,6 +112,12 @@ def library():
         L.lc_axpy_f64.argtypes = [_vp, _d, _vp, _d, _vp, _vp, ctypes.c_uint64]
         for f in (L.lc_stencil_apply_f64, L.lc_residual_f64, L.lc_jacobi_step_f64, L.lc_dot_f64, L.lc_axpy_f64):
             f.restype = ctypes.c_int
+        L.lc_ctx_set_option.argtypes = [_vp, ctypes.c_int, ctypes.c_longlong]
+        L.lc_ctx_set_option.restype = ctypes.c_int
+        L.lc_ctx_get_stat.argtypes = [_vp, ctypes.c_int]
+        L.lc_ctx_get_stat.restype = ctypes.c_longlong
+        L.lc_debug_codebook.argtypes = [_vp, _vp, ctypes.c_uint32, _vp, _vp, ctypes.POINTER(ctypes.c_int)]
+        L.lc_debug_codebook.restype = ctypes.c_int
         L.lc_result_sync.argtypes = [_vp, _vp, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
         L.lc_result_sync.restype = ctypes.c_int
         L.lc_decompress_v2_f64.argtypes = [_vp, ctypes.c_uint64, ctypes.c_double, ctypes.c_double, _vp,
@@ -127,7 +133,8 @@ EXPORTED = ["lc_ctx_create", "lc_ctx_destroy", "lc_last_error", "lc_range_f64", 
             "lc_result_fetch", "lc_result_device", "lc_decompress_f64", "lc_last_device_ms",
             "lc_phase_ms", "lc_launch_count", "lc_error_stats_f64", "lc_stencil_apply_f64",
             "lc_residual_f64", "lc_jacobi_step_f64", "lc_dot_f64", "lc_axpy_f64", "lc_result_sync",
-            "lc_decompress_v2_f64", "lc_trace_mark_api", "lc_trace_read", "lc_compress_auto_f64"]
+            "lc_decompress_v2_f64", "lc_trace_mark_api", "lc_trace_read", "lc_compress_auto_f64", "lc_ctx_set_option", "lc_ctx_get_stat",
+            "lc_debug_codebook"]
 
 
 class Context:
@@ -157,29 +164,41 @@ class Context:
 
 
 _ctx_local = threading.local()
+_MAX_STREAM_CTXS = 8          # cached contexts per thread (one per (device, stream) pair)
 
 
-def bind_stream(device, stream_ptr):
-    """Make this thread's context for `device` run on the given CUDA stream
-    (cudaStream_t as int); used by workers that must overlap with the caller."""
+def _ctx_map():
     ctxs = getattr(_ctx_local, "ctxs", None)
     if ctxs is None:
         ctxs = _ctx_local.ctxs = {}
-    old = ctxs.get(device)
-    if old is not None and getattr(old, "stream", None) == stream_ptr:
-        return old
-    ctx = Context(device, stream=_vp(stream_ptr))
-    ctx.stream = stream_ptr
-    ctxs[device] = ctx
-    if old is not None:
-        old.close()
+    return ctxs
+
+
+def _for_stream(device, stream_ptr):
+    ctxs = _ctx_map()
+    key = (int(device), int(stream_ptr))
+    ctx = ctxs.pop(key, None)
+    if ctx is None:
+        ctx = Context(device, stream=_vp(stream_ptr) if stream_ptr else None)
+        ctx.stream = int(stream_ptr)
+        while len(ctxs) >= _MAX_STREAM_CTXS:       # evict the least recently used
+            ctxs.pop(next(iter(ctxs))).close()
+    ctxs[key] = ctx                               # most recently used last
     return ctx
 
 
+def bind_stream(device, stream_ptr):
+    """Context for `device` whose launches go to the given CUDA stream
+    (cudaStream_t as int).  Kept for callers that pass a raw stream; `context`
+    already follows torch's current stream."""
+    return _for_stream(device, stream_ptr)
+
+
 def context(device=0):
-    ctxs = getattr(_ctx_local, "ctxs", None)
-    if ctxs is None:
-        ctxs = _ctx_local.ctxs = {}
-    if device not in ctxs:
-        ctxs[device] = Context(device)
-    return ctxs[device]
+    """This thread's codec context for `device`, ordered on torch's current CUDA
+    stream of that device: the codec's kernels start after the work already
+    queued on that stream (e.g. the kernel that produced x) and later work on it
+    sees the codec's outputs, whatever stream the caller made current."""
+    import torch
+    stream = torch.cuda.current_stream(int(device)).cuda_stream
+    return _for_stream(device, stream)

@@ -6,9 +6,11 @@ device: the DMA of one chunk overlaps the (multi-threaded) host copy of the
 other, so both directions run near PCIe speed.  Device buffers owned by the
 native library are viewed through __cuda_array_interface__ (no copies).
 
-Ordering: the codec context and torch both use the legacy default stream
-unless a caller binds another one, so these copies are stream-ordered after
-the kernels that produce their sources.
+Ordering: the codec context runs on torch's current stream of the device
+(_native.context), and these copies are issued on that same stream, so they
+are stream-ordered after the kernels that produce their sources.  The staging
+events are recorded on the stream of the device the copy runs on (not on the
+current device's stream), so a buffer is reused only after its own DMA.
 """
 
 from __future__ import annotations
@@ -79,7 +81,7 @@ def to_device(host_u8, device):
         evs[k].synchronize()                     # DMA that last used this buffer is done
         bufs[k][:m].copy_(src[off:off + m])
         out[off:off + m].copy_(bufs[k][:m], non_blocking=True)
-        evs[k].record()
+        evs[k].record(torch.cuda.current_stream(out.device))
     evs[0].synchronize()
     evs[1].synchronize()
     return out
@@ -96,12 +98,13 @@ def pinned_to_device(t, chunk=CHUNK):
     step = max(1, chunk // t.element_size())
     for off in range(0, t.numel(), step):
         out[off:off + step].copy_(t[off:off + step], non_blocking=True)
-    torch.cuda.current_stream().synchronize()
+    torch.cuda.current_stream(out.device).synchronize()
     return out
 
 
 def to_host_into(dev_u8, host_u8):
     """Device uint8 tensor -> existing writable host uint8 tensor (chunked, pinned)."""
+    import torch
     n = dev_u8.numel()
     if n == 0:
         return
@@ -116,7 +119,7 @@ def to_host_into(dev_u8, host_u8):
             m = min(CHUNK, n - off)
             evs[k].synchronize()                 # host copy of this buffer finished below
             bufs[k][:m].copy_(dev_u8[off:off + m], non_blocking=True)
-            evs[k].record()
+            evs[k].record(torch.cuda.current_stream(dev_u8.device))
         if i > 0:
             p = offs[i - 1]
             kp = (i - 1) & 1

@@ -40,9 +40,14 @@ struct lc_ctx {
     const char *tname[256] = {};
     double thost[256] = {};
     int tn = 0;
-    int qslot = -1;                 // __constant__ bounds slot (lc_compress_auto_f64), -1: none free
     LcBuf timeline;
     int64_t timeline_tiles = 0;
+    // lc_ctx_set_option knobs (tests / diagnostics)
+    long long opt[8] = {64, 64, -1, -1, 0, 0, 0, 0};
+    // per-context (hence per-device) launch state of the decoder (lc_decode.cu)
+    int dec_state[40] = {};
+    int quant_serial = 0;           // last compress finished with the sequential kernel
+    uint32_t quant_relaunches = 0;
     uint64_t launches = 0;
     // scratch
     LcBuf xbuf, codes, hist, desc, counters, bad_end, pe, pe_rec, lengths, cw, gkeys, ifreq,
@@ -95,24 +100,11 @@ void lc_set_err(lc_ctx *ctx, const char *msg) { ctx->err = msg; }
 LcBuf *lc_dec_bufs(lc_ctx *ctx) { return ctx->dec; }
 cudaEvent_t lc_phase_ev(lc_ctx *ctx, int i) { return ctx->pev[i]; }
 void lc_count_launch(lc_ctx *ctx, int k) { ctx->launches += k; }
+long long lc_opt(lc_ctx *ctx, int key) { return (key >= 0 && key < 8) ? ctx->opt[key] : 0; }
+int *lc_dec_state(lc_ctx *ctx) { return ctx->dec_state; }
+
+int lc_ctx_device(lc_ctx *ctx) { return ctx->device; }
 void lc_set_kind(lc_ctx *ctx, int k) { ctx->last_kind = k; }
-static std::mutex g_qslot_mu;
-static uint32_t g_qslot_used = 0;
-
-static int lc_qslot_acquire()
-{
-    std::lock_guard<std::mutex> g(g_qslot_mu);
-    for (int i = 0; i < LC_QDYN_SLOTS; ++i)
-        if (!(g_qslot_used & (1u << i))) { g_qslot_used |= 1u << i; return i; }
-    return -1;
-}
-
-static void lc_qslot_release(int i)
-{
-    if (i < 0) return;
-    std::lock_guard<std::mutex> g(g_qslot_mu);
-    g_qslot_used &= ~(1u << i);
-}
 
 static double lc_host_us()
 {
@@ -142,6 +134,7 @@ extern "C" {
 
 int lc_ctx_create(lc_ctx **out, int device, void *stream)
 {
+    LcDeviceGuard guard(device);
     lc_ctx *ctx = new lc_ctx();
     ctx->device = device;
     *out = nullptr;
@@ -151,8 +144,7 @@ int lc_ctx_create(lc_ctx **out, int device, void *stream)
     ctx->timeline_on = tlv && tlv[0] == '1';
     const char *trv = getenv("LC_TRACE");
     ctx->trace_on = trv && trv[0] == '1';
-    ctx->qslot = lc_qslot_acquire();
-    LC_CUDA_OK(cudaSetDevice(device));
+    if (!guard.ok) LC_CUDA_OK(cudaSetDevice(device));
     cudaDeviceProp prop;
     LC_CUDA_OK(cudaGetDeviceProperties(&prop, device));
     ctx->sm_count = prop.multiProcessorCount;
@@ -185,8 +177,8 @@ int lc_ctx_create(lc_ctx **out, int device, void *stream)
 void lc_ctx_destroy(lc_ctx *ctx)
 {
     if (!ctx) return;
+    LcDeviceGuard guard(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    lc_qslot_release(ctx->qslot);
     LcBuf *bufs[] = {&ctx->xbuf, &ctx->codes, &ctx->hist, &ctx->desc, &ctx->counters, &ctx->bad_end,
                      &ctx->pe, &ctx->pe_rec, &ctx->lengths, &ctx->cw, &ctx->gkeys, &ctx->ifreq,
                      &ctx->parent, &ctx->cbout, &ctx->payload, &ctx->esc_idx, &ctx->esc_val,
@@ -228,6 +220,7 @@ int lc_range_f64(lc_ctx *ctx, const double *x, uint64_t n, int x_on_device, doub
                  int *nonfinite)
 {
     if (!ctx || n == 0) return 12;
+    LcDeviceGuard guard(ctx->device);
     int rc;
     const double *dx = lc_device_input(ctx, x, n, x_on_device, &rc);
     if (rc) return rc;
@@ -256,6 +249,7 @@ int lc_error_stats_f64(lc_ctx *ctx, const double *original, const double *recon,
                        const double *pe, const double *pe_rec, lc_stats *out)
 {
     if (!ctx || !out || n == 0) return 12;
+    LcDeviceGuard guard(ctx->device);
     cudaStream_t st = ctx->stream;
     int rc;
     const double *da = lc_device_input(ctx, original, n, on_device, &rc);
@@ -319,7 +313,6 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
 
     LcQuantParams P;
     P.dyn = dyn;
-    P.dyn_slot = dyn ? ctx->qslot : -1;
     P.x = dx;
     P.n = n;
     P.Q.delta = 2.0 * eb_abs;
@@ -359,6 +352,8 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     unsigned long long *hbad = (unsigned long long *)ctx->pinned;
     LcCodebookOut *hcb = (LcCodebookOut *)((char *)ctx->pinned + 64);
     uint32_t relaunches = 0;
+    ctx->quant_serial = 0;
+    P.inject_chunk = ctx->opt[LC_OPT_INJECT_QUANT];
     LC_CUDA_OK(cudaEventRecord(ctx->pev[1], st));
     // split-pass buffers
     LC_CUDA_OK(lc_reserve(ctx->pred, (size_t)nchunks * (sizeof(int) + 5 * sizeof(double)) + 64));
@@ -494,7 +489,8 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
             P.first_chunk = (int64_t)fb;
             P.anchor_val = anchor;
             P.count_hist = 0;
-            if (relaunches > 64) {                      // pathological input: exact serial chain
+            if ((long long)relaunches > ctx->opt[LC_OPT_MAX_QUANT]) {   // pathological input: exact serial chain
+                ctx->quant_serial = 1;
                 lc_quant_serial_kernel<CodeT><<<1, 32, 0, st>>>(P, codes);
                 { int _rc = lc_debug_check(ctx, "lc_quant_serial_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
                 ctx->launches += 1;
@@ -538,6 +534,7 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     res->max_len = (uint32_t)ctx->cb.max_len;
     res->used_symbols = (uint32_t)ctx->cb.used;
     res->relaunches = relaunches;
+    ctx->quant_relaunches = relaunches;
     return 0;
 }
 
@@ -549,7 +546,8 @@ int lc_compress_f64(lc_ctx *ctx, const double *x, uint64_t n, int x_on_device, d
     if (!ctx || !res || n < 2 || n_bins_half < 1 || !(eb_abs > 0.0)) return 12;
     if (!isfinite(2.0 * eb_abs)) return 11;
     if (n_bins_half > (1u << 30)) return 12;
-    LC_CUDA_OK(cudaSetDevice(ctx->device));
+    LcDeviceGuard guard(ctx->device);
+    if (!guard.ok) LC_CUDA_OK(cudaSetDevice(ctx->device));
     LC_CUDA_OK(cudaEventRecord(ctx->ev0, ctx->stream));
     LC_CUDA_OK(cudaEventRecord(ctx->pev[0], ctx->stream));
     int rc;
@@ -564,7 +562,8 @@ int lc_compress_auto_f64(lc_ctx *ctx, const double *x, uint64_t n, int x_on_devi
 {
     if (!ctx || !res || !bounds || n < 2 || n_bins_half < 1 || !(eb_param > 0.0) || !isfinite(eb_param)) return 12;
     if (n_bins_half > (1u << 30)) return 12;
-    LC_CUDA_OK(cudaSetDevice(ctx->device));
+    LcDeviceGuard guard(ctx->device);
+    if (!guard.ok) LC_CUDA_OK(cudaSetDevice(ctx->device));
     LC_CUDA_OK(cudaEventRecord(ctx->ev0, ctx->stream));
     LC_CUDA_OK(cudaEventRecord(ctx->pev[0], ctx->stream));
     int rc;
@@ -584,21 +583,8 @@ int lc_compress_auto_f64(lc_ctx *ctx, const double *x, uint64_t n, int x_on_devi
     { int _rc = lc_debug_check(ctx, "lc_quant_setup_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
     ctx->rng_ptr = nullptr;
     LcQuantDyn *hdyn = (LcQuantDyn *)((char *)ctx->pinned + 512);
-    if (ctx->qslot < 0) {
-        // no __constant__ slot left (more than LC_QDYN_SLOTS live contexts): read the
-        // bounds back and take the host path
-        LC_CUDA_OK(cudaMemcpyAsync(hdyn, dyn, sizeof(LcQuantDyn), cudaMemcpyDeviceToHost, ctx->stream));
-        LC_CUDA_OK(cudaStreamSynchronize(ctx->stream));
-        rc = hdyn->status;
-        if (!rc) {
-            if (2ull * n_bins_half <= 65536ull) rc = lc_compress_t<uint16_t>(ctx, dx, n, hdyn->eb_abs, n_bins_half, record_traces, res);
-            else rc = lc_compress_t<uint32_t>(ctx, dx, n, hdyn->eb_abs, n_bins_half, record_traces, res);
-        }
-    } else {
-        LC_CUDA_OK(lc_qdyn_to_slot(dyn, ctx->qslot, ctx->stream));
-        if (2ull * n_bins_half <= 65536ull) rc = lc_compress_t<uint16_t>(ctx, dx, n, 0.0, n_bins_half, record_traces, res, dyn, hdyn);
-        else rc = lc_compress_t<uint32_t>(ctx, dx, n, 0.0, n_bins_half, record_traces, res, dyn, hdyn);
-    }
+    if (2ull * n_bins_half <= 65536ull) rc = lc_compress_t<uint16_t>(ctx, dx, n, 0.0, n_bins_half, record_traces, res, dyn, hdyn);
+    else rc = lc_compress_t<uint32_t>(ctx, dx, n, 0.0, n_bins_half, record_traces, res, dyn, hdyn);
     bounds->vmin = hdyn->vmin;
     bounds->vmax = hdyn->vmax;
     bounds->value_range = hdyn->value_range;
@@ -613,6 +599,7 @@ int lc_result_fetch(lc_ctx *ctx, uint8_t *code_lengths, uint8_t *payload, uint64
                     double *pe, double *pe_rec)
 {
     if (!ctx) return 12;
+    LcDeviceGuard guard(ctx->device);
     cudaStream_t st = ctx->stream;
     if (code_lengths) LC_CUDA_OK(cudaMemcpyAsync(code_lengths, ctx->lengths.p, ctx->nbins, cudaMemcpyDeviceToHost, st));
     const uint64_t pbytes = (ctx->cb.total_bits + 7) / 8;
@@ -644,6 +631,7 @@ int lc_result_device(lc_ctx *ctx, const uint8_t **payload, const uint8_t **code_
 int lc_trace_read(lc_ctx *ctx, char *out, int cap)
 {
     if (!ctx || !out || cap <= 0) return 0;
+    LcDeviceGuard guard(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     int w = 0;
     out[0] = 0;
@@ -685,13 +673,33 @@ int lc_phase_ms(lc_ctx *ctx, double *ms, int cap)
 
 uint64_t lc_launch_count(lc_ctx *ctx) { return ctx ? ctx->launches : 0; }
 
+int lc_ctx_set_option(lc_ctx *ctx, int key, long long value)
+{
+    if (!ctx || key < 0 || key >= 8) return 12;
+    ctx->opt[key] = value;
+    return 0;
+}
+
+long long lc_ctx_get_stat(lc_ctx *ctx, int key)
+{
+    if (!ctx) return -1;
+    switch (key) {
+    case LC_STAT_QUANT_RELAUNCHES: return ctx->quant_relaunches;
+    case LC_STAT_QUANT_SERIAL: return ctx->quant_serial;
+    case LC_STAT_REC_RELAUNCHES: return ctx->dec_state[31];
+    case LC_STAT_REC_SERIAL: return ctx->dec_state[30];
+    default: return -1;
+    }
+}
+
 int lc_decompress_f64(lc_ctx *ctx, uint64_t n, double eb_abs, double first_value, const uint8_t *code_lengths,
                       uint64_t n_lengths, const uint8_t *payload, uint64_t payload_bytes, uint64_t payload_bits,
                       const uint64_t *esc_idx, const double *esc_val, uint64_t n_esc, int inputs_on_device,
                       double *out, int out_on_device, int64_t *esc_used)
 {
     if (!ctx) return 12;
-    LC_CUDA_OK(cudaSetDevice(ctx->device));
+    LcDeviceGuard guard(ctx->device);
+    if (!guard.ok) LC_CUDA_OK(cudaSetDevice(ctx->device));
     return lc_decompress_impl2(ctx, n, eb_abs, first_value, code_lengths, n_lengths, payload, payload_bytes,
                                payload_bits, esc_idx, esc_val, n_esc, inputs_on_device, out, out_on_device,
                                esc_used, nullptr, 0);
@@ -700,6 +708,7 @@ int lc_decompress_f64(lc_ctx *ctx, uint64_t n, double eb_abs, double first_value
 int lc_result_sync(lc_ctx *ctx, uint64_t *offsets, uint64_t cap, uint64_t *count)
 {
     if (!ctx) return 12;
+    LcDeviceGuard guard(ctx->device);
     if (count) *count = ctx->nsync;
     if (offsets && cap) {
         const uint64_t k = cap < ctx->nsync ? cap : ctx->nsync;
@@ -717,16 +726,51 @@ int lc_decompress_v2_f64(lc_ctx *ctx, uint64_t n, double eb_abs, double first_va
 {
     if (!ctx) return 12;
     if (!sync || sync_k != LC_SYNC_K || n < 2 || n_sync != (n - 1 + LC_SYNC_K - 1) / LC_SYNC_K) return 12;
-    LC_CUDA_OK(cudaSetDevice(ctx->device));
+    LcDeviceGuard guard(ctx->device);
+    if (!guard.ok) LC_CUDA_OK(cudaSetDevice(ctx->device));
     return lc_decompress_impl2(ctx, n, eb_abs, first_value, code_lengths, n_lengths, payload, payload_bytes,
                                payload_bits, esc_idx, esc_val, n_esc, inputs_on_device, out, out_on_device,
                                esc_used, sync, n_sync);
+}
+
+// Debug/test hook: the device codebook (lc_codebook_kernel: the
+// huffman.code_lengths + canonical_codes replacement) on a caller-given
+// histogram, so adversarial frequency tables (ties, Fibonacci depths) can be
+// checked against the reference without crafting data that produces them.
+int lc_debug_codebook(lc_ctx *ctx, const uint32_t *hist, uint32_t nbins, uint8_t *lengths_out,
+                      uint64_t *codes_out, int *max_len_out)
+{
+    if (!ctx || !hist || nbins < 1) return 12;
+    LcDeviceGuard guard(ctx->device);
+    cudaStream_t st = ctx->stream;
+    LC_CUDA_OK(lc_reserve(ctx->hist, nbins * sizeof(uint32_t)));
+    LC_CUDA_OK(lc_reserve(ctx->lengths, nbins));
+    LC_CUDA_OK(lc_reserve(ctx->cw, nbins * sizeof(unsigned long long)));
+    LC_CUDA_OK(lc_reserve(ctx->gkeys, 3 * (size_t)nbins * sizeof(unsigned long long)));
+    LC_CUDA_OK(lc_reserve(ctx->ifreq, (size_t)nbins * sizeof(unsigned long long)));
+    LC_CUDA_OK(lc_reserve(ctx->parent, 2 * (size_t)nbins * sizeof(int)));
+    LC_CUDA_OK(lc_reserve(ctx->cbout, sizeof(LcCodebookOut)));
+    LC_CUDA_OK(cudaMemcpyAsync(ctx->hist.p, hist, nbins * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    lc_codebook_kernel<<<1, 1024, lc_codebook_smem_bytes(), st>>>(
+        (const uint32_t *)ctx->hist.p, nbins, (uint8_t *)ctx->lengths.p, (unsigned long long *)ctx->cw.p,
+        (unsigned long long *)ctx->gkeys.p, (unsigned long long *)ctx->ifreq.p, (int *)ctx->parent.p,
+        (LcCodebookOut *)ctx->cbout.p, nullptr);
+    ctx->launches += 1;
+    { int _rc = lc_debug_check(ctx, "lc_codebook_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+    LcCodebookOut *h = (LcCodebookOut *)((char *)ctx->pinned + 1024);
+    LC_CUDA_OK(cudaMemcpyAsync(h, ctx->cbout.p, sizeof(LcCodebookOut), cudaMemcpyDeviceToHost, st));
+    if (lengths_out) LC_CUDA_OK(cudaMemcpyAsync(lengths_out, ctx->lengths.p, nbins, cudaMemcpyDeviceToHost, st));
+    if (codes_out) LC_CUDA_OK(cudaMemcpyAsync(codes_out, ctx->cw.p, nbins * 8, cudaMemcpyDeviceToHost, st));
+    LC_CUDA_OK(cudaStreamSynchronize(st));
+    if (max_len_out) *max_len_out = h->max_len;
+    return h->status;
 }
 
 // Debug/test hook: copy an intermediate of the last compress to host.
 // what: 0 codes, 1 histogram (u32), 2 code lengths (u8), 3 codewords (u64)
 int lc_debug_copy(lc_ctx *ctx, int what, void *host, uint64_t bytes)
 {
+    LcDeviceGuard guard(ctx->device);
     const void *src = what == 0 ? ctx->codes.p : what == 1 ? ctx->hist.p : what == 2 ? ctx->lengths.p
                     : what == 3 ? ctx->cw.p : what == 5 ? ctx->cbout.p : ctx->timeline.p;
     LC_CUDA_OK(cudaMemcpyAsync(host, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));

@@ -1001,6 +1001,7 @@ struct LcRecParams {
     long long *chunk_esc;       // escapes up to each chunk's start (inclusive of position cL)
     int *esc_flags;             // [0] more escape codes than values, [1] position mismatch
     const int *abort_a, *abort_b;   // decode status / cascade flag: non-zero -> kernels exit (no host sync before)
+    long long inject_chunk;     // test hook: perturb this chunk's predicted start (fresh launch only), -1 off
 };
 
 __device__ __forceinline__ bool lc_rec_aborted(const LcRecParams &P)
@@ -1358,6 +1359,9 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_rec_b_kernel(LcRecParams P, LcRe
             const double g0 = S.pred.g0[c];
             e = P.chunk_esc[c];
             start = lc_apply_offset(g0, lc_map_eval(m, S.tile_D[t]));
+            // test hook (lc_ctx_set_option LC_OPT_INJECT_REC): a wrong prediction for this
+            // chunk, so its predecessor's end check fails and the host relaunches
+            if (c == P.inject_chunk && P.first_chunk == 0) start = lc_from_bits(lc_bits(start) ^ 1);
         }
         __syncthreads();                                 // previous tile's ys/starts reads are done
         starts[tid] = start;
@@ -1444,6 +1448,8 @@ cudaEvent_t lc_phase_ev(lc_ctx *ctx, int i);
 void lc_count_launch(lc_ctx *ctx, int k);
 void lc_set_kind(lc_ctx *ctx, int k);
 int lc_debug_check(lc_ctx *ctx, const char *what, const char *file, int line);
+long long lc_opt(lc_ctx *ctx, int key);
+int *lc_dec_state(lc_ctx *ctx);
 
 static int lc_reconstruct(lc_ctx *ctx, uint64_t n, double eb_abs, double first_value, const double *esc_val_in,
                           uint64_t n_esc, double *out, int out_on_device, int64_t *esc_used, void *codes,
@@ -1571,7 +1577,7 @@ int lc_decompress_impl2(lc_ctx *ctx, uint64_t n, double eb_abs, double first_val
     }
     // one resident wave: the CTAs stride over the payload ranges, so a grid
     // larger than what fits leaves its late CTAs running at partial occupancy
-    static int s_occ[17] = {0};
+    int *s_occ = lc_dec_state(ctx);                 // [0..16] per-context (per-device) cache
     if (!s_occ[sub]) {
         int occ = 0;
         switch (sub) {
@@ -1690,6 +1696,42 @@ __global__ void lc_rec_final_kernel(LcRecParams P, LcRecSplit S, long long last,
     f->abort_b = P.abort_b ? *P.abort_b : 0;
 }
 
+// Sequential exact reconstruction from chunk first_chunk (the reference loop,
+// compressor.py:358-376, on one thread): the decoder's fallback when chunk
+// predictions keep failing (more than LC_OPT_MAX_REC relaunches).  Writes the
+// escape count the same way the split passes report it.
+template <int CB>
+__global__ void lc_rec_serial_kernel(LcRecParams P, LcRecFinal *f)
+{
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double r = P.anchor_val;
+    long long e = P.anchor_cnt;
+    for (uint64_t i = (uint64_t)P.first_chunk * LC_L + 1; i < P.n; ++i) {
+        const uint32_t code = CB == 2 ? (uint32_t)reinterpret_cast<const uint16_t *>(P.codes)[i - 1]
+                                      : reinterpret_cast<const uint32_t *>(P.codes)[i - 1];
+        if (code == 0) {                                       // compressor.py:365-369
+            if (e < (long long)P.n_esc) {
+                r = P.esc_val[e];
+                if (P.esc_idx[e] != (unsigned long long)i) P.esc_flags[1] = 1;
+            } else {
+                P.esc_flags[0] = 1;
+            }
+            ++e;
+        } else {                                               // :370-374
+            const int mm = lc_code_m_nz(code);
+            if (mm != 0) r = LC_ADD(r, LC_MUL((double)mm, P.delta));
+        }
+        P.out[i] = r;
+    }
+    f->first_bad = ~0ULL;
+    f->esc_flags[0] = P.esc_flags[0];
+    f->esc_flags[1] = P.esc_flags[1];
+    f->cnt_a = e;
+    f->cnt_b = 0;
+    f->abort_a = P.abort_a ? *P.abort_a : 0;
+    f->abort_b = P.abort_b ? *P.abort_b : 0;
+}
+
 static int lc_reconstruct(lc_ctx *ctx, uint64_t n, double eb_abs, double first_value, const double *esc_val_in,
                           uint64_t n_esc, double *out, int out_on_device, int64_t *esc_used, void *codes,
                           int code_bytes, const int *abort_a, const int *abort_b, int *abort_hit)
@@ -1728,6 +1770,7 @@ static int lc_reconstruct(lc_ctx *ctx, uint64_t n, double eb_abs, double first_v
     R.esc_flags = esc_flags;
     R.abort_a = abort_a;
     R.abort_b = abort_b;
+    R.inject_chunk = lc_opt(ctx, LC_OPT_INJECT_REC);
     LcRecFinal *dfin = (LcRecFinal *)((char *)baux.p + 160);
     LcRecFinal *hfin = (LcRecFinal *)((char *)lc_pinned(ctx) + 256);
     *abort_hit = 0;
@@ -1751,7 +1794,7 @@ static int lc_reconstruct(lc_ctx *ctx, uint64_t n, double eb_abs, double first_v
         RS.pred.g0 = (double *)pp;               pp += nchunks * sizeof(double);
         RS.pred.kind = (int *)pp;
     }
-    static bool attr_b = false;
+    int &attr_b = lc_dec_state(ctx)[20];            // per context, hence per device
     if (!attr_b) {
         LC_CUDA_OK(cudaFuncSetAttribute(lc_rec_a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)lc_rec_a_smem_bytes()));
@@ -1759,12 +1802,13 @@ static int lc_reconstruct(lc_ctx *ctx, uint64_t n, double eb_abs, double first_v
                                         (int)lc_rec_b_smem_bytes()));
         LC_CUDA_OK(cudaFuncSetAttribute(lc_rec_b_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)lc_rec_b_smem_bytes()));
-        attr_b = true;
+        attr_b = 1;
     }
     LC_CUDA_OK(cudaMemsetAsync(esc_flags, 0, 8, st));
     lc_set_first_kernel<<<1, 1, 0, st>>>(dout, first_value);
     lc_count_launch(ctx, 1);
     int relaunches = 0;
+    lc_dec_state(ctx)[30] = 0;
     for (;;) {
         R.ntiles = (nchunks - R.first_chunk + LC_TPB - 1) / LC_TPB;
         LC_CUDA_OK(cudaMemsetAsync(R.first_bad, 0xff, 8, st));
@@ -1796,8 +1840,19 @@ static int lc_reconstruct(lc_ctx *ctx, uint64_t n, double eb_abs, double first_v
         R.first_chunk = (int64_t)fb;
         R.anchor_val = anchor;
         R.anchor_cnt = acnt;
-        if (relaunches > 100000) { lc_set_err(ctx, "reconstruction did not converge"); return 20; }
+        if (relaunches > lc_opt(ctx, LC_OPT_MAX_REC)) {
+            // chunk predictions keep failing: finish with the exact sequential chain
+            if (code_bytes == 2) lc_rec_serial_kernel<2><<<1, 32, 0, st>>>(R, dfin);
+            else lc_rec_serial_kernel<4><<<1, 32, 0, st>>>(R, dfin);
+            { int _rc = lc_debug_check(ctx, "lc_rec_serial_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+            lc_count_launch(ctx, 1);
+            LC_CUDA_OK(cudaMemcpyAsync(hfin, dfin, sizeof(LcRecFinal), cudaMemcpyDeviceToHost, st));
+            LC_CUDA_OK(cudaStreamSynchronize(st));
+            lc_dec_state(ctx)[30] = 1;                   // serial path taken (lc_ctx_get_stat)
+            break;
+        }
     }
+    lc_dec_state(ctx)[31] = relaunches;                  // relaunches of the last decompress
     // escape checks (compressor.py:435-439)
     const int hflags[2] = {hfin->esc_flags[0], hfin->esc_flags[1]};
     const long long total_esc = hfin->cnt_a + hfin->cnt_b;

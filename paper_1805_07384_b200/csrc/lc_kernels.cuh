@@ -3,6 +3,38 @@
 #pragma once
 #include "lc_common.cuh"
 
+// Host side: make a context's device current for one API call and restore
+// the caller's current device on return (the C ABI never changes the calling
+// thread's device as a side effect).
+struct lc_ctx;
+int lc_ctx_device(lc_ctx *ctx);
+
+// lc_ctx_set_option keys (include/lossyckpt_b200.h)
+#define LC_OPT_MAX_QUANT 0      // quantizer relaunches before the sequential fallback (default 64)
+#define LC_OPT_MAX_REC 1        // decoder relaunches before the sequential fallback (default 64)
+#define LC_OPT_INJECT_QUANT 2   // test hook: chunk whose predicted start is perturbed (-1 off)
+#define LC_OPT_INJECT_REC 3     // test hook: the same in the decoder
+#define LC_OPT_VERIFY 4         // 1: quantizer re-runs every chunk exactly (no certified skip)
+// lc_ctx_get_stat keys
+#define LC_STAT_QUANT_RELAUNCHES 0
+#define LC_STAT_QUANT_SERIAL 1
+#define LC_STAT_REC_RELAUNCHES 2
+#define LC_STAT_REC_SERIAL 3
+struct LcDeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit LcDeviceGuard(int dev)
+    {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~LcDeviceGuard()
+    {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
 struct LcRangePart { double vmin, vmax, maxstep; int nonfinite; };
 
 // Per-chunk prediction data written by pass A, read by pass B (SoA, [nchunks]).
@@ -26,11 +58,8 @@ struct LcQuantDyn {
     int nonfinite;
 };
 
-#define LC_QDYN_SLOTS 32      // __constant__ copies of device-resolved bounds (one per context slot)
-
 struct LcQuantParams {
-    const LcQuantDyn *dyn;   // non-null: Q / esc_thresh / use_anchors come from the device ...
-    int dyn_slot;            // ... through the context's __constant__ slot c_qdyn[dyn_slot]
+    const LcQuantDyn *dyn;   // non-null: Q / esc_thresh / use_anchors come from the device
     const double *x;
     uint64_t n;              // elements; codes cover positions 1..n-1
     LcQuant Q;
@@ -55,6 +84,7 @@ struct LcQuantParams {
     LcChunkPred pred;            // pass A -> pass B
     OffMap *tile_agg;            // [ntiles] pass A -> scan
     double *tile_D;              // [ntiles + 1] scan -> pass B (offset at each tile start)
+    long long inject_chunk;      // test hook: perturb this chunk's predicted start (fresh launch only), -1 off
 };
 
 // v2 blocks: a bit offset for every LC_SYNC_K-th symbol (a multiple of LC_L)
@@ -113,9 +143,6 @@ __global__ void lc_anchor_scan_kernel(const long long *__restrict__ last, long l
                                       long long ntiles, long long launch_pos, const LcQuantDyn *dyn);
 __global__ void lc_quant_setup_kernel(const LcRangePart *__restrict__ r, const double *__restrict__ x, uint64_t n,
                                       int eb_relative, double eb_param, uint32_t nbh, LcQuantDyn *d);
-// copy a call's device-resolved bounds into the context's __constant__ slot
-// (in-stream device-to-device copy; lc_quant.cu)
-cudaError_t lc_qdyn_to_slot(const LcQuantDyn *dyn, int slot, cudaStream_t st);
 __global__ void lc_quant_a_kernel(LcQuantParams P);
 __global__ void lc_map_scan_kernel(const OffMap *__restrict__ agg, double *__restrict__ tileD, long long ntiles,
                                    long long per, OffMap *gagg, int *gflag);

@@ -14,22 +14,24 @@
 #include <cub/block/block_scan.cuh>
 #include "lc_kernels.cuh"
 
-__constant__ LcQuantDyn c_qdyn[LC_QDYN_SLOTS];
-
-// the slots live in lc_quant.cu (the quantizer kernels read them); the host
-// copies a call's LcQuantDyn into its context's slot with an in-stream
-// device-to-device cudaMemcpyToSymbolAsync, so the kernels see the bounds as
-// constant-bank operands like kernel parameters
-
-// kernel entry: take the device-resolved bounds; false = nothing to do
+// kernel entry: take the device-resolved bounds (written by
+// lc_quant_setup_kernel earlier in the same stream; every CTA reads the
+// context's own LcQuantDyn through the read-only path into registers, so
+// concurrent calls on other streams and contexts never share them);
+// false = nothing to do
 __device__ __forceinline__ bool lc_quant_dyn(LcQuantParams &P)
 {
-    if (P.dyn_slot < 0) return true;
-    const LcQuantDyn &d = c_qdyn[P.dyn_slot];
-    if (d.skip) return false;
-    P.Q = d.Q;
-    P.esc_thresh = d.esc_thresh;
-    P.use_anchors = d.use_anchors;
+    if (!P.dyn) return true;
+    const LcQuantDyn *d = P.dyn;
+    if (__ldg(&d->skip)) return false;
+    P.Q.delta = __ldg(&d->Q.delta);
+    P.Q.eb = __ldg(&d->Q.eb);
+    P.Q.max_m = __ldg(&d->Q.max_m);
+    P.Q.max_m1 = __ldg(&d->Q.max_m1);
+    P.Q.inv = __ldg(&d->Q.inv);
+    P.Q.cert = __ldg(&d->Q.cert);
+    P.esc_thresh = __ldg(&d->esc_thresh);
+    P.use_anchors = __ldg(&d->use_anchors);
     return true;
 }
 
@@ -156,12 +158,6 @@ __global__ void __launch_bounds__(256) lc_range_kernel(const double *__restrict_
         out->vmin = mn; out->vmax = mx; out->maxstep = ms; out->nonfinite = nf;
         *done = 0u;
     }
-}
-
-cudaError_t lc_qdyn_to_slot(const LcQuantDyn *dyn, int slot, cudaStream_t st)
-{
-    return cudaMemcpyToSymbolAsync(c_qdyn, dyn, sizeof(LcQuantDyn), (size_t)slot * sizeof(LcQuantDyn),
-                                   cudaMemcpyDeviceToDevice, st);
 }
 
 // Quantizer setup on the device from the range pass (same IEEE operations as
@@ -537,6 +533,8 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_quant_b_kernel(LcQuantParams P, 
             m.kind = P.pred.kind[c]; m.B = P.pred.B[c]; m.t0 = P.pred.t0[c]; m.t1 = P.pred.t1[c]; m.y = P.pred.y[c];
             m.v = 0.0; m.og = 0.0;
             start = lc_apply_offset(P.pred.g0[c], lc_map_eval(m, Dt));
+            // test hook (LC_OPT_INJECT_QUANT): a wrong prediction, so the predecessor's end check fails
+            if (c == P.inject_chunk && P.first_chunk == 0) start = lc_from_bits(lc_bits(start) ^ 1);
         }
         starts[tid] = start;
         if (tid == LC_TPB - 1) {

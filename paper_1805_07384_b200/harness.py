@@ -88,101 +88,12 @@ def measure_n_prime(method: str, a, m, b, solve_config: solvers.SolveConfig,
     return NPrimeResult(baseline_n=base_n, samples=tuple(samples))
 
 
-# --- Poisson-failure trials over a GPU solver workload (simulate.py:39-384) ----------
-
-import math  # noqa: E402
-from dataclasses import dataclass as _dc  # noqa: E402
-
-_POLICIES = ("traditional", "lossy", "none")
-
-
-@_dc(frozen=True)
-class FailureProcess:
-    """Poisson failures: i.i.d. exponential inter-arrival times with rate lam (simulate.py:41-57)."""
-
-    lam: float
-    rng_seed: int
-
-    def __post_init__(self):
-        if self.lam < 0:
-            raise ParameterError("failure rate must be non-negative")
-
-    def arrivals(self):
-        rng = np.random.default_rng(self.rng_seed)
-        scale = 1.0 / self.lam if self.lam > 0 else math.inf
-
-        def draw() -> float:
-            return float(rng.exponential(scale)) if self.lam > 0 else math.inf
-
-        return draw
-
-
-@_dc(frozen=True)
-class SimConfig:
-    """Reproducible simulation setup for GPU solver workloads (simulate.py:60-121).
-
-    Problems: poisson2d:M, poisson1d:N (the reference's) and laplacian3d:M,
-    convdiff3d:M (BASELINE.json configs 3-5).  The reference's synthetic
-    workload is host bookkeeping only and not reproduced here.
-    """
-
-    method: str = "jacobi"
-    problem: str = "poisson2d:64"
-    policy: str = "traditional"
-    ckpt_intvl: int = 100
-    t_it: float = 1.0
-    lam: float = 0.0
-    seed: int = 0
-    trials: int = 1
-    max_time: float = math.inf
-    tolerance: float = 1e-8
-    max_iterations: int = 200_000
-    restart_len: Optional[int] = None
-    compressor_config: Optional[CompressorConfig] = None
-    t_ckpt: Optional[float] = None
-    t_rc: Optional[float] = None
-    t_comp: float = 0.0
-    t_decomp: float = 0.0
-    write_bandwidth: Optional[float] = None
-    read_bandwidth: Optional[float] = None
-    failures_during_ckpt: bool = True
-
-    def __post_init__(self):
-        if self.method not in solvers.METHOD_NAMES:
-            raise ParameterError(f"unknown method {self.method!r}")
-        if self.policy not in _POLICIES:
-            raise ParameterError(f"unknown policy {self.policy!r}")
-        if self.trials < 1 or self.ckpt_intvl < 1 or self.t_it <= 0 or self.lam < 0:
-            raise ParameterError("trials, ckpt_intvl must be >= 1; t_it > 0; lam >= 0")
-        if self.policy == "lossy" and self.compressor_config is None:
-            raise ParameterError("real lossy policy needs a compressor_config")
-
-    @property
-    def effective_restart_len(self) -> int:
-        return self.ckpt_intvl if self.restart_len is None else self.restart_len
-
-
-@_dc(frozen=True)
-class TrialReport:
-    """Exact bookkeeping of one trial in simulated time units (simulate.py:124-142)."""
-
-    seed: int
-    converged: bool
-    truncated: bool
-    diverged: bool
-    total_time: float
-    productive_time: float
-    ckpt_time: float
-    rc_time: float
-    rollback_time: float
-    iterations_final: int
-    iterations_executed: int
-    n_failures: int
-    n_checkpoints: int
-    n_checkpoints_voided: int
-    n_recoveries: int
-    n_lossy_recoveries: int
-
+# --- GPU workload for the reference's Poisson-failure trials (simulate.py:207-384) ----
+#
+# The event loop itself is the reference's: lossyckpt.simulate.run_trial(config,
+# seed, workload=GpuSolverWorkload(config)) accepts any workload with this
+# protocol, so it is not re-implemented here (the event loop
+# has no data-parallel work).
 
 def build_problem(problem: str, device="cuda"):
     """(matrix, preconditioner, b) on the device (simulate.py:145-158 + the 3-D configs)."""
@@ -215,8 +126,11 @@ class GpuSolverWorkload:
 
     Same protocol as the reference's _SolverWorkload (simulate.py:207-270):
     iteration, converged, diverged, remaining(), advance(n), capture(now),
-    recovery_cost(image), restore(image), reset().  It can also be handed to
-    the reference's own run_trial(config, seed, workload=...).
+    recovery_cost(image), restore(image), reset().  `config` is the
+    reference's SimConfig (simulate.py:62-120; duck-typed: method, problem,
+    tolerance, max_iterations, effective_restart_len, ckpt_intvl, policy,
+    compressor_config, bandwidths and injected durations); hand the workload
+    to the reference's own run_trial(config, seed, workload=...).
     """
 
     def __init__(self, config, problem=None):
@@ -279,99 +193,3 @@ class GpuSolverWorkload:
 
     def reset(self) -> None:
         self.solver = solvers.init(self._config.method, self.a, self.m, self.b, self.solve_config)
-
-
-def run_trial(config: SimConfig, seed: int, workload=None) -> TrialReport:
-    """One trial: iterate, checkpoint every ckpt_intvl iterations, inject Poisson
-    failures, recover from the last image (simulate.py:277-384, same event order)."""
-    if workload is None:
-        workload = GpuSolverWorkload(config)
-    draw = FailureProcess(config.lam, seed).arrivals()
-    k = config.ckpt_intvl
-    interruptible = config.failures_during_ckpt and config.lam > 0
-    t = 0.0
-    next_fail = draw()
-    ckpt_time = rc_time = fragments = 0.0
-    executed = 0
-    n_failures = n_ckpts = n_voided = n_recoveries = n_lossy = 0
-    last_image = None
-    last_ckpt_iter = -1
-    pending_failure = False
-    truncated = False
-    while True:
-        if workload.converged or workload.diverged:
-            break
-        if t >= config.max_time:
-            truncated = True
-            break
-        if pending_failure:
-            pending_failure = False
-            n_failures += 1
-            next_fail = t + draw()
-            while True:                      # recovery, possibly struck by further failures
-                cost = workload.recovery_cost(last_image)
-                if interruptible and next_fail < t + cost:
-                    rc_time += next_fail - t
-                    t = next_fail
-                    n_failures += 1
-                    next_fail = t + draw()
-                    if t >= config.max_time:
-                        truncated = True
-                        break
-                    continue
-                rc_time += cost
-                t += cost
-                if last_image is not None:
-                    workload.restore(last_image)
-                    if config.policy == "lossy":
-                        n_lossy += 1
-                else:
-                    workload.reset()
-                last_ckpt_iter = -1
-                n_recoveries += 1
-                break
-            if truncated:
-                break
-            continue
-        i = workload.iteration
-        if config.policy != "none" and i > 0 and i % k == 0 and i != last_ckpt_iter:
-            image, cost = workload.capture(t)
-            if interruptible and next_fail < t + cost:
-                ckpt_time += next_fail - t       # in-flight image is voided
-                t = next_fail
-                n_voided += 1
-                pending_failure = True
-                continue
-            ckpt_time += cost
-            t += cost
-            last_image = image
-            last_ckpt_iter = i
-            n_ckpts += 1
-            continue
-        if config.lam > 0:
-            headroom = (next_fail - t) / config.t_it
-            if headroom < 1.0:
-                frag = max(0.0, next_fail - t)
-                fragments += frag
-                t += frag
-                pending_failure = True
-                continue
-            budget = int(headroom)
-        else:
-            budget = config.max_iterations + 1
-        n = min(budget, (k - i % k) if config.policy != "none" else budget)
-        rem = workload.remaining()
-        if rem is not None:
-            n = min(n, rem)
-        done = workload.advance(n)
-        executed += done
-        t += done * config.t_it
-    final_iter = workload.iteration
-    productive = final_iter * config.t_it
-    rollback = (executed - final_iter) * config.t_it + fragments
-    return TrialReport(seed=seed, converged=bool(workload.converged), truncated=truncated,
-                       diverged=bool(workload.diverged), total_time=t, productive_time=productive,
-                       ckpt_time=ckpt_time, rc_time=rc_time, rollback_time=rollback,
-                       iterations_final=final_iter, iterations_executed=executed, n_failures=n_failures,
-                       n_checkpoints=n_ckpts, n_checkpoints_voided=n_voided, n_recoveries=n_recoveries,
-                       n_lossy_recoveries=n_lossy)

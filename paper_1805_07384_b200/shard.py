@@ -9,9 +9,19 @@ all ranks write their blocks concurrently (positional writes, no funnel
 through rank 0).
 
 Sharded image "LCKPSHD1" (little-endian):
-    magic 8 B | u32 version=1 | u32 world | world x (u64 offset, u64 bytes, u64 n)
+    magic 8 B | u32 version=2 | u32 world
+    | world x (u64 offset, u64 bytes, u64 n, u64 blake2b-64 of the blob)
     | world concatenated CompressedBlock.to_bytes() blobs
-The blobs are exactly the reference's LCKP0001 bytes (compressor.py:251-266).
+The blobs are exactly the reference's LCKP0001 bytes (compressor.py:251-266);
+the per-shard checksum is the reference's image checksum function
+(BLAKE2b, digest 8, little-endian; checkpoint.py:34-36).
+
+Commits are atomic like the reference's StorageTarget.commit (write, then
+os.replace; checkpoint.py:104-113): every rank writes its blob positionally
+into `path + ".tmp"` (created and sized by rank 0 before a barrier) and
+fsyncs it; after a second barrier rank 0 renames the file over `path`.  A
+crash at any point leaves the previous image intact, and a torn or stale
+shard fails its checksum in read_shard.
 
 Works with any torch.distributed backend: NCCL (CUDA tensors) on the GPU
 path, gloo (CPU tensors) in the CPU tests.
@@ -19,6 +29,7 @@ path, gloo (CPU tensors) in the CPU tests.
 
 from __future__ import annotations
 
+import hashlib
 import os
 import struct
 from dataclasses import dataclass
@@ -30,9 +41,15 @@ from .compressor import CompressedBlock
 from .errors import IntegrityError, ParameterError
 
 SHARD_MAGIC = b"LCKPSHD1"
-SHARD_VERSION = 1
+SHARD_VERSION = 2
 _SHD_HEAD = "<II"
-_SHD_ENTRY = "<QQQ"
+_SHD_ENTRY = "<QQQQ"
+_META = 5                                  # n, payload_bits, n_esc, block_bytes, checksum
+
+
+def blob_checksum(blob: bytes) -> int:
+    """BLAKE2b-64 of a shard blob, the reference's image checksum (checkpoint.py:34-36)."""
+    return int.from_bytes(hashlib.blake2b(blob, digest_size=8).digest(), "little")
 
 
 def shard_bounds(n_total: int, world: int, rank: int) -> Tuple[int, int]:
@@ -55,6 +72,7 @@ class ShardLayout:
     nbytes: Tuple[int, ...]
     offsets: Tuple[int, ...]            # absolute byte offsets of each rank's blob
     total_bytes: int
+    checksums: Tuple[int, ...] = ()     # BLAKE2b-64 per blob (0: not known)
 
     @property
     def world(self) -> int:
@@ -66,20 +84,23 @@ def header_bytes(world: int) -> int:
 
 
 def layout_from_meta(meta: np.ndarray) -> ShardLayout:
-    """meta: [world, 4] int64 rows (n, payload_bits, n_esc, block_bytes) -> layout
-    (exclusive scan of block sizes after the header)."""
-    meta = np.asarray(meta, dtype=np.int64).reshape(-1, 4)
+    """meta: [world, 5] int64 rows (n, payload_bits, n_esc, block_bytes, checksum bits)
+    -> layout (exclusive scan of block sizes after the header)."""
+    meta = np.asarray(meta, dtype=np.int64).reshape(-1, _META)
     world = meta.shape[0]
     sizes = meta[:, 3]
     offs = header_bytes(world) + np.concatenate([[0], np.cumsum(sizes)[:-1]])
     return ShardLayout(tuple(int(v) for v in meta[:, 0]), tuple(int(v) for v in meta[:, 1]),
                        tuple(int(v) for v in meta[:, 2]), tuple(int(v) for v in sizes),
-                       tuple(int(v) for v in offs), int(header_bytes(world) + sizes.sum()))
+                       tuple(int(v) for v in offs), int(header_bytes(world) + sizes.sum()),
+                       tuple(int(v) for v in meta[:, 4].view(np.uint64)))
 
 
 def block_meta(block: CompressedBlock, blob: Optional[bytes] = None) -> np.ndarray:
-    nbytes = len(blob) if blob is not None else block.nbytes
-    return np.array([block.n, block.payload_bits, len(block.escape_indices), nbytes], dtype=np.int64)
+    if blob is None:
+        blob = block.to_bytes()
+    ck = np.array([blob_checksum(blob)], dtype=np.uint64).view(np.int64)[0]
+    return np.array([block.n, block.payload_bits, len(block.escape_indices), len(blob), ck], dtype=np.int64)
 
 
 def gather_layout(local_meta: np.ndarray, group=None, device=None) -> ShardLayout:
@@ -90,9 +111,9 @@ def gather_layout(local_meta: np.ndarray, group=None, device=None) -> ShardLayou
     world = dist.get_world_size(group)
     dev = device if device is not None else ("cuda" if dist.get_backend(group) == "nccl" else "cpu")
     t = torch.as_tensor(np.asarray(local_meta, dtype=np.int64), device=dev)
-    out = torch.empty(world * 4, dtype=torch.int64, device=dev)
+    out = torch.empty(world * _META, dtype=torch.int64, device=dev)
     dist.all_gather_into_tensor(out, t, group=group)
-    return layout_from_meta(out.cpu().numpy().reshape(world, 4))
+    return layout_from_meta(out.cpu().numpy().reshape(world, _META))
 
 
 def max_over_ranks(value: float, group=None, device=None) -> float:
@@ -109,8 +130,9 @@ def max_over_ranks(value: float, group=None, device=None) -> float:
 
 def encode_header(layout: ShardLayout) -> bytes:
     out = [SHARD_MAGIC, struct.pack(_SHD_HEAD, SHARD_VERSION, layout.world)]
-    for off, nb, n in zip(layout.offsets, layout.nbytes, layout.n):
-        out.append(struct.pack(_SHD_ENTRY, off, nb, n))
+    cks = layout.checksums or (0,) * layout.world
+    for off, nb, n, ck in zip(layout.offsets, layout.nbytes, layout.n, cks):
+        out.append(struct.pack(_SHD_ENTRY, off, nb, n, ck))
     return b"".join(out)
 
 
@@ -128,26 +150,54 @@ def decode_header(blob: bytes) -> ShardLayout:
     offs = tuple(e[0] for e in ents)
     sizes = tuple(e[1] for e in ents)
     ns = tuple(e[2] for e in ents)
+    cks = tuple(e[3] for e in ents)
     expect = need
     for o, s in zip(offs, sizes):
         if o != expect:
             raise IntegrityError("sharded image offsets are not contiguous")
         expect += s
-    return ShardLayout(ns, (0,) * world, (0,) * world, sizes, offs, expect)
+    return ShardLayout(ns, (0,) * world, (0,) * world, sizes, offs, expect, cks)
 
 
-def write_shard(path, rank: int, blob: bytes, layout: ShardLayout) -> None:
-    """Positional write of this rank's blob (rank 0 also writes the header).
-    Every rank opens the same file; no data moves between ranks."""
+def write_shard(path, rank: int, blob: bytes, layout: ShardLayout, fsync: bool = True) -> None:
+    """Positional write of this rank's blob into an existing image file (rank 0
+    also writes the header).  Every rank opens the same file; no data moves
+    between ranks.  checkpoint_sharded calls this on the temporary file of an
+    atomic commit."""
     if len(blob) != layout.nbytes[rank]:
         raise ParameterError("blob size disagrees with the gathered layout")
+    if layout.checksums and blob_checksum(blob) != layout.checksums[rank]:
+        raise ParameterError("blob checksum disagrees with the gathered layout")
     fd = os.open(str(path), os.O_WRONLY | os.O_CREAT, 0o644)
     try:
         if rank == 0:
             os.pwrite(fd, encode_header(layout), 0)
         os.pwrite(fd, blob, layout.offsets[rank])
+        if fsync:
+            os.fsync(fd)
     finally:
         os.close(fd)
+
+
+def prepare_image(tmp_path, layout: ShardLayout) -> None:
+    """Rank 0, before the writes of a commit: create (truncating any stale
+    leftover) the temporary image file at its final size."""
+    fd = os.open(str(tmp_path), os.O_WRONLY | os.O_CREAT | os.O_TRUNC, 0o644)
+    try:
+        os.ftruncate(fd, layout.total_bytes)
+    finally:
+        os.close(fd)
+
+
+def publish_image(tmp_path, path) -> None:
+    """Rank 0, after every rank's write is durable: atomically replace the
+    previous image (os.replace), then make the rename durable (directory fsync)."""
+    os.replace(str(tmp_path), str(path))
+    d = os.open(os.path.dirname(os.path.abspath(str(path))) or ".", os.O_RDONLY)
+    try:
+        os.fsync(d)
+    finally:
+        os.close(d)
 
 
 def read_shard(path, rank: int) -> CompressedBlock:
@@ -164,6 +214,8 @@ def read_shard(path, rank: int) -> CompressedBlock:
         blob = f.read(layout.nbytes[rank])
     if len(blob) != layout.nbytes[rank]:
         raise IntegrityError("sharded image truncated")
+    if layout.checksums and blob_checksum(blob) != layout.checksums[rank]:
+        raise IntegrityError("shard checksum mismatch: image is corrupt")
     blk = CompressedBlock.from_bytes(blob)
     if blk.n != layout.n[rank]:
         raise IntegrityError("shard length disagrees with the header")
@@ -178,9 +230,23 @@ def checkpoint_sharded(x_local, config, path, group=None) -> Tuple[CompressedBlo
     block = compress(x_local, config)
     blob = block.to_bytes()
     layout = gather_layout(block_meta(block, blob), group=group)
-    write_shard(path, rank, blob, layout)
-    dist.barrier(group=group)
+    commit_sharded(path, rank, blob, layout, group=group)
     return block, layout
+
+
+def commit_sharded(path, rank: int, blob: bytes, layout: ShardLayout, group=None) -> None:
+    """Atomic multi-rank commit: rank 0 sizes path.tmp, barrier, every rank
+    writes + fsyncs its blob, barrier, rank 0 renames over `path`, barrier."""
+    import torch.distributed as dist
+    tmp = str(path) + ".tmp"
+    if rank == 0:
+        prepare_image(tmp, layout)
+    dist.barrier(group=group)
+    write_shard(tmp, rank, blob, layout)
+    dist.barrier(group=group)
+    if rank == 0:
+        publish_image(tmp, path)
+    dist.barrier(group=group)
 
 
 def restore_sharded(path, group=None, device=None):

@@ -108,7 +108,7 @@ def test_escape_table_truncation_matches_reference():
 def test_c_abi_exports_every_declared_symbol():
     """The library loads without a GPU and exports every include/*.h entry point."""
     header = open(f"{ROOT}/include/lossyckpt_b200.h").read()
-    declared = set(re.findall(r"^\s*(?:int|void|double|uint64_t|const char \*)\s*\**(lc_\w+)\(", header, re.M))
+    declared = set(re.findall(r"^\s*(?:int|void|double|uint64_t|long long|const char \*)\s*\**(lc_\w+)\(", header, re.M))
     assert declared >= set(_native.EXPORTED)
     lib = ctypes.CDLL(_native.LIB_PATH)
     for sym in declared:

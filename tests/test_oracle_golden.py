@@ -6,6 +6,7 @@ serialized blocks, reconstructions, Huffman code lengths and decode statuses.
 """
 
 import hashlib
+import os
 
 import numpy as np
 import pytest
@@ -84,3 +85,28 @@ def test_oracle_rejects_like_reference():
         orc.compress(np.array([1.0, np.inf]), "absolute", 1.0)
     with pytest.raises(orc.OracleIntegrityError):
         orc.from_bytes(b"WRONG!!!" + bytes(64))
+
+
+def test_oracle_matches_reference_stress_hashes():
+    """The oracle on the large stress corpora (tests/stress_inputs.py, <= 2^21 elements
+    here to keep the CPU suite short) reproduces the real reference's block and
+    reconstruction hashes (tests/golden/stress_golden.json)."""
+    import hashlib
+    import json
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, here)
+    import stress_inputs
+    gold = json.load(open(os.path.join(here, "golden", "stress_golden.json")))
+    checked = 0
+    for name, gen, mode, eb, nbh in stress_inputs.CASES:
+        g = gold[name]
+        if g["n"] > (1 << 21):
+            continue
+        x = gen()
+        assert hashlib.sha256(x.tobytes()).hexdigest() == g["x_sha256"], name
+        d = orc.compress(x, mode, eb, n_bins_half=nbh)
+        assert hashlib.sha256(orc.to_bytes(d)).hexdigest() == g["block_sha256"], name
+        assert hashlib.sha256(d["recon"].tobytes()).hexdigest() == g["recon_sha256"], name
+        checked += 1
+    assert checked >= 4

@@ -57,8 +57,10 @@ def _worker(rank, port, path, outdir):
         blk = _oracle_block(x[lo:hi], 1e-5)
         blob = blk.to_bytes()
         layout = shard.gather_layout(shard.block_meta(blk, blob))
-        shard.write_shard(path, rank, blob, layout)
-        dist.barrier()
+        if os.path.exists(path) and rank == 0:
+            assert open(path, "rb").read() == b"previous image"
+        shard.commit_sharded(path, rank, blob, layout)     # atomic: tmp + fsync + replace
+        assert not os.path.exists(path + ".tmp")
         slowest = shard.max_over_ranks(10.0 + rank)
         # every rank can read every shard; its own is byte-identical
         got = [shard.read_shard(path, r) for r in range(WORLD)]
@@ -82,17 +84,20 @@ def test_shard_bounds_partition():
 
 
 def test_layout_exclusive_scan():
-    meta = np.array([[10, 80, 0, 100], [12, 90, 1, 120], [9, 70, 0, 90]])
+    meta = np.array([[10, 80, 0, 100, 1], [12, 90, 1, 120, 2], [9, 70, 0, 90, -3]])
     lay = shard.layout_from_meta(meta)
     h = shard.header_bytes(3)
     assert lay.offsets == (h, h + 100, h + 220) and lay.total_bytes == h + 310
     assert shard.decode_header(shard.encode_header(lay)).offsets == lay.offsets
+    assert shard.decode_header(shard.encode_header(lay)).checksums == (1, 2, 2 ** 64 - 3)
     with pytest.raises(IntegrityError):
         shard.decode_header(b"LCKPSHD0" + shard.encode_header(lay)[8:])
 
 
 def test_gloo_world2_sharded_image(tmp_path):
     path = str(tmp_path / "sharded.img")
+    with open(path, "wb") as f:                          # the image a commit replaces
+        f.write(b"previous image")
     mp.spawn(_worker, args=(_free_port(), path, str(tmp_path)), nprocs=WORLD, join=True)
     rows = [np.load(str(tmp_path / f"r{r}.npy")) for r in range(WORLD)]
     assert [int(r[3]) for r in rows] == [11, 11]                       # max over ranks
@@ -109,3 +114,21 @@ def test_gloo_world2_sharded_image(tmp_path):
         d = orc.from_bytes(blk.to_bytes())
         rec = orc.decompress(d)
         assert np.all(np.abs(rec - x[lo:hi]) <= blk.eb_abs)
+
+
+def test_corrupt_shard_detected(tmp_path):
+    """A flipped payload byte (a torn write over stale bytes) fails the per-shard
+    BLAKE2b-64 check instead of decoding to a wrong vector."""
+    x = _global_vector()[:5000]
+    blk = _oracle_block(x, 1e-4)
+    blob = blk.to_bytes()
+    layout = shard.layout_from_meta(shard.block_meta(blk, blob)[None, :])
+    path = str(tmp_path / "one.img")
+    shard.prepare_image(path, layout)
+    shard.write_shard(path, 0, blob, layout)
+    assert shard.read_shard(path, 0).to_bytes() == blob
+    raw = bytearray(open(path, "rb").read())
+    raw[-10] ^= 0x40
+    open(path, "wb").write(bytes(raw))
+    with pytest.raises(IntegrityError, match="checksum"):
+        shard.read_shard(path, 0)

@@ -152,31 +152,24 @@ def test_config1_n_prime(dev, sg):
 TG = os.path.join(ROOT, "tests", "golden", "trial_golden.json")
 
 
-def test_sim_config_validation():
-    from paper_1805_07384_b200 import harness
-    from paper_1805_07384_b200.errors import ParameterError
-    for bad in (dict(method="synthetic"), dict(policy="x"), dict(ckpt_intvl=0), dict(policy="lossy")):
-        with pytest.raises(ParameterError):
-            harness.SimConfig(**bad)
-    draw = harness.FailureProcess(0.5, 3).arrivals()
-    r = np.random.default_rng(3)
-    assert [draw() for _ in range(4)] == [float(r.exponential(2.0)) for _ in range(4)]
-
-
 @pytest.mark.gpu
-def test_run_trial_matches_reference(dev):
-    """Poisson-failure trials on the GPU workload against the reference's run_trial with
-    its CPU workload: identical event bookkeeping for Jacobi (bit-identical iterates);
-    CG/GMRES recoveries may shift the convergence step by one per recovery."""
+def test_run_trial_matches_reference(dev, reference):
+    """The reference's own Poisson-failure event loop (simulate.run_trial) driving the
+    GPU workload, against the same loop over its CPU workload (golden reports): identical
+    event bookkeeping for Jacobi (bit-identical iterates); CG/GMRES recoveries may shift
+    the convergence step by one per recovery."""
     import json
+    from lossyckpt import simulate
+    from lossyckpt.compressor import CompressorConfig as RefConfig
     from paper_1805_07384_b200 import harness
-    from paper_1805_07384_b200.compressor import CompressorConfig
     for case in json.load(open(TG)):
         c = dict(case["config"])
         eb = c.pop("eb_rel")
+        seed = c["seed"]
         if eb is not None:
-            c["compressor_config"] = CompressorConfig.value_range_relative(eb)
-        rep = harness.run_trial(harness.SimConfig(**c), c["seed"])
+            c["compressor_config"] = RefConfig.value_range_relative(eb)
+        cfg = simulate.SimConfig(**c)
+        rep = simulate.run_trial(cfg, seed, workload=harness.GpuSolverWorkload(cfg))
         ref = case["report"]
         assert rep.converged == ref["converged"] and rep.diverged == ref["diverged"], c
         if c["method"] == "jacobi":
