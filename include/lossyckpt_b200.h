@@ -76,7 +76,9 @@ typedef struct {
 /* compressor.py:400-413 for n >= 2 and a non-constant vector: quantize with
  * the closed-loop order-1 predictor at eb_abs, histogram, build the Huffman
  * code on device and encode.  x is device or host memory.  Results stay in
- * the context until lc_result_fetch / lc_result_device.                   */
+ * the context until lc_result_fetch / lc_result_device.  Runs the value-range
+ * pass like lc_compress_auto_f64 (absolute mode): returns 10 for non-finite
+ * input and 15 for a constant vector (no results).                        */
 int lc_compress_f64(lc_ctx *ctx, const double *x, uint64_t n, int x_on_device,
                     double eb_abs, uint32_t n_bins_half, int record_traces,
                     lc_result *res);

@@ -48,10 +48,13 @@ struct lc_ctx {
     int dec_state[40] = {};
     int quant_serial = 0;           // last compress finished with the sequential kernel
     uint32_t quant_relaunches = 0;
+    unsigned long long quant_exact_chunks = 0;
+    int quantw_occ[2][2] = {};      // resident CTAs per SM: [u32 codes][pass A, fix-up]
+    void *mapscan_scratch = nullptr;
     uint64_t launches = 0;
     // scratch
     LcBuf xbuf, codes, hist, desc, counters, bad_end, pe, pe_rec, lengths, cw, gkeys, ifreq,
-        parent, cbout, payload, esc_idx, esc_val, encdesc, range_parts, small, pred, tiles;
+        parent, cbout, payload, esc_idx, esc_val, encdesc, range_parts, small, tiles;
     LcBuf st_b, st_pe, st_pr, st_parts, solver, sync;
     uint64_t nsync = 0;                 // v2 sync offsets of the last compress
     // last lc_range_f64 on device data (lets compress skip the anchor pass)
@@ -154,16 +157,22 @@ int lc_ctx_create(lc_ctx **out, int device, void *stream)
     LC_CUDA_OK(cudaEventCreate(&ctx->ev1));
     for (int i = 0; i < 12; ++i) LC_CUDA_OK(cudaEventCreate(&ctx->pev[i]));
     LC_CUDA_OK(cudaMallocHost(&ctx->pinned, 4096));
-    LC_CUDA_OK(cudaFuncSetAttribute(lc_quant_a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)lc_quant_a_smem_bytes()));
-    LC_CUDA_OK(cudaFuncSetAttribute(lc_quant_b_kernel<uint16_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)lc_quant_b_smem_bytes()));
-    LC_CUDA_OK(cudaFuncSetAttribute(lc_quant_b_kernel<uint32_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)lc_quant_b_smem_bytes()));
-    LC_CUDA_OK(cudaFuncSetAttribute(lc_quant_b_kernel<uint16_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)lc_quant_b_smem_bytes()));
-    LC_CUDA_OK(cudaFuncSetAttribute(lc_quant_b_kernel<uint32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)lc_quant_b_smem_bytes()));
+    {
+        const size_t q16 = lc_quantw_smem_bytes(2), q32 = lc_quantw_smem_bytes(4), qf = lc_quantw_fix_smem_bytes();
+        LC_CUDA_OK(cudaFuncSetAttribute(lc_quant_wa_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)q16));
+        LC_CUDA_OK(cudaFuncSetAttribute(lc_quant_wa_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)q32));
+        LC_CUDA_OK(cudaFuncSetAttribute(lc_quant_wfix_kernel<uint16_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qf));
+        LC_CUDA_OK(cudaFuncSetAttribute(lc_quant_wfix_kernel<uint32_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qf));
+        LC_CUDA_OK(cudaFuncSetAttribute(lc_quant_wfix_kernel<uint16_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qf));
+        LC_CUDA_OK(cudaFuncSetAttribute(lc_quant_wfix_kernel<uint32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qf));
+        // persistent grids sized to one resident wave
+        LC_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->quantw_occ[0][0], lc_quant_wa_kernel<uint16_t>, LC_QW_TPB, q16));
+        LC_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->quantw_occ[1][0], lc_quant_wa_kernel<uint32_t>, LC_QW_TPB, q32));
+        LC_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->quantw_occ[0][1], lc_quant_wfix_kernel<uint16_t, false>, LC_QW_TPB, qf));
+        LC_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->quantw_occ[1][1], lc_quant_wfix_kernel<uint32_t, false>, LC_QW_TPB, qf));
+        for (auto &a2 : ctx->quantw_occ)
+            for (int &o : a2) o = o > 0 ? o : 1;
+    }
     LC_CUDA_OK(cudaFuncSetAttribute(lc_codebook_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)lc_codebook_smem_bytes()));
     LC_CUDA_OK(cudaFuncSetAttribute(lc_encode_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -182,7 +191,7 @@ void lc_ctx_destroy(lc_ctx *ctx)
     LcBuf *bufs[] = {&ctx->xbuf, &ctx->codes, &ctx->hist, &ctx->desc, &ctx->counters, &ctx->bad_end,
                      &ctx->pe, &ctx->pe_rec, &ctx->lengths, &ctx->cw, &ctx->gkeys, &ctx->ifreq,
                      &ctx->parent, &ctx->cbout, &ctx->payload, &ctx->esc_idx, &ctx->esc_val,
-                     &ctx->encdesc, &ctx->range_parts, &ctx->small, &ctx->pred, &ctx->tiles, &ctx->dec[0], &ctx->dec[1],
+                     &ctx->encdesc, &ctx->range_parts, &ctx->small, &ctx->tiles, &ctx->dec[0], &ctx->dec[1],
                      &ctx->dec[2], &ctx->dec[3], &ctx->dec[4], &ctx->dec[5], &ctx->dec[6],
                      &ctx->dec[7], &ctx->dec[8], &ctx->dec[9], &ctx->st_b, &ctx->st_pe, &ctx->st_pr,
                      &ctx->st_parts, &ctx->solver, &ctx->sync};
@@ -297,11 +306,10 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     cudaStream_t st = ctx->stream;
     const uint32_t nbins = 2u * nbh;
     const int64_t nchunks = (int64_t)((n - 1 + LC_L - 1) / LC_L);
-    const int64_t ntiles = (nchunks + LC_TPB - 1) / LC_TPB;
+    const int64_t ntiles = (nchunks + 31) / 32;          // warp tiles (lc_quantw.cu)
     const uint64_t m = n - 1;
     LC_CUDA_OK(lc_reserve(ctx->codes, m * sizeof(CodeT)));
     LC_CUDA_OK(lc_reserve(ctx->hist, nbins * sizeof(uint32_t)));
-    LC_CUDA_OK(lc_reserve(ctx->desc, ntiles * sizeof(LcTileDesc)));
     LC_CUDA_OK(lc_reserve(ctx->counters, 64));
     LC_CUDA_OK(lc_reserve(ctx->bad_end, nchunks * sizeof(double)));
     if (record) {
@@ -310,12 +318,14 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     }
     unsigned int *tile_counter = (unsigned int *)ctx->counters.p;
     unsigned long long *first_bad = (unsigned long long *)((char *)ctx->counters.p + 16);
+    unsigned long long *exact_count = (unsigned long long *)((char *)ctx->counters.p + 32);
 
     LcQuantParams P;
+    memset(&P, 0, sizeof P);
     P.dyn = dyn;
     P.x = dx;
     P.n = n;
-    P.Q.delta = 2.0 * eb_abs;
+    P.Q.delta = 2.0 * eb_abs;          // host bounds are only used when dyn is null (never in practice)
     P.Q.eb = eb_abs;
     P.Q.max_m = (double)(nbh - 1);
     P.Q.max_m1 = P.Q.max_m + 1.0;
@@ -326,20 +336,22 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
         P.Q.cert = 0.5 - ldexp(1.0, e2 - 50);
     }
     P.esc_thresh = (double)nbh * P.Q.delta * (1.0 + 0x1p-40);
+    P.rmax = INFINITY;                 // no range known: certification off
     P.first_chunk = 0;
     P.anchor_val = 0.0;
     P.nchunks = nchunks;
-    P.desc = (LcTileDesc *)ctx->desc.p;
     P.tile_counter = tile_counter;
     P.hist = (uint32_t *)ctx->hist.p;
     P.nbins = nbins;
-    P.count_hist = sizeof(CodeT) == 2 ? 0 : 1;           // u16 codes: lc_hist16_kernel after pass B
+    P.count_hist = 1;
     P.first_bad = first_bad;
     P.bad_end = (double *)ctx->bad_end.p;
     P.pe = record ? (double *)ctx->pe.p : nullptr;
     P.pe_rec = record ? (double *)ctx->pe_rec.p : nullptr;
+    P.verify = ctx->opt[LC_OPT_VERIFY] ? 1 : 0;
+    P.exact_count = exact_count;
     P.timeline = nullptr;
-    if (ctx->timeline_on) {
+    if (ctx->timeline_on) {                    // LC_TIMELINE=1: per-tile globaltimer stamps (diagnostics)
         LC_CUDA_OK(lc_reserve(ctx->timeline, ntiles * 128));
         LC_CUDA_OK(cudaMemsetAsync(ctx->timeline.p, 0, ntiles * 128, st));
         P.timeline = (unsigned long long *)ctx->timeline.p;
@@ -348,59 +360,50 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     CodeT *codes = (CodeT *)ctx->codes.p;
 
     LC_CUDA_OK(cudaMemsetAsync(P.hist, 0, nbins * sizeof(uint32_t), st));
+    LC_CUDA_OK(cudaMemsetAsync(exact_count, 0, 8, st));
 
     unsigned long long *hbad = (unsigned long long *)ctx->pinned;
     LcCodebookOut *hcb = (LcCodebookOut *)((char *)ctx->pinned + 64);
+    unsigned long long *hexact = (unsigned long long *)((char *)ctx->pinned + 192);
     uint32_t relaunches = 0;
     ctx->quant_serial = 0;
     P.inject_chunk = ctx->opt[LC_OPT_INJECT_QUANT];
     LC_CUDA_OK(cudaEventRecord(ctx->pev[1], st));
-    // split-pass buffers
-    LC_CUDA_OK(lc_reserve(ctx->pred, (size_t)nchunks * (sizeof(int) + 5 * sizeof(double)) + 64));
+    LC_CUDA_OK(lc_reserve(ctx->tiles, (size_t)(ntiles + 1) * (2 * sizeof(long long) + sizeof(OffMap) + 2 * sizeof(double))
+                                          + LC_MAPSCAN_SCRATCH + 256));
     {
-        char *pp = (char *)ctx->pred.p;
-        P.pred.B = (double *)pp;
-        P.pred.t0 = P.pred.B + nchunks;
-        P.pred.t1 = P.pred.t0 + nchunks;
-        P.pred.y = P.pred.t1 + nchunks;
-        P.pred.g0 = P.pred.y + nchunks;
-        P.pred.kind = (int *)(P.pred.g0 + nchunks);
+        char *pp = (char *)ctx->tiles.p;
+        P.tile_agg = (OffMap *)pp;               pp += (ntiles + 1) * sizeof(OffMap);
+        P.tile_D = (double *)pp;                 pp += (ntiles + 1) * sizeof(double);
+        P.tile_S = (double *)pp;                 pp += (ntiles + 1) * sizeof(double);
+        P.tile_last_esc = (long long *)pp;       pp += (ntiles + 1) * sizeof(long long);
+        P.anc_in = (const long long *)pp;        pp += (ntiles + 1) * sizeof(long long);
+        ctx->mapscan_scratch = (void *)(((uintptr_t)pp + 63) & ~(uintptr_t)63);
     }
-    LC_CUDA_OK(lc_reserve(ctx->tiles, (size_t)(ntiles + 1) * (sizeof(OffMap) + sizeof(double) + 2 * sizeof(long long))
-                                          + LC_MAPSCAN_SCRATCH));
-    P.tile_agg = (OffMap *)ctx->tiles.p;
-    P.tile_D = (double *)(P.tile_agg + ntiles + 1);
-    P.tile_last_esc = (long long *)(P.tile_D + ntiles + 1);
-    void *mapscan_scratch = (void *)(P.tile_last_esc + 2 * (ntiles + 1));
-    P.anc_in = (const long long *)(P.tile_last_esc + ntiles + 1);
-    long long *anc_in = (long long *)(P.tile_last_esc + ntiles + 1);
-    // definite escapes possible?  Same test as lc_definite_escape on the largest step.
+    long long *anc_in = (long long *)P.anc_in;
     P.use_anchors = 1;                                   // with dyn: the device decides
-    if (!dyn && ctx->rng_ptr == (const void *)dx && ctx->rng_n == n) {
-        const double ms = ctx->rng_maxstep;
-        P.use_anchors = ((ms * (1.0 - 0x1p-50)) - (eb_abs * (1.0 + 0x1p-50))) >= P.esc_thresh || !isfinite(ms);
-    }
-    const int ga = 3 * ctx->sm_count, gb = 3 * ctx->sm_count;
+    const size_t qsmem = lc_quantw_smem_bytes(sizeof(CodeT)), fsmem = lc_quantw_fix_smem_bytes();
+    const int ga = 3 * ctx->sm_count;
+    const int *occ = ctx->quantw_occ[sizeof(CodeT) == 2 ? 0 : 1];
     auto quant_launch = [&]() -> int {
-        P.ntiles = (nchunks - P.first_chunk + LC_TPB - 1) / LC_TPB;
+        P.ntiles = (nchunks - P.first_chunk + 31) / 32;
         LC_CUDA_OK(cudaMemsetAsync(first_bad, 0xff, 8, st));
         if (P.use_anchors) {
-            lc_anchor_tiles_kernel<<<(int)(P.ntiles < ga ? P.ntiles : ga), LC_TPB, 0, st>>>(P);
+            lc_anchor_tiles_kernel<<<(int)((P.ntiles + 7) / 8 < ga ? (P.ntiles + 7) / 8 : ga), LC_TPB, 0, st>>>(P);
             lc_anchor_scan_kernel<<<1, 1024, 0, st>>>(P.tile_last_esc, anc_in, P.ntiles, P.first_chunk * LC_L, dyn);
             ctx->launches += 2;
         }
-        lc_quant_a_kernel<<<(int)(P.ntiles < ga ? P.ntiles : ga), LC_TPB, lc_quant_a_smem_bytes(), st>>>(P);
-        { int _rc = lc_debug_check(ctx, "lc_quant_a_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
-        LC_CUDA_OK((cudaError_t)lc_launch_map_scan(P.tile_agg, P.tile_D, P.ntiles, mapscan_scratch, ctx->sm_count, st));
-        if (P.pe) lc_quant_b_kernel<CodeT, true><<<(int)(P.ntiles < gb ? P.ntiles : gb), LC_TPB, lc_quant_b_smem_bytes(), st>>>(P, codes);
-        else lc_quant_b_kernel<CodeT, false><<<(int)(P.ntiles < gb ? P.ntiles : gb), LC_TPB, lc_quant_b_smem_bytes(), st>>>(P, codes);
-        { int _rc = lc_debug_check(ctx, "lc_quant_b_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+        const long long wcta = (P.ntiles + LC_QW_TPB / 32 - 1) / (LC_QW_TPB / 32);
+        LC_CUDA_OK(cudaMemsetAsync(tile_counter, 0, 4, st));
+        const long long ga2 = (long long)occ[0] * ctx->sm_count, gf = (long long)occ[1] * ctx->sm_count;
+        lc_quant_wa_kernel<CodeT><<<(int)(wcta < ga2 ? wcta : ga2), LC_QW_TPB, qsmem, st>>>(P, codes);
+        { int _rc = lc_debug_check(ctx, "lc_quant_wa_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+        LC_CUDA_OK((cudaError_t)lc_launch_map_scan(P.tile_agg, P.tile_D, P.ntiles, ctx->mapscan_scratch,
+                                                   ctx->sm_count, st));
+        if (P.pe) lc_quant_wfix_kernel<CodeT, true><<<(int)(wcta < gf ? wcta : gf), LC_QW_TPB, fsmem, st>>>(P, codes);
+        else lc_quant_wfix_kernel<CodeT, false><<<(int)(wcta < gf ? wcta : gf), LC_QW_TPB, fsmem, st>>>(P, codes);
+        { int _rc = lc_debug_check(ctx, "lc_quant_wfix_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
         ctx->launches += 3;
-        if (sizeof(CodeT) == 2 && P.first_chunk == 0) {
-            lc_hist16_kernel<<<4 * ctx->sm_count, 256, 0, st>>>((const uint16_t *)codes, m, P.hist, nbins, dyn);
-            { int _rc = lc_debug_check(ctx, "lc_hist16_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
-            ctx->launches += 1;
-        }
         return 0;
     };
 
@@ -465,6 +468,7 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     };
     auto readback = [&]() -> int {                       // the one host round trip
         LC_CUDA_OK(cudaMemcpyAsync(hbad, first_bad, 8, cudaMemcpyDeviceToHost, st));
+        LC_CUDA_OK(cudaMemcpyAsync(hexact, exact_count, 8, cudaMemcpyDeviceToHost, st));
         LC_CUDA_OK(cudaMemcpyAsync(hcb, cbo, sizeof(LcCodebookOut), cudaMemcpyDeviceToHost, st));
         if (dyn) LC_CUDA_OK(cudaMemcpyAsync(hdyn, dyn, sizeof(LcQuantDyn), cudaMemcpyDeviceToHost, st));
         LC_CUDA_OK(cudaStreamSynchronize(st));
@@ -486,9 +490,15 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
             ++relaunches;
             double anchor;
             LC_CUDA_OK(cudaMemcpy(&anchor, P.bad_end + (fb - 1), sizeof(double), cudaMemcpyDeviceToHost));
-            P.first_chunk = (int64_t)fb;
-            P.anchor_val = anchor;
-            P.count_hist = 0;
+            if (!isfinite(anchor)) {
+                // a prediction failed before any exact start was known (the offset
+                // look-back gave no finite value): restart this launch sequentially
+                relaunches = (uint32_t)ctx->opt[LC_OPT_MAX_QUANT] + 1;
+            } else {
+                P.first_chunk = (int64_t)fb;
+                P.anchor_val = anchor;
+            }
+            P.inject_chunk = -1;
             if ((long long)relaunches > ctx->opt[LC_OPT_MAX_QUANT]) {   // pathological input: exact serial chain
                 ctx->quant_serial = 1;
                 lc_quant_serial_kernel<CodeT><<<1, 32, 0, st>>>(P, codes);
@@ -508,6 +518,7 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
         { int _rc = encode_launch(); if (_rc) return _rc; }
         { int _rc = readback(); if (_rc) return _rc; }
     }
+    ctx->quant_exact_chunks = *hexact;
     ctx->cb = *hcb;
     if (ctx->cb.status) {
         ctx->err = "code length exceeds 64 bits";
@@ -546,15 +557,11 @@ int lc_compress_f64(lc_ctx *ctx, const double *x, uint64_t n, int x_on_device, d
     if (!ctx || !res || n < 2 || n_bins_half < 1 || !(eb_abs > 0.0)) return 12;
     if (!isfinite(2.0 * eb_abs)) return 11;
     if (n_bins_half > (1u << 30)) return 12;
-    LcDeviceGuard guard(ctx->device);
-    if (!guard.ok) LC_CUDA_OK(cudaSetDevice(ctx->device));
-    LC_CUDA_OK(cudaEventRecord(ctx->ev0, ctx->stream));
-    LC_CUDA_OK(cudaEventRecord(ctx->pev[0], ctx->stream));
-    int rc;
-    const double *dx = lc_device_input(ctx, x, n, x_on_device, &rc);
-    if (rc) return rc;
-    if (2ull * n_bins_half <= 65536ull) return lc_compress_t<uint16_t>(ctx, dx, n, eb_abs, n_bins_half, record_traces, res);
-    return lc_compress_t<uint32_t>(ctx, dx, n, eb_abs, n_bins_half, record_traces, res);
+    // the same one-round-trip path as lc_compress_auto_f64 in absolute mode: the
+    // range pass supplies the non-finite check, the anchor decision and the
+    // chain-value bound the quantizer's certification uses
+    lc_bounds b;
+    return lc_compress_auto_f64(ctx, x, n, x_on_device, 0, eb_abs, n_bins_half, record_traces, res, &b);
 }
 
 int lc_compress_auto_f64(lc_ctx *ctx, const double *x, uint64_t n, int x_on_device, int eb_relative,
@@ -688,6 +695,7 @@ long long lc_ctx_get_stat(lc_ctx *ctx, int key)
     case LC_STAT_QUANT_SERIAL: return ctx->quant_serial;
     case LC_STAT_REC_RELAUNCHES: return ctx->dec_state[31];
     case LC_STAT_REC_SERIAL: return ctx->dec_state[30];
+    case LC_STAT_QUANT_EXACT_CHUNKS: return (long long)ctx->quant_exact_chunks;
     default: return -1;
     }
 }

@@ -20,6 +20,7 @@ int lc_ctx_device(lc_ctx *ctx);
 #define LC_STAT_QUANT_SERIAL 1
 #define LC_STAT_REC_RELAUNCHES 2
 #define LC_STAT_REC_SERIAL 3
+#define LC_STAT_QUANT_EXACT_CHUNKS 4
 struct LcDeviceGuard {
     int prev = -1;
     bool ok = true;
@@ -52,6 +53,7 @@ struct LcQuantDyn {
     LcQuant Q;
     double esc_thresh;
     double eb_abs, value_range, vmin, vmax, first_value;
+    double rmax;             // (max |x| + eb)(1 + 2^-50): bounds every chain value (certification)
     int use_anchors;
     int skip;
     int status;
@@ -83,8 +85,12 @@ struct LcQuantParams {
     long long *tile_last_esc;    // [ntiles] pass 0 output
     LcChunkPred pred;            // pass A -> pass B
     OffMap *tile_agg;            // [ntiles] pass A -> scan
+    double *tile_S;              // [ntiles] pass A: certification slack of each warp tile
     double *tile_D;              // [ntiles + 1] scan -> pass B (offset at each tile start)
     long long inject_chunk;      // test hook: perturb this chunk's predicted start (fresh launch only), -1 off
+    double rmax;                 // bound on |chain values| (from dyn)
+    int verify;                  // 1: every chunk re-run exactly (no certified skip)
+    unsigned long long *exact_count;   // chunks re-run exactly (diagnostic)
 };
 
 // v2 blocks: a bit offset for every LC_SYNC_K-th symbol (a multiple of LC_L)
@@ -143,7 +149,12 @@ __global__ void lc_anchor_scan_kernel(const long long *__restrict__ last, long l
                                       long long ntiles, long long launch_pos, const LcQuantDyn *dyn);
 __global__ void lc_quant_setup_kernel(const LcRangePart *__restrict__ r, const double *__restrict__ x, uint64_t n,
                                       int eb_relative, double eb_param, uint32_t nbh, LcQuantDyn *d);
-__global__ void lc_quant_a_kernel(LcQuantParams P);
+template <typename CodeT> __global__ void lc_quant_wa_kernel(LcQuantParams P, CodeT *__restrict__ codes);
+template <typename CodeT, bool REC> __global__ void lc_quant_wfix_kernel(LcQuantParams P, CodeT *__restrict__ codes);
+size_t lc_quantw_smem_bytes(int code_bytes);
+size_t lc_quantw_fix_smem_bytes();
+#define LC_WTILE (32 * LC_L)     // elements (codes) of one warp tile
+#define LC_QW_TPB 128            // threads per CTA of the warp-tile quantizer kernels
 __global__ void lc_map_scan_kernel(const OffMap *__restrict__ agg, double *__restrict__ tileD, long long ntiles,
                                    long long per, OffMap *gagg, int *gflag);
 // map scan launch: G co-resident CTAs of 1024 threads, `per` tiles per thread;
@@ -152,9 +163,6 @@ __global__ void lc_map_scan_kernel(const OffMap *__restrict__ agg, double *__res
 #define LC_MAPSCAN_SCRATCH (LC_MAPSCAN_MAXG * (sizeof(OffMap) + sizeof(int)))
 int lc_launch_map_scan(const OffMap *agg, double *tileD, long long ntiles, void *scratch, int sm_count,
                        cudaStream_t st);
-template <typename CodeT, bool REC> __global__ void lc_quant_b_kernel(LcQuantParams P, CodeT *__restrict__ codes);
-size_t lc_quant_a_smem_bytes();
-size_t lc_quant_b_smem_bytes();
 template <typename CodeT> __global__ void lc_quant_serial_kernel(LcQuantParams P, CodeT *__restrict__ codes);
 template <typename CodeT>
 __global__ void lc_hist_kernel(const CodeT *__restrict__ codes, uint64_t m, uint32_t *__restrict__ hist, uint32_t nbins);

@@ -194,6 +194,8 @@ __global__ void lc_quant_setup_kernel(const LcRangePart *__restrict__ r, const d
     const double ms = r->maxstep;
     o.use_anchors = (__dsub_rn(__dmul_rn(ms, 1.0 - 0x1p-50), __dmul_rn(eb, 1.0 + 0x1p-50)) >= o.esc_thresh) ||
                     !isfinite(ms);
+    // every chain value r satisfies |r| <= max|x| + eb (kept: |x - r| <= eb, escaped: r = x)
+    o.rmax = __dmul_rn(__dadd_rn(fmax(fabs(vmin), fabs(vmax)), eb), 1.0 + 0x1p-50);
     *d = o;
 }
 
@@ -209,88 +211,27 @@ __device__ __forceinline__ bool lc_definite_escape(double xi, double xprev, cons
     return LC_SUB(LC_MUL(d, 1.0 - 0x1p-50), LC_MUL(P.Q.eb, 1.0 + 0x1p-50)) >= P.esc_thresh;
 }
 
-// Lattice guess for the chain value at position pos given an anchor.
-__device__ __forceinline__ double lc_guess(const LcQuantParams &P, double xpos, long long pos,
-                                           long long apos, double aval)
-{
-    if (apos == pos) return aval;
-    // a guess only has to be near the chain (the offset maps carry the rest), and chunk
-    // c's end guess and chunk c+1's start guess come from identical inputs: RN(1/delta)
-    // instead of a division
-    const double k = floor(LC_ADD(LC_MUL(LC_SUB(xpos, aval), P.Q.inv), 0.5));
-    if (k == 0.0) return aval;
-    const double g = LC_ADD(aval, LC_MUL(k, P.Q.delta));
-    return isfinite(g) ? g : xpos;
-}
-
 // ---------------------------------------------------------------------------
-// Split quantizer: pass 0 (anchors, only when escapes are possible), pass A
-// (guess chains + maps + in-tile scan), map scan over tiles, pass B (exact
-// chain).  No tile ever waits for another tile.
-
-// Load one tile of x into padded smem rows; xhalo[LC_L] = x[tile start].
-// Coalesced 8-byte cp.async copies (no register staging: all 32 per thread are
-// in flight at once); the caller publishes the tile with lc_cp_async_wait()
-// + __syncthreads().  lc_prefetch_x_tile warms L2 with the tile a CTA
-// processes next while it computes the current one.
-__device__ __forceinline__ void lc_load_x_tile(const LcQuantParams &P, long long pbeg, double *xs, double *xhalo)
-{
-    const int tid = threadIdx.x;
-    const long long nel = (long long)P.n - 1;
-    // element off = k * LC_TPB + tid goes to row off / 32, column off % 32: both
-    // addresses advance by a constant per k (immediate offsets, no per-copy math)
-    double *dst = xs + (tid >> 5) * LC_ROW + (tid & 31);
-    const double *src = P.x + pbeg + 1 + tid;
-    if (pbeg + LC_TILE <= nel) {                         // full tile
-#pragma unroll
-        for (int k = 0; k < LC_L; ++k) lc_cp_async8(dst + k * (LC_TPB / 32) * LC_ROW, src + k * LC_TPB);
-    } else {
-#pragma unroll
-        for (int k = 0; k < LC_L; ++k)
-            if (pbeg + 1 + k * LC_TPB + tid <= nel) lc_cp_async8(dst + k * (LC_TPB / 32) * LC_ROW, src + k * LC_TPB);
-    }
-    lc_cp_async_commit();
-    if (tid <= LC_L) {
-        const long long pos = pbeg - LC_L + tid;
-        xhalo[tid] = pos >= 0 ? P.x[pos] : 0.0;
-    }
-}
-
-__device__ __forceinline__ void lc_prefetch_x_tile(const LcQuantParams &P, long long t_next)
-{
-    if (t_next >= P.ntiles) return;
-    const long long pbeg = (P.first_chunk + t_next * LC_TPB) * LC_L;
-    const long long nel = (long long)P.n - 1;
-    // LC_TILE doubles = 512 lines of 128 B: two per thread
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        const long long pos = pbeg + 1 + (long long)(k * LC_TPB + threadIdx.x) * 16;
-        if (pos <= nel) lc_prefetch_l2(P.x + pos);
-    }
-}
+// Anchor pre-pass (only when definite escapes are possible): the last
+// definite escape of every tile and their running max (lc_quantf_kernel reads
+// anc_in[t]).
 
 __global__ void __launch_bounds__(LC_TPB) lc_anchor_tiles_kernel(LcQuantParams P)
 {
     if (!lc_quant_dyn(P) || !P.use_anchors) return;
-    // last definite escape position of every tile (escapes certain from the data)
-    __shared__ long long wmax[LC_TPB / 32];
-    const int tid = threadIdx.x;
+    // last definite escape position of every warp tile (escapes certain from the data)
+    const int lane = threadIdx.x & 31;
     const long long nel = (long long)P.n - 1;
-    for (long long t = blockIdx.x; t < P.ntiles; t += gridDim.x) {
-        const long long pbeg = (P.first_chunk + t * LC_TPB) * LC_L;
+    const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < P.ntiles; w += nwarps) {
+        const long long pbeg = (P.first_chunk + w * 32) * LC_L;
         long long last = -1;
-        for (int k = 0; k < LC_L; ++k) {
-            const long long pos = pbeg + 1 + k * LC_TPB + tid;
+        for (int k = 0; k < 32; ++k) {
+            const long long pos = pbeg + 1 + k * 32 + lane;
             if (pos <= nel && lc_definite_escape(P.x[pos], P.x[pos - 1], P)) last = max(last, pos);
         }
         for (int o = 16; o; o >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
-        if ((tid & 31) == 0) wmax[tid >> 5] = last;
-        __syncthreads();
-        if (tid == 0) {
-            for (int w = 0; w < LC_TPB / 32; ++w) last = max(last, wmax[w]);
-            P.tile_last_esc[t] = last;
-        }
-        __syncthreads();
+        if (lane == 0) P.tile_last_esc[w] = last;
     }
 }
 
@@ -318,128 +259,6 @@ __global__ void __launch_bounds__(1024) lc_anchor_scan_kernel(const long long *_
     }
 }
 
-__global__ void __launch_bounds__(LC_TPB, 3) lc_quant_a_kernel(LcQuantParams P)
-{
-    if (!lc_quant_dyn(P)) return;
-    typedef cub::BlockScan<long long, LC_TPB> ScanLL;
-    extern __shared__ __align__(16) unsigned char lc_dyn_smem[];
-    double *xs = reinterpret_cast<double *>(lc_dyn_smem);
-    __shared__ double xhalo[LC_L + 1];
-    __shared__ typename ScanLL::TempStorage scan_tmp;
-    __shared__ OffMap warp_agg[LC_TPB / 32];
-    __shared__ LcReplayItem s_rq[LC_TPB];
-    __shared__ int s_rcnt[LC_TPB / 32];
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const long long nel = (long long)P.n - 1;
-    const long long launch_apos = P.first_chunk * LC_L;
-
-    for (long long t = blockIdx.x; t < P.ntiles; t += gridDim.x) {
-        const long long cbeg = P.first_chunk + t * LC_TPB;
-        const long long pbeg = cbeg * LC_L;
-        const long long c = cbeg + tid;
-        const long long p0 = c * LC_L;
-        const int len = (c < P.nchunks) ? (int)min((long long)LC_L, nel - p0) : 0;
-        __syncthreads();
-        lc_load_x_tile(P, pbeg, xs, xhalo);
-        lc_cp_async_wait();
-        __syncthreads();
-        lc_prefetch_x_tile(P, t + gridDim.x);
-        const double *row = xs + tid * LC_ROW;
-        const double xstart = tid == 0 ? xhalo[LC_L] : xs[(tid - 1) * LC_ROW + LC_L - 1];
-
-        // anchors
-        long long apos, apos_next;
-        if (P.use_anchors) {
-            long long last_esc = -1;
-            double xp = xstart;
-            for (int j = 0; j < len; ++j) {
-                const double xi = row[j];
-                if (lc_definite_escape(xi, xp, P)) last_esc = p0 + 1 + j;
-                xp = xi;
-            }
-            struct MaxOp { __device__ long long operator()(long long a, long long b) const { return a > b ? a : b; } };
-            long long esc_excl;
-            ScanLL(scan_tmp).ExclusiveScan(last_esc, esc_excl, -1LL, MaxOp());
-            const long long in = P.anc_in[t];
-            apos = max(in, esc_excl);
-            apos_next = max(apos, last_esc);
-        } else {
-            apos = apos_next = launch_apos;
-        }
-        // the launch anchor is x[0] itself on a fresh run (first_chunk 0)
-        const bool relaunch = P.first_chunk != 0;
-        const double aval = (relaunch && apos == launch_apos) ? P.anchor_val : P.x[apos];
-        const double aval_next = (relaunch && apos_next == launch_apos) ? P.anchor_val : P.x[apos_next];
-        const double xend = len > 0 ? row[len - 1] : xstart;
-        const double g0 = lc_guess(P, xstart, p0, apos, aval);
-        const double g1 = lc_guess(P, xend, p0 + len, apos_next, aval_next);
-
-        // guess chain with superset event flags (lc_flags_*); flagged chunks are
-        // replayed below by a compacted queue of threads
-        OffMap H;
-        bool need = false;
-        unsigned mask = 0u;
-        double r = g0, rs = g0;                      // rs: chain value before the first flagged step
-        if (len > 0) {
-            LcFlags F;
-            lc_flags_init(F, g0);
-            int anyesc = 0;
-            for (int j = 0; j < len; ++j) {
-                int esc; double inc;
-                const double rn = lc_step_guess(P.Q, row[j], r, &esc, &inc);
-                anyesc |= esc;
-                const bool f = lc_flag_test(F, r, inc, rn);
-                rs = (f && F.mask == 0u) ? r : rs;
-                F.mask |= (unsigned)f << (j & 31);
-                r = rn;
-            }
-            if (anyesc) H = lc_map_const(0.0);
-            else {
-                H = lc_map_identity(lc_ulp(g0));
-                mask = F.mask;
-                need = mask != 0u;
-            }
-        } else {
-            H = lc_map_neutral();
-        }
-        lc_tile_replay(need, mask, g0, rs, s_rq, s_rcnt, [&](const LcReplayItem &it) {
-            double *rw = xs + lc_replay_ch(it) * LC_ROW;
-            const int j0 = __ffs(it.mask) - 1, j1 = 31 - __clz(it.mask);
-            OffMap Hr = lc_map_identity(lc_replay_ulp(it));
-            double r2 = it.rs;
-            for (int j = j0; j <= j1; ++j) {
-                int esc; double inc;
-                const double rn = lc_step_guess(P.Q, rw[j], r2, &esc, &inc);
-                if (((it.mask >> j) & 1u) && inc != 0.0) lc_map_step(Hr, r2, inc, rn);
-                r2 = rn;
-            }
-            lc_map_to_words(reinterpret_cast<uint32_t *>(rw), Hr);
-        });
-        if (need) H = lc_map_from_words(reinterpret_cast<const uint32_t *>(row));
-        if (len > 0 && c + 1 < P.nchunks) lc_map_shift_out(H, LC_SUB(r, g1));
-
-        // in-tile inclusive scan of maps
-        OffMap inc_map = H;
-        lc_warp_scan_maps(inc_map);
-        if (lane == 31) warp_agg[wid] = inc_map;
-        __syncthreads();
-        lc_scan_warp_maps(warp_agg, LC_TPB / 32);
-        __syncthreads();
-        if (wid > 0) inc_map = lc_map_compose(inc_map, warp_agg[wid - 1]);
-        OffMap exc_map = lc_shfl_up_map(inc_map, 1);
-        if (lane == 0) exc_map = wid > 0 ? warp_agg[wid - 1] : lc_map_neutral();
-        if (len > 0) {
-            P.pred.kind[c] = exc_map.kind;
-            P.pred.B[c] = exc_map.B;
-            P.pred.t0[c] = exc_map.t0;
-            P.pred.t1[c] = exc_map.t1;
-            P.pred.y[c] = exc_map.y;
-            P.pred.g0[c] = g0;
-        }
-        if (tid == 0) P.tile_agg[t] = warp_agg[LC_TPB / 32 - 1];
-    }
-}
-
 // Offsets at every tile start: D_0 = 0, D_{t+1} = agg_t(D_t).  G co-resident
 // CTAs of 1024 threads (G <= SM count); thread i composes `per` consecutive tile
 // maps, a block scan gives each thread's in-group exclusive map and the group
@@ -456,11 +275,7 @@ __global__ void __launch_bounds__(1024) lc_map_scan_kernel(const OffMap *__restr
     OffMap run = lc_map_neutral();
     for (long long t = b0; t < b1; ++t) run = lc_map_compose(agg[t], run);
     OffMap inc = run;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const OffMap up = lc_shfl_up_map(inc, o);
-        if (lane >= o) inc = lc_map_compose(inc, up);
-    }
+    lc_warp_scan_maps(inc);                          // prefix sum when every map is a translation
     if (lane == 31) wsum[wid] = inc;
     __syncthreads();
     lc_scan_warp_maps(wsum, 32);
@@ -468,16 +283,32 @@ __global__ void __launch_bounds__(1024) lc_map_scan_kernel(const OffMap *__restr
     if (wid > 0) inc = lc_map_compose(inc, wsum[wid - 1]);
     OffMap exc = lc_shfl_up_map(inc, 1);
     if (lane == 0) exc = wid > 0 ? wsum[wid - 1] : lc_map_neutral();
-    if (tid == 0) {
-        gagg[g] = wsum[31];
-        __threadfence();
-        st_release(gflag + g, 1);
-        double D = 0.0;
-        for (int j = 0; j < g; ++j) {
-            while (ld_acquire(gflag + j) != 1) { }
-            D = lc_map_eval(gagg[j], D);
+    if (wid == 0) {
+        // publish this group's aggregate, then fold the aggregates of all earlier
+        // groups 32 at a time (parallel acquire loads, shuffle-tree composition)
+        if (lane == 0) {
+            gagg[g] = wsum[31];
+            __threadfence();
+            st_release(gflag + g, 1);
         }
-        s_D = D;
+        OffMap acc = lc_map_neutral();
+        for (int base = 0; base < g; base += 32) {
+            const int j = base + lane;
+            OffMap v = lc_map_neutral();
+            if (j < g) {
+                while (ld_acquire(gflag + j) != 1) { }
+                const OffMap *q = gagg + j;         // L2 reads (written by another CTA)
+                v.kind = __ldcg(&q->kind); v.v = __ldcg(&q->v); v.B = __ldcg(&q->B); v.t0 = __ldcg(&q->t0);
+                v.t1 = __ldcg(&q->t1); v.y = __ldcg(&q->y); v.og = __ldcg(&q->og);
+            }
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const OffMap other = lc_shfl_down_map(v, off);   // a later group
+                if (lane + off < 32) v = lc_map_compose(other, v);
+            }
+            acc = lc_map_compose(v, acc);
+        }
+        if (lane == 0) s_D = lc_map_eval(acc, 0.0);
     }
     __syncthreads();
     double D = lc_map_eval(exc, s_D);
@@ -503,164 +334,6 @@ int lc_launch_map_scan(const OffMap *agg, double *tileD, long long ntiles, void 
     lc_map_scan_kernel<<<(int)G, 1024, 0, st>>>(agg, tileD, ntiles, per, gagg, gflag);
     return (int)cudaGetLastError();
 }
-
-template <typename CodeT, bool REC>
-__global__ void __launch_bounds__(LC_TPB, 3) lc_quant_b_kernel(LcQuantParams P, CodeT *__restrict__ codes)
-{
-    if (!lc_quant_dyn(P)) return;
-    extern __shared__ __align__(16) unsigned char lc_dyn_smem[];
-    double *xs = reinterpret_cast<double *>(lc_dyn_smem);
-    uint32_t *hs = reinterpret_cast<uint32_t *>(xs + LC_TPB * LC_ROW);
-    __shared__ double xhalo[LC_L + 1];
-    __shared__ double starts[LC_TPB + 1];
-    const int tid = threadIdx.x;
-    const long long nel = (long long)P.n - 1;
-    const uint32_t hb = P.nbins < LC_HBINS_B ? P.nbins : LC_HBINS_B;
-    for (uint32_t i = tid; i < LC_HBINS_B; i += LC_TPB) hs[i] = 0;
-
-    for (long long t = blockIdx.x; t < P.ntiles; t += gridDim.x) {
-        const long long cbeg = P.first_chunk + t * LC_TPB;
-        const long long pbeg = cbeg * LC_L;
-        const long long c = cbeg + tid;
-        const long long p0 = c * LC_L;
-        const int len = (c < P.nchunks) ? (int)min((long long)LC_L, nel - p0) : 0;
-        __syncthreads();
-        lc_load_x_tile(P, pbeg, xs, xhalo);
-        const double Dt = P.tile_D[t];
-        double start = 0.0;
-        if (len > 0) {
-            OffMap m;
-            m.kind = P.pred.kind[c]; m.B = P.pred.B[c]; m.t0 = P.pred.t0[c]; m.t1 = P.pred.t1[c]; m.y = P.pred.y[c];
-            m.v = 0.0; m.og = 0.0;
-            start = lc_apply_offset(P.pred.g0[c], lc_map_eval(m, Dt));
-            // test hook (LC_OPT_INJECT_QUANT): a wrong prediction, so the predecessor's end check fails
-            if (c == P.inject_chunk && P.first_chunk == 0) start = lc_from_bits(lc_bits(start) ^ 1);
-        }
-        starts[tid] = start;
-        if (tid == LC_TPB - 1) {
-            const long long cn = cbeg + LC_TPB;          // first chunk of the next tile
-            starts[LC_TPB] = (cn < P.nchunks) ? lc_apply_offset(P.pred.g0[cn], P.tile_D[t + 1]) : 0.0;
-        }
-        lc_cp_async_wait();
-        __syncthreads();
-        lc_prefetch_x_tile(P, t + gridDim.x);
-        if (t + gridDim.x < P.ntiles) {                      // next tile's chunk predictions
-            const long long cn = P.first_chunk + (t + gridDim.x) * LC_TPB;
-            lc_prefetch_bytes(P.pred.kind + cn, LC_TPB * sizeof(int));
-            lc_prefetch_bytes(P.pred.B + cn, LC_TPB * sizeof(double));
-            lc_prefetch_bytes(P.pred.t0 + cn, LC_TPB * sizeof(double));
-            lc_prefetch_bytes(P.pred.t1 + cn, LC_TPB * sizeof(double));
-            lc_prefetch_bytes(P.pred.y + cn, LC_TPB * sizeof(double));
-            lc_prefetch_bytes(P.pred.g0 + cn, LC_TPB * sizeof(double));
-        }
-        const double *row = xs + tid * LC_ROW;
-        {
-            double r = start;
-            uint32_t *crow = reinterpret_cast<uint32_t *>(xs + tid * LC_ROW);
-            bool ok = true;
-            for (int j = 0; j < len; ++j) {
-                uint32_t code; int esc; double inc, pe;
-                const double rn = lc_step_nb(P.Q, row[j], r, &code, &inc, &esc, &pe, ok);
-                crow[j] = code;
-                if (REC) {
-                    P.pe[p0 + j] = pe;
-                    P.pe_rec[p0 + j] = LC_SUB(rn, r);
-                }
-                r = rn;
-            }
-            if (!ok) {                                        // a quotient was not certified: IEEE path
-                r = start;
-                for (int j = 0; j < len; ++j) {
-                    uint32_t code; int esc; double inc, pe;
-                    const double rn = lc_step(P.Q, P.x[p0 + 1 + j], r, &code, &esc, &inc, &pe);
-                    crow[j] = code;
-                    if (REC) {
-                        P.pe[p0 + j] = pe;
-                        P.pe_rec[p0 + j] = LC_SUB(rn, r);
-                    }
-                    r = rn;
-                }
-            }
-            if (len > 0 && c + 1 < P.nchunks && lc_bits(r) != lc_bits(starts[tid + 1])) {
-                P.bad_end[c] = r;
-                atomicMin(P.first_bad, (unsigned long long)(c + 1));
-            }
-        }
-        // histogram: codes 1..16 (the small |m| that dominate smooth data) in
-        // packed per-thread byte counters (a chunk adds at most 32 to a code),
-        // summed per warp with redux.sync; every other code atomically
-        if (P.count_hist) {
-            const uint32_t *crow = reinterpret_cast<const uint32_t *>(xs + tid * LC_ROW);
-            unsigned long long A = 0ull, B = 0ull;
-            for (int j = 0; j < len; ++j) {
-                const uint32_t code = crow[j];
-                const uint32_t idx = code - 1u;                   // escape (code 0) -> 2^32 - 1
-                const unsigned long long one = 1ull << ((idx & 7u) * 8u);
-                A += idx < 8u ? one : 0ull;
-                B += idx - 8u < 8u ? one : 0ull;
-                if (idx >= 16u) {
-                    if (code < hb) atomicAdd(&hs[code], 1u);
-                    else atomicAdd(&P.hist[code], 1u);
-                }
-            }
-            uint32_t w[8];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                w[k] = (uint32_t)((A >> (16 * k)) & 0xffull) | ((uint32_t)((A >> (16 * k + 8)) & 0xffull) << 16);
-                w[4 + k] = (uint32_t)((B >> (16 * k)) & 0xffull) | ((uint32_t)((B >> (16 * k + 8)) & 0xffull) << 16);
-            }
-#pragma unroll
-            for (int k = 0; k < 8; ++k) w[k] = __reduce_add_sync(0xffffffffu, w[k]);   // halves <= 1024
-            // lane L < 16 adds the warp's count of code L + 1 (one atomic per lane, in parallel)
-            const int lane = tid & 31;
-            uint32_t mine = 0;
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-                if ((lane >> 1) == k) mine = (lane & 1) ? (w[k] >> 16) : (w[k] & 0xffffu);
-            if (lane < 16 && mine) {
-                const uint32_t code = (uint32_t)lane + 1u;
-                if (code < hb) atomicAdd(&hs[code], mine);
-                else atomicAdd(&P.hist[code], mine);
-            }
-        }
-        __syncthreads();
-        // coalesced 16-byte code stores: 16 / sizeof(CodeT) consecutive codes per thread
-        {
-            constexpr int V = 16 / sizeof(CodeT);
-            const long long tile_n = min((long long)LC_TILE, nel - pbeg);
-            for (int g = tid; g * V < tile_n; g += LC_TPB) {
-                const int off = g * V;                       // first element of the group
-                const uint32_t *src = reinterpret_cast<const uint32_t *>(xs) + (off >> 5) * (2 * LC_ROW) + (off & 31);
-                if (off + V <= tile_n) {
-                    uint4 v;
-                    if (V == 8) {
-                        v.x = (src[0] & 0xffffu) | (src[1] << 16);
-                        v.y = (src[2] & 0xffffu) | (src[3] << 16);
-                        v.z = (src[4] & 0xffffu) | (src[5] << 16);
-                        v.w = (src[6] & 0xffffu) | (src[7] << 16);
-                    } else {
-                        v.x = src[0]; v.y = src[1]; v.z = src[2]; v.w = src[3];
-                    }
-                    *reinterpret_cast<uint4 *>(codes + pbeg + off) = v;
-                } else {
-                    for (int k = 0; off + k < tile_n; ++k) codes[pbeg + off + k] = (CodeT)src[k];
-                }
-            }
-        }
-    }
-    __syncthreads();
-    if (P.count_hist)
-        for (uint32_t i = tid; i < hb; i += LC_TPB)
-            if (hs[i]) atomicAdd(&P.hist[i], hs[i]);
-}
-
-size_t lc_quant_a_smem_bytes() { return sizeof(double) * LC_TPB * LC_ROW; }
-size_t lc_quant_b_smem_bytes() { return sizeof(double) * LC_TPB * LC_ROW + sizeof(uint32_t) * LC_HBINS_B; }
-
-template __global__ void lc_quant_b_kernel<uint16_t, false>(LcQuantParams, uint16_t *);
-template __global__ void lc_quant_b_kernel<uint32_t, false>(LcQuantParams, uint32_t *);
-template __global__ void lc_quant_b_kernel<uint16_t, true>(LcQuantParams, uint16_t *);
-template __global__ void lc_quant_b_kernel<uint32_t, true>(LcQuantParams, uint32_t *);
 
 // Sequential exact chain from chunk `first_chunk` (fallback for inputs whose
 // chunk predictions keep failing).  One thread; correct for every input.

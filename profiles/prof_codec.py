@@ -1,7 +1,8 @@
 """Profiling driver: one warm-up + one measured compress/decompress of the config-2 vector
-(n = 2^26) at one bound through the public API.  Used under ncu (profiles/README in DESIGN.md):
+(n = 2^26) at one bound through the public API.  Used under ncu:
 
     python profiles/prof_codec.py [eb_rel] [log2n]
+Prints the quantizer's relaunches and exactly re-run chunks of the last compress.
 """
 import os
 import sys
@@ -11,6 +12,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1805_07384_b200 as lc  # noqa: E402
+from paper_1805_07384_b200 import _native  # noqa: E402
 from bench import make_vector  # noqa: E402
 
 eb = float(sys.argv[1]) if len(sys.argv) > 1 else 1e-4
@@ -23,4 +25,6 @@ for _ in range(2):
 torch.cuda.synchronize()
 err = float((rec - xd).abs().max())
 assert err <= blk.eb_abs, (err, blk.eb_abs)
-print("ok", n, eb, blk.payload_bits, err / blk.eb_abs)
+ctx = _native.context(0)
+print("ok", n, eb, blk.payload_bits, err / blk.eb_abs, "relaunches", ctx.lib.lc_ctx_get_stat(ctx.h, 0),
+      "exact_chunks", ctx.lib.lc_ctx_get_stat(ctx.h, 4))
