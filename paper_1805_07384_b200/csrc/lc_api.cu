@@ -173,6 +173,7 @@ int lc_ctx_create(lc_ctx **out, int device, void *stream)
         for (auto &a2 : ctx->quantw_occ)
             for (int &o : a2) o = o > 0 ? o : 1;
     }
+    LC_CUDA_OK((cudaError_t)lc_decode_init_attrs());
     LC_CUDA_OK(cudaFuncSetAttribute(lc_codebook_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)lc_codebook_smem_bytes()));
     LC_CUDA_OK(cudaFuncSetAttribute(lc_encode_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -1494,7 +1494,6 @@ int lc_decompress_impl2(lc_ctx *ctx, uint64_t n, double eb_abs, double first_val
     uint32_t *sorted = (uint32_t *)((char *)btab.p + sizeof(LcDecTables));
     if (n_lengths <= LC_DEC_LEN_SMEM) {
         const size_t lsm = (n_lengths + 15) / 16 * 16;
-        LC_CUDA_OK(cudaFuncSetAttribute(lc_dec_tables_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
         lc_dec_tables_kernel<true><<<1, 1024, lsm, st>>>((const uint8_t *)blen.p, (uint32_t)n_lengths, T, sorted);
     } else {
         lc_dec_tables_kernel<false><<<1, 1024, 0, st>>>((const uint8_t *)blen.p, (uint32_t)n_lengths, T, sorted);
@@ -1569,12 +1568,6 @@ int lc_decompress_impl2(lc_ctx *ctx, uint64_t n, double eb_abs, double first_val
     DP.seg_bits = seg_bits;
     DP.nwords = words;
     const size_t ssm = lc_dec_stage_bytes(sub);
-    switch (sub) {
-    case 2: LC_CUDA_OK(cudaFuncSetAttribute(lc_dec_sync_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm)); break;
-    case 4: LC_CUDA_OK(cudaFuncSetAttribute(lc_dec_sync_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm)); break;
-    case 8: LC_CUDA_OK(cudaFuncSetAttribute(lc_dec_sync_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm)); break;
-    default: LC_CUDA_OK(cudaFuncSetAttribute(lc_dec_sync_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm)); break;
-    }
     // one resident wave: the CTAs stride over the payload ranges, so a grid
     // larger than what fits leaves its late CTAs running at partial occupancy
     int *s_occ = lc_dec_state(ctx);                 // [0..16] per-context (per-device) cache
@@ -1642,10 +1635,8 @@ int lc_decompress_impl2(lc_ctx *ctx, uint64_t n, double eb_abs, double first_val
             const size_t wsm = lc_dec_write_smem((int)cap, code_bytes, seg_bits);
             const int wgrid = (int)(nblk < (long long)(2 * lc_sm_count(ctx)) ? nblk : 2 * lc_sm_count(ctx));
             if (code_bytes == 2) {
-                LC_CUDA_OK(cudaFuncSetAttribute(lc_dec_write_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
                 lc_dec_write_kernel<uint16_t><<<wgrid, LC_DEC_TPB, wsm, st>>>(DP, segs, offs, bcodes.p, m, endpos, (int)cap);
             } else {
-                LC_CUDA_OK(cudaFuncSetAttribute(lc_dec_write_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
                 lc_dec_write_kernel<uint32_t><<<wgrid, LC_DEC_TPB, wsm, st>>>(DP, segs, offs, bcodes.p, m, endpos, (int)cap);
             }
         }
@@ -1794,16 +1785,6 @@ static int lc_reconstruct(lc_ctx *ctx, uint64_t n, double eb_abs, double first_v
         RS.pred.g0 = (double *)pp;               pp += nchunks * sizeof(double);
         RS.pred.kind = (int *)pp;
     }
-    int &attr_b = lc_dec_state(ctx)[20];            // per context, hence per device
-    if (!attr_b) {
-        LC_CUDA_OK(cudaFuncSetAttribute(lc_rec_a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)lc_rec_a_smem_bytes()));
-        LC_CUDA_OK(cudaFuncSetAttribute(lc_rec_b_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)lc_rec_b_smem_bytes()));
-        LC_CUDA_OK(cudaFuncSetAttribute(lc_rec_b_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)lc_rec_b_smem_bytes()));
-        attr_b = 1;
-    }
     LC_CUDA_OK(cudaMemsetAsync(esc_flags, 0, 8, st));
     lc_set_first_kernel<<<1, 1, 0, st>>>(dout, first_value);
     lc_count_launch(ctx, 1);
@@ -1867,4 +1848,28 @@ static int lc_reconstruct(lc_ctx *ctx, uint64_t n, double eb_abs, double first_v
     LC_CUDA_OK(cudaEventRecord(lc_ev(ctx, 1), st));
     LC_CUDA_OK(cudaStreamSynchronize(st));
     return 0;
+}
+
+// Dynamic shared-memory ceilings of the decoder kernels, set once per device
+// (lc_ctx_create) to the largest size any call can request.  Calls never
+// change them, so concurrent decodes on other host threads cannot race a
+// smaller ceiling in between another thread's set and launch.
+int lc_decode_init_attrs()
+{
+    const int wmax16 = (int)lc_dec_write_smem(4096, 2, 64 * 16), wmax32 = (int)lc_dec_write_smem(4096, 4, 64 * 16);
+    cudaError_t e = cudaSuccess;
+    auto set = [&](const void *f, size_t bytes) {
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    };
+    set((const void *)lc_dec_tables_kernel<true>, (LC_DEC_LEN_SMEM + 15) / 16 * 16);
+    set((const void *)lc_dec_sync_kernel<2>, lc_dec_stage_bytes(2));
+    set((const void *)lc_dec_sync_kernel<4>, lc_dec_stage_bytes(4));
+    set((const void *)lc_dec_sync_kernel<8>, lc_dec_stage_bytes(8));
+    set((const void *)lc_dec_sync_kernel<16>, lc_dec_stage_bytes(16));
+    set((const void *)lc_dec_write_kernel<uint16_t>, wmax16);
+    set((const void *)lc_dec_write_kernel<uint32_t>, wmax32);
+    set((const void *)lc_rec_a_kernel, lc_rec_a_smem_bytes());
+    set((const void *)lc_rec_b_kernel<2>, lc_rec_b_smem_bytes());
+    set((const void *)lc_rec_b_kernel<4>, lc_rec_b_smem_bytes());
+    return (int)e;
 }

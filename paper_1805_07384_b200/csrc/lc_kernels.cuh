@@ -152,6 +152,7 @@ __global__ void lc_quant_setup_kernel(const LcRangePart *__restrict__ r, const d
 template <typename CodeT> __global__ void lc_quant_wa_kernel(LcQuantParams P, CodeT *__restrict__ codes);
 template <typename CodeT, bool REC> __global__ void lc_quant_wfix_kernel(LcQuantParams P, CodeT *__restrict__ codes);
 size_t lc_quantw_smem_bytes(int code_bytes);
+int lc_decode_init_attrs();
 size_t lc_quantw_fix_smem_bytes();
 #define LC_WTILE (32 * LC_L)     // elements (codes) of one warp tile
 #define LC_QW_TPB 128            // threads per CTA of the warp-tile quantizer kernels
