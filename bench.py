@@ -26,8 +26,9 @@ flush is needed between steps.
   cpu_baseline  the CPU oracle port (oracle/, C restatement of the reference
             numba kernels) on this host, rank 0, N = 1
 
---impl reference times that CPU port alone (the reference is Python+numba;
-its path has no compiled artefact to build).
+--impl reference times that CPU port alone on the same three vectors, one block
+per bound, three host threads (the reference is Python+numba; its path has no
+compiled artefact to build).
 Multi-GPU (torchrun): every rank compresses its own 2^26 shard (weak
 scaling); NCCL carries only the barrier, the max-time reduction and an
 all-gather of per-rank block metadata.
@@ -155,66 +156,46 @@ def ncu_traffic():
 # --------------------------------------------------------------------------------------------
 # CPU oracle (reference arm and cpu_baseline)
 
-def cpu_oracle_sample(n, bounds, threads):
-    """compress+decompress with the CPU oracle port; returns (bytes, seconds, cores)."""
-    from oracle import oracle as orc
-    orc.lib()
-    x = make_vector(n, seed=0)
-    results = {}
-
-    def work(eb):
-        blk = orc.compress(x, "value_range_relative", eb)
-        rec = orc.decompress(blk)
-        results[eb] = (rec.size, blk["payload_bits"])
-
-    t0 = time.perf_counter()
-    if threads <= 1:
-        for eb in bounds:
-            work(eb)
-    else:
-        ts = [threading.Thread(target=work, args=(eb,)) for eb in bounds]
-        for t in ts:
-            t.start()
-        for t in ts:
-            t.join()
-    dt = time.perf_counter() - t0
-    return 8 * n * len(bounds), dt, min(threads, len(bounds)) if threads > 1 else 1
-
-
-def cpu_oracle_sharded(n, bounds, threads, x):
-    """All host cores: the vector is cut into `threads` contiguous shards, each compressed +
-    decompressed as an independent block (how a user parallelises the single-threaded
-    reference), for every bound.  Returns (bytes, seconds)."""
+def cpu_oracle_round_trips(xs, bounds, threads):
+    """compress+decompress of vector xs[i] at bounds[i] with the CPU oracle port (C
+    restatement of the reference's numba kernels), one block per bound, on up to
+    `threads` host threads (the port, like the reference, is single-threaded per
+    call; ctypes releases the GIL).  Returns (raw bytes, seconds, threads used)."""
     from concurrent.futures import ThreadPoolExecutor
     from oracle import oracle as orc
-    shards = np.array_split(x, threads)
+    orc.lib()
 
-    def work(args):
-        eb, sh = args
-        blk = orc.compress(sh, "value_range_relative", eb)
+    def work(i):
+        blk = orc.compress(xs[i], "value_range_relative", bounds[i])
         orc.decompress(blk)
 
-    jobs = [(eb, sh) for eb in bounds for sh in shards]
+    used = max(1, min(threads, len(bounds)))
     t0 = time.perf_counter()
-    with ThreadPoolExecutor(max_workers=threads) as ex:      # ctypes releases the GIL
-        list(ex.map(work, jobs))
-    return 8 * n * len(bounds), time.perf_counter() - t0
+    if used == 1:
+        for i in range(len(bounds)):
+            work(i)
+    else:
+        with ThreadPoolExecutor(max_workers=used) as ex:
+            list(ex.map(work, range(len(bounds))))
+    return sum(8 * v.size for v in xs), time.perf_counter() - t0, used
 
 
 def run_reference(args, rank):
+    """Reference arm: the reference's CPU path (the oracle C port; the reference is
+    Python+numba with no compiled artefact) on the SAME workload as the
+    B200 arm: the three config-2 vectors of 2^log2 elements (seeds 0, 1, 2), one block
+    per bound, compress+decompress, the three bounds on three host threads."""
     if rank != 0:
         return
-    from oracle import oracle as orc
-    orc.lib()
-    threads = os.cpu_count() or 1
-    n = 1 << args.ref_log2
-    x = make_vector(n, seed=0)
+    n = 1 << args.log2
+    xs = [make_vector(n, seed=i) for i in range(len(BOUNDS))]
+    threads = len(BOUNDS)
     for _ in range(args.warmup):
-        cpu_oracle_sharded(n, BOUNDS, threads, x)
+        cpu_oracle_round_trips(xs, BOUNDS, threads)
     times = []
     nbytes = 0
     for _ in range(args.steps):
-        nbytes, dt = cpu_oracle_sharded(n, BOUNDS, threads, x)
+        nbytes, dt, used = cpu_oracle_round_trips(xs, BOUNDS, threads)
         times.append(dt)
     ms = 1e3 * sum(times) / len(times)
     value = nbytes / (ms / 1e3) / 1e9
@@ -222,12 +203,11 @@ def run_reference(args, rank):
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-        "config": {"workload": WORKLOAD, "n": 1 << args.log2, "eb_rel": list(BOUNDS)},
-        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port",
-                         "sample": f"per step: compress+decompress of a 2^{args.ref_log2} slice of the "
-                                   f"config-2 generator at each of the 3 bounds, split into {threads} "
-                                   f"independent shards on {threads} threads (all host cores; the reference "
-                                   f"itself is single-threaded per call)"},
+        "config": {"workload": WORKLOAD, "n": n, "eb_rel": list(BOUNDS), "same_config": True},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": used, "kind": "port",
+                         "sample": f"per step: compress+decompress of the three config-2 vectors (n=2^{args.log2}, "
+                                   f"seeds 0-2), one block per bound, the three bounds on {used} threads (the "
+                                   f"reference is single-threaded per call)"},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -246,8 +226,11 @@ def run_b200(args, rank, world, local_rank):
     if world > 1:
         import torch.distributed as dist
     n = 1 << args.log2
-    x = make_vector(n, seed=rank)
-    xd = torch.from_numpy(x).cuda()
+    # every bound's round trip compresses its own vector (config-2 generator, seed per
+    # rank and bound): concurrent lanes share no input through L2
+    xs = [make_vector(n, seed=16 * rank + i) for i in range(len(BOUNDS))]
+    xds = [torch.from_numpy(v).cuda() for v in xs]
+    x = xs[0]
     ctx = _native.context(local_rank)
     L = ctx.lib
     out = torch.empty(n, dtype=torch.float64, device="cuda")
@@ -262,6 +245,8 @@ def run_b200(args, rank, world, local_rank):
     def rt(eb_rel, stats=None, ctx=ctx, out=out):
         # value range + device-resolved bounds + quantizer + codebook + encoder (one host
         # round trip, the path paper_1805_07384_b200.compress takes), then the decoder
+        i = BOUNDS.index(eb_rel)
+        xd = xds[i]
         res, bnd = _native.LcResult(), _native.LcBounds()
         rc = L.lc_compress_auto_f64(ctx.h, xd.data_ptr(), n, 1, 1, eb_rel, 32768, 0, ctypes.byref(res),
                                     ctypes.byref(bnd))
@@ -275,7 +260,7 @@ def run_b200(args, rank, world, local_rank):
         pay, cl, ei, ev = vp(), vp(), vp(), vp()
         L.lc_result_device(ctx.h, ctypes.byref(pay), ctypes.byref(cl), ctypes.byref(ei), ctypes.byref(ev))
         used = ctypes.c_int64()
-        rc = L.lc_decompress_f64(ctx.h, n, eb_abs, float(x[0]), cl, res.n_symbols, pay, res.payload_bytes,
+        rc = L.lc_decompress_f64(ctx.h, n, eb_abs, float(xs[i][0]), cl, res.n_symbols, pay, res.payload_bytes,
                                  res.payload_bits, ei, ev, res.n_esc, 1, out.data_ptr(), 1, ctypes.byref(used))
         assert rc == 0, (rc, ctx.error())
         if stats is not None:
@@ -365,8 +350,13 @@ def run_b200(args, rank, world, local_rank):
         bb = block_bytes(res.payload_bytes, cl, res.n_esc)
         cms = statistics.median(r["compress_ms"] for r in runs)
         dms = statistics.median(r["decompress_ms"] for r in runs)
+        pk = measured_peak()[0]
+        alg_c = 8 * n + res.payload_bytes + 16 * res.n_esc       # x read, payload + escapes written
+        alg_d = res.payload_bytes + 16 * res.n_esc + 8 * n       # payload + escapes read, x' written
         per[f"{eb:g}"] = {
             "compress_gbs": 8 * n / (cms / 1e3) / 1e9, "decompress_gbs": 8 * n / (dms / 1e3) / 1e9,
+            "compress_roofline_frac": alg_c / (cms / 1e3) / 1e9 / pk,
+            "decompress_roofline_frac": alg_d / (dms / 1e3) / 1e9 / pk,
             "compress_ms": cms, "decompress_ms": dms, "ratio": 8 * n / bb, "payload_bits": int(res.payload_bits),
             "escapes": int(res.n_esc), "max_len": int(res.max_len), "symbols": int(res.used_symbols),
             "relaunches": int(res.relaunches),
@@ -386,7 +376,7 @@ def run_b200(args, rank, world, local_rank):
     # encoder / read by the decoder); codes are an internal intermediate.
     peak, peak_src = measured_peak()
     groups = {
-        "quantizer[lc_quant_a+lc_map_scan+lc_quant_b+lc_hist16]": lambda d: d["compress_phase_ms"]["quantize"],
+        "quantizer[lc_quant_wa+lc_map_scan+lc_quant_wfix]": lambda d: d["compress_phase_ms"]["quantize"],
         "reconstruction[lc_rec_a+lc_map_scan+lc_rec_b]":
             lambda d: d["decompress_phase_ms"]["reconstruct"],
         "huffman_decode[lc_dec_tables+lc_dec_sync+lc_dec_scan+lc_dec_write]":
@@ -414,7 +404,7 @@ def run_b200(args, rank, world, local_rank):
     # and codec context via _native.bind_stream) runs its bounds' compress ->
     # decompress -> D2H, so one lane's transfers overlap another lane's kernels.
     import queue
-    xh = torch.from_numpy(x).pin_memory()
+    xhs = [torch.from_numpy(v).pin_memory() for v in xs]
     # two lanes per round trip of the step (each runs half of the steps): more transfers in
     # flight in both directions
     elanes = 2 * nstr
@@ -433,7 +423,7 @@ def run_b200(args, rank, world, local_rank):
             _native.bind_stream(local_rank, estreams[k].cuda_stream)
             for _ in range(reps):
                 for i in range(k % nstr, len(BOUNDS), nstr):
-                    blk = lc.compress(xh, cfgs[i])             # H2D x, D2H block
+                    blk = lc.compress(xhs[i], cfgs[i])         # H2D x, D2H block
                     rec = lc.decompress(blk, device="cuda")   # H2D block
                     # D2H of the reconstruction on the lane's copy stream (32 MB pieces), so it
                     # overlaps the lane's next host->device copy of x
@@ -502,14 +492,21 @@ def run_b200(args, rank, world, local_rank):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        nb, dt, cores = cpu_oracle_sample(1 << args.cpu_log2, BOUNDS, 1)
+        cx = xs if args.cpu_log2 == args.log2 else [make_vector(1 << args.cpu_log2, seed=i) for i in range(3)]
+        nb, dt, cores = cpu_oracle_round_trips(cx, BOUNDS, 1)
         cpu = {"value": nb / dt / 1e9, "unit": "GB/s", "cores": cores, "kind": "port",
-               "sample": f"oracle C port, compress+decompress of the config-2 vector at n=2^{args.cpu_log2} "
-                         f"for each of the 3 bounds, single thread ({dt:.1f} s)"}
+               "sample": f"oracle C port, compress+decompress of the step's three config-2 vectors "
+                         f"(n=2^{args.cpu_log2}), one bound each, single thread ({dt:.1f} s)"}
 
-    solver = None
-    if rank == 0 and world == 1 and not args.no_solver:
-        solver = config1_harness(lc)
+    solver = {}
+    if not args.no_solver:
+        if rank == 0 and world == 1:
+            solver["config1"] = config1_harness(lc)
+            solver["config3"] = config3_harness(lc)
+            if args.cfg4_side:
+                solver["config4"] = config4_harness(lc, args.cfg4_side)
+        if args.cfg5_side:
+            solver["config5"] = config5_harness(lc, world, rank, local_rank, args.cfg5_side)
 
     if rank == 0:
         line = {
@@ -522,7 +519,7 @@ def run_b200(args, rank, world, local_rank):
                            "note": "same step, the three round trips one after the other on one stream"},
             "clocks": clk, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "per_bound": per,
-            "config1_solver_harness": solver,
+            "solver_configs": solver,
         }
         print(json.dumps(line), flush=True)
     torch.cuda.synchronize()
@@ -535,7 +532,6 @@ def config1_harness(lc):
     poisson2d(256), b ~ U(-1,1) seed 0, x0 = 0, lossy checkpoint every 10 iterations at
     rel eb 1e-4, failure at 200 -> restart from 190, run to ||r||/||b|| < 1e-6."""
     import torch
-    from types import SimpleNamespace
     from paper_1805_07384_b200 import checkpoint as ck, harness, solvers
     a, _ = solvers.generate_poisson2d(256)
     m = solvers.jacobi_preconditioner(a)
@@ -546,8 +542,7 @@ def config1_harness(lc):
     res = harness.measure_n_prime("jacobi", a, m, b, cfg, comp, [200])
     t_np = time.perf_counter() - t0
     s = solvers.init("jacobi", a, m, b, cfg)
-    while s.iteration < 190:
-        s.step()
+    s.advance(190)
     img, cost = ck.checkpoint_lossy(s, comp, ck.StorageTarget())
     blk = lc.CompressedBlock.from_bytes(img.payload)
     torch.cuda.synchronize()
@@ -560,6 +555,136 @@ def config1_harness(lc):
             "decompress_ms": 1e3 * (time.perf_counter() - t1), "harness_seconds": t_np}
 
 
+def _golden(name):
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "config_golden.json")) as fh:
+            return json.load(fh).get(name)
+    except (OSError, ValueError):
+        return None
+
+
+def _trial_summary(res, extra=None):
+    d = {"baseline_iterations": res.baseline_n, "final_iterations": res.final_n, "n_prime": res.n_prime,
+         "recovered_from": list(res.recovered_from), "ratios": [round(r, 4) for r in res.ratios],
+         "t_compress_ms": [round(1e3 * t, 3) for t in res.t_compress],
+         "t_decompress_ms": [round(1e3 * t, 3) for t in res.t_decompress], "seconds": round(res.seconds, 3)}
+    d.update(extra or {})
+    return d
+
+
+def config3_harness(lc):
+    """BASELINE.json config 3: CG on the 3-D 7-point Laplacian 128^3, b ~ U(-1,1) seed 1,
+    tol 1e-8, lossy checkpoints every 20 iterations at rel eb 1e-5 (restart length 20:
+    r and p are rebuilt from x at every checkpoint boundary and after recovery),
+    failures at iterations 100 and 300 (harness.multi_failure_trial; the reference's
+    numbers from tests/golden/config_golden.json)."""
+    import torch
+    from paper_1805_07384_b200 import harness, solvers
+    a = solvers.generate_laplacian3d(128)
+    m = solvers.jacobi_preconditioner(a)
+    b = torch.from_numpy(np.random.default_rng(1).uniform(-1, 1, a.n_rows)).cuda()
+    cfg = solvers.SolveConfig(tolerance=1e-8, restart_len=20, ckpt_intvl=20, max_iterations=100_000)
+    t0 = time.perf_counter()
+    base = solvers.solve_to_convergence(solvers.init("cg", a, m, b, cfg))
+    torch.cuda.synchronize()
+    t_base = time.perf_counter() - t0
+    res = harness.multi_failure_trial("cg", a, m, b, cfg, lc.CompressorConfig.value_range_relative(1e-5),
+                                      [100, 300], 20, baseline_n=base.iteration)
+    g = _golden("config3") or {}
+    return _trial_summary(res, {"reference_baseline": g.get("baseline"), "reference_n_prime": g.get("n_prime"),
+                                "baseline_solve_seconds": round(t_base, 3),
+                                "ms_per_iteration": round(1e3 * t_base / max(1, base.iteration), 4)})
+
+
+def config4_harness(lc, side):
+    """BASELINE.json config 4: restarted GMRES(30) on the upwind convection-diffusion
+    stencil side^3 (256^3 = 16.8M unknowns by default), b ~ U(-1,1) seed 2, tol 1e-8,
+    checkpoint every 2 restart cycles (60 iterations), failure at the end of cycle 5
+    (iteration 150), rel eb 1e-4 and 1e-6.  (The reference takes hours per solve at
+    256^3; its numbers are pinned at 32^3 and 64^3 in tests/golden/config_golden.json.)"""
+    import torch
+    from paper_1805_07384_b200 import harness, solvers
+    a = solvers.generate_convdiff3d(side)
+    m = solvers.jacobi_preconditioner(a)
+    b = torch.from_numpy(np.random.default_rng(2).uniform(-1, 1, a.n_rows)).cuda()
+    cfg = solvers.SolveConfig(tolerance=1e-8, restart_len=30, ckpt_intvl=60, max_iterations=100_000)
+    t0 = time.perf_counter()
+    base = solvers.solve_to_convergence(solvers.init("gmres", a, m, b, cfg))
+    torch.cuda.synchronize()
+    t_base = time.perf_counter() - t0
+    out = {"grid": side, "baseline_iterations": base.iteration, "baseline_solve_seconds": round(t_base, 3),
+           "ms_per_iteration": round(1e3 * t_base / max(1, base.iteration), 4)}
+    for eb in (1e-4, 1e-6):
+        res = harness.multi_failure_trial("gmres", a, m, b, cfg, lc.CompressorConfig.value_range_relative(eb),
+                                          [150], 60, baseline_n=base.iteration)
+        out[f"{eb:g}"] = _trial_summary(res)
+    return out
+
+
+def config5_harness(lc, world, rank, local_rank, side, iters=100, k=25, eb=1e-5):
+    """BASELINE.json config 5: CG on the 3-D 7-point Laplacian side^3 (512^3 = 134M
+    unknowns, a 1 GB fp64 vector), z-slab sharded over the `world` GPUs (NCCL halo
+    exchange and partial all-gathers, solvers.SlabComm).  Every k iterations each GPU
+    compresses its own x slab at rel eb 1e-5 with the range its CG update kernel
+    produced (lc_compress_ranged_f64: no range pass) and decompresses it into HBM;
+    device times are the max over ranks.  Throughput per GPU = slab bytes / time."""
+    import torch
+    from paper_1805_07384_b200 import _native, solvers
+    comm = solvers.SlabComm() if world > 1 else None
+    a = solvers.generate_laplacian3d(side)
+    m = solvers.jacobi_preconditioner(a)
+    nl = a.n_rows // world
+    b = np.random.default_rng(3).uniform(-1, 1, a.n_rows)[rank * nl:(rank + 1) * nl]
+    cfg = solvers.SolveConfig(tolerance=1e-8, restart_len=k, ckpt_intvl=k, max_iterations=100_000)
+    s = solvers.init("cg", a, m, torch.from_numpy(b).cuda(), cfg, comm=comm)
+    ctx = _native.context(local_rank)
+    L = ctx.lib
+    out = torch.empty(nl, dtype=torch.float64, device="cuda")
+    vp = ctypes.c_void_p
+    tc, td, ratios, errs, solve_ms = [], [], [], [], []
+    while s.iteration < iters and not s.converged:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        s.advance(k)
+        torch.cuda.synchronize()
+        solve_ms.append(1e3 * (time.perf_counter() - t0) / k)
+        res, bnd = _native.LcResult(), _native.LcBounds()
+        rc = L.lc_compress_ranged_f64(ctx.h, s.x.data_ptr(), nl, 1, eb, 32768, 0, s.x_range.data_ptr(),
+                                      ctypes.byref(res), ctypes.byref(bnd))
+        assert rc == 0, (rc, ctx.error())
+        tc.append(L.lc_last_device_ms(ctx.h))
+        pay, cl, ei, ev = vp(), vp(), vp(), vp()
+        L.lc_result_device(ctx.h, ctypes.byref(pay), ctypes.byref(cl), ctypes.byref(ei), ctypes.byref(ev))
+        used = ctypes.c_int64()
+        rc = L.lc_decompress_f64(ctx.h, nl, bnd.eb_abs, bnd.first_value, cl, res.n_symbols, pay, res.payload_bytes,
+                                 res.payload_bits, ei, ev, res.n_esc, 1, out.data_ptr(), 1, ctypes.byref(used))
+        assert rc == 0, (rc, ctx.error())
+        td.append(L.lc_last_device_ms(ctx.h))
+        errs.append(float((out - s.x).abs().max()) / bnd.eb_abs)
+        cl_h = np.zeros(res.n_symbols, np.uint8)
+        L.lc_result_fetch(ctx.h, cl_h.ctypes.data, None, None, None, None, None)
+        ratios.append(8 * nl / block_bytes(res.payload_bytes, cl_h, res.n_esc))
+    tcm, tdm = statistics.median(tc), statistics.median(td)
+    if comm is not None:
+        import torch.distributed as dist
+        t = torch.tensor([tcm, tdm], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tcm, tdm = float(t[0]), float(t[1])
+    pk = measured_peak()[0]
+    cg = 8 * nl / (tcm / 1e3) / 1e9
+    dg = 8 * nl / (tdm / 1e3) / 1e9
+    return {"grid": side, "ranks": world, "slab_elements": nl, "eb_rel": eb, "checkpoints": len(tc),
+            "iterations": s.iteration, "cg_ms_per_iteration": round(statistics.median(solve_ms), 4),
+            "compress_ms": tcm, "decompress_ms": tdm,
+            "compress_gbs_per_gpu": cg, "decompress_gbs_per_gpu": dg,
+            "compress_gbs_aggregate": cg * world, "decompress_gbs_aggregate": dg * world,
+            "compress_roofline_frac": cg / pk, "decompress_roofline_frac": dg / pk,
+            "ratio": statistics.median(ratios), "max_err_over_eb": max(errs),
+            "note": "device time of lc_compress_ranged_f64 (range fused into the CG update) and "
+                    "lc_decompress_f64 per checkpoint, median over checkpoints, max over ranks; "
+                    "roofline frac = raw slab bytes / time / measured HBM peak"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -568,9 +693,10 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--log2", type=int, default=26)
     ap.add_argument("--cpu-log2", type=int, default=26)
-    ap.add_argument("--ref-log2", type=int, default=24)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-solver", action="store_true")
+    ap.add_argument("--cfg4-side", type=int, default=256, help="config-4 grid side (0: skip)")
+    ap.add_argument("--cfg5-side", type=int, default=512, help="config-5 grid side (0: skip)")
     ap.add_argument("--streams", type=int, default=3,
                     help="concurrent round trips per step (each bound on its own stream and context)")
     args = ap.parse_args()

@@ -107,6 +107,16 @@ int lc_compress_auto_f64(lc_ctx *ctx, const double *x, uint64_t n, int x_on_devi
                          int eb_relative, double eb_param, uint32_t n_bins_half,
                          int record_traces, lc_result *res, lc_bounds *bounds);
 
+/* lc_compress_auto_f64 for a device vector whose value range its producer
+ * already computed (range_dev: device LcRangePart {double vmin, vmax,
+ * maxstep; int nonfinite} -- lc_kr_fold_f64's range_out; maxstep may be any
+ * upper bound of |x_i - x_{i-1}|): the value-range pass over x is skipped, so
+ * a checkpoint of solver state reads x once (compressor.py:384-387 fused
+ * into the solver's update kernel).  Same results and statuses.          */
+int lc_compress_ranged_f64(lc_ctx *ctx, const double *x, uint64_t n, int eb_relative, double eb_param,
+                           uint32_t n_bins_half, int record_traces, const void *range_dev, lc_result *res,
+                           lc_bounds *bounds);
+
 /* Copy the last compress result to host buffers (any may be NULL):
  * code_lengths[n_symbols], payload[payload_bytes], esc_idx/esc_val[n_esc],
  * pe/pe_rec[n-1] (only when record_traces was set).                       */
@@ -237,6 +247,78 @@ int lc_dot_f64(lc_ctx *ctx, const double *a, const double *b, uint64_t n, double
 /* y += alpha x, alpha = a_scale * (*a_dev) when a_dev is set, else a         */
 int lc_axpy_f64(lc_ctx *ctx, double a, const double *a_dev, double a_scale, const double *x, double *y,
                 uint64_t n);
+
+/* ---- device-resident Krylov harness (lc_krylov.cu) -------------------------
+ * Slab of a global stencil grid: planes [z0, z0 + nzl) of st (x fastest).
+ * Vectors a stencil reads are passed as the address of their first local
+ * element; the nx*ny halo planes before and after it must hold the
+ * neighbouring ranks' planes wherever a neighbour exists.  Reductions are
+ * sums of per-chunk partials over LC_KR_CHUNK_ELEMS consecutive GLOBAL
+ * elements, folded in one fixed order (bit-identical for any slab split
+ * whose slabs start on chunk boundaries).  Scalars live in lc_kscalars on
+ * the device; once status != LC_KS_RUNNING the solver's kernels do nothing.
+ * Replaces the per-iteration work of solvers.py:92-241 and sparse.py:150-157. */
+#define LC_KR_CHUNK_ELEMS 4096
+typedef struct lc_slab {
+    lc_stencil st;         /* global grid and coefficients                  */
+    int64_t z0, nzl;       /* first global plane, local planes             */
+} lc_slab;
+
+typedef struct lc_kscalars {
+    double rho, pq, alpha, beta;
+    double rr;             /* last folded sum of squares                   */
+    double res;            /* residual norm (solvers.py _set_residual)     */
+    double tol_abs;        /* tolerance * ||b||, set by the host           */
+    double spare;
+    int64_t iteration;
+    int32_t status;        /* LC_KS_*                                       */
+    int32_t pad;
+} lc_kscalars;
+#define LC_KS_RUNNING 0
+#define LC_KS_CONVERGED 1
+#define LC_KS_BREAKDOWN 2  /* CG zero curvature or zero rho                */
+#define LC_KS_NONFINITE 3  /* residual norm not finite                     */
+/* fold ops */
+#define LC_KOP_DOT 0           /* *out = sum                               */
+#define LC_KOP_NORM 1          /* *out = sqrt(sum)                         */
+#define LC_KOP_ALPHA 2         /* CG: pq = sum, alpha = rho / pq            */
+#define LC_KOP_BETA 3          /* CG: rho' = sum0, beta = rho'/rho, res = sqrt(sum1), iteration++ */
+#define LC_KOP_REBUILD_INIT 4  /* CG: rho = sum0, res = sqrt(sum1), converged test */
+#define LC_KOP_REBUILD_STEP 5  /* CG restart inside a step: no converged test */
+#define LC_KOP_RESID 6         /* Jacobi: res = sqrt(sum) (width 2: column 1), iteration++ */
+#define LC_KOP_RESID_INIT 7    /* res = sqrt(sum) (width 2: column 1), converged test */
+
+/* y = A vh on the slab; part[c] (optional) = chunk sums of vh*y             */
+int lc_kr_spmv_f64(lc_ctx *ctx, const lc_slab *s, const double *vh, double *y, double *part,
+                   const lc_kscalars *sc);
+/* r = b - A xh; z_p (optional) = inv*r; part[2c] = sum r*z, part[2c+1] = sum r^2 */
+int lc_kr_residual_f64(lc_ctx *ctx, const lc_slab *s, const double *xh, const double *b, double *r,
+                       double inv_diag, double *z_p, double *part, const lc_kscalars *sc_gate);
+/* CG (solvers.py:139-143): x += alpha p, r -= alpha q, part = (r.z, r.r) per
+ * chunk, range_parts (optional, one LcRangePart per chunk) = range of x      */
+int lc_kr_cg_update_f64(lc_ctx *ctx, uint64_t n, const double *p, const double *q, double *x, double *r,
+                        double inv_diag, const lc_kscalars *sc, double *part, void *range_parts);
+/* CG (solvers.py:145): p = inv*r + beta p                                    */
+int lc_kr_cg_dir_f64(lc_ctx *ctx, uint64_t n, const double *r, double *p, double inv_diag, const lc_kscalars *sc);
+/* Jacobi (solvers.py:104-110): x2 = x + inv*r, r2 = b - A x2, part = r2^2    */
+int lc_kr_jacobi_f64(lc_ctx *ctx, const lc_slab *s, double inv_diag, const double *xh, const double *rh,
+                     const double *b, double *x2, double *r2, const lc_kscalars *sc, double *part,
+                     void *range_parts);
+/* part[c] = chunk sums of a*b                                               */
+int lc_kr_dot_f64(lc_ctx *ctx, uint64_t n, const double *a, const double *b, double *part, const lc_kscalars *sc);
+/* y -= (*h_dev) x   (GMRES modified Gram-Schmidt, solvers.py:217-219)      */
+int lc_kr_subh_f64(lc_ctx *ctx, uint64_t n, const double *x, double *y, const double *h_dev, const lc_kscalars *sc);
+/* y = x / (*d_dev)  (GMRES normalisation, solvers.py:184,237)               */
+int lc_kr_div_f64(lc_ctx *ctx, uint64_t n, const double *x, double *y, const double *d_dev, const lc_kscalars *sc);
+/* x = xbase + sum_{i<j} y_i basis[i*ld ..]  (GMRES, solvers.py:196)         */
+int lc_kr_combine_f64(lc_ctx *ctx, uint64_t n, int j, const double *basis, uint64_t ld, const double *y_dev,
+                      const double *xbase, double *x, void *range_parts);
+/* Fold part[nchunks][width] in the fixed order and apply op to *sc (out_dev
+ * receives the DOT/NORM value, or the residual norm for the other ops);
+ * range_parts (optional) fold into *range_out (an LcRangePart: vmin, vmax,
+ * maxstep = vmax - vmin, nonfinite) for lc_compress_ranged_f64.             */
+int lc_kr_fold_f64(lc_ctx *ctx, const double *part, int width, uint64_t nchunks, int op, lc_kscalars *sc,
+                   double *out_dev, const void *range_parts, uint64_t n_range_parts, void *range_out);
 
 #ifdef __cplusplus
 }

@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "liblossyckpt_b200.so")
-SOURCES = ["lc_api.cu", "lc_quant.cu", "lc_quantw.cu", "lc_huff.cu", "lc_decode.cu", "lc_stats.cu", "lc_solver.cu"]
+SOURCES = ["lc_api.cu", "lc_quant.cu", "lc_quantw.cu", "lc_huff.cu", "lc_decode.cu", "lc_stats.cu", "lc_solver.cu", "lc_krylov.cu"]
 HEADERS = ["lc_chain.cuh", "lc_common.cuh", "lc_kernels.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fmad=false",
               "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

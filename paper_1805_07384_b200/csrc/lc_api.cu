@@ -565,8 +565,9 @@ int lc_compress_f64(lc_ctx *ctx, const double *x, uint64_t n, int x_on_device, d
     return lc_compress_auto_f64(ctx, x, n, x_on_device, 0, eb_abs, n_bins_half, record_traces, res, &b);
 }
 
-int lc_compress_auto_f64(lc_ctx *ctx, const double *x, uint64_t n, int x_on_device, int eb_relative,
-                         double eb_param, uint32_t n_bins_half, int record_traces, lc_result *res, lc_bounds *bounds)
+static int lc_compress_auto_impl(lc_ctx *ctx, const double *x, uint64_t n, int x_on_device, int eb_relative,
+                                 double eb_param, uint32_t n_bins_half, int record_traces, lc_result *res,
+                                 lc_bounds *bounds, const LcRangePart *range_dev)
 {
     if (!ctx || !res || !bounds || n < 2 || n_bins_half < 1 || !(eb_param > 0.0) || !isfinite(eb_param)) return 12;
     if (n_bins_half > (1u << 30)) return 12;
@@ -584,10 +585,15 @@ int lc_compress_auto_f64(lc_ctx *ctx, const double *x, uint64_t n, int x_on_devi
     LcRangePart *parts = (LcRangePart *)ctx->range_parts.p;
     unsigned *done = (unsigned *)(parts + nb + 1);
     LcQuantDyn *dyn = (LcQuantDyn *)(((uintptr_t)(done + 4) + 63) & ~(uintptr_t)63);
-    LC_CUDA_OK(cudaMemsetAsync(done, 0, sizeof(unsigned), ctx->stream));
-    lc_range_kernel<<<nb, 256, 0, ctx->stream>>>(dx, n, parts, done);
-    lc_quant_setup_kernel<<<1, 32, 0, ctx->stream>>>(parts + nb, dx, n, eb_relative, eb_param, n_bins_half, dyn);
-    ctx->launches += 2;
+    if (!range_dev) {
+        LC_CUDA_OK(cudaMemsetAsync(done, 0, sizeof(unsigned), ctx->stream));
+        lc_range_kernel<<<nb, 256, 0, ctx->stream>>>(dx, n, parts, done);
+        ctx->launches += 1;
+    }
+    // the producer's fused range (lc_compress_ranged_f64) replaces the range pass
+    lc_quant_setup_kernel<<<1, 32, 0, ctx->stream>>>(range_dev ? range_dev : parts + nb, dx, n, eb_relative,
+                                                     eb_param, n_bins_half, dyn);
+    ctx->launches += 1;
     { int _rc = lc_debug_check(ctx, "lc_quant_setup_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
     ctx->rng_ptr = nullptr;
     LcQuantDyn *hdyn = (LcQuantDyn *)((char *)ctx->pinned + 512);
@@ -601,6 +607,22 @@ int lc_compress_auto_f64(lc_ctx *ctx, const double *x, uint64_t n, int x_on_devi
     bounds->nonfinite = hdyn->nonfinite;
     bounds->status = hdyn->status;
     return rc;
+}
+
+int lc_compress_auto_f64(lc_ctx *ctx, const double *x, uint64_t n, int x_on_device, int eb_relative,
+                         double eb_param, uint32_t n_bins_half, int record_traces, lc_result *res, lc_bounds *bounds)
+{
+    return lc_compress_auto_impl(ctx, x, n, x_on_device, eb_relative, eb_param, n_bins_half, record_traces, res,
+                                 bounds, nullptr);
+}
+
+int lc_compress_ranged_f64(lc_ctx *ctx, const double *x, uint64_t n, int eb_relative, double eb_param,
+                           uint32_t n_bins_half, int record_traces, const void *range_dev, lc_result *res,
+                           lc_bounds *bounds)
+{
+    if (!range_dev) return 12;
+    return lc_compress_auto_impl(ctx, x, n, 1, eb_relative, eb_param, n_bins_half, record_traces, res, bounds,
+                                 (const LcRangePart *)range_dev);
 }
 
 int lc_result_fetch(lc_ctx *ctx, uint8_t *code_lengths, uint8_t *payload, uint64_t *esc_idx, double *esc_val,

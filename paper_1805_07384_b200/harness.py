@@ -73,7 +73,8 @@ def measure_n_prime(method: str, a, m, b, solve_config: solvers.SolveConfig,
                     last_image, _ = ckpt.checkpoint_traditional(solver, store)
                 else:
                     last_image, _ = ckpt.checkpoint_lossy(solver, comp_config, store)
-            solver.step()
+            # to the next checkpoint or the failure in one host round trip
+            solver.advance(min(k - it % k, j - it))
         if last_image is not None:
             solver, _ = ckpt.recover(last_image, method, a, m, b, solve_config, rebuild=rebuild,
                                      device=solver.x.device)
@@ -86,6 +87,81 @@ def measure_n_prime(method: str, a, m, b, solve_config: solvers.SolveConfig,
                                     n_prime=solver.iteration - base_n if solver.converged else None,
                                     converged=solver.converged))
     return NPrimeResult(baseline_n=base_n, samples=tuple(samples))
+
+
+@dataclass(frozen=True)
+class TrialResult:
+    baseline_n: int
+    final_n: int
+    converged: bool
+    recovered_from: tuple
+    ratios: tuple              # compression ratio (raw bytes / block bytes) of every lossy checkpoint
+    t_compress: tuple          # seconds per lossy checkpoint (compress, host wall clock)
+    t_decompress: tuple        # seconds per recovery (decode)
+    seconds: float             # whole trial
+
+    @property
+    def n_prime(self):
+        return self.final_n - self.baseline_n if self.converged else None
+
+
+def multi_failure_trial(method, a, m, b, solve_config: solvers.SolveConfig, comp_config: Optional[CompressorConfig],
+                        failures, ckpt_intvl: Optional[int] = None, baseline_n: Optional[int] = None,
+                        comm=None) -> TrialResult:
+    """One run with several injected failures (BASELINE.json config 3: failures
+    at iterations 100 and 300).  A checkpoint is taken every k iterations
+    (not again at the iteration just recovered to); when the solver first
+    reaches a listed iteration its state is lost and rebuilt from the last
+    image (from scratch if none).  N' = final - baseline iterations.  The
+    same protocol as tests/golden/make_config_golden.py runs on the real
+    reference (simulate.measure_n_prime, simulate.py:461-508, with more than
+    one failure per run)."""
+    import time
+    k = solve_config.ckpt_intvl if ckpt_intvl is None else ckpt_intvl
+    if k < 1:
+        raise ParameterError("ckpt_intvl must be >= 1")
+    if baseline_n is None:
+        base = solvers.solve_to_convergence(solvers.init(method, a, m, b, solve_config, comm=comm))
+        if not base.converged:
+            raise ParameterError("failure-free baseline did not converge; fix the setup first")
+        baseline_n = base.iteration
+    t0 = time.perf_counter()
+    store = ckpt.StorageTarget()
+    solver = solvers.init(method, a, m, b, solve_config, comm=comm)
+    pending = sorted(int(f) for f in failures)
+    last, recovered_at = None, None
+    recs, ratios, tc, td = [], [], [], []
+
+    def rebuild(method_, a_, m_, b_, x, iteration, config):
+        return solvers.rebuild_from_solution(method_, a_, m_, b_, x, iteration, config, comm=comm)
+
+    while not solver.converged and solver.iteration < solve_config.max_iterations:
+        it = solver.iteration
+        if pending and it == pending[0]:
+            pending.pop(0)
+            if last is None:
+                solver = solvers.init(method, a, m, b, solve_config, comm=comm)
+            else:
+                solver, cost = ckpt.recover(last, method, a, m, b, solve_config, rebuild=rebuild,
+                                            device=solver.x.device)
+                td.append(cost.t_decompress)
+            recs.append(solver.iteration)
+            recovered_at = solver.iteration
+            continue
+        if it > 0 and it % k == 0 and it != recovered_at:
+            if comp_config is None:
+                last, cost = ckpt.checkpoint_traditional(solver, store)
+            else:
+                last, cost = ckpt.checkpoint_lossy(solver, comp_config, store)
+                ratios.append(solver.x.numel() * 8 / len(last.payload))
+                tc.append(cost.t_compress)
+        nxt = [it - it % k + k]
+        if pending:
+            nxt.append(pending[0])
+        solver.advance(max(1, min(nxt) - it))
+    return TrialResult(baseline_n=baseline_n, final_n=solver.iteration, converged=solver.converged,
+                       recovered_from=tuple(recs), ratios=tuple(ratios), t_compress=tuple(tc),
+                       t_decompress=tuple(td), seconds=time.perf_counter() - t0)
 
 
 # --- GPU workload for the reference's Poisson-failure trials (simulate.py:207-384) ----
@@ -159,8 +235,7 @@ class GpuSolverWorkload:
         done = 0
         cap = self.solve_config.max_iterations
         while done < n and not self.solver.converged and self.solver.iteration < cap:
-            self.solver.step()
-            done += 1
+            done += self.solver.advance(min(n - done, solvers.BATCH))
         if not self.solver.converged and self.solver.iteration >= cap:
             self.diverged = True
         return done
