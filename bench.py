@@ -653,6 +653,10 @@ def config5_harness(lc, world, rank, local_rank, side, iters=100, k=25, eb=1e-5)
                                       ctypes.byref(res), ctypes.byref(bnd))
         assert rc == 0, (rc, ctx.error())
         tc.append(L.lc_last_device_ms(ctx.h))
+        ph = (ctypes.c_double * 8)()
+        L.lc_phase_ms(ctx.h, ph, 8)
+        cph = [round(ph[i], 4) for i in range(4)]
+        relaunch = int(res.relaunches)
         pay, cl, ei, ev = vp(), vp(), vp(), vp()
         L.lc_result_device(ctx.h, ctypes.byref(pay), ctypes.byref(cl), ctypes.byref(ei), ctypes.byref(ev))
         used = ctypes.c_int64()
@@ -660,6 +664,8 @@ def config5_harness(lc, world, rank, local_rank, side, iters=100, k=25, eb=1e-5)
                                  res.payload_bits, ei, ev, res.n_esc, 1, out.data_ptr(), 1, ctypes.byref(used))
         assert rc == 0, (rc, ctx.error())
         td.append(L.lc_last_device_ms(ctx.h))
+        L.lc_phase_ms(ctx.h, ph, 8)
+        dph = [round(ph[i], 4) for i in range(4, 8)]
         errs.append(float((out - s.x).abs().max()) / bnd.eb_abs)
         cl_h = np.zeros(res.n_symbols, np.uint8)
         L.lc_result_fetch(ctx.h, cl_h.ctypes.data, None, None, None, None, None)
@@ -680,6 +686,9 @@ def config5_harness(lc, world, rank, local_rank, side, iters=100, k=25, eb=1e-5)
             "compress_gbs_aggregate": cg * world, "decompress_gbs_aggregate": dg * world,
             "compress_roofline_frac": cg / pk, "decompress_roofline_frac": dg / pk,
             "ratio": statistics.median(ratios), "max_err_over_eb": max(errs),
+            "last_compress_phase_ms": dict(zip(["setup", "quantize", "codebook", "encode"], cph)),
+            "last_decompress_phase_ms": dict(zip(["huffman_sync", "huffman_scan", "huffman_write", "reconstruct"], dph)),
+            "last_relaunches": relaunch, "symbols": int(res.used_symbols), "escapes": int(res.n_esc),
             "note": "device time of lc_compress_ranged_f64 (range fused into the CG update) and "
                     "lc_decompress_f64 per checkpoint, median over checkpoints, max over ranks; "
                     "roofline frac = raw slab bytes / time / measured HBM peak"}

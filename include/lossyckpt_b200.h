@@ -164,6 +164,9 @@ uint64_t lc_launch_count(lc_ctx *ctx);
  *   4 LC_OPT_VERIFY        1: the quantizer re-runs every chunk with the exact
  *                          reference step and checks every chunk end (no
  *                          certified skip); 0 default
+ *   5 LC_OPT_QUANT_RESUME  1 (default): a failed chunk prediction resumes the
+ *                          exact pass from the failing chunk (pass A kept, new
+ *                          offsets by a map scan); 0: relaunch the quantizer
  * lc_ctx_get_stat: 0 quantizer relaunches and 1 sequential-fallback flag of the
  * last compress, 2 / 3 the same for the last decompress, 4 chunks the last
  * compress re-ran exactly (uncertified).  Returns -1 for unknown keys.     */
@@ -295,7 +298,8 @@ int lc_kr_spmv_f64(lc_ctx *ctx, const lc_slab *s, const double *vh, double *y, d
 int lc_kr_residual_f64(lc_ctx *ctx, const lc_slab *s, const double *xh, const double *b, double *r,
                        double inv_diag, double *z_p, double *part, const lc_kscalars *sc_gate);
 /* CG (solvers.py:139-143): x += alpha p, r -= alpha q, part = (r.z, r.r) per
- * chunk, range_parts (optional, one LcRangePart per chunk) = range of x      */
+ * chunk, range_parts (optional: one 48-byte record per chunk -- vmin, vmax,
+ * max |x_k - x_{k-1}| inside the chunk, first, last, non-finite) = range of x */
 int lc_kr_cg_update_f64(lc_ctx *ctx, uint64_t n, const double *p, const double *q, double *x, double *r,
                         double inv_diag, const lc_kscalars *sc, double *part, void *range_parts);
 /* CG (solvers.py:145): p = inv*r + beta p                                    */
@@ -315,8 +319,9 @@ int lc_kr_combine_f64(lc_ctx *ctx, uint64_t n, int j, const double *basis, uint6
                       const double *xbase, double *x, void *range_parts);
 /* Fold part[nchunks][width] in the fixed order and apply op to *sc (out_dev
  * receives the DOT/NORM value, or the residual norm for the other ops);
- * range_parts (optional) fold into *range_out (an LcRangePart: vmin, vmax,
- * maxstep = vmax - vmin, nonfinite) for lc_compress_ranged_f64.             */
+ * range_parts (optional) fold into *range_out (vmin, vmax, maxstep = the
+ * largest |x_k - x_{k-1}| including the chunk boundaries, nonfinite) for
+ * lc_compress_ranged_f64 -- the same record lc_range_f64's pass produces.   */
 int lc_kr_fold_f64(lc_ctx *ctx, const double *part, int width, uint64_t nchunks, int op, lc_kscalars *sc,
                    double *out_dev, const void *range_parts, uint64_t n_range_parts, void *range_out);
 

@@ -43,7 +43,7 @@ struct lc_ctx {
     LcBuf timeline;
     int64_t timeline_tiles = 0;
     // lc_ctx_set_option knobs (tests / diagnostics)
-    long long opt[8] = {64, 64, -1, -1, 0, 0, 0, 0};
+    long long opt[8] = {64, 64, -1, -1, 0, 1, 0, 0};
     // per-context (hence per-device) launch state of the decoder (lc_decode.cu)
     int dec_state[40] = {};
     int quant_serial = 0;           // last compress finished with the sequential kernel
@@ -212,6 +212,7 @@ const char *lc_last_error(lc_ctx *ctx) { return ctx ? ctx->err.c_str() : "no con
 double lc_last_device_ms(lc_ctx *ctx)
 {
     float ms = -1.0f;
+    if (cudaEventSynchronize(ctx->ev1) != cudaSuccess) return -1.0;   // the end event may still be queued
     if (cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1) != cudaSuccess) return -1.0;
     return ms;
 }
@@ -351,6 +352,11 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     P.pe_rec = record ? (double *)ctx->pe_rec.p : nullptr;
     P.verify = ctx->opt[LC_OPT_VERIFY] ? 1 : 0;
     P.exact_count = exact_count;
+    P.resume = 0;
+    P.first_tile = 0;
+    P.resume_chunk = -1;
+    P.resume_start = nullptr;
+    P.resume_D0 = (double *)((char *)ctx->counters.p + 48);
     P.timeline = nullptr;
     if (ctx->timeline_on) {                    // LC_TIMELINE=1: per-tile globaltimer stamps (diagnostics)
         LC_CUDA_OK(lc_reserve(ctx->timeline, ntiles * 128));
@@ -367,6 +373,7 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     LcCodebookOut *hcb = (LcCodebookOut *)((char *)ctx->pinned + 64);
     unsigned long long *hexact = (unsigned long long *)((char *)ctx->pinned + 192);
     uint32_t relaunches = 0;
+    bool full = false;                                   // a full quantizer relaunch happened
     ctx->quant_serial = 0;
     P.inject_chunk = ctx->opt[LC_OPT_INJECT_QUANT];
     LC_CUDA_OK(cudaEventRecord(ctx->pev[1], st));
@@ -461,7 +468,7 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
         lc_zero_words_kernel<<<2 * ctx->sm_count, 256, 0, st>>>((uint32_t *)ctx->payload.p, cbo);
         LC_CUDA_OK(cudaMemsetAsync(ctx->encdesc.p, 0, etiles * sizeof(LcEncDesc), st));
         LC_CUDA_OK(cudaMemsetAsync(ctx->counters.p, 0, 16, st));
-        lc_encode_kernel<CodeT><<<egrid, LC_TPB, lc_encode_smem_bytes(), st>>>(E);
+        lc_encode_kernel<CodeT><<<egrid, LC_TPB + 32, lc_encode_smem_bytes(), st>>>(E);
         { int _rc = lc_debug_check(ctx, "lc_encode_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
         ctx->launches += 2;
         LC_CUDA_OK(cudaEventRecord(ctx->pev[4], st));
@@ -483,12 +490,50 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     { int _rc = readback(); if (_rc) return _rc; }
     if (dyn && hdyn->status) return hdyn->status;        // non-finite / constant / bad bound: no results
     if (*hbad != ~0ULL) {
-        // a chunk prediction failed: relaunch from the first bad chunk (anchor =
-        // the exact end of its predecessor) until every check passes
+        // a chunk prediction failed.  Resume (default): pass A's results stand, the
+        // chunks from the first bad one to the end of its warp tile are re-run from
+        // its exact start, the remaining tiles get new offsets from a map scan and
+        // go through pass B again (lc_quant_wfix_kernel modes 1 and 2; the
+        // histogram is kept exact by pass B's per-code updates).  A full relaunch
+        // from the first bad chunk (anchor = the exact end of its predecessor) is
+        // the fallback when the new offset is not representable, or when resuming
+        // is switched off (LC_OPT_QUANT_RESUME = 0).
+        double *hD0 = (double *)((char *)ctx->pinned + 200);
         for (;;) {
             const unsigned long long fb = *hbad;
             if (fb == ~0ULL) break;
             ++relaunches;
+            P.inject_chunk = -1;
+            if (ctx->opt[LC_OPT_QUANT_RESUME] && (long long)relaunches <= ctx->opt[LC_OPT_MAX_QUANT]) {
+                const long long wf = ((long long)fb - P.first_chunk) / 32;
+                const long long wcta = (P.ntiles + LC_QW_TPB / 32 - 1) / (LC_QW_TPB / 32);
+                const long long gf = (long long)occ[1] * ctx->sm_count;
+                P.resume = 1;
+                P.resume_chunk = (long long)fb;
+                P.resume_start = P.bad_end + (fb - 1);
+                LC_CUDA_OK(cudaMemsetAsync(first_bad, 0xff, 8, st));
+                if (P.pe) lc_quant_wfix_kernel<CodeT, true><<<1, 32, fsmem, st>>>(P, codes);
+                else lc_quant_wfix_kernel<CodeT, false><<<1, 32, fsmem, st>>>(P, codes);
+                ctx->launches += 1;
+                if (wf + 1 < P.ntiles) {
+                    LC_CUDA_OK((cudaError_t)lc_launch_map_scan(P.tile_agg + wf + 1, P.tile_D + wf + 1,
+                                                               P.ntiles - wf - 1, ctx->mapscan_scratch,
+                                                               ctx->sm_count, st, P.resume_D0));
+                    P.resume = 2;
+                    P.first_tile = wf + 1;
+                    if (P.pe) lc_quant_wfix_kernel<CodeT, true><<<(int)(wcta < gf ? wcta : gf), LC_QW_TPB, fsmem, st>>>(P, codes);
+                    else lc_quant_wfix_kernel<CodeT, false><<<(int)(wcta < gf ? wcta : gf), LC_QW_TPB, fsmem, st>>>(P, codes);
+                    ctx->launches += 2;
+                }
+                { int _rc = lc_debug_check(ctx, "lc_quant_wfix_kernel (resume)", __FILE__, __LINE__); if (_rc) return _rc; }
+                P.resume = 0;
+                P.first_tile = 0;
+                LC_CUDA_OK(cudaMemcpyAsync(hbad, first_bad, 8, cudaMemcpyDeviceToHost, st));
+                LC_CUDA_OK(cudaMemcpyAsync(hD0, P.resume_D0, 8, cudaMemcpyDeviceToHost, st));
+                LC_CUDA_OK(cudaStreamSynchronize(st));
+                if (*hD0 == *hD0 || *hbad != fb) continue;   // resumed (or the next failure is elsewhere)
+            }
+            full = true;
             double anchor;
             LC_CUDA_OK(cudaMemcpy(&anchor, P.bad_end + (fb - 1), sizeof(double), cudaMemcpyDeviceToHost));
             if (!isfinite(anchor)) {
@@ -511,10 +556,18 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
             LC_CUDA_OK(cudaMemcpyAsync(hbad, first_bad, 8, cudaMemcpyDeviceToHost, st));
             LC_CUDA_OK(cudaStreamSynchronize(st));
         }
+    }
+    if (relaunches) {
+        if (full) {                       // a full relaunch counted its chunks' codes again: recount
         LC_CUDA_OK(cudaMemsetAsync(P.hist, 0, nbins * sizeof(uint32_t), st));
-        lc_hist_kernel<CodeT><<<4 * ctx->sm_count, 256, 0, st>>>(codes, m, P.hist, nbins);
+        if (sizeof(CodeT) == 2)      // streaming pass with packed per-thread counters for codes 1..16
+            lc_hist16_kernel<<<4 * ctx->sm_count, 256, 0, st>>>(reinterpret_cast<const uint16_t *>(codes), m, P.hist,
+                                                               nbins, nullptr);
+        else
+            lc_hist_kernel<CodeT><<<4 * ctx->sm_count, 256, 0, st>>>(codes, m, P.hist, nbins);
         { int _rc = lc_debug_check(ctx, "lc_hist_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
         ctx->launches += 1;
+        }
         { int _rc = codebook_launch(); if (_rc) return _rc; }
         { int _rc = encode_launch(); if (_rc) return _rc; }
         { int _rc = readback(); if (_rc) return _rc; }

@@ -388,6 +388,7 @@ __device__ __forceinline__ void lc_put_word(uint32_t *payload, uint64_t w, uint3
 // only the tile's first and last words with the neighbouring tiles (the
 // payload is zeroed first).  huffman.encode (huffman.py:52-72) packs MSB-first.
 #define LC_ENC_WBUF 4096                 // tile buffer words (16 bits per symbol on average)
+#define LC_ENC_NT (LC_TPB + 32)          // 8 packing warps + 1 look-back warp
 
 template <typename CodeT>
 struct LcCodeRegs {
@@ -401,10 +402,10 @@ struct LcCodeRegs {
 };
 
 template <typename CodeT>
-__global__ void __launch_bounds__(LC_TPB) lc_encode_kernel(LcEncParams P)
+__global__ void __launch_bounds__(LC_ENC_NT) lc_encode_kernel(LcEncParams P)
 {
     if (P.dyn && P.dyn->skip) return;
-    typedef cub::BlockScan<unsigned long long, LC_TPB> ScanU;
+    typedef cub::BlockScan<unsigned long long, LC_ENC_NT> ScanU;
     extern __shared__ __align__(16) unsigned char lc_dyn_smem[];
     unsigned long long *tpk = reinterpret_cast<unsigned long long *>(lc_dyn_smem);   // (len << 32) | code
     uint32_t *wbuf = reinterpret_cast<uint32_t *>(tpk + LC_ENC_TAB);
@@ -415,7 +416,7 @@ __global__ void __launch_bounds__(LC_TPB) lc_encode_kernel(LcEncParams P)
     const CodeT *codes = reinterpret_cast<const CodeT *>(P.codes);
     const bool fast = P.cb->max_len <= 32;
     const uint32_t tab = P.nbins < LC_ENC_TAB ? P.nbins : LC_ENC_TAB;
-    for (uint32_t s = tid; s < tab; s += LC_TPB)
+    for (uint32_t s = tid; s < tab; s += LC_ENC_NT)
         tpk[s] = ((unsigned long long)P.lengths[s] << 32) | (fast ? (uint32_t)P.cw[s] : 0u);
     auto entry = [&](uint32_t s) -> unsigned long long {
         return s < LC_ENC_TAB ? tpk[s] : (((unsigned long long)P.lengths[s] << 32) | (uint32_t)P.cw[s]);
@@ -428,7 +429,8 @@ __global__ void __launch_bounds__(LC_TPB) lc_encode_kernel(LcEncParams P)
         const long long t = sh_tile;
         if (t >= (long long)P.ntiles) break;
         const long long p0 = t * (long long)LC_TILE + (long long)tid * LC_L;
-        const int len = (int)max(0LL, min((long long)LC_L, (long long)P.m - p0));
+        // warps 0..7 pack 32 symbols per thread; warp 8 only runs the look-back
+        const int len = tid < LC_TPB ? (int)max(0LL, min((long long)LC_L, (long long)P.m - p0)) : 0;
         LcCodeRegs<CodeT> C;
         if (len == LC_L) {
             const uint4 *src = reinterpret_cast<const uint4 *>(codes + p0);
@@ -504,7 +506,7 @@ __global__ void __launch_bounds__(LC_TPB) lc_encode_kernel(LcEncParams P)
                         return st == 2 ? make_ulonglong2(__ldcg(&P.desc[k].incl_bits), __ldcg(&P.desc[k].incl_esc))
                                        : make_ulonglong2(__ldcg(&P.desc[k].agg_bits), __ldcg(&P.desc[k].agg_esc));
                     });
-            if (tid == 0) {
+            if (tid == LC_TPB) {
                 __stcg(&d->incl_bits, in.x + abits);
                 __stcg(&d->incl_esc, in.y + aesc);
                 st_release(&d->st, 2);
@@ -512,9 +514,9 @@ __global__ void __launch_bounds__(LC_TPB) lc_encode_kernel(LcEncParams P)
             }
         };
         if (fast_tile) {
-            for (unsigned i = tid; i <= nwt0; i += LC_TPB) wbuf[i] = 0;
+            for (unsigned i = tid; i <= nwt0; i += LC_ENC_NT) wbuf[i] = 0;
             __syncthreads();
-            if (tid < 32) lookback();
+            if (tid >= LC_TPB) lookback();
             if (bits) {
                 const unsigned lb = (unsigned)(ex & 0xffffffffull);            // bit in the tile buffer
                 const unsigned wfirst = lb >> 5, wlast = (unsigned)((lb + bits - 1) >> 5);
@@ -545,7 +547,7 @@ __global__ void __launch_bounds__(LC_TPB) lc_encode_kernel(LcEncParams P)
             }
             __syncthreads();
         } else {
-            if (tid < 32) lookback();
+            if (tid >= LC_TPB) lookback();
             __syncthreads();
         }
         const unsigned long long B0 = sh_in_bits;
@@ -571,7 +573,7 @@ __global__ void __launch_bounds__(LC_TPB) lc_encode_kernel(LcEncParams P)
             const unsigned sft = (unsigned)(B0 & 31);
             const unsigned nout = (unsigned)((sft + abits + 31) >> 5);
             const unsigned long long gw0 = B0 >> 5;
-            for (unsigned i = tid; i < nout; i += LC_TPB) {
+            for (unsigned i = tid; i < nout; i += LC_ENC_NT) {
                 const uint32_t cur = i < nwt0 ? wbuf[i] : 0u;
                 const uint32_t prev = (i > 0 && sft) ? wbuf[i - 1] : 0u;
                 const uint32_t word = sft ? ((cur >> sft) | (prev << (32 - sft))) : cur;

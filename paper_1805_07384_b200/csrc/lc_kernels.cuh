@@ -15,6 +15,7 @@ int lc_ctx_device(lc_ctx *ctx);
 #define LC_OPT_INJECT_QUANT 2   // test hook: chunk whose predicted start is perturbed (-1 off)
 #define LC_OPT_INJECT_REC 3     // test hook: the same in the decoder
 #define LC_OPT_VERIFY 4         // 1: quantizer re-runs every chunk exactly (no certified skip)
+#define LC_OPT_QUANT_RESUME 5   // 1 (default): a failed prediction resumes pass B; 0: full relaunch
 // lc_ctx_get_stat keys
 #define LC_STAT_QUANT_RELAUNCHES 0
 #define LC_STAT_QUANT_SERIAL 1
@@ -91,6 +92,12 @@ struct LcQuantParams {
     double rmax;                 // bound on |chain values| (from dyn)
     int verify;                  // 1: every chunk re-run exactly (no certified skip)
     unsigned long long *exact_count;   // chunks re-run exactly (diagnostic)
+    // resume after a failed prediction without re-running pass A (lc_quant_wfix_kernel):
+    int resume;                  // 0 first pass; 1 resume tile only; 2 the tiles after it
+    int64_t first_tile;          // mode 2: first warp tile to process
+    long long resume_chunk;      // first chunk whose predicted start was wrong
+    const double *resume_start;  // its exact start (bad_end of its predecessor)
+    double *resume_D0;           // mode 1 output: offset at the next tile start (NaN: resume impossible)
 };
 
 // v2 blocks: a bit offset for every LC_SYNC_K-th symbol (a multiple of LC_L)
@@ -157,13 +164,13 @@ size_t lc_quantw_fix_smem_bytes();
 #define LC_WTILE (32 * LC_L)     // elements (codes) of one warp tile
 #define LC_QW_TPB 128            // threads per CTA of the warp-tile quantizer kernels
 __global__ void lc_map_scan_kernel(const OffMap *__restrict__ agg, double *__restrict__ tileD, long long ntiles,
-                                   long long per, OffMap *gagg, int *gflag);
+                                   long long per, OffMap *gagg, int *gflag, const double *D0p);
 // map scan launch: G co-resident CTAs of 1024 threads, `per` tiles per thread;
 // scratch = LC_MAPSCAN_SCRATCH bytes (group aggregates + flags)
 #define LC_MAPSCAN_MAXG 1024
 #define LC_MAPSCAN_SCRATCH (LC_MAPSCAN_MAXG * (sizeof(OffMap) + sizeof(int)))
 int lc_launch_map_scan(const OffMap *agg, double *tileD, long long ntiles, void *scratch, int sm_count,
-                       cudaStream_t st);
+                       cudaStream_t st, const double *D0p = nullptr);
 template <typename CodeT> __global__ void lc_quant_serial_kernel(LcQuantParams P, CodeT *__restrict__ codes);
 template <typename CodeT>
 __global__ void lc_hist_kernel(const CodeT *__restrict__ codes, uint64_t m, uint32_t *__restrict__ hist, uint32_t nbins);

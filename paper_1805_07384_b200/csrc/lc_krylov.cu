@@ -98,23 +98,61 @@ __device__ __forceinline__ void lc_kr_cta_sum(double (&v)[W], double *sw)
 
 __device__ __forceinline__ bool lc_kr_stopped(const lc_kscalars *sc) { return sc && *(volatile const int *)&sc->status; }
 
-// Range partial of one chunk (min, max, non-finite flag) into rp[c].
-__device__ __forceinline__ void lc_kr_range_chunk(double mn, double mx, int nf, LcRangePart *rp, long long c)
+// Per-chunk range partial of the iterate: min, max, non-finite flag, the
+// largest |x_k - x_{k-1}| inside the chunk and the chunk's first and last
+// values (the step across a chunk boundary is folded by lc_kr_fold_kernel).
+// The compressor's value-range record (lc_compress_ranged_f64) needs all of
+// them: vmin/vmax/non-finite for the bounds and maxstep for the test that
+// rules out definite escapes (no anchor pass, compressor.py:384-387).
+struct LcKrRange {
+    double vmin, vmax, maxstep, first, last;
+    int nonfinite, pad;
+};
+
+// xv[j] = new value of element base + tid + 256 j (valid when < n).  All
+// threads of the CTA call it.
+__device__ __forceinline__ void lc_kr_range_chunk(const double (&xv)[LC_KR_EPT], long long base, long long n,
+                                                  LcKrRange *rp, long long c)
 {
-    __shared__ double smn[LC_KR_TPB / 32], smx[LC_KR_TPB / 32];
+    __shared__ double s_l31[LC_KR_TPB / 32][LC_KR_EPT];          // lane-31 value of each warp, per j
+    __shared__ double smn[LC_KR_TPB / 32], smx[LC_KR_TPB / 32], sms[LC_KR_TPB / 32];
     __shared__ int snf[LC_KR_TPB / 32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    __syncthreads();                                              // smem reuse across chunks
+    if (lane == 31)
+#pragma unroll
+        for (int j = 0; j < LC_KR_EPT; ++j) s_l31[wid][j] = xv[j];
+    __syncthreads();
+    double mn = INFINITY, mx = -INFINITY, ms = 0.0;
+    int nf = 0;
+#pragma unroll
+    for (int j = 0; j < LC_KR_EPT; ++j) {
+        const double up = __shfl_up_sync(0xffffffffu, xv[j], 1);
+        const long long k = base + tid + (long long)j * LC_KR_TPB;
+        if (k < n) {
+            const double v = xv[j];
+            mn = fmin(mn, v); mx = fmax(mx, v); nf |= !isfinite(v);
+            if (k > base) {
+                const double prev = lane > 0 ? up : (wid > 0 ? s_l31[wid - 1][j] : s_l31[LC_KR_TPB / 32 - 1][j - 1]);
+                ms = fmax(ms, fabs(__dsub_rn(v, prev)));
+            }
+            if (k == base) rp[c].first = v;
+            if (k == min(base + LC_KR_CHUNK, n) - 1) rp[c].last = v;
+        }
+    }
     for (int o = 16; o; o >>= 1) {
         mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
         mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        ms = fmax(ms, __shfl_xor_sync(0xffffffffu, ms, o));
         nf |= __shfl_xor_sync(0xffffffffu, nf, o);
     }
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) { smn[wid] = mn; smx[wid] = mx; sms[wid] = ms; snf[wid] = nf; }
     __syncthreads();
-    if (lane == 0) { smn[wid] = mn; smx[wid] = mx; snf[wid] = nf; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int i = 1; i < LC_KR_TPB / 32; ++i) { mn = fmin(mn, smn[i]); mx = fmax(mx, smx[i]); nf |= snf[i]; }
-        rp[c].vmin = mn; rp[c].vmax = mx; rp[c].maxstep = 0.0; rp[c].nonfinite = nf;
+    if (tid == 0) {
+        for (int i = 1; i < LC_KR_TPB / 32; ++i) {
+            mn = fmin(mn, smn[i]); mx = fmax(mx, smx[i]); ms = fmax(ms, sms[i]); nf |= snf[i];
+        }
+        rp[c].vmin = mn; rp[c].vmax = mx; rp[c].maxstep = ms; rp[c].nonfinite = nf;
     }
 }
 
@@ -188,7 +226,7 @@ __global__ void __launch_bounds__(LC_KR_TPB) lc_kr_cg_update_kernel(long long n,
                                                                    const double *__restrict__ q,
                                                                    double *__restrict__ x, double *__restrict__ r,
                                                                    double inv, const lc_kscalars *sc,
-                                                                   double *__restrict__ part, LcRangePart *rp)
+                                                                   double *__restrict__ part, LcKrRange *rp)
 {
     if (lc_kr_stopped(sc)) return;
     __shared__ double sw[16];
@@ -196,25 +234,24 @@ __global__ void __launch_bounds__(LC_KR_TPB) lc_kr_cg_update_kernel(long long n,
     const long long nch = (n + LC_KR_CHUNK - 1) / LC_KR_CHUNK;
     for (long long c = blockIdx.x; c < nch; c += gridDim.x) {
         double s[2] = {0.0, 0.0};
-        double mn = INFINITY, mx = -INFINITY;
-        int nf = 0;
+        double xv[LC_KR_EPT];
         const long long base = c * LC_KR_CHUNK + threadIdx.x;
-#pragma unroll 4
+#pragma unroll
         for (int j = 0; j < LC_KR_EPT; ++j) {
             const long long k = base + (long long)j * LC_KR_TPB;
+            xv[j] = 0.0;
             if (k < n) {
-                const double xv = __dadd_rn(x[k], __dmul_rn(alpha, p[k]));
-                x[k] = xv;
+                xv[j] = __dadd_rn(x[k], __dmul_rn(alpha, p[k]));
+                x[k] = xv[j];
                 const double rv = __dsub_rn(r[k], __dmul_rn(alpha, q[k]));
                 r[k] = rv;
                 s[0] = __dadd_rn(s[0], __dmul_rn(rv, __dmul_rn(inv, rv)));
                 s[1] = __dadd_rn(s[1], __dmul_rn(rv, rv));
-                mn = fmin(mn, xv); mx = fmax(mx, xv); nf |= !isfinite(xv);
             }
         }
         lc_kr_cta_sum<2>(s, sw);
         if (threadIdx.x == 0) { part[2 * c] = s[0]; part[2 * c + 1] = s[1]; }
-        if (rp) lc_kr_range_chunk(mn, mx, nf, rp, c);
+        if (rp) lc_kr_range_chunk(xv, c * LC_KR_CHUNK, n, rp, c);
     }
 }
 
@@ -238,7 +275,7 @@ __global__ void __launch_bounds__(LC_KR_TPB) lc_kr_jacobi_kernel(LcSlabDev S, do
                                                                 const double *__restrict__ b,
                                                                 double *__restrict__ x2, double *__restrict__ r2,
                                                                 const lc_kscalars *sc, double *__restrict__ part,
-                                                                LcRangePart *rp)
+                                                                LcKrRange *rp)
 {
     if (lc_kr_stopped(sc)) {                            // stopped: carry the state over (the host swaps buffers)
         for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < S.n; k += (long long)gridDim.x * blockDim.x) {
@@ -251,12 +288,12 @@ __global__ void __launch_bounds__(LC_KR_TPB) lc_kr_jacobi_kernel(LcSlabDev S, do
     const long long nch = (S.n + LC_KR_CHUNK - 1) / LC_KR_CHUNK;
     for (long long c = blockIdx.x; c < nch; c += gridDim.x) {
         double s[1] = {0.0};
-        double mn = INFINITY, mx = -INFINITY;
-        int nf = 0;
+        double xv[LC_KR_EPT];
         const long long base = c * LC_KR_CHUNK + threadIdx.x;
-#pragma unroll 2
+#pragma unroll
         for (int j = 0; j < LC_KR_EPT; ++j) {
             const long long k = base + (long long)j * LC_KR_TPB;
+            xv[j] = 0.0;
             if (k < S.n) {
                 auto xn = [&](long long q) { return __dadd_rn(xh[q], __dmul_rn(inv, rh[q])); };
                 const long long lz = k / S.plane, rem = k - lz * S.plane, iy = rem / S.nx, ix = rem - iy * S.nx;
@@ -274,12 +311,12 @@ __global__ void __launch_bounds__(LC_KR_TPB) lc_kr_jacobi_kernel(LcSlabDev S, do
                 x2[k] = xk;
                 r2[k] = v;
                 s[0] = __dadd_rn(s[0], __dmul_rn(v, v));
-                mn = fmin(mn, xk); mx = fmax(mx, xk); nf |= !isfinite(xk);
+                xv[j] = xk;
             }
         }
         lc_kr_cta_sum<1>(s, sw);
         if (threadIdx.x == 0) part[c] = s[0];
-        if (rp) lc_kr_range_chunk(mn, mx, nf, rp, c);
+        if (rp) lc_kr_range_chunk(xv, c * LC_KR_CHUNK, S.n, rp, c);
     }
 }
 
@@ -331,24 +368,24 @@ __global__ void __launch_bounds__(LC_KR_TPB) lc_kr_div_kernel(long long n, const
 __global__ void __launch_bounds__(LC_KR_TPB) lc_kr_combine_kernel(long long n, int j, const double *__restrict__ basis,
                                                                  long long ld, const double *__restrict__ yv,
                                                                  const double *__restrict__ xbase,
-                                                                 double *__restrict__ x, LcRangePart *rp)
+                                                                 double *__restrict__ x, LcKrRange *rp)
 {
     const long long nch = (n + LC_KR_CHUNK - 1) / LC_KR_CHUNK;
     for (long long c = blockIdx.x; c < nch; c += gridDim.x) {
-        double mn = INFINITY, mx = -INFINITY;
-        int nf = 0;
+        double xv[LC_KR_EPT];
         const long long base = c * LC_KR_CHUNK + threadIdx.x;
+#pragma unroll
         for (int jj = 0; jj < LC_KR_EPT; ++jj) {
             const long long k = base + (long long)jj * LC_KR_TPB;
+            xv[jj] = 0.0;
             if (k < n) {
                 double t = j > 0 ? __dmul_rn(yv[0], basis[k]) : 0.0;
                 for (int i = 1; i < j; ++i) t = __dadd_rn(t, __dmul_rn(yv[i], basis[(long long)i * ld + k]));
-                const double xv = j > 0 ? __dadd_rn(xbase[k], t) : xbase[k];
-                x[k] = xv;
-                mn = fmin(mn, xv); mx = fmax(mx, xv); nf |= !isfinite(xv);
+                xv[jj] = j > 0 ? __dadd_rn(xbase[k], t) : xbase[k];
+                x[k] = xv[jj];
             }
         }
-        if (rp) lc_kr_range_chunk(mn, mx, nf, rp, c);
+        if (rp) lc_kr_range_chunk(xv, c * LC_KR_CHUNK, n, rp, c);
     }
 }
 
@@ -366,7 +403,7 @@ __device__ __forceinline__ void lc_kr_set_residual(lc_kscalars *sc, double v, bo
 __global__ void __launch_bounds__(LC_KR_FOLD_TPB) lc_kr_fold_kernel(const double *__restrict__ part, int W,
                                                                    long long nch, int op, lc_kscalars *sc,
                                                                    double *__restrict__ out,
-                                                                   const LcRangePart *__restrict__ rp, long long nrp,
+                                                                   const LcKrRange *__restrict__ rp, long long nrp,
                                                                    LcRangePart *rout)
 {
     __shared__ double sw[2][32];
@@ -389,11 +426,13 @@ __global__ void __launch_bounds__(LC_KR_FOLD_TPB) lc_kr_fold_kernel(const double
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     if (lane == 0) { sw[0][wid] = s0; sw[1][wid] = s1; }
     // range of the iterate (order-free: min/max)
-    double mn = INFINITY, mx = -INFINITY;
+    double mn = INFINITY, mx = -INFINITY, ms = 0.0;
     int nf = 0;
     if (rp)
         for (long long c = threadIdx.x; c < nrp; c += LC_KR_FOLD_TPB) {
             mn = fmin(mn, rp[c].vmin); mx = fmax(mx, rp[c].vmax); nf |= rp[c].nonfinite;
+            ms = fmax(ms, rp[c].maxstep);
+            if (c > 0) ms = fmax(ms, fabs(__dsub_rn(rp[c].first, rp[c - 1].last)));   // across the boundary
         }
     __syncthreads();
     if (wid == 0) {
@@ -405,19 +444,22 @@ __global__ void __launch_bounds__(LC_KR_FOLD_TPB) lc_kr_fold_kernel(const double
         }
     }
     if (rp) {
-        __shared__ double smn[32], smx[32];
+        __shared__ double smn[32], smx[32], sms[32];
         __shared__ int snf[32];
         for (int o = 16; o; o >>= 1) {
             mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
             mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            ms = fmax(ms, __shfl_xor_sync(0xffffffffu, ms, o));
             nf |= __shfl_xor_sync(0xffffffffu, nf, o);
         }
-        if (lane == 0) { smn[wid] = mn; smx[wid] = mx; snf[wid] = nf; }
+        if (lane == 0) { smn[wid] = mn; smx[wid] = mx; sms[wid] = ms; snf[wid] = nf; }
         __syncthreads();
         if (threadIdx.x == 0) {
-            for (int i = 1; i < LC_KR_FOLD_TPB / 32; ++i) { mn = fmin(mn, smn[i]); mx = fmax(mx, smx[i]); nf |= snf[i]; }
+            for (int i = 1; i < LC_KR_FOLD_TPB / 32; ++i) {
+                mn = fmin(mn, smn[i]); mx = fmax(mx, smx[i]); ms = fmax(ms, sms[i]); nf |= snf[i];
+            }
             rout->vmin = mn; rout->vmax = mx; rout->nonfinite = nf;
-            rout->maxstep = nf ? INFINITY : __dsub_rn(mx, mn);
+            rout->maxstep = nf ? INFINITY : ms;
         }
     }
     if (threadIdx.x != 0) return;
@@ -534,7 +576,7 @@ int lc_kr_cg_update_f64(lc_ctx *ctx, uint64_t n, const double *p, const double *
     if (!ctx || !sc || !part) return 12;
     LcDeviceGuard guard(lc_ctx_device(ctx));
     lc_kr_cg_update_kernel<<<lc_kr_grid_chunks(ctx, (long long)n), LC_KR_TPB, 0, lc_stream(ctx)>>>(
-        (long long)n, p, q, x, r, inv_diag, sc, part, (LcRangePart *)range_parts);
+        (long long)n, p, q, x, r, inv_diag, sc, part, (LcKrRange *)range_parts);
     return lc_kr_done(ctx);
 }
 
@@ -555,7 +597,7 @@ int lc_kr_jacobi_f64(lc_ctx *ctx, const lc_slab *s, double inv_diag, const doubl
     LcDeviceGuard guard(lc_ctx_device(ctx));
     const LcSlabDev S = lc_slab_dev(s);
     lc_kr_jacobi_kernel<<<lc_kr_grid_chunks(ctx, S.n), LC_KR_TPB, 0, lc_stream(ctx)>>>(
-        S, inv_diag, xh, rh, b, x2, r2, sc, part, (LcRangePart *)range_parts);
+        S, inv_diag, xh, rh, b, x2, r2, sc, part, (LcKrRange *)range_parts);
     return lc_kr_done(ctx);
 }
 
@@ -592,7 +634,7 @@ int lc_kr_combine_f64(lc_ctx *ctx, uint64_t n, int j, const double *basis, uint6
     if (!ctx || j < 0 || (j > 0 && (!basis || !y_dev))) return 12;
     LcDeviceGuard guard(lc_ctx_device(ctx));
     lc_kr_combine_kernel<<<lc_kr_grid_chunks(ctx, (long long)n), LC_KR_TPB, 0, lc_stream(ctx)>>>(
-        (long long)n, j, basis, (long long)ld, y_dev, xbase, x, (LcRangePart *)range_parts);
+        (long long)n, j, basis, (long long)ld, y_dev, xbase, x, (LcKrRange *)range_parts);
     return lc_kr_done(ctx);
 }
 
@@ -604,7 +646,7 @@ int lc_kr_fold_f64(lc_ctx *ctx, const double *part, int width, uint64_t nchunks,
     if ((op == LC_KOP_DOT || op == LC_KOP_NORM) && !out_dev) return 12;
     LcDeviceGuard guard(lc_ctx_device(ctx));
     lc_kr_fold_kernel<<<1, LC_KR_FOLD_TPB, 0, lc_stream(ctx)>>>(part, width, (long long)nchunks, op, sc, out_dev,
-                                                               (const LcRangePart *)range_parts,
+                                                               (const LcKrRange *)range_parts,
                                                                (long long)n_range_parts, (LcRangePart *)range_out);
     return lc_kr_done(ctx);
 }

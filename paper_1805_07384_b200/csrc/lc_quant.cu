@@ -265,9 +265,14 @@ __global__ void __launch_bounds__(1024) lc_anchor_scan_kernel(const long long *_
 // aggregate, which is published (release flag).  Thread 0 folds the aggregates
 // of all earlier groups (acquire; they never wait on later groups) into the
 // offset at the group start; every thread then evaluates its tiles.
+// D0p (optional): the offset at the first tile's start (resume after a failed
+// prediction); 0 at a launch anchor.  A NaN offset means no resume: exit.
 __global__ void __launch_bounds__(1024) lc_map_scan_kernel(const OffMap *__restrict__ agg, double *__restrict__ tileD,
-                                                          long long ntiles, long long per, OffMap *gagg, int *gflag)
+                                                          long long ntiles, long long per, OffMap *gagg, int *gflag,
+                                                          const double *D0p)
 {
+    const double D0 = D0p ? *D0p : 0.0;
+    if (D0 != D0) return;
     __shared__ OffMap wsum[32];
     __shared__ double s_D;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, g = blockIdx.x;
@@ -308,7 +313,7 @@ __global__ void __launch_bounds__(1024) lc_map_scan_kernel(const OffMap *__restr
             }
             acc = lc_map_compose(v, acc);
         }
-        if (lane == 0) s_D = lc_map_eval(acc, 0.0);
+        if (lane == 0) s_D = lc_map_eval(acc, D0);
     }
     __syncthreads();
     double D = lc_map_eval(exc, s_D);
@@ -320,8 +325,9 @@ __global__ void __launch_bounds__(1024) lc_map_scan_kernel(const OffMap *__restr
 }
 
 int lc_launch_map_scan(const OffMap *agg, double *tileD, long long ntiles, void *scratch, int sm_count,
-                       cudaStream_t st)
+                       cudaStream_t st, const double *D0p)
 {
+    if (ntiles <= 0) return 0;
     long long G = (ntiles + 1023) / 1024;
     if (G > sm_count) G = sm_count;
     if (G > LC_MAPSCAN_MAXG) G = LC_MAPSCAN_MAXG;
@@ -331,7 +337,7 @@ int lc_launch_map_scan(const OffMap *agg, double *tileD, long long ntiles, void 
     int *gflag = (int *)(gagg + LC_MAPSCAN_MAXG);
     cudaError_t e = cudaMemsetAsync(gflag, 0, G * sizeof(int), st);
     if (e != cudaSuccess) return (int)e;
-    lc_map_scan_kernel<<<(int)G, 1024, 0, st>>>(agg, tileD, ntiles, per, gagg, gflag);
+    lc_map_scan_kernel<<<(int)G, 1024, 0, st>>>(agg, tileD, ntiles, per, gagg, gflag, D0p);
     return (int)cudaGetLastError();
 }
 

@@ -360,6 +360,57 @@ __global__ void __launch_bounds__(LC_QW_TPB, 5) lc_quant_wa_kernel(LcQuantParams
         if (hs[i]) atomicAdd(&P.hist[i], hs[i]);
 }
 
+// Exact reference chain of one chunk from `start` (certified decisions, IEEE
+// division on doubt), codes and histogram entries replaced where they differ
+// from what the chunk holds, end checked against `next` (the successor's
+// predicted start): a mismatch records the first failing chunk.
+template <typename CodeT, bool REC>
+__device__ __forceinline__ void lc_qw_exact_chunk(const LcQuantParams &P, CodeT *__restrict__ codes,
+                                                  const double *row, const LcQwLane &L, double start, double next)
+{
+    const long long q0 = L.p0;
+    const int ln = L.len;
+    double r2 = start;
+    bool ok = true;
+    for (int j = 0; j < ln; ++j) {
+        uint32_t code; int esc; double inc, pe;
+        const double rn = lc_step_nb(P.Q, row[j], r2, &code, &inc, &esc, &pe, ok);
+        r2 = rn;
+    }
+    const bool ieee = !ok;
+    r2 = start;
+    for (int j = 0; j < ln; ++j) {                      // second run: write (same results when ok)
+        uint32_t code; int esc; double inc, pe;
+        bool ok2 = true;
+        const double rn = ieee ? lc_step(P.Q, row[j], r2, &code, &esc, &inc, &pe)
+                               : lc_step_nb(P.Q, row[j], r2, &code, &inc, &esc, &pe, ok2);
+        const uint32_t old = (uint32_t)codes[q0 + j];
+        if (old != code) {
+            atomicAdd(&P.hist[old], 0xffffffffu);
+            atomicAdd(&P.hist[code], 1u);
+            codes[q0 + j] = (CodeT)code;
+        }
+        if (REC) { P.pe[q0 + j] = pe; P.pe_rec[q0 + j] = LC_SUB(rn, r2); }
+        r2 = rn;
+    }
+    if (L.c + 1 < P.nchunks && lc_bits(r2) != lc_bits(next)) {
+        P.bad_end[L.c] = r2;
+        atomicMin(P.first_bad, (unsigned long long)(L.c + 1));
+    }
+}
+
+// Pass B.  P.resume = 0: the first pass over all warp tiles; a tile whose chunk
+// codes get rewritten (modes 0 and 2) is marked (tile_S = -inf).  P.resume = 1 (one warp):
+// resume at chunk P.resume_chunk, whose predicted start was wrong -- its exact
+// start is known, so the chunks from there to the end of its warp tile are
+// re-run exactly from offsets composed from that start (suffix scan of the
+// tile's chunk maps, pass A recomputed), and the offset at the next tile start
+// goes to *P.resume_D0 for the map scan of the remaining tiles.  P.resume = 2:
+// the tiles after it with the new offsets; a tile marked in the first pass is
+// re-run exactly in full (its codes came from wrong starts).  Pass A's codes,
+// histogram, maps and slacks stay valid throughout (they do not depend on the
+// offsets), so a failed prediction costs a map scan and this pass instead of a
+// relaunch of the whole quantizer.
 template <typename CodeT, bool REC>
 __global__ void __launch_bounds__(LC_QW_TPB, 5) lc_quant_wfix_kernel(LcQuantParams P, CodeT *__restrict__ codes)
 {
@@ -367,13 +418,47 @@ __global__ void __launch_bounds__(LC_QW_TPB, 5) lc_quant_wfix_kernel(LcQuantPara
     extern __shared__ __align__(16) unsigned char lc_dyn_smem[];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     double *xw = reinterpret_cast<double *>(lc_dyn_smem) + wid * LC_QW_ROWS;
-    const long long nel = (long long)P.n - 1;
-    const long long nwarps = (long long)gridDim.x * (LC_QW_TPB / 32);
     unsigned long long exact_chunks = 0;
     const bool force = P.verify || REC || !(P.rmax < INFINITY) || P.inject_chunk >= 0;
+    if (P.resume == 1) {
+        if (wid != 0) return;
+        const long long rel = P.resume_chunk - P.first_chunk;
+        const long long w = rel / 32;
+        const int f0 = (int)(rel % 32);
+        LcQwLane L;
+        lc_qw_pass_a<CodeT, false>(P, w, xw, nullptr, nullptr, 0u, nullptr, L);
+        OffMap sinc = lane >= f0 ? L.H : lc_map_neutral();
+        lc_warp_scan_maps(sinc);
+        OffMap sexc = lc_shfl_up_map(sinc, 1);
+        if (lane <= f0) sexc = lc_map_neutral();
+        const double exact = *P.resume_start;
+        const double D0l = LC_SUB(exact, L.g0);
+        const bool okl = lane == f0 && lc_bits(lc_apply_offset(L.g0, D0l)) == lc_bits(exact);
+        const double D = __shfl_sync(0xffffffffu, D0l, f0);
+        const bool ok = __shfl_sync(0xffffffffu, okl ? 1 : 0, f0) != 0;
+        const double Dnext = lc_map_eval(sinc, D);       // lane 31: offset at the next tile start
+        if (!ok) {                                       // offset not representable: full relaunch
+            if (lane == 0) { *P.resume_D0 = NAN; atomicMin(P.first_bad, (unsigned long long)P.resume_chunk); }
+            return;
+        }
+        double start = 0.0;
+        if (lane >= f0 && L.len > 0) start = lane == f0 ? exact : lc_apply_offset(L.g0, lc_map_eval(sexc, D));
+        double next = __shfl_down_sync(0xffffffffu, start, 1);
+        if (lane == 31) next = lc_apply_offset(L.g1, Dnext);
+        if (lane >= f0 && L.len > 0) {
+            lc_qw_exact_chunk<CodeT, REC>(P, codes, xw + lane * LC_ROW, L, start, next);
+            ++exact_chunks;
+        }
+        if (lane == 31) *P.resume_D0 = Dnext;
+        if (exact_chunks) atomicAdd(P.exact_count, exact_chunks);
+        return;
+    }
+    if (P.resume == 2 && !(*P.resume_D0 == *P.resume_D0)) return;   // resume impossible (NaN)
+    const long long nwarps = (long long)gridDim.x * (LC_QW_TPB / 32);
     // 32 warp tiles are checked per round (one per lane, coalesced loads); the
     // uncertified ones (rare) are then redone one after the other by the warp
-    for (long long w0 = ((long long)blockIdx.x * (LC_QW_TPB / 32) + wid) * 32; w0 < P.ntiles; w0 += nwarps * 32) {
+    for (long long w0 = P.first_tile + ((long long)blockIdx.x * (LC_QW_TPB / 32) + wid) * 32; w0 < P.ntiles;
+         w0 += nwarps * 32) {
         const long long wl = w0 + lane;
         const bool redo = wl < P.ntiles && !(fabs(P.tile_D[wl]) < P.tile_S[wl]);
         unsigned todo = __ballot_sync(0xffffffffu, redo);
@@ -381,6 +466,7 @@ __global__ void __launch_bounds__(LC_QW_TPB, 5) lc_quant_wfix_kernel(LcQuantPara
         const long long w = w0 + __ffs(todo) - 1;
         todo &= todo - 1;
         const double Dw = P.tile_D[w];
+        const bool marked = P.resume == 2 && P.tile_S[w] == -INFINITY;   // rewritten by the first pass
         LcQwLane L;
         lc_qw_pass_a<CodeT, false>(P, w, xw, nullptr, nullptr, 0u, nullptr, L);
         const double Dc = lc_map_eval(L.exc, Dw);
@@ -392,41 +478,13 @@ __global__ void __launch_bounds__(LC_QW_TPB, 5) lc_quant_wfix_kernel(LcQuantPara
         }
         double next = __shfl_down_sync(0xffffffffu, start, 1);
         if (lane == 31) next = lc_apply_offset(L.g1, lc_map_eval(L.inc, Dw));
-        const bool cert = !force && L.len > 0 && fabs(Dc) < lc_qw_margin(P, L);
-        if (L.len > 0 && !cert) {
-            // exact reference step from the predicted start (certified decisions, IEEE on doubt)
-            const double *row = xw + lane * LC_ROW;
-            const long long q0 = L.p0;
-            const int ln = L.len;
-            double r2 = start;
-            bool ok = true;
-            for (int j = 0; j < ln; ++j) {
-                uint32_t code; int esc; double inc, pe;
-                const double rn = lc_step_nb(P.Q, row[j], r2, &code, &inc, &esc, &pe, ok);
-                r2 = rn;
-            }
-            const bool ieee = !ok;
-            r2 = start;
-            for (int j = 0; j < ln; ++j) {                      // second run: write (same results when ok)
-                uint32_t code; int esc; double inc, pe;
-                bool ok2 = true;
-                const double rn = ieee ? lc_step(P.Q, row[j], r2, &code, &esc, &inc, &pe)
-                                       : lc_step_nb(P.Q, row[j], r2, &code, &inc, &esc, &pe, ok2);
-                const uint32_t old = (uint32_t)codes[q0 + j];
-                if (old != code) {
-                    atomicAdd(&P.hist[old], 0xffffffffu);
-                    atomicAdd(&P.hist[code], 1u);
-                    codes[q0 + j] = (CodeT)code;
-                }
-                if (REC) { P.pe[q0 + j] = pe; P.pe_rec[q0 + j] = LC_SUB(rn, r2); }
-                r2 = rn;
-            }
-            if (L.c + 1 < P.nchunks && lc_bits(r2) != lc_bits(next)) {
-                P.bad_end[L.c] = r2;
-                atomicMin(P.first_bad, (unsigned long long)(L.c + 1));
-            }
+        const bool cert = !force && !marked && L.len > 0 && fabs(Dc) < lc_qw_margin(P, L);
+        const bool rerun = L.len > 0 && !cert;
+        if (rerun) {
+            lc_qw_exact_chunk<CodeT, REC>(P, codes, xw + lane * LC_ROW, L, start, next);
             ++exact_chunks;
         }
+        if (__any_sync(0xffffffffu, rerun) && lane == 0) P.tile_S[w] = -INFINITY;   // codes rewritten
         __syncwarp();
       }
     }

@@ -241,13 +241,18 @@ class DeviceOps:
         self.device = torch.device(device)
         if self.device.type != "cuda":
             raise ParameterError("DeviceOps needs a CUDA device")
-
-    def _ctx(self):
-        return _native.context(self.device.index or 0)
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        # the solver's kernels are ordered on the stream current at construction
+        # (the calling thread's codec context for that stream)
+        self.stream = torch.cuda.current_stream(self.device.index).cuda_stream
+        self.lib = _native.library()
 
     def _call(self, name, *args):
-        ctx = self._ctx()
-        _check(ctx, getattr(ctx.lib, name)(ctx.h, *args), name)
+        ctx = _native.bind_stream(self.device.index, self.stream)
+        rc = getattr(self.lib, name)(ctx.h, *args)
+        if rc != 0:
+            _check(ctx, rc, name)
 
     # storage
     def empty(self, n):
@@ -422,7 +427,7 @@ class _SolverBase:
             self._xh[L.halo:L.halo + L.n].copy_(xv)
         self._part = ops.empty(2 * L.nch)
         self._gpart = ops.empty(2 * L.nch_global) if L.world > 1 else None
-        self._rparts = ops.empty(4 * L.nch)
+        self._rparts = ops.empty(6 * L.nch)          # per-chunk range records (LcKrRange, 48 B)
         self._range = ops.range_record()
         self._range_valid = False
         self._out = ops.zeros(4)

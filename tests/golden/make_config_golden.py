@@ -85,6 +85,14 @@ CASES = {
                             k=60, eb=1e-4, failures=[150]),
     "config4_64_1e-6": dict(st=lambda: generate_convdiff3d(64), method="gmres", seed=2, tol=1e-8, restart=30,
                             k=60, eb=1e-6, failures=[150]),
+    "config4_128_1e-4": dict(st=lambda: generate_convdiff3d(128), method="gmres", seed=2, tol=1e-8, restart=30,
+                             k=60, eb=1e-4, failures=[150]),
+    "config4_128_1e-6": dict(st=lambda: generate_convdiff3d(128), method="gmres", seed=2, tol=1e-8, restart=30,
+                             k=60, eb=1e-6, failures=[150]),
+    "config4_256_1e-4": dict(st=lambda: generate_convdiff3d(256), method="gmres", seed=2, tol=1e-8, restart=30,
+                             k=60, eb=1e-4, failures=[150]),
+    "config4_256_1e-6": dict(st=lambda: generate_convdiff3d(256), method="gmres", seed=2, tol=1e-8, restart=30,
+                             k=60, eb=1e-6, failures=[150]),
 }
 
 gold = json.load(open(OUT)) if os.path.exists(OUT) else {}

@@ -89,11 +89,13 @@ class NumpyOps:
     def _range(self, x, rparts):
         if rparts is None:
             return
-        rp = rparts.numpy().reshape(-1, 4)
+        rp = rparts.numpy().reshape(-1, 6)            # vmin, vmax, maxstep, first, last, nonfinite
         for i, c in enumerate(range(0, x.size, CH)):
             seg = x[c:c + CH]
-            rp[i, 0], rp[i, 1], rp[i, 2] = seg.min(), seg.max(), 0.0
-            rp[i, 3] = float(not np.all(np.isfinite(seg)))
+            rp[i, 0], rp[i, 1] = seg.min(), seg.max()
+            rp[i, 2] = np.max(np.abs(np.diff(seg))) if seg.size > 1 else 0.0
+            rp[i, 3], rp[i, 4] = seg[0], seg[-1]
+            rp[i, 5] = float(not np.all(np.isfinite(seg)))
 
     # kernels
     def spmv(self, slab, vh, off, y, part, sc):
@@ -186,10 +188,11 @@ class NumpyOps:
         s0 = float(np.sum(pp[:, 0]))
         s1 = float(np.sum(pp[:, 1])) if width > 1 else 0.0
         if rparts is not None:
-            rp = rparts.numpy().reshape(-1, 4)[:nrp]
+            rp = rparts.numpy().reshape(-1, 6)[:nrp]
             ro = rout.numpy()
-            ro[0], ro[1], ro[3] = rp[:, 0].min(), rp[:, 1].max(), float(rp[:, 3].max())
-            ro[2] = math.inf if ro[3] else ro[1] - ro[0]
+            ro[0], ro[1], ro[3] = rp[:, 0].min(), rp[:, 1].max(), float(rp[:, 5].max())
+            ms = max(float(rp[:, 2].max()), float(np.max(np.abs(rp[1:, 3] - rp[:-1, 4]))) if nrp > 1 else 0.0)
+            ro[2] = math.inf if ro[3] else ms
 
         def set_res(v, conv):
             if not math.isfinite(v):

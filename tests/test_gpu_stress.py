@@ -29,7 +29,7 @@ import stress_inputs  # noqa: E402
 
 GOLD = json.load(open(os.path.join(HERE, "golden", "stress_golden.json")))
 
-OPT_MAX_QUANT, OPT_MAX_REC, OPT_INJECT_QUANT, OPT_INJECT_REC, OPT_VERIFY = 0, 1, 2, 3, 4
+OPT_MAX_QUANT, OPT_MAX_REC, OPT_INJECT_QUANT, OPT_INJECT_REC, OPT_VERIFY, OPT_RESUME = 0, 1, 2, 3, 4, 5
 STAT_QUANT_RELAUNCHES, STAT_QUANT_SERIAL, STAT_REC_RELAUNCHES, STAT_REC_SERIAL = 0, 1, 2, 3
 
 
@@ -57,7 +57,7 @@ def ctx(lc):
     c = _native.context(0)
     yield c
     for k, v in ((OPT_MAX_QUANT, 64), (OPT_MAX_REC, 64), (OPT_INJECT_QUANT, -1), (OPT_INJECT_REC, -1),
-                 (OPT_VERIFY, 0)):
+                 (OPT_VERIFY, 0), (OPT_RESUME, 1)):
         c.lib.lc_ctx_set_option(c.h, k, v)
 
 
@@ -90,11 +90,13 @@ def _smooth(n=300_000):
     return stress_inputs.sine_mix(n, 302)
 
 
-@pytest.mark.parametrize("max_relaunch", [64, 0])
-def test_quantizer_relaunch_and_serial_paths(lc, ctx, max_relaunch):
+@pytest.mark.parametrize("max_relaunch,resume", [(64, 1), (64, 0), (0, 1)])
+def test_quantizer_relaunch_and_serial_paths(lc, ctx, max_relaunch, resume):
     """A wrong chunk prediction (injected) is caught by its predecessor's end check and
-    repaired by a relaunch (max 64) or by the sequential exact chain (max 0); the block
-    is the oracle's either way.  (Smooth data: the injected failure is the only one.)"""
+    repaired by resuming the exact pass from the failing chunk (resume 1, the default),
+    a full relaunch (resume 0) or the sequential exact chain (max 0); the block is the
+    oracle's every way.  (Smooth data: the injected failure is the only one.)"""
+    ctx.lib.lc_ctx_set_option(ctx.h, OPT_RESUME, resume)
     x = _smooth()
     ref = orc.to_bytes(orc.compress(x, "absolute", 1e-3))
     ctx.lib.lc_ctx_set_option(ctx.h, OPT_INJECT_QUANT, -1)
@@ -165,5 +167,9 @@ def test_edge_corpus_relaunches_reported(lc, ctx):
     ref = orc.to_bytes(orc.compress(x, "absolute", 1e-3))
     blk = lc.compress(torch.from_numpy(x).cuda(), lc.CompressorConfig.absolute(1e-3))
     assert blk.to_bytes() == ref
+    ctx.lib.lc_ctx_set_option(ctx.h, OPT_RESUME, 0)          # the same through full relaunches
+    assert lc.compress(torch.from_numpy(x).cuda(), lc.CompressorConfig.absolute(1e-3)).to_bytes() == ref
+    ctx.lib.lc_ctx_set_option(ctx.h, OPT_RESUME, 1)
+    blk = lc.compress(torch.from_numpy(x).cuda(), lc.CompressorConfig.absolute(1e-3))
     assert ctx.lib.lc_ctx_get_stat(ctx.h, STAT_QUANT_RELAUNCHES) >= 1
     assert ctx.lib.lc_ctx_get_stat(ctx.h, 4) >= 1                          # chunks re-run exactly

@@ -130,7 +130,7 @@ def test_x_range_record():
     s.advance(5)
     rr = s.x_range.numpy()
     x = s.x.numpy()
-    assert rr[0] == x.min() and rr[1] == x.max() and rr[3] == 0.0 and rr[2] >= np.max(np.abs(np.diff(x)))
+    assert rr[0] == x.min() and rr[1] == x.max() and rr[3] == 0.0 and rr[2] == np.max(np.abs(np.diff(x)))
 
 
 def test_uneven_split_rejected():

@@ -273,21 +273,28 @@ def test_sharded_cg_bit_identical_on_device(dev, world):
     for _ in range(3):
         one.advance(17)
         ref_norms.append(one.residual_norm)
-    shared = {"items": [None] * world, "barrier": threading.Barrier(world)}
+    shared = {"items": [None] * world, "barrier": threading.Barrier(world, timeout=120)}
     out = [None] * world
+    errs = []
 
     def run(r):
-        with torch.cuda.stream(torch.cuda.Stream()):
-            s = solvers.init("cg", a, m, torch.from_numpy(b).to(dev), cfg, comm=_ThreadComm(r, world, shared))
-            norms = [s.residual_norm]
-            for _ in range(3):
-                s.advance(17)
-                norms.append(s.residual_norm)
-            out[r] = (norms, s.x.cpu().numpy(), s.iteration)
+        try:
+            with torch.cuda.stream(torch.cuda.Stream()):
+                s = solvers.init("cg", a, m, torch.from_numpy(b).to(dev), cfg, comm=_ThreadComm(r, world, shared))
+                norms = [s.residual_norm]
+                for _ in range(3):
+                    s.advance(17)
+                    norms.append(s.residual_norm)
+                out[r] = (norms, s.x.cpu().numpy(), s.iteration)
+        except BaseException as exc:                    # a failed rank must not leave the others waiting
+            errs.append(exc)
+            shared["barrier"].abort()
 
     ts = [threading.Thread(target=run, args=(r,)) for r in range(world)]
     [t.start() for t in ts]
     [t.join() for t in ts]
+    if errs:
+        raise errs[0]
     for norms, _, it in out:
         assert norms == ref_norms and it == one.iteration
     xs = np.concatenate([o[1] for o in out])
