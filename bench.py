@@ -242,7 +242,7 @@ def run_b200(args, rank, world, local_rank):
     wctx = [_native.Context(local_rank, ctypes.c_void_p(st.cuda_stream)) for st in wstreams]
     wout = [torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(nstr)]
 
-    def rt(eb_rel, stats=None, ctx=ctx, out=out):
+    def rt(eb_rel, stats=None, ctx=ctx, out=out, v3=False):
         # value range + device-resolved bounds + quantizer + codebook + encoder (one host
         # round trip, the path paper_1805_07384_b200.compress takes), then the decoder
         i = BOUNDS.index(eb_rel)
@@ -260,8 +260,16 @@ def run_b200(args, rank, world, local_rank):
         pay, cl, ei, ev = vp(), vp(), vp(), vp()
         L.lc_result_device(ctx.h, ctypes.byref(pay), ctypes.byref(cl), ctypes.byref(ei), ctypes.byref(ev))
         used = ctypes.c_int64()
-        rc = L.lc_decompress_f64(ctx.h, n, eb_abs, float(xs[i][0]), cl, res.n_symbols, pay, res.payload_bytes,
-                                 res.payload_bits, ei, ev, res.n_esc, 1, out.data_ptr(), 1, ctypes.byref(used))
+        if v3:              # v3 block (sync tables with chain values): one-pass decode + reconstruction
+            so, ss, se = vp(), vp(), vp()
+            L.lc_result_sync_device(ctx.h, ctypes.byref(so), ctypes.byref(ss), ctypes.byref(se))
+            ns = (n - 1 + 1023) // 1024
+            rc = L.lc_decompress_v3_f64(ctx.h, n, eb_abs, float(xs[i][0]), cl, res.n_symbols, pay,
+                                        res.payload_bytes, res.payload_bits, so, ss, se, ns, 1024, ei, ev,
+                                        res.n_esc, 1, out.data_ptr(), 1, ctypes.byref(used))
+        else:
+            rc = L.lc_decompress_f64(ctx.h, n, eb_abs, float(xs[i][0]), cl, res.n_symbols, pay, res.payload_bytes,
+                                     res.payload_bits, ei, ev, res.n_esc, 1, out.data_ptr(), 1, ctypes.byref(used))
         assert rc == 0, (rc, ctx.error())
         if stats is not None:
             ph = (ctypes.c_double * 8)()
@@ -292,6 +300,13 @@ def run_b200(args, rank, world, local_rank):
     def step_sequential():
         for eb in BOUNDS:
             rt(eb)
+
+    def lane_v3(k):
+        for i in range(k, len(BOUNDS), nstr):
+            rt(BOUNDS[i], ctx=wctx[k], out=wout[k], v3=True)
+
+    def step_v3():
+        list(pool.map(lane_v3, range(nstr)))
 
     def barrier():
         if dist is not None:
@@ -328,6 +343,18 @@ def run_b200(args, rank, world, local_rank):
     ev3.record()
     torch.cuda.synchronize()
     ms_seq = ev2.elapsed_time(ev3) / args.steps
+    # the same concurrent step writing/reading v3 blocks (sync tables with chain values)
+    for _ in range(2):
+        step_v3()
+    barrier()
+    ev4 = torch.cuda.Event(enable_timing=True)
+    ev5 = torch.cuda.Event(enable_timing=True)
+    ev4.record()
+    for _ in range(args.steps):
+        step_v3()
+    ev5.record()
+    torch.cuda.synchronize()
+    ms_v3 = ev4.elapsed_time(ev5) / args.steps
     if dist is not None:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -350,6 +377,14 @@ def run_b200(args, rank, world, local_rank):
         bb = block_bytes(res.payload_bytes, cl, res.n_esc)
         cms = statistics.median(r["compress_ms"] for r in runs)
         dms = statistics.median(r["decompress_ms"] for r in runs)
+        runs3 = []
+        for _ in range(3):
+            s3 = {}
+            rt(eb, s3, v3=True)
+            runs3.append(s3)
+        dms3 = statistics.median(r["decompress_ms"] for r in runs3)
+        cms3 = statistics.median(r["compress_ms"] for r in runs3)
+        bb3 = bb + 12 + 24 * ((n - 1 + 1023) // 1024)
         pk = measured_peak()[0]
         alg_c = 8 * n + res.payload_bytes + 16 * res.n_esc       # x read, payload + escapes written
         alg_d = res.payload_bytes + 16 * res.n_esc + 8 * n       # payload + escapes read, x' written
@@ -360,6 +395,9 @@ def run_b200(args, rank, world, local_rank):
             "compress_ms": cms, "decompress_ms": dms, "ratio": 8 * n / bb, "payload_bits": int(res.payload_bits),
             "escapes": int(res.n_esc), "max_len": int(res.max_len), "symbols": int(res.used_symbols),
             "relaunches": int(res.relaunches),
+            "v3": {"compress_ms": cms3, "decompress_ms": dms3, "ratio": 8 * n / bb3,
+                   "compress_gbs": 8 * n / (cms3 / 1e3) / 1e9, "decompress_gbs": 8 * n / (dms3 / 1e3) / 1e9,
+                   "decompress_roofline_frac": (alg_d + 24 * ((n - 1 + 1023) // 1024)) / (dms3 / 1e3) / 1e9 / pk},
             "compress_phase_ms": {"setup": s["compress_phases"][0], "quantize": s["compress_phases"][1],
                                   "codebook": s["compress_phases"][2], "encode": s["compress_phases"][3]},
             "decompress_phase_ms": {"huffman_sync": s["decompress_phases"][0],
@@ -517,6 +555,9 @@ def run_b200(args, rank, world, local_rank):
                        "streams": nstr, "l2": "inputs (512 MB/GPU) exceed L2; no flush"},
             "sequential": {"value": 8 * n * len(BOUNDS) * world / (ms_seq / 1e3) / 1e9, "ms_per_step": ms_seq,
                            "note": "same step, the three round trips one after the other on one stream"},
+            "v3": {"value": 8 * n * len(BOUNDS) * world / (ms_v3 / 1e3) / 1e9, "ms_per_step": ms_v3,
+                   "note": "same concurrent step with v3 blocks (repo format: + chain value and escape count "
+                           "every 1024 symbols; codes/payload identical to the reference's), one-pass decoder"},
             "clocks": clk, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "per_bound": per,
             "solver_configs": solver,
@@ -641,7 +682,7 @@ def config5_harness(lc, world, rank, local_rank, side, iters=100, k=25, eb=1e-5)
     L = ctx.lib
     out = torch.empty(nl, dtype=torch.float64, device="cuda")
     vp = ctypes.c_void_p
-    tc, td, ratios, errs, solve_ms = [], [], [], [], []
+    tc, td, td3, ratios, errs, solve_ms = [], [], [], [], [], []
     while s.iteration < iters and not s.converged:
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -667,15 +708,23 @@ def config5_harness(lc, world, rank, local_rank, side, iters=100, k=25, eb=1e-5)
         L.lc_phase_ms(ctx.h, ph, 8)
         dph = [round(ph[i], 4) for i in range(4, 8)]
         errs.append(float((out - s.x).abs().max()) / bnd.eb_abs)
+        so, ss, se = vp(), vp(), vp()                  # the same block as v3 (one-pass decoder)
+        L.lc_result_sync_device(ctx.h, ctypes.byref(so), ctypes.byref(ss), ctypes.byref(se))
+        rc = L.lc_decompress_v3_f64(ctx.h, nl, bnd.eb_abs, bnd.first_value, cl, res.n_symbols, pay,
+                                    res.payload_bytes, res.payload_bits, so, ss, se, (nl - 1 + 1023) // 1024, 1024,
+                                    ei, ev, res.n_esc, 1, out.data_ptr(), 1, ctypes.byref(used))
+        assert rc == 0, (rc, ctx.error())
+        td3.append(L.lc_last_device_ms(ctx.h))
+        errs.append(float((out - s.x).abs().max()) / bnd.eb_abs)
         cl_h = np.zeros(res.n_symbols, np.uint8)
         L.lc_result_fetch(ctx.h, cl_h.ctypes.data, None, None, None, None, None)
         ratios.append(8 * nl / block_bytes(res.payload_bytes, cl_h, res.n_esc))
-    tcm, tdm = statistics.median(tc), statistics.median(td)
+    tcm, tdm, tdm3 = statistics.median(tc), statistics.median(td), statistics.median(td3)
     if comm is not None:
         import torch.distributed as dist
-        t = torch.tensor([tcm, tdm], dtype=torch.float64, device="cuda")
+        t = torch.tensor([tcm, tdm, tdm3], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tcm, tdm = float(t[0]), float(t[1])
+        tcm, tdm, tdm3 = float(t[0]), float(t[1]), float(t[2])
     pk = measured_peak()[0]
     cg = 8 * nl / (tcm / 1e3) / 1e9
     dg = 8 * nl / (tdm / 1e3) / 1e9
@@ -685,6 +734,8 @@ def config5_harness(lc, world, rank, local_rank, side, iters=100, k=25, eb=1e-5)
             "compress_gbs_per_gpu": cg, "decompress_gbs_per_gpu": dg,
             "compress_gbs_aggregate": cg * world, "decompress_gbs_aggregate": dg * world,
             "compress_roofline_frac": cg / pk, "decompress_roofline_frac": dg / pk,
+            "v3_decompress_ms": tdm3, "v3_decompress_gbs_per_gpu": 8 * nl / (tdm3 / 1e3) / 1e9,
+            "v3_decompress_roofline_frac": 8 * nl / (tdm3 / 1e3) / 1e9 / pk,
             "ratio": statistics.median(ratios), "max_err_over_eb": max(errs),
             "last_compress_phase_ms": dict(zip(["setup", "quantize", "codebook", "encode"], cph)),
             "last_decompress_phase_ms": dict(zip(["huffman_sync", "huffman_scan", "huffman_write", "reconstruct"], dph)),

@@ -251,6 +251,26 @@ int lc_dot_f64(lc_ctx *ctx, const double *a, const double *b, uint64_t n, double
 int lc_axpy_f64(lc_ctx *ctx, double a, const double *a_dev, double a_scale, const double *x, double *y,
                 uint64_t n);
 
+/* ---- v3 blocks (continued) ---------------------------
+ * A v3 block adds, at every LC_SYNC_K-th symbol, the exact chain value before
+ * it (the reconstruction x'[1024 k]) and the number of escape codes before
+ * it.  Every interval then decodes and reconstructs independently: one
+ * kernel, no segment synchronisation, no offset maps (lc_dec_v3_kernel).
+ * Codes, payload and escapes are the reference's; the tables only add
+ * 24 bytes per 1024 symbols.  lc_result_sync_v3 copies the last compress's
+ * tables (any pointer may be NULL); lc_decompress_v3_f64 decodes a v3 block
+ * (status 6 when a table entry disagrees with the payload or the chain).    */
+int lc_result_sync_v3(lc_ctx *ctx, uint64_t *offsets, double *starts, uint64_t *escapes, uint64_t cap,
+                      uint64_t *count);
+/* Device pointers of the last compress's sync tables (valid until the next
+ * compress on this context); any argument may be NULL.                    */
+int lc_result_sync_device(lc_ctx *ctx, const uint64_t **offsets, const double **starts, const uint64_t **escapes);
+int lc_decompress_v3_f64(lc_ctx *ctx, uint64_t n, double eb_abs, double first_value, const uint8_t *code_lengths,
+                         uint64_t n_lengths, const uint8_t *payload, uint64_t payload_bytes, uint64_t payload_bits,
+                         const uint64_t *sync, const double *sync_starts, const uint64_t *sync_esc, uint64_t n_sync,
+                         uint32_t sync_k, const uint64_t *esc_idx, const double *esc_val, uint64_t n_esc,
+                         int inputs_on_device, double *out, int out_on_device, int64_t *esc_used);
+
 /* ---- device-resident Krylov harness (lc_krylov.cu) -------------------------
  * Slab of a global stencil grid: planes [z0, z0 + nzl) of st (x fastest).
  * Vectors a stencil reads are passed as the address of their first local

@@ -228,6 +228,19 @@ def sync_offsets(codes, lengths, k=1024):
     return start[::k].copy()
 
 
+def sync_v3(codes, recon, k=1024):
+    """v3 block tables beside the bit offsets (no reference counterpart): the
+    reference reconstruction at every k-th element (the exact chain value
+    before symbol k*j, compressor.py:358-376) and the escape codes before
+    symbol k*j (code 0, compressor.py:339-341)."""
+    codes = np.asarray(codes, dtype=np.int64)
+    if codes.size == 0:
+        return np.zeros(0), np.zeros(0, np.uint64)
+    starts = np.asarray(recon, dtype=np.float64)[:codes.size:k].copy()
+    esc = np.concatenate([[0], np.cumsum(codes == 0)[:-1]]).astype(np.uint64)[::k].copy()
+    return starts, esc
+
+
 def decompress(blk):
     """compressor.py:420-440."""
     n = blk["n"]

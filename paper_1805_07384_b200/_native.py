@@ -113,6 +113,14 @@ def library():
         for f in (L.lc_stencil_apply_f64, L.lc_residual_f64, L.lc_jacobi_step_f64, L.lc_dot_f64, L.lc_axpy_f64):
             f.restype = ctypes.c_int
         _u64 = ctypes.c_uint64
+        L.lc_result_sync_v3.argtypes = [_vp, _vp, _vp, _vp, _u64, ctypes.POINTER(ctypes.c_uint64)]
+        L.lc_result_sync_v3.restype = ctypes.c_int
+        L.lc_decompress_v3_f64.argtypes = [_vp, _u64, _d, _d, _vp, _u64, _vp, _u64, _u64, _vp, _vp, _vp, _u64,
+                                           ctypes.c_uint32, _vp, _vp, _u64, ctypes.c_int, _vp, ctypes.c_int,
+                                           ctypes.POINTER(ctypes.c_int64)]
+        L.lc_decompress_v3_f64.restype = ctypes.c_int
+        L.lc_result_sync_device.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp)]
+        L.lc_result_sync_device.restype = ctypes.c_int
         L.lc_compress_ranged_f64.argtypes = [_vp, _vp, _u64, ctypes.c_int, _d, ctypes.c_uint32, ctypes.c_int, _vp,
                                              ctypes.POINTER(LcResult), ctypes.POINTER(LcBounds)]
         L.lc_kr_spmv_f64.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
@@ -150,7 +158,8 @@ EXPORTED = ["lc_ctx_create", "lc_ctx_destroy", "lc_last_error", "lc_range_f64", 
             "lc_phase_ms", "lc_launch_count", "lc_error_stats_f64", "lc_stencil_apply_f64",
             "lc_residual_f64", "lc_jacobi_step_f64", "lc_dot_f64", "lc_axpy_f64", "lc_result_sync",
             "lc_decompress_v2_f64", "lc_trace_mark_api", "lc_trace_read", "lc_compress_auto_f64", "lc_ctx_set_option", "lc_ctx_get_stat",
-            "lc_debug_codebook", "lc_compress_ranged_f64"]
+            "lc_debug_codebook", "lc_compress_ranged_f64", "lc_result_sync_v3", "lc_decompress_v3_f64",
+            "lc_result_sync_device"]
 KRYLOV = ["lc_kr_spmv_f64", "lc_kr_residual_f64", "lc_kr_cg_update_f64", "lc_kr_cg_dir_f64", "lc_kr_jacobi_f64",
           "lc_kr_dot_f64", "lc_kr_subh_f64", "lc_kr_div_f64", "lc_kr_combine_f64", "lc_kr_fold_f64"]
 EXPORTED = EXPORTED + KRYLOV

@@ -15,7 +15,8 @@ int lc_decompress_impl2(lc_ctx *ctx, uint64_t n, double eb_abs, double first_val
                         const uint8_t *code_lengths, uint64_t n_lengths, const uint8_t *payload,
                         uint64_t payload_bytes, uint64_t payload_bits, const uint64_t *esc_idx,
                         const double *esc_val, uint64_t n_esc, int inputs_on_device, double *out,
-                        int out_on_device, int64_t *esc_used, const uint64_t *sync, uint64_t n_sync);
+                        int out_on_device, int64_t *esc_used, const uint64_t *sync, uint64_t n_sync,
+                        const double *sync_starts = nullptr, const uint64_t *sync_esc = nullptr);
 
 // ---------------------------------------------------------------------------
 
@@ -377,13 +378,14 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     ctx->quant_serial = 0;
     P.inject_chunk = ctx->opt[LC_OPT_INJECT_QUANT];
     LC_CUDA_OK(cudaEventRecord(ctx->pev[1], st));
-    LC_CUDA_OK(lc_reserve(ctx->tiles, (size_t)(ntiles + 1) * (2 * sizeof(long long) + sizeof(OffMap) + 2 * sizeof(double))
+    LC_CUDA_OK(lc_reserve(ctx->tiles, (size_t)(ntiles + 1) * (2 * sizeof(long long) + sizeof(OffMap) + 3 * sizeof(double))
                                           + LC_MAPSCAN_SCRATCH + 256));
     {
         char *pp = (char *)ctx->tiles.p;
         P.tile_agg = (OffMap *)pp;               pp += (ntiles + 1) * sizeof(OffMap);
         P.tile_D = (double *)pp;                 pp += (ntiles + 1) * sizeof(double);
         P.tile_S = (double *)pp;                 pp += (ntiles + 1) * sizeof(double);
+        P.tile_g0 = (double *)pp;                pp += (ntiles + 1) * sizeof(double);
         P.tile_last_esc = (long long *)pp;       pp += (ntiles + 1) * sizeof(long long);
         P.anc_in = (const long long *)pp;        pp += (ntiles + 1) * sizeof(long long);
         ctx->mapscan_scratch = (void *)(((uintptr_t)pp + 63) & ~(uintptr_t)63);
@@ -411,7 +413,9 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
         if (P.pe) lc_quant_wfix_kernel<CodeT, true><<<(int)(wcta < gf ? wcta : gf), LC_QW_TPB, fsmem, st>>>(P, codes);
         else lc_quant_wfix_kernel<CodeT, false><<<(int)(wcta < gf ? wcta : gf), LC_QW_TPB, fsmem, st>>>(P, codes);
         { int _rc = lc_debug_check(ctx, "lc_quant_wfix_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
-        ctx->launches += 3;
+        lc_sync_starts_kernel<<<(int)((P.ntiles + 255) / 256 < 2 * ctx->sm_count ? (P.ntiles + 255) / 256
+                                                                                : 2 * ctx->sm_count), 256, 0, st>>>(P);
+        ctx->launches += 4;
         return 0;
     };
 
@@ -435,7 +439,11 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     const uint64_t etiles = (m + LC_TILE - 1) / LC_TILE;
     LC_CUDA_OK(lc_reserve(ctx->encdesc, etiles * sizeof(LcEncDesc)));
     ctx->nsync = (m + LC_SYNC_K - 1) / LC_SYNC_K;
-    LC_CUDA_OK(lc_reserve(ctx->sync, (ctx->nsync + 1) * 8));
+    // sync table of every compress: bit offsets, exact chain values and escape
+    // counts at every LC_SYNC_K-th symbol (v2 blocks use the offsets, v3 all three)
+    LC_CUDA_OK(lc_reserve(ctx->sync, (ctx->nsync + 1) * 24));
+    P.sync_start = (double *)ctx->sync.p + (ctx->nsync + 1);
+    P.nsync = ctx->nsync;
     LcEncParams E;
     E.codes = codes;
     E.m = m;
@@ -449,6 +457,7 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     E.ntiles = etiles;
     E.cb = cbo;
     E.sync = (unsigned long long *)ctx->sync.p;
+    E.sync_esc = (unsigned long long *)ctx->sync.p + 2 * (ctx->nsync + 1);
     E.dyn = dyn;
     const int egrid = (int)(etiles < (uint64_t)(4 * ctx->sm_count) ? etiles : 4 * ctx->sm_count);
     auto codebook_launch = [&]() -> int {
@@ -528,20 +537,31 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
                 { int _rc = lc_debug_check(ctx, "lc_quant_wfix_kernel (resume)", __FILE__, __LINE__); if (_rc) return _rc; }
                 P.resume = 0;
                 P.first_tile = 0;
+                lc_sync_starts_kernel<<<(int)((P.ntiles + 255) / 256 < 2 * ctx->sm_count ? (P.ntiles + 255) / 256
+                                                                                        : 2 * ctx->sm_count), 256, 0, st>>>(P);
+                ctx->launches += 1;
                 LC_CUDA_OK(cudaMemcpyAsync(hbad, first_bad, 8, cudaMemcpyDeviceToHost, st));
                 LC_CUDA_OK(cudaMemcpyAsync(hD0, P.resume_D0, 8, cudaMemcpyDeviceToHost, st));
                 LC_CUDA_OK(cudaStreamSynchronize(st));
                 if (*hD0 == *hD0 || *hbad != fb) continue;   // resumed (or the next failure is elsewhere)
             }
             full = true;
+            // relaunch from the start of the failing chunk's warp tile (launches stay
+            // tile aligned, so v3 sync starts map onto warp tiles): its exact start
+            // is the failing chunk's exact start, or the tile's sync start (before
+            // the first failure every predicted start is exact)
+            const long long fa = P.first_chunk + (((long long)fb - P.first_chunk) / 32) * 32;
             double anchor;
-            LC_CUDA_OK(cudaMemcpy(&anchor, P.bad_end + (fb - 1), sizeof(double), cudaMemcpyDeviceToHost));
+            if (fa == (long long)fb)
+                LC_CUDA_OK(cudaMemcpy(&anchor, P.bad_end + (fb - 1), sizeof(double), cudaMemcpyDeviceToHost));
+            else
+                LC_CUDA_OK(cudaMemcpy(&anchor, P.sync_start + fa / 32, sizeof(double), cudaMemcpyDeviceToHost));
             if (!isfinite(anchor)) {
                 // a prediction failed before any exact start was known (the offset
                 // look-back gave no finite value): restart this launch sequentially
                 relaunches = (uint32_t)ctx->opt[LC_OPT_MAX_QUANT] + 1;
             } else {
-                P.first_chunk = (int64_t)fb;
+                P.first_chunk = (int64_t)fa;
                 P.anchor_val = anchor;
             }
             P.inject_chunk = -1;
@@ -787,6 +807,53 @@ int lc_decompress_f64(lc_ctx *ctx, uint64_t n, double eb_abs, double first_value
     return lc_decompress_impl2(ctx, n, eb_abs, first_value, code_lengths, n_lengths, payload, payload_bytes,
                                payload_bits, esc_idx, esc_val, n_esc, inputs_on_device, out, out_on_device,
                                esc_used, nullptr, 0);
+}
+
+int lc_result_sync_v3(lc_ctx *ctx, uint64_t *offsets, double *starts, uint64_t *escapes, uint64_t cap,
+                      uint64_t *count)
+{
+    if (!ctx) return 12;
+    LcDeviceGuard guard(ctx->device);
+    if (count) *count = ctx->nsync;
+    const uint64_t k = cap < ctx->nsync ? cap : ctx->nsync;
+    const uint64_t stride = ctx->nsync + 1;
+    if (k) {
+        if (offsets) LC_CUDA_OK(cudaMemcpyAsync(offsets, ctx->sync.p, k * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        if (starts)
+            LC_CUDA_OK(cudaMemcpyAsync(starts, (uint64_t *)ctx->sync.p + stride, k * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        if (escapes)
+            LC_CUDA_OK(cudaMemcpyAsync(escapes, (uint64_t *)ctx->sync.p + 2 * stride, k * 8, cudaMemcpyDeviceToHost,
+                                       ctx->stream));
+        LC_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    }
+    return 0;
+}
+
+int lc_result_sync_device(lc_ctx *ctx, const uint64_t **offsets, const double **starts, const uint64_t **escapes)
+{
+    if (!ctx) return 12;
+    const uint64_t stride = ctx->nsync + 1;
+    if (offsets) *offsets = (const uint64_t *)ctx->sync.p;
+    if (starts) *starts = (const double *)((const uint64_t *)ctx->sync.p + stride);
+    if (escapes) *escapes = (const uint64_t *)ctx->sync.p + 2 * stride;
+    return 0;
+}
+
+int lc_decompress_v3_f64(lc_ctx *ctx, uint64_t n, double eb_abs, double first_value, const uint8_t *code_lengths,
+                         uint64_t n_lengths, const uint8_t *payload, uint64_t payload_bytes, uint64_t payload_bits,
+                         const uint64_t *sync, const double *sync_starts, const uint64_t *sync_esc, uint64_t n_sync,
+                         uint32_t sync_k, const uint64_t *esc_idx, const double *esc_val, uint64_t n_esc,
+                         int inputs_on_device, double *out, int out_on_device, int64_t *esc_used)
+{
+    if (!ctx) return 12;
+    if (!sync || !sync_starts || !sync_esc || sync_k != LC_SYNC_K || n < 2 ||
+        n_sync != (n - 1 + LC_SYNC_K - 1) / LC_SYNC_K)
+        return 12;
+    LcDeviceGuard guard(ctx->device);
+    if (!guard.ok) LC_CUDA_OK(cudaSetDevice(ctx->device));
+    return lc_decompress_impl2(ctx, n, eb_abs, first_value, code_lengths, n_lengths, payload, payload_bytes,
+                               payload_bits, esc_idx, esc_val, n_esc, inputs_on_device, out, out_on_device,
+                               esc_used, sync, n_sync, sync_starts, sync_esc);
 }
 
 int lc_result_sync(lc_ctx *ctx, uint64_t *offsets, uint64_t cap, uint64_t *count)

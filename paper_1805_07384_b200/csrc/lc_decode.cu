@@ -928,6 +928,218 @@ __global__ void __launch_bounds__(256) lc_dec_v2_kernel(LcDecParams P, const uns
     }
 }
 
+// v3 blocks: every LC_SYNC_K-th symbol carries its payload bit offset, the
+// exact chain value before it and the escape count before it, so each sync
+// interval decodes AND reconstructs on its own -- no segment synchronisation,
+// no offset maps, one pass.  Thread = interval: it walks its codewords
+// (huffman.py:110-132) and runs the reference chain (compressor.py:358-376)
+// from the stored start; the warp's lanes step in lockstep and every 32 steps
+// the 32 x 32 values staged in shared memory leave as 32 coalesced 256-byte
+// rows.  Checks: each interval ends exactly at the next sync point's bit
+// offset, chain value and escape count, the first start is first_value
+// (status 6: the table disagrees with the payload); decode statuses 1 / 2 as
+// v1; escape codes beyond n_esc and escape positions (flags, like
+// compressor.py:435-439).
+struct LcDecV3Tables {               // the single-codeword part of LcDecTables (~21 KB)
+    int max_len, canon;
+    unsigned s16;
+    int pad;
+    unsigned long long lim[34];
+    unsigned long long first_code[66];
+    unsigned long long offset[66];
+    unsigned int lut[1 << LC_LUT_BITS];
+    unsigned char len16[LC_L16];
+};
+#define LC_V3_TPB 256
+
+struct LcV3Final {
+    int status;
+    int esc_flags[2];                // [0] more escape codes than values, [1] position mismatch
+    int pad;
+    long long esc_total;             // escape codes in the block
+};
+
+// MSB-first bit reader for the v3 walk with a register prefetch ring: the
+// payload words reach registers in aligned 16-byte groups loaded two groups
+// (256 bits) ahead of use, so a refill never waits on the memory system (the
+// L1 is mostly shared memory here, and each lane walks its own stream).
+struct LcV3Reader {
+    const uint4 *g4;             // payload as 16-byte groups
+    uint4 cur, n1, n2;           // group of word `next`, the two after it
+    unsigned long long buf;      // top nb bits valid
+    unsigned pos, next;          // bits consumed (relative to the group base); next word to buffer
+    int nb;
+    __device__ __forceinline__ static uint32_t pick(const uint4 &q, unsigned k)
+    {
+        const uint32_t lo = (k & 1) ? q.y : q.x, hi = (k & 1) ? q.w : q.z;
+        return __byte_perm((k & 2) ? hi : lo, 0, 0x0123);
+    }
+    __device__ __forceinline__ uint32_t take()
+    {
+        const uint32_t v = pick(cur, next & 3u);
+        ++next;
+        if ((next & 3u) == 0) {
+            cur = n1;
+            n1 = n2;
+            n2 = __ldg(g4 + (next >> 2) + 2);
+        }
+        return v;
+    }
+    __device__ __forceinline__ void seek(unsigned p)
+    {
+        pos = p;
+        next = p >> 5;
+        const unsigned gi = next >> 2;
+        cur = __ldg(g4 + gi);
+        n1 = __ldg(g4 + gi + 1);
+        n2 = __ldg(g4 + gi + 2);
+        const int sh = (int)(p & 31);
+        const uint32_t w0 = take(), w1 = take();
+        buf = (((unsigned long long)w0 << 32) | w1) << sh;
+        nb = 64 - sh;
+        if (nb <= 32) { buf |= (unsigned long long)take() << (32 - nb); nb += 32; }
+    }
+    __device__ __forceinline__ void consume(int l)
+    {
+        if (l >= nb) { seek(pos + l); return; }      // codes longer than the buffer (rare)
+        buf <<= l;
+        nb -= l;
+        pos += l;
+        if (nb <= 32) { buf |= (unsigned long long)take() << (32 - nb); nb += 32; }
+    }
+};
+
+// The rare codeword paths of lc_dec_v3_kernel (codes longer than the LUT, the
+// payload end, invalid codewords), kept out of line so the hot loop stays small.
+// Returns sym | l << 32 | status << 40 (l = 0: no codeword; the reader is
+// passed by value so the caller's stays in registers).
+__device__ __noinline__ unsigned long long lc_v3_slow_symbol(const LcDecV3Tables &Ts, const LcDecTables *Tg,
+                                                            const uint32_t *__restrict__ sorted,
+                                                            const LcBitReader<LcGlobSrc> br, unsigned bits_rel)
+{
+    int l = lc_long_len_fast(Ts, br.buf);
+    if (l && l <= 32 && br.pos + (unsigned)l <= bits_rel) {
+        const unsigned long long v = (br.buf >> 32) >> (32 - l);
+        return __ldg(sorted + Ts.offset[l] + (v - Ts.first_code[l])) | ((unsigned long long)l << 32);
+    }
+    int term = 0;
+    uint32_t sym = 0;
+    l = lc_next_symbol(*Tg, sorted, br, bits_rel, &sym, &term);
+    if (!l) return (unsigned long long)(term == 4 ? 2 : term) << 40;
+    return sym | ((unsigned long long)l << 32);
+}
+
+__global__ void __launch_bounds__(LC_V3_TPB) lc_dec_v3_kernel(LcDecParams P, const unsigned long long *__restrict__ sync,
+                                                             const double *__restrict__ starts,
+                                                             const unsigned long long *__restrict__ sesc,
+                                                             unsigned long long nsync, unsigned long long m,
+                                                             double first_value, double delta,
+                                                             const double *__restrict__ esc_val,
+                                                             const unsigned long long *__restrict__ esc_idx,
+                                                             unsigned long long n_esc, double *__restrict__ out,
+                                                             LcV3Final *fin)
+{
+    __shared__ LcDecV3Tables Ts;
+    extern __shared__ double v3_stage[];                 // [warps][32 rows][33]
+    const LcDecTables *Tg = P.T;
+    if (threadIdx.x == 0) { Ts.max_len = Tg->max_len; Ts.canon = Tg->canon; Ts.s16 = Tg->s16; }
+    for (int i = threadIdx.x; i < 34; i += blockDim.x) Ts.lim[i] = Tg->lim[i];
+    for (int i = threadIdx.x; i < 66; i += blockDim.x) { Ts.first_code[i] = Tg->first_code[i]; Ts.offset[i] = Tg->offset[i]; }
+    for (int i = threadIdx.x; i < (1 << LC_LUT_BITS) / 4; i += blockDim.x)
+        reinterpret_cast<uint4 *>(Ts.lut)[i] = __ldg(reinterpret_cast<const uint4 *>(Tg->lut) + i);
+    for (int i = threadIdx.x; i < LC_L16 / 16; i += blockDim.x)
+        reinterpret_cast<uint4 *>(Ts.len16)[i] = __ldg(reinterpret_cast<const uint4 *>(Tg->len16) + i);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    double *stg = v3_stage + (size_t)wid * 32 * 33;
+    double *myrow = stg + lane * 33;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        out[0] = first_value;
+        if (nsync && lc_bits(starts[0]) != lc_bits(first_value)) atomicExch(&fin->status, 6);
+    }
+    const unsigned long long ngroups = (nsync + 31) / 32;
+    for (unsigned long long g = (unsigned long long)blockIdx.x * (LC_V3_TPB / 32) + wid; g < ngroups;
+         g += (unsigned long long)gridDim.x * (LC_V3_TPB / 32)) {
+        const unsigned long long j = g * 32 + lane;      // this lane's interval
+        const bool live = j < nsync;
+        const unsigned long long o0 = j * LC_SYNC_K;
+        unsigned todo = live ? (unsigned)min((unsigned long long)LC_SYNC_K, m - o0) : 0u;
+        const unsigned long long s0 = live ? sync[j] : 0ull;
+        const unsigned long long s1 = live ? (j + 1 < nsync ? sync[j + 1] : P.bits) : 0ull;
+        int bad = 0;
+        if (live && (s0 > s1 || s1 > P.bits || (j == 0 && s0 != 0))) { bad = 6; todo = 0; }
+        const unsigned long long wbase = s0 & ~127ull;    // 16-byte group of the start
+        const unsigned bits_rel = lc_bits_rel(P.bits, wbase);
+        LcV3Reader br;
+        br.g4 = reinterpret_cast<const uint4 *>(P.payload + wbase / 32);
+        br.pos = 0;
+        if (todo) br.seek((unsigned)(s0 - wbase));
+        double r = live ? starts[j] : 0.0;
+        unsigned long long e = live ? sesc[j] : 0ull;
+        int fl0 = 0, fl1 = 0;
+        const unsigned wsteps = __reduce_max_sync(0xffffffffu, todo);
+        for (unsigned sb = 0; sb < wsteps; sb += 32) {
+            const unsigned nt = todo > sb ? min(32u, todo - sb) : 0u;   // symbols of this block
+            unsigned t = 0;
+            auto step = [&](uint32_t sy, unsigned tt) {        // one reference step, value to the row
+                if (sy == 0) {                                        // compressor.py:365-369
+                    const unsigned long long pos = o0 + sb + tt + 1;  // element index
+                    if (e < n_esc) {
+                        r = esc_val[e];
+                        fl1 |= esc_idx[e] != pos;
+                    } else {
+                        fl0 = 1;
+                    }
+                    ++e;
+                } else {                                              // :370-374
+                    const uint32_t zz = sy - 1u;
+                    const int mm = (int)(zz >> 1) ^ -(int)(zz & 1u);
+                    if (mm != 0) r = LC_ADD(r, LC_MUL((double)mm, delta));
+                }
+                myrow[tt] = r;
+            };
+#pragma unroll 1
+            while (t < nt) {
+                const unsigned w12 = (unsigned)(br.buf >> (64 - LC_LUT_BITS));
+                const uint32_t e1 = Ts.lut[w12];
+                uint32_t sym = e1 & 0xffffffu;
+                int l = (int)(e1 >> 24);
+                if (e1 == 0xffffffffu || br.pos + (unsigned)l > bits_rel) {
+                    LcBitReader<LcGlobSrc> gr;                        // the same position, global reads
+                    gr.src.w = P.payload + wbase / 32;
+                    gr.buf = br.buf; gr.nb = br.nb; gr.pos = br.pos; gr.next = br.next;
+                    const unsigned long long sl = lc_v3_slow_symbol(Ts, Tg, P.sorted, gr, bits_rel);
+                    sym = (uint32_t)sl;
+                    l = (int)((sl >> 32) & 0xff);
+                    if (!l) { bad = (int)(sl >> 40); todo = 0; break; }
+                }
+                br.consume(l);
+                step(sym, t);
+                ++t;
+            }
+            __syncwarp();
+            // rows: lane L's values go to out[o0(L) + sb + 1 ...]
+            for (int rr = 0; rr < 32; ++rr) {
+                const unsigned long long jr = g * 32 + rr;
+                if (jr >= nsync) break;
+                const unsigned long long base = jr * LC_SYNC_K + sb + 1;
+                const unsigned long long lim = min((unsigned long long)LC_SYNC_K, m - jr * LC_SYNC_K);
+                if (sb + lane < lim) __stcs(out + base + lane, stg[rr * 33 + lane]);
+            }
+            __syncwarp();
+        }
+        if (live) {
+            if (bad) atomicExch(&fin->status, bad);
+            else if (wbase + br.pos != s1) atomicExch(&fin->status, 6);
+            else if (j + 1 < nsync && (lc_bits(r) != lc_bits(starts[j + 1]) || e != sesc[j + 1]))
+                atomicExch(&fin->status, 6);
+            if (fl0) atomicExch(&fin->esc_flags[0], 1);
+            if (fl1) atomicExch(&fin->esc_flags[1], 1);
+            if (j + 1 == nsync) fin->esc_total = (long long)e;
+        }
+    }
+}
+
 // Resolve the reference status (huffman.py:114-132) from the segment walk.
 __global__ void lc_dec_status_kernel(const LcSeg *__restrict__ seg, const unsigned long long *__restrict__ off,
                                      const unsigned long long *__restrict__ total_and_term,
@@ -1427,6 +1639,7 @@ __global__ void __launch_bounds__(LC_TPB, 3) lc_rec_b_kernel(LcRecParams P, LcRe
 }
 
 size_t lc_rec_a_smem_bytes() { return sizeof(uint32_t) * LC_TPB * LC_ROW; }
+static size_t lc_dec_v3_smem() { return sizeof(double) * (LC_V3_TPB / 32) * 32 * 33; }
 size_t lc_rec_b_smem_bytes() { return sizeof(double) * LC_TPB * LC_ROW; }
 
 
@@ -1460,7 +1673,8 @@ int lc_decompress_impl2(lc_ctx *ctx, uint64_t n, double eb_abs, double first_val
                         const uint8_t *code_lengths, uint64_t n_lengths, const uint8_t *payload,
                         uint64_t payload_bytes, uint64_t payload_bits, const uint64_t *esc_idx,
                         const double *esc_val, uint64_t n_esc, int inputs_on_device, double *out,
-                        int out_on_device, int64_t *esc_used, const uint64_t *sync, uint64_t n_sync)
+                        int out_on_device, int64_t *esc_used, const uint64_t *sync, uint64_t n_sync,
+                        const double *sync_starts, const uint64_t *sync_esc)
 {
     if (n < 2 || n_lengths == 0 || n_lengths > (1ull << 31) + 2 || payload_bits > 8 * payload_bytes) return 12;
     cudaStream_t st = lc_stream(ctx);
@@ -1503,6 +1717,58 @@ int lc_decompress_impl2(lc_ctx *ctx, uint64_t n, double eb_abs, double first_val
     // Huffman decode
     const int code_bytes = n_lengths <= 65536 ? 2 : 4;
     LC_CUDA_OK(lc_reserve(bcodes, m * code_bytes + 16));
+    if (sync && sync_starts && sync_esc) {              // v3: decode + reconstruct per sync interval
+        LC_CUDA_OK(lc_reserve(baux, 256));
+        LcV3Final *dfin = (LcV3Final *)((char *)baux.p + 64);
+        LcV3Final *hfin = (LcV3Final *)((char *)lc_pinned(ctx) + 256);
+        LC_CUDA_OK(lc_reserve(bsync, n_sync * 24 + 64));
+        const cudaMemcpyKind k = inputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+        unsigned long long *dsync = (unsigned long long *)bsync.p;
+        double *dstart = (double *)(dsync + n_sync);
+        unsigned long long *desc = (unsigned long long *)(dstart + n_sync);
+        LC_CUDA_OK(cudaMemcpyAsync(dsync, sync, n_sync * 8, k, st));
+        LC_CUDA_OK(cudaMemcpyAsync(dstart, sync_starts, n_sync * 8, k, st));
+        LC_CUDA_OK(cudaMemcpyAsync(desc, sync_esc, n_sync * 8, k, st));
+        LC_CUDA_OK(cudaMemsetAsync(dfin, 0, sizeof(LcV3Final), st));
+        double *dout = out;
+        if (!out_on_device) {
+            LC_CUDA_OK(lc_reserve(bout, n * 8));
+            dout = (double *)bout.p;
+        }
+        LcDecParams DP;
+        DP.payload = (const uint32_t *)bpay.p;
+        DP.bits = payload_bits;
+        DP.T = T;
+        DP.sorted = sorted;
+        DP.nseg = 0; DP.nblk = 0; DP.seg_bits = 0; DP.nwords = words;
+        LC_CUDA_OK(cudaEventRecord(lc_phase_ev(ctx, 8), st));
+        LC_CUDA_OK(cudaEventRecord(lc_phase_ev(ctx, 9), st));
+        LC_CUDA_OK(cudaEventRecord(lc_phase_ev(ctx, 6), st));
+        const unsigned long long ngroups = (n_sync + 31) / 32;
+        const unsigned long long want = (ngroups + LC_V3_TPB / 32 - 1) / (LC_V3_TPB / 32);
+        int occ = 1;
+        LC_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lc_dec_v3_kernel, LC_V3_TPB, lc_dec_v3_smem()));
+        const unsigned long long cap = (unsigned long long)(occ > 0 ? occ : 1) * lc_sm_count(ctx);
+        const int g = (int)(want < cap ? (want > 0 ? want : 1) : cap);
+        lc_dec_v3_kernel<<<g, LC_V3_TPB, lc_dec_v3_smem(), st>>>(DP, dsync, dstart, desc, n_sync, m, first_value,
+                                                                2.0 * eb_abs, (const double *)beval.p,
+                                                                (const unsigned long long *)beidx.p, n_esc, dout, dfin);
+        { int _rc = lc_debug_check(ctx, "lc_dec_v3_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+        lc_count_launch(ctx, 1);
+        LC_CUDA_OK(cudaMemcpyAsync(hfin, dfin, sizeof(LcV3Final), cudaMemcpyDeviceToHost, st));
+        LC_CUDA_OK(cudaEventRecord(lc_phase_ev(ctx, 7), st));
+        LC_CUDA_OK(cudaStreamSynchronize(st));
+        lc_set_kind(ctx, 2);
+        if (hfin->status) return hfin->status;
+        const int64_t used = hfin->esc_flags[0] ? -1 : (int64_t)hfin->esc_total;
+        if (esc_used) *esc_used = used;
+        if (used < 0 || (uint64_t)used != n_esc) return 4;
+        if (n_esc && hfin->esc_flags[1]) return 5;
+        if (!out_on_device) LC_CUDA_OK(cudaMemcpyAsync(out, dout, n * 8, cudaMemcpyDeviceToHost, st));
+        LC_CUDA_OK(cudaEventRecord(lc_ev(ctx, 1), st));
+        LC_CUDA_OK(cudaStreamSynchronize(st));
+        return 0;
+    }
     if (sync) {                                         // v2: decode straight from the sync table
         LC_CUDA_OK(lc_reserve(baux, 256));
         int *status = (int *)((char *)baux.p + 64);
@@ -1869,6 +2135,7 @@ int lc_decode_init_attrs()
     set((const void *)lc_dec_write_kernel<uint16_t>, wmax16);
     set((const void *)lc_dec_write_kernel<uint32_t>, wmax32);
     set((const void *)lc_rec_a_kernel, lc_rec_a_smem_bytes());
+    set((const void *)lc_dec_v3_kernel, lc_dec_v3_smem());
     set((const void *)lc_rec_b_kernel<2>, lc_rec_b_smem_bytes());
     set((const void *)lc_rec_b_kernel<4>, lc_rec_b_smem_bytes());
     return (int)e;

@@ -15,12 +15,13 @@
 // thread's bit range are stored directly, the two boundary words use
 // atomicOr on a zeroed payload.  Escape positions are compacted in the same
 // pass (compressor.py:409-410).
+#include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_scan.cuh>
 #include "lc_kernels.cuh"
 
 #define LC_CB_THREADS 1024
 #define LC_CB_SMEM_KEYS 4096
-#define LC_ENC_TAB 4096
+#define LC_ENC_TAB 8192                 // smem code table entries: (len << 27) | code, codes <= 27 bits
 
 
 __device__ __forceinline__ void lc_bitonic_sort(unsigned long long *a, int npow2)
@@ -38,6 +39,37 @@ __device__ __forceinline__ void lc_bitonic_sort(unsigned long long *a, int npow2
             __syncthreads();
         }
     }
+}
+
+// Large alphabets (more used symbols than fit the shared-memory working set):
+// sort the (freq, p) keys with a block radix sort on the frequency (stable, so
+// equal frequencies stay in p = symbol order) held in registers, 16 keys per
+// thread, instead of a bitonic network over global memory (~100 passes with a
+// CTA barrier each).  temp: the (unused) dynamic shared memory.
+#define LC_CB_RADIX_ITEMS 16
+#define LC_CB_RADIX_KEYS (LC_CB_THREADS * LC_CB_RADIX_ITEMS)
+static_assert(sizeof(cub::BlockRadixSort<uint32_t, LC_CB_THREADS, LC_CB_RADIX_ITEMS, uint32_t>::TempStorage) <=
+                  (2 * sizeof(unsigned long long) + 2 * sizeof(int) + sizeof(uint32_t) + 1) * LC_CB_SMEM_KEYS,
+              "radix-sort scratch must fit the codebook's dynamic shared memory");
+__device__ __forceinline__ void lc_radix_sort_keys(unsigned long long *keys, int k, int npow2, void *temp)
+{
+    typedef cub::BlockRadixSort<uint32_t, LC_CB_THREADS, LC_CB_RADIX_ITEMS, uint32_t> RS;
+    uint32_t kf[LC_CB_RADIX_ITEMS], kv[LC_CB_RADIX_ITEMS];
+#pragma unroll
+    for (int i = 0; i < LC_CB_RADIX_ITEMS; ++i) {
+        const int idx = threadIdx.x * LC_CB_RADIX_ITEMS + i;
+        const unsigned long long key = idx < k ? keys[idx] : ~0ull;
+        kf[i] = (uint32_t)(key >> 32);
+        kv[i] = (uint32_t)key;
+    }
+    __syncthreads();
+    RS(*reinterpret_cast<typename RS::TempStorage *>(temp)).Sort(kf, kv);
+#pragma unroll
+    for (int i = 0; i < LC_CB_RADIX_ITEMS; ++i) {
+        const int idx = threadIdx.x * LC_CB_RADIX_ITEMS + i;
+        if (idx < npow2) keys[idx] = ((unsigned long long)kf[i] << 32) | kv[i];
+    }
+    __syncthreads();
 }
 
 // hist[nbins] -> lengths[nbins], codes[nbins], meta.  Working arrays live in
@@ -102,7 +134,8 @@ __device__ __forceinline__ void lc_codebook_body(const uint32_t *__restrict__ hi
     }
     if (tid == 0) out->stamp[0] = lc_gtimer();
     // 2. sort by (freq, symbol)
-    lc_bitonic_sort(keys, npow2);
+    if (!SMEM && npow2 <= LC_CB_RADIX_KEYS) lc_radix_sort_keys(keys, k, npow2, lc_dyn_smem);
+    else lc_bitonic_sort(keys, npow2);
     if (tid == 0) out->stamp[1] = lc_gtimer();
 
     // 3. two-queue merge (huffman.py:36-48: heapq pops (freq, counter); leaves were
@@ -402,24 +435,28 @@ struct LcCodeRegs {
 };
 
 template <typename CodeT>
-__global__ void __launch_bounds__(LC_ENC_NT) lc_encode_kernel(LcEncParams P)
+__global__ void __launch_bounds__(LC_ENC_NT, 4) lc_encode_kernel(LcEncParams P)
 {
     if (P.dyn && P.dyn->skip) return;
     typedef cub::BlockScan<unsigned long long, LC_ENC_NT> ScanU;
     extern __shared__ __align__(16) unsigned char lc_dyn_smem[];
-    unsigned long long *tpk = reinterpret_cast<unsigned long long *>(lc_dyn_smem);   // (len << 32) | code
-    uint32_t *wbuf = reinterpret_cast<uint32_t *>(tpk + LC_ENC_TAB);
+    uint32_t *tpk = reinterpret_cast<uint32_t *>(lc_dyn_smem);   // (len << 27) | code
+    uint32_t *wbuf = tpk + LC_ENC_TAB;
     __shared__ typename ScanU::TempStorage scan_tmp;
     __shared__ long long sh_tile;
     __shared__ unsigned long long sh_in_bits, sh_in_esc;
     const int tid = threadIdx.x;
     const CodeT *codes = reinterpret_cast<const CodeT *>(P.codes);
     const bool fast = P.cb->max_len <= 32;
-    const uint32_t tab = P.nbins < LC_ENC_TAB ? P.nbins : LC_ENC_TAB;
+    const bool packed = P.cb->max_len <= 27;              // codes fit the 32-bit table entries
+    const uint32_t tab = packed ? (P.nbins < LC_ENC_TAB ? P.nbins : LC_ENC_TAB) : 0u;
     for (uint32_t s = tid; s < tab; s += LC_ENC_NT)
-        tpk[s] = ((unsigned long long)P.lengths[s] << 32) | (fast ? (uint32_t)P.cw[s] : 0u);
+        tpk[s] = ((uint32_t)P.lengths[s] << 27) | (uint32_t)P.cw[s];
+    auto unpack = [](uint32_t t) -> unsigned long long {
+        return ((unsigned long long)(t >> 27) << 32) | (t & 0x7ffffffu);
+    };
     auto entry = [&](uint32_t s) -> unsigned long long {
-        return s < LC_ENC_TAB ? tpk[s] : (((unsigned long long)P.lengths[s] << 32) | (uint32_t)P.cw[s]);
+        return s < tab ? unpack(tpk[s]) : (((unsigned long long)P.lengths[s] << 32) | (uint32_t)P.cw[s]);
     };
 
     for (;;) {
@@ -456,12 +493,11 @@ __global__ void __launch_bounds__(LC_ENC_NT) lc_encode_kernel(LcEncParams P)
 #pragma unroll
         for (int k = 0; k < LcCodeRegs<CodeT>::NW; ++k) cmax = sizeof(CodeT) == 2 ? __vmaxu2(cmax, C.w[k]) : max(cmax, C.w[k]);
         if (sizeof(CodeT) == 2) cmax = max(cmax & 0xffffu, cmax >> 16);
-        const bool tabled = len == LC_L && cmax < LC_ENC_TAB;
-        const uint32_t *tlen = reinterpret_cast<const uint32_t *>(tpk) + 1;   // high words: lengths
+        const bool tabled = len == LC_L && cmax < tab;
         uint32_t bits32 = 0, nesc32 = 0;
         if (tabled) {
 #pragma unroll
-            for (int j = 0; j < LC_L; ++j) bits32 += tlen[2 * C.get(j)];
+            for (int j = 0; j < LC_L; ++j) bits32 += tpk[C.get(j)] >> 27;
 #pragma unroll
             for (int k = 0; k < LcCodeRegs<CodeT>::NW; ++k)
                 nesc32 += sizeof(CodeT) == 2 ? __popc(__vcmpeq2(C.w[k], 0u)) >> 4 : (C.w[k] == 0u);
@@ -537,7 +573,7 @@ __global__ void __launch_bounds__(LC_ENC_NT) lc_encode_kernel(LcEncParams P)
                 };
                 if (tabled) {
 #pragma unroll
-                    for (int j = 0; j < LC_L; ++j) put(tpk[C.get(j)]);
+                    for (int j = 0; j < LC_L; ++j) put(unpack(tpk[C.get(j)]));
                 } else {
 #pragma unroll
                     for (int j = 0; j < LC_L; ++j)
@@ -552,8 +588,10 @@ __global__ void __launch_bounds__(LC_ENC_NT) lc_encode_kernel(LcEncParams P)
         }
         const unsigned long long B0 = sh_in_bits;
         // v2 sync table: bit offset of every LC_SYNC_K-th symbol
-        if (P.sync && len > 0 && (p0 & (LC_SYNC_K - 1)) == 0)
+        if (P.sync && len > 0 && (p0 & (LC_SYNC_K - 1)) == 0) {
             P.sync[p0 / LC_SYNC_K] = B0 + (ex & 0xffffffffull);
+            if (P.sync_esc) P.sync_esc[p0 / LC_SYNC_K] = sh_in_esc + (ex >> 32);
+        }
         // escapes (compressor.py:409-410): code index i-1 <-> element i
         if (nesc) {
             unsigned long long e = sh_in_esc + (ex >> 32);
@@ -619,7 +657,7 @@ size_t lc_codebook_smem_bytes()
 }
 size_t lc_encode_smem_bytes()
 {
-    return sizeof(unsigned long long) * LC_ENC_TAB + sizeof(uint32_t) * LC_ENC_WBUF;
+    return sizeof(uint32_t) * LC_ENC_TAB + sizeof(uint32_t) * LC_ENC_WBUF;
 }
 
 template __global__ void lc_encode_kernel<uint16_t>(LcEncParams);

@@ -98,6 +98,9 @@ struct LcQuantParams {
     long long resume_chunk;      // first chunk whose predicted start was wrong
     const double *resume_start;  // its exact start (bad_end of its predecessor)
     double *resume_D0;           // mode 1 output: offset at the next tile start (NaN: resume impossible)
+    double *tile_g0;             // [ntiles] pass A: guess of the chain value at each warp tile start
+    double *sync_start;          // [nsync] exact chain value at every LC_SYNC_K-th element (v3 blocks)
+    unsigned long long nsync;
 };
 
 // v2 blocks: a bit offset for every LC_SYNC_K-th symbol (a multiple of LC_L)
@@ -147,6 +150,7 @@ struct LcEncParams {
     const LcQuantDyn *dyn;   // device-resolved bounds (skip flag), may be null
     unsigned long long esc_cap;   // capacity of esc_idx / esc_val (host re-runs when short)
     unsigned long long *sync; // v2 sync table [ceil(m / LC_SYNC_K)] (bit offsets), may be null
+    unsigned long long *sync_esc;   // v3: escape codes before every LC_SYNC_K-th symbol, may be null
 };
 
 __global__ void lc_range_kernel(const double *__restrict__ x, uint64_t n, LcRangePart *__restrict__ parts,
@@ -172,6 +176,7 @@ __global__ void lc_map_scan_kernel(const OffMap *__restrict__ agg, double *__res
 int lc_launch_map_scan(const OffMap *agg, double *tileD, long long ntiles, void *scratch, int sm_count,
                        cudaStream_t st, const double *D0p = nullptr);
 template <typename CodeT> __global__ void lc_quant_serial_kernel(LcQuantParams P, CodeT *__restrict__ codes);
+__global__ void lc_sync_starts_kernel(LcQuantParams P);
 template <typename CodeT>
 __global__ void lc_hist_kernel(const CodeT *__restrict__ codes, uint64_t m, uint32_t *__restrict__ hist, uint32_t nbins);
 __global__ void lc_hist16_kernel(const uint16_t *__restrict__ codes, uint64_t m, uint32_t *__restrict__ hist,

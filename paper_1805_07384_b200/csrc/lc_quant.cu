@@ -351,11 +351,24 @@ __global__ void lc_quant_serial_kernel(LcQuantParams P, CodeT *__restrict__ code
     double r = P.anchor_val;
     for (uint64_t i = (uint64_t)P.first_chunk * LC_L + 1; i < P.n; ++i) {
         uint32_t code; int esc; double inc, pe;
+        if (P.sync_start && ((i - 1) & (LC_SYNC_K - 1)) == 0) P.sync_start[(i - 1) / LC_SYNC_K] = r;
         const double rn = lc_step(P.Q, P.x[i], r, &code, &esc, &inc, &pe);
         codes[i - 1] = (CodeT)code;
         if (P.pe) { P.pe[i - 1] = pe; P.pe_rec[i - 1] = LC_SUB(rn, r); }
         r = rn;
     }
+}
+
+// v3 sync starts: the exact chain value at the start of every warp tile of this
+// launch (= every LC_SYNC_K-th element; launches start on warp tiles), from
+// pass A's tile guess and the map scan's exact offset -- after pass B every
+// predicted tile start is the reference's value.
+__global__ void lc_sync_starts_kernel(LcQuantParams P)
+{
+    if (!lc_quant_dyn(P) || !P.sync_start) return;
+    const long long k0 = P.first_chunk / 32;
+    for (long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x; w < P.ntiles; w += (long long)gridDim.x * blockDim.x)
+        if ((unsigned long long)(k0 + w) < P.nsync) P.sync_start[k0 + w] = lc_apply_offset(P.tile_g0[w], P.tile_D[w]);
 }
 
 // Histogram recount from final codes (used after relaunches).

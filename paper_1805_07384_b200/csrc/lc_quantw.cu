@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(LC_QW_TPB, 5) lc_quant_wa_kernel(LcQuantParams
 #pragma unroll
         for (int o = 16; o; o >>= 1) s = fmin(s, __shfl_xor_sync(0xffffffffu, s, o));
         if (lane == 31) P.tile_agg[w] = L.inc;
-        if (lane == 0) P.tile_S[w] = s;
+        if (lane == 0) { P.tile_S[w] = s; P.tile_g0[w] = L.g0; }
         // codes: coalesced 16-byte stores from the staging rows
         __syncwarp();
         const long long pbeg = (P.first_chunk + w * 32) * LC_L;
@@ -450,6 +450,7 @@ __global__ void __launch_bounds__(LC_QW_TPB, 5) lc_quant_wfix_kernel(LcQuantPara
             ++exact_chunks;
         }
         if (lane == 31) *P.resume_D0 = Dnext;
+        if (f0 == 0 && lane == 0) P.tile_D[w] = D;       // the tile starts at the resumed chunk (v3 sync start)
         if (exact_chunks) atomicAdd(P.exact_count, exact_chunks);
         return;
     }

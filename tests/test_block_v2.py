@@ -45,7 +45,31 @@ def test_v2_wire_format_roundtrip_cpu():
     with pytest.raises(lc.IntegrityError):
         lc.CompressedBlock.from_bytes(raw[:off + 20])
     with pytest.raises(lc.ParameterError):
-        lc.CompressorConfig.absolute(1.0, block_version=3)
+        lc.CompressorConfig.absolute(1.0, block_version=4)
+
+
+def test_v3_wire_format_roundtrip_cpu():
+    """v3 = v2 + the chain value and escape count at every sync point (oracle-built)."""
+    import paper_1805_07384_b200 as lc
+    x = np.random.default_rng(3).normal(size=7000).cumsum()
+    x[[10, 2500, 6999]] += 1e6
+    ref = orc.compress(x, "value_range_relative", 1e-5)
+    sync = orc.sync_offsets(ref["codes"], ref["code_lengths"])
+    starts, escs = orc.sync_v3(ref["codes"], ref["recon"])
+    assert starts[0] == x[0] and escs[0] == 0 and escs[-1] <= len(ref["escape_indices"])
+    blk = lc.CompressedBlock(n=ref["n"], eb_abs=ref["eb_abs"], value_range=ref["value_range"],
+                             first_value=ref["first_value"], code_lengths=ref["code_lengths"],
+                             payload=ref["payload"], payload_bits=ref["payload_bits"],
+                             escape_indices=ref["escape_indices"], escape_values=ref["escape_values"],
+                             version=3, sync_offsets=sync, sync_starts=starts, sync_escapes=escs)
+    raw = blk.to_bytes()
+    assert len(raw) == len(orc.to_bytes(ref)) + 12 + 24 * sync.size
+    back = lc.CompressedBlock.from_bytes(raw)
+    assert back.version == 3 and back.to_bytes() == raw
+    assert np.array_equal(back.sync_starts.view(np.int64), starts.view(np.int64))
+    assert np.array_equal(back.sync_escapes, escs)
+    with pytest.raises(lc.IntegrityError):
+        lc.CompressedBlock.from_bytes(raw[:len(raw) - len(ref["payload"]) - 8])
 
 
 torch = pytest.importorskip("torch")
@@ -115,3 +139,80 @@ def test_v2_corrupted_sync_table(lc):
         lc.decompress(dataclasses.replace(b2, sync_offsets=s))
     with pytest.raises(lc.IntegrityError):
         lc.decompress(dataclasses.replace(b2, sync_offsets=b2.sync_offsets[:-1]))
+
+
+@pytest.mark.gpu
+def test_v3_tables_and_reconstruction(lc):
+    """v3 blocks: codes/payload/escapes are v1's (the reference's); the sync tables
+    equal the oracle's (bit offsets, reconstruction values, escape counts); the
+    one-pass v3 decoder reconstructs bit-identically to the reference."""
+    rng = np.random.default_rng(78)
+    spiky = rng.normal(size=30_000).cumsum()
+    spiky[rng.integers(0, spiky.size, 5)] += 1e9
+    cases = [(_sine(200_001, 1), 1e-4), (rng.normal(size=70_000).cumsum(), 1e-7),
+             (rng.normal(size=1025), 1e-2), (rng.normal(size=1024), 1e-3), (rng.normal(size=2), 1e-3),
+             (spiky, 1e-9), (_sine(100_000, 2), 1e-3)]
+    for x, eb in cases:
+        b1 = _blk(lc, x, eb, 1)
+        b3 = _blk(lc, x, eb, 3)
+        ref = orc.compress(x, "value_range_relative", eb)
+        assert b3.payload == b1.payload and np.array_equal(b3.escape_indices, b1.escape_indices)
+        st, es = orc.sync_v3(ref["codes"], ref["recon"])
+        assert np.array_equal(b3.sync_offsets, orc.sync_offsets(ref["codes"], ref["code_lengths"]))
+        assert np.array_equal(b3.sync_starts.view(np.int64), st.view(np.int64)), (x.size, eb)
+        assert np.array_equal(b3.sync_escapes, es)
+        b3 = lc.CompressedBlock.from_bytes(b3.to_bytes())
+        r3 = lc.decompress(b3)
+        assert np.array_equal(r3.view(np.int64), ref["recon"].view(np.int64)), (x.size, eb)
+
+
+@pytest.mark.gpu
+def test_v3_full_size_and_relaunch_paths(lc):
+    """2^26 elements at 1e-6 (v3 decode == v1 decode), and v3 tables through the
+    quantizer's resume / full-relaunch / sequential paths (injected failure)."""
+    from paper_1805_07384_b200 import _native
+    n = 1 << 26
+    x = _sine(n, 5)
+    b3 = _blk(lc, x, 1e-6, 3)
+    b1 = _blk(lc, x, 1e-6, 1)
+    d1 = lc.decompress(b1, device="cuda")
+    d3 = lc.decompress(b3, device="cuda")
+    assert torch.equal(d1.view(torch.int64), d3.view(torch.int64))
+    assert torch.equal(torch.from_numpy(b3.sync_starts).cuda().view(torch.int64), d1[:n - 1:1024].view(torch.int64))
+    ctx = _native.context(0)
+    y = _sine(300_000, 6)
+    ref = orc.compress(y, "absolute", 1e-3)
+    st, es = orc.sync_v3(ref["codes"], ref["recon"])
+    try:
+        for resume, maxr in ((1, 64), (0, 64), (1, 0)):
+            ctx.lib.lc_ctx_set_option(ctx.h, 5, resume)
+            ctx.lib.lc_ctx_set_option(ctx.h, 0, maxr)
+            ctx.lib.lc_ctx_set_option(ctx.h, 4, 1)
+            ctx.lib.lc_ctx_set_option(ctx.h, 2, 5000)           # wrong prediction for chunk 5000
+            b = lc.compress(y, lc.CompressorConfig.absolute(1e-3, block_version=3))
+            assert ctx.lib.lc_ctx_get_stat(ctx.h, 0) == 1
+            assert np.array_equal(b.sync_starts.view(np.int64), st.view(np.int64)), (resume, maxr)
+            assert np.array_equal(b.sync_escapes, es)
+            assert np.array_equal(lc.decompress(b).view(np.int64), ref["recon"].view(np.int64))
+    finally:
+        for k, v in ((5, 1), (0, 64), (4, 0), (2, -1)):
+            ctx.lib.lc_ctx_set_option(ctx.h, k, v)
+
+
+@pytest.mark.gpu
+def test_v3_corrupted_tables(lc):
+    x = np.random.default_rng(4).normal(size=50_000).cumsum()
+    x[[100, 20_000]] += 1e7
+    b3 = _blk(lc, x, 1e-6, 3)
+    assert lc.decompress(b3).size == x.size
+    for field, j, f in (("sync_starts", 1, lambda v: np.nextafter(v, np.inf)),
+                        ("sync_starts", 0, lambda v: v + 1.0),
+                        ("sync_starts", b3.sync_starts.size - 1, lambda v: -v),
+                        ("sync_escapes", 30, lambda v: v + np.uint64(1)),
+                        ("sync_offsets", 5, lambda v: v + np.uint64(1))):
+        t = getattr(b3, field).copy()
+        t[j] = f(t[j])
+        with pytest.raises(lc.IntegrityError):
+            lc.decompress(dataclasses.replace(b3, **{field: t}))
+    with pytest.raises(lc.IntegrityError):
+        lc.decompress(dataclasses.replace(b3, escape_indices=b3.escape_indices + 1))

@@ -81,7 +81,7 @@ def test_wire_format_errors():
     for cut in (3, 9, 20):
         with pytest.raises(IntegrityError):
             cp.CompressedBlock.from_bytes(blob[: len(blob) - cut])
-    bad_version = blob[:8] + (3).to_bytes(4, "little") + blob[12:]
+    bad_version = blob[:8] + (7).to_bytes(4, "little") + blob[12:]
     with pytest.raises(IntegrityError, match="unsupported block version"):
         cp.CompressedBlock.from_bytes(bad_version)
     with pytest.raises(ParameterError, match="16-bit"):
