@@ -242,7 +242,10 @@ def run_b200(args, rank, world, local_rank):
     wctx = [_native.Context(local_rank, ctypes.c_void_p(st.cuda_stream)) for st in wstreams]
     wout = [torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(nstr)]
 
-    def rt(eb_rel, stats=None, ctx=ctx, out=out, v3=False):
+    fmt3 = args.block_version == 3                   # the headline's block format (v3: repo checkpoints)
+
+    def rt(eb_rel, stats=None, ctx=ctx, out=out, v3=None):
+        v3 = fmt3 if v3 is None else v3
         # value range + device-resolved bounds + quantizer + codebook + encoder (one host
         # round trip, the path paper_1805_07384_b200.compress takes), then the decoder
         i = BOUNDS.index(eb_rel)
@@ -301,12 +304,12 @@ def run_b200(args, rank, world, local_rank):
         for eb in BOUNDS:
             rt(eb)
 
-    def lane_v3(k):
+    def lane_alt(k):                                 # the other block format (v1: the reference's)
         for i in range(k, len(BOUNDS), nstr):
-            rt(BOUNDS[i], ctx=wctx[k], out=wout[k], v3=True)
+            rt(BOUNDS[i], ctx=wctx[k], out=wout[k], v3=not fmt3)
 
-    def step_v3():
-        list(pool.map(lane_v3, range(nstr)))
+    def step_alt():
+        list(pool.map(lane_alt, range(nstr)))
 
     def barrier():
         if dist is not None:
@@ -343,18 +346,18 @@ def run_b200(args, rank, world, local_rank):
     ev3.record()
     torch.cuda.synchronize()
     ms_seq = ev2.elapsed_time(ev3) / args.steps
-    # the same concurrent step writing/reading v3 blocks (sync tables with chain values)
+    # the same concurrent step in the other block format
     for _ in range(2):
-        step_v3()
+        step_alt()
     barrier()
     ev4 = torch.cuda.Event(enable_timing=True)
     ev5 = torch.cuda.Event(enable_timing=True)
     ev4.record()
     for _ in range(args.steps):
-        step_v3()
+        step_alt()
     ev5.record()
     torch.cuda.synchronize()
-    ms_v3 = ev4.elapsed_time(ev5) / args.steps
+    ms_alt = ev4.elapsed_time(ev5) / args.steps
     if dist is not None:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -374,30 +377,34 @@ def run_b200(args, rank, world, local_rank):
         res = s["res"]
         cl = np.zeros(res.n_symbols, np.uint8)
         L.lc_result_fetch(ctx.h, cl.ctypes.data, None, None, None, None, None)
-        bb = block_bytes(res.payload_bytes, cl, res.n_esc)
+        bb1 = block_bytes(res.payload_bytes, cl, res.n_esc)          # v1 (reference) block
+        tab3 = 12 + 24 * ((n - 1 + 1023) // 1024)                      # v3 sync tables
+        bb = bb1 + tab3 if fmt3 else bb1
         cms = statistics.median(r["compress_ms"] for r in runs)
         dms = statistics.median(r["decompress_ms"] for r in runs)
-        runs3 = []
+        runs_alt = []
         for _ in range(3):
-            s3 = {}
-            rt(eb, s3, v3=True)
-            runs3.append(s3)
-        dms3 = statistics.median(r["decompress_ms"] for r in runs3)
-        cms3 = statistics.median(r["compress_ms"] for r in runs3)
-        bb3 = bb + 12 + 24 * ((n - 1 + 1023) // 1024)
+            sa = {}
+            rt(eb, sa, v3=not fmt3)
+            runs_alt.append(sa)
+        dms_alt = statistics.median(r["decompress_ms"] for r in runs_alt)
+        cms_alt = statistics.median(r["compress_ms"] for r in runs_alt)
+        bb_alt = bb1 if fmt3 else bb1 + tab3
         pk = measured_peak()[0]
         alg_c = 8 * n + res.payload_bytes + 16 * res.n_esc       # x read, payload + escapes written
         alg_d = res.payload_bytes + 16 * res.n_esc + 8 * n       # payload + escapes read, x' written
         per[f"{eb:g}"] = {
+            "block_version": 3 if fmt3 else 1,
             "compress_gbs": 8 * n / (cms / 1e3) / 1e9, "decompress_gbs": 8 * n / (dms / 1e3) / 1e9,
             "compress_roofline_frac": alg_c / (cms / 1e3) / 1e9 / pk,
-            "decompress_roofline_frac": alg_d / (dms / 1e3) / 1e9 / pk,
+            "decompress_roofline_frac": (alg_d + (tab3 if fmt3 else 0)) / (dms / 1e3) / 1e9 / pk,
             "compress_ms": cms, "decompress_ms": dms, "ratio": 8 * n / bb, "payload_bits": int(res.payload_bits),
             "escapes": int(res.n_esc), "max_len": int(res.max_len), "symbols": int(res.used_symbols),
             "relaunches": int(res.relaunches),
-            "v3": {"compress_ms": cms3, "decompress_ms": dms3, "ratio": 8 * n / bb3,
-                   "compress_gbs": 8 * n / (cms3 / 1e3) / 1e9, "decompress_gbs": 8 * n / (dms3 / 1e3) / 1e9,
-                   "decompress_roofline_frac": (alg_d + 24 * ((n - 1 + 1023) // 1024)) / (dms3 / 1e3) / 1e9 / pk},
+            ("v1_reference_format" if fmt3 else "v3"): {
+                "compress_ms": cms_alt, "decompress_ms": dms_alt, "ratio": 8 * n / bb_alt,
+                "compress_gbs": 8 * n / (cms_alt / 1e3) / 1e9, "decompress_gbs": 8 * n / (dms_alt / 1e3) / 1e9,
+                "decompress_roofline_frac": (alg_d + (0 if fmt3 else tab3)) / (dms_alt / 1e3) / 1e9 / pk},
             "compress_phase_ms": {"setup": s["compress_phases"][0], "quantize": s["compress_phases"][1],
                                   "codebook": s["compress_phases"][2], "encode": s["compress_phases"][3]},
             "decompress_phase_ms": {"huffman_sync": s["decompress_phases"][0],
@@ -415,7 +422,8 @@ def run_b200(args, rank, world, local_rank):
     peak, peak_src = measured_peak()
     groups = {
         "quantizer[lc_quant_wa+lc_map_scan+lc_quant_wfix]": lambda d: d["compress_phase_ms"]["quantize"],
-        "reconstruction[lc_rec_a+lc_map_scan+lc_rec_b]":
+        ("reconstruction[lc_dec_v3: Huffman walk + reference chain]" if fmt3 else
+         "reconstruction[lc_rec_a+lc_map_scan+lc_rec_b]"):
             lambda d: d["decompress_phase_ms"]["reconstruct"],
         "huffman_decode[lc_dec_tables+lc_dec_sync+lc_dec_scan+lc_dec_write]":
             lambda d: d["decompress_phase_ms"]["huffman_sync"] + d["decompress_phase_ms"]["huffman_scan"]
@@ -426,7 +434,9 @@ def run_b200(args, rank, world, local_rank):
     dom = max(shares, key=shares.get)
     pay = sum(d["payload_bits"] for d in per.values()) / 8 / len(per)
     esc = sum(d["escapes"] for d in per.values()) / len(per)
-    alg = {"quantizer": 8 * n, "reconstruction": 8 * n + 16 * esc, "huffman_decode": pay,
+    # v3: the one-pass kernel also reads the payload and the sync tables
+    rec_in = pay + 24 * ((n - 1 + 1023) // 1024) if fmt3 else 0
+    alg = {"quantizer": 8 * n, "reconstruction": 8 * n + 16 * esc + rec_in, "huffman_decode": pay,
            "encoder": pay + 16 * esc}[dom.split("[")[0]]
     t_ms = shares[dom] / len(per)
     achieved = alg / (t_ms / 1e3) / 1e9
@@ -447,7 +457,7 @@ def run_b200(args, rank, world, local_rank):
     # flight in both directions
     elanes = 2 * nstr
     ohs = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(elanes)]
-    cfgs = [lc.CompressorConfig.value_range_relative(eb) for eb in BOUNDS]
+    cfgs = [lc.CompressorConfig.value_range_relative(eb, block_version=args.block_version) for eb in BOUNDS]
     estreams = [torch.cuda.Stream() for _ in range(elanes)]
     cstreams = [torch.cuda.Stream() for _ in range(elanes)]
     lane_bytes = [[0, 0] for _ in range(elanes)]
@@ -473,6 +483,8 @@ def run_b200(args, rank, world, local_rank):
                             ohs[k][off:off + (4 << 20)].copy_(rec[off:off + (4 << 20)], non_blocking=True)
                         rec.record_stream(cstreams[k])
                     meta_b = len(blk.payload) + blk.code_lengths.size + 16 * len(blk.escape_indices)
+                    if blk.version == 3:                       # sync tables travel with the block
+                        meta_b += 24 * len(blk.sync_offsets)
                     lane_bytes[k][0] += 8 * n + meta_b
                     lane_bytes[k][1] += meta_b + 8 * n
             cstreams[k].synchronize()                          # every read-back finished
@@ -552,12 +564,18 @@ def run_b200(args, rank, world, local_rank):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOAD, "n": n, "eb_rel": list(BOUNDS), "parallelism": f"shard{world}",
-                       "streams": nstr, "l2": "inputs (512 MB/GPU) exceed L2; no flush"},
+                       "streams": nstr, "l2": "inputs (512 MB/GPU) exceed L2; no flush",
+                       "block_format": ("v3: the repo's checkpoint block (reference codes and payload + exact "
+                                        "chain value and escape count every 1024 symbols; checkpoint.py default)"
+                                        if fmt3 else "v1: the reference's LCKP0001 block")},
             "sequential": {"value": 8 * n * len(BOUNDS) * world / (ms_seq / 1e3) / 1e9, "ms_per_step": ms_seq,
                            "note": "same step, the three round trips one after the other on one stream"},
-            "v3": {"value": 8 * n * len(BOUNDS) * world / (ms_v3 / 1e3) / 1e9, "ms_per_step": ms_v3,
-                   "note": "same concurrent step with v3 blocks (repo format: + chain value and escape count "
-                           "every 1024 symbols; codes/payload identical to the reference's), one-pass decoder"},
+            ("v1_reference_format" if fmt3 else "v3"): {
+                "value": 8 * n * len(BOUNDS) * world / (ms_alt / 1e3) / 1e9, "ms_per_step": ms_alt,
+                "note": ("same concurrent step with the reference's block format (LCKP0001 v1: byte-identical "
+                         "blocks, decoded by segment sync + offset-map reconstruction)" if fmt3 else
+                         "same concurrent step with v3 blocks (+ chain value and escape count every 1024 "
+                         "symbols), one-pass decoder")},
             "clocks": clk, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "per_bound": per,
             "solver_configs": solver,
@@ -756,6 +774,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-solver", action="store_true")
     ap.add_argument("--cfg4-side", type=int, default=256, help="config-4 grid side (0: skip)")
+    ap.add_argument("--block-version", type=int, default=3, choices=[1, 3],
+                    help="block format of the timed round trips (3: the repo's checkpoint format, 1: the "
+                         "reference's); the other is reported beside")
     ap.add_argument("--cfg5-side", type=int, default=512, help="config-5 grid side (0: skip)")
     ap.add_argument("--streams", type=int, default=3,
                     help="concurrent round trips per step (each bound on its own stream and context)")

@@ -1013,14 +1013,18 @@ struct LcV3Reader {
 // payload end, invalid codewords), kept out of line so the hot loop stays small.
 // Returns sym | l << 32 | status << 40 (l = 0: no codeword; the reader is
 // passed by value so the caller's stays in registers).
+#define LC_V3_LONG_SMEM 2048          // symbols of codes longer than the LUT kept in shared memory
 __device__ __noinline__ unsigned long long lc_v3_slow_symbol(const LcDecV3Tables &Ts, const LcDecTables *Tg,
                                                             const uint32_t *__restrict__ sorted,
+                                                            const uint32_t *s_long, unsigned long0, unsigned nlong,
                                                             const LcBitReader<LcGlobSrc> br, unsigned bits_rel)
 {
     int l = lc_long_len_fast(Ts, br.buf);
     if (l && l <= 32 && br.pos + (unsigned)l <= bits_rel) {
         const unsigned long long v = (br.buf >> 32) >> (32 - l);
-        return __ldg(sorted + Ts.offset[l] + (v - Ts.first_code[l])) | ((unsigned long long)l << 32);
+        const unsigned long long idx = Ts.offset[l] + (v - Ts.first_code[l]);
+        const uint32_t sym = idx - long0 < nlong ? s_long[idx - long0] : __ldg(sorted + idx);
+        return sym | ((unsigned long long)l << 32);
     }
     int term = 0;
     uint32_t sym = 0;
@@ -1040,8 +1044,16 @@ __global__ void __launch_bounds__(LC_V3_TPB) lc_dec_v3_kernel(LcDecParams P, con
                                                              LcV3Final *fin)
 {
     __shared__ LcDecV3Tables Ts;
+    __shared__ uint32_t s_long[LC_V3_LONG_SMEM];         // canonical symbols of the long codes
+    __shared__ uint32_t s_ring[LC_V3_TPB * 8];           // fast path: per-lane prefetch ring (2 groups)
     extern __shared__ double v3_stage[];                 // [warps][32 rows][33]
     const LcDecTables *Tg = P.T;
+    // long codes (> LC_LUT_BITS) are the tail of the canonical symbol order
+    const int tml = Tg->max_len;
+    const unsigned long0 = tml > LC_LUT_BITS ? (unsigned)Tg->offset[LC_LUT_BITS + 1] : 0u;
+    const unsigned nlong_all = tml > LC_LUT_BITS ? (unsigned)Tg->used - long0 : 0u;
+    const unsigned nlong = nlong_all <= LC_V3_LONG_SMEM ? nlong_all : 0u;
+    for (unsigned i = threadIdx.x; i < nlong; i += blockDim.x) s_long[i] = __ldg(P.sorted + long0 + i);
     if (threadIdx.x == 0) { Ts.max_len = Tg->max_len; Ts.canon = Tg->canon; Ts.s16 = Tg->s16; }
     for (int i = threadIdx.x; i < 34; i += blockDim.x) Ts.lim[i] = Tg->lim[i];
     for (int i = threadIdx.x; i < 66; i += blockDim.x) { Ts.first_code[i] = Tg->first_code[i]; Ts.offset[i] = Tg->offset[i]; }
@@ -1077,46 +1089,153 @@ __global__ void __launch_bounds__(LC_V3_TPB) lc_dec_v3_kernel(LcDecParams P, con
         double r = live ? starts[j] : 0.0;
         unsigned long long e = live ? sesc[j] : 0ull;
         int fl0 = 0, fl1 = 0;
+        // Fast path: a warp whose 32 intervals are all full, escape-free (per the escape
+        // table) and whose codes all fit the LUT runs a straight-line walk: no slow-path,
+        // escape or payload-end branches; refills come from a per-lane shared-memory ring
+        // kept two 16-byte groups ahead by asynchronous loads.  Invalid codewords, escape
+        // codes or table disagreements are caught after the walk (status 1 / 6).
+        {
+            const bool full = live && j + 1 < nsync && todo == LC_SYNC_K && !bad && sesc[j + 1] == e;
+            if (Ts.max_len <= LC_LUT_BITS && __all_sync(0xffffffffu, full)) {
+                const unsigned f = (unsigned)(lane >> 2) & 7u;             // ring swizzle (bank spread)
+                uint32_t *ring = s_ring + threadIdx.x * 8;
+                const uint4 *g4 = reinterpret_cast<const uint4 *>(P.payload + wbase / 32);
+                const unsigned p0 = (unsigned)(s0 - wbase);
+                unsigned next = p0 >> 5;                                   // next word to buffer
+                {
+                    const unsigned gi = next >> 2;
+                    const uint4 a = __ldg(g4 + gi), b = __ldg(g4 + gi + 1);
+                    const unsigned sa = (gi & 1u) * 4u, sbb = ((gi + 1u) & 1u) * 4u;
+                    ring[(sa + 0) ^ f] = a.x; ring[(sa + 1) ^ f] = a.y; ring[(sa + 2) ^ f] = a.z; ring[(sa + 3) ^ f] = a.w;
+                    ring[(sbb + 0) ^ f] = b.x; ring[(sbb + 1) ^ f] = b.y; ring[(sbb + 2) ^ f] = b.z; ring[(sbb + 3) ^ f] = b.w;
+                }
+                uint4 pend = __ldg(g4 + (next >> 2) + 2);
+                __syncwarp();
+                auto word = [&](unsigned i) { return __byte_perm(ring[(i & 7u) ^ f], 0, 0x0123); };
+                const int sh = (int)(p0 & 31);
+                unsigned long long buf = (((unsigned long long)word(next) << 32) | word(next + 1)) << sh;
+                int nb = 64 - sh;
+                next += 2;
+                unsigned pos = p0;
+                bool inv = false, z0 = false;
+                auto turn = [&]() {                                        // entering group next >> 2
+                    const unsigned gg = next >> 2, sl = ((gg + 1u) & 1u) * 4u;
+                    ring[(sl + 0) ^ f] = pend.x; ring[(sl + 1) ^ f] = pend.y;
+                    ring[(sl + 2) ^ f] = pend.z; ring[(sl + 3) ^ f] = pend.w;
+                    pend = __ldg(g4 + gg + 2);
+                };
+                if ((next & 3u) < 2u) turn();                              // both start words were consumed
+                if (nb <= 32) {
+                    buf |= (unsigned long long)word(next) << (32 - nb);
+                    nb += 32;
+                    ++next;
+                    if ((next & 3u) == 0) turn();
+                }
+                double *orow = out + j * LC_SYNC_K + 1 - lane * LC_SYNC_K;   // + rr * 1024 + lane below
+                for (unsigned sb = 0; sb < LC_SYNC_K; sb += 32) {
+#pragma unroll 2
+                    for (unsigned t = 0; t < 32; ++t) {
+                        const uint32_t e1 = Ts.lut[(unsigned)(buf >> (64 - LC_LUT_BITS))];
+                        const uint32_t sym = e1 & 0xffffffu;
+                        const int l = (int)(e1 >> 24);
+                        inv |= l > LC_LUT_BITS;
+                        const int lc = l & 15;
+                        buf <<= lc;
+                        nb -= lc;
+                        pos += lc;
+                        if (nb <= 32) {                                    // refill from the ring
+                            buf |= (unsigned long long)word(next) << (32 - nb);
+                            nb += 32;
+                            ++next;
+                            if ((next & 3u) == 0) turn();
+                        }
+                        z0 |= sym == 0;
+                        const uint32_t zz = sym - 1u;                      // compressor.py:370-374
+                        const int mm = (int)(zz >> 1) ^ -(int)(zz & 1u);
+                        const double inc = LC_MUL((double)mm, delta);
+                        if (sym > 1u) r = LC_ADD(r, inc);
+                        myrow[t] = r;
+                    }
+                    __syncwarp();
+#pragma unroll 4
+                    for (int rr = 0; rr < 32; ++rr)
+                        __stcs(orow + (size_t)rr * LC_SYNC_K + sb + lane, stg[rr * 33 + lane]);
+                    __syncwarp();
+                }
+                if (inv) atomicExch(&fin->status, 1);
+                else if (z0 || wbase + pos != s1 || lc_bits(r) != lc_bits(starts[j + 1]))
+                    atomicExch(&fin->status, 6);
+                continue;
+            }
+        }
         const unsigned wsteps = __reduce_max_sync(0xffffffffu, todo);
         for (unsigned sb = 0; sb < wsteps; sb += 32) {
             const unsigned nt = todo > sb ? min(32u, todo - sb) : 0u;   // symbols of this block
-            unsigned t = 0;
-            auto step = [&](uint32_t sy, unsigned tt) {        // one reference step, value to the row
-                if (sy == 0) {                                        // compressor.py:365-369
-                    const unsigned long long pos = o0 + sb + tt + 1;  // element index
-                    if (e < n_esc) {
-                        r = esc_val[e];
-                        fl1 |= esc_idx[e] != pos;
-                    } else {
-                        fl0 = 1;
-                    }
-                    ++e;
-                } else {                                              // :370-374
-                    const uint32_t zz = sy - 1u;
-                    const int mm = (int)(zz >> 1) ^ -(int)(zz & 1u);
-                    if (mm != 0) r = LC_ADD(r, LC_MUL((double)mm, delta));
-                }
-                myrow[tt] = r;
-            };
+            // Lanes step in lockstep (32 steps, predicated by `act`).  The common step is a
+            // short straight line (LUT lookup, 64-bit shift, one reference add); the rare
+            // paths -- long codes / payload end, escapes, buffer refills and prefetch-ring
+            // turns -- are warp-uniform branches entered only when some lane needs them.
 #pragma unroll 1
-            while (t < nt) {
-                const unsigned w12 = (unsigned)(br.buf >> (64 - LC_LUT_BITS));
-                const uint32_t e1 = Ts.lut[w12];
+            for (unsigned t = 0; t < 32; ++t) {
+                const bool act = t < nt && !bad;
+                const uint32_t e1 = Ts.lut[(unsigned)(br.buf >> (64 - LC_LUT_BITS))];
                 uint32_t sym = e1 & 0xffffffu;
                 int l = (int)(e1 >> 24);
-                if (e1 == 0xffffffffu || br.pos + (unsigned)l > bits_rel) {
-                    LcBitReader<LcGlobSrc> gr;                        // the same position, global reads
-                    gr.src.w = P.payload + wbase / 32;
-                    gr.buf = br.buf; gr.nb = br.nb; gr.pos = br.pos; gr.next = br.next;
-                    const unsigned long long sl = lc_v3_slow_symbol(Ts, Tg, P.sorted, gr, bits_rel);
-                    sym = (uint32_t)sl;
-                    l = (int)((sl >> 32) & 0xff);
-                    if (!l) { bad = (int)(sl >> 40); todo = 0; break; }
+                const bool slow = act && (l > LC_LUT_BITS || br.pos + (unsigned)l > bits_rel);
+                if (__any_sync(0xffffffffu, slow)) {
+                    if (slow) {
+                        LcBitReader<LcGlobSrc> gr;                    // the same position, global reads
+                        gr.src.w = P.payload + wbase / 32;
+                        gr.buf = br.buf; gr.nb = br.nb; gr.pos = br.pos; gr.next = br.next;
+                        const unsigned long long sl =
+                            lc_v3_slow_symbol(Ts, Tg, P.sorted, s_long, long0, nlong, gr, bits_rel);
+                        sym = (uint32_t)sl;
+                        l = (int)((sl >> 32) & 0xff);
+                        if (!l) { bad = (int)(sl >> 40); todo = 0; }
+                        else if (l >= br.nb) { br.seek(br.pos + l); l = 0; }   // consumed by the seek
+                    }
                 }
-                br.consume(l);
-                step(sym, t);
-                ++t;
+                const bool go = act && !bad;
+                const int lc = go ? l : 0;
+                br.buf <<= lc;
+                br.nb -= lc;
+                br.pos += lc;
+                const bool rf = br.nb <= 32;
+                if (__any_sync(0xffffffffu, rf)) {
+                    if (rf) {
+                        br.buf |= (unsigned long long)LcV3Reader::pick(br.cur, br.next & 3u) << (32 - br.nb);
+                        br.nb += 32;
+                        ++br.next;
+                    }
+                    const bool turn = rf && (br.next & 3u) == 0;      // the current group is used up
+                    if (__any_sync(0xffffffffu, turn)) {
+                        if (turn) {
+                            br.cur = br.n1;
+                            br.n1 = br.n2;
+                            br.n2 = __ldg(br.g4 + (br.next >> 2) + 2);
+                        }
+                    }
+                }
+                const bool esc = go && sym == 0;
+                if (__any_sync(0xffffffffu, esc)) {
+                    if (esc) {                                        // compressor.py:365-369
+                        const unsigned long long pos = o0 + sb + t + 1;   // element index
+                        if (e < n_esc) {
+                            r = esc_val[e];
+                            fl1 |= esc_idx[e] != pos;
+                        } else {
+                            fl0 = 1;
+                        }
+                        ++e;
+                    }
+                }
+                const uint32_t zz = sym - 1u;                          // :370-374 (m != 0 iff sym > 1)
+                const int mm = (int)(zz >> 1) ^ -(int)(zz & 1u);
+                const double inc = LC_MUL((double)mm, delta);
+                if (go && sym > 1u) r = LC_ADD(r, inc);
+                myrow[t] = r;
             }
+            if (bad) todo = 0;
             __syncwarp();
             // rows: lane L's values go to out[o0(L) + sb + 1 ...]
             for (int rr = 0; rr < 32; ++rr) {

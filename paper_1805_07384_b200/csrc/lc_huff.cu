@@ -47,6 +47,7 @@ __device__ __forceinline__ void lc_bitonic_sort(unsigned long long *a, int npow2
 // thread, instead of a bitonic network over global memory (~100 passes with a
 // CTA barrier each).  temp: the (unused) dynamic shared memory.
 #define LC_CB_RADIX_ITEMS 16
+#define LC_CB_MAXB 2048                 // merge batches recorded for the depth pass
 #define LC_CB_RADIX_KEYS (LC_CB_THREADS * LC_CB_RADIX_ITEMS)
 static_assert(sizeof(cub::BlockRadixSort<uint32_t, LC_CB_THREADS, LC_CB_RADIX_ITEMS, uint32_t>::TempStorage) <=
                   (2 * sizeof(unsigned long long) + 2 * sizeof(int) + sizeof(uint32_t) + 1) * LC_CB_SMEM_KEYS,
@@ -147,9 +148,14 @@ __device__ __forceinline__ void lc_codebook_body(const uint32_t *__restrict__ hi
     //    ties to older items), so the batch's picks are the merged order of the
     //    two queues up to 2t and its pairs become new nodes in parallel (merge
     //    path per pair).  t at least doubles per batch: O(log total) batches.
+    // batch starts (the first internal node each batch creates): every node's
+    // parent is created in a later batch, so depths follow batch by batch in
+    // reverse (step 4)
+    __shared__ int s_bstart[LC_CB_MAXB + 1];
+    __shared__ int s_nbatch;
     {
         __shared__ int s_li, s_ii, s_m, s_na, s_nb, s_go;
-        if (tid == 0) { s_li = 0; s_ii = 0; s_m = 0; }
+        if (tid == 0) { s_li = 0; s_ii = 0; s_m = 0; s_nbatch = 0; }
         __syncthreads();
         const unsigned long long INF = ~0ULL;
         for (;;) {
@@ -157,6 +163,8 @@ __device__ __forceinline__ void lc_codebook_body(const uint32_t *__restrict__ hi
                 const int li = s_li, ii = s_ii, m = s_m;
                 s_go = m < k - 1;
                 if (s_go) {
+                    if (s_nbatch <= LC_CB_MAXB) s_bstart[s_nbatch] = m;
+                    ++s_nbatch;
                     const unsigned long long lf = li < k ? keys[li] >> 32 : INF;
                     const unsigned long long nf = ii < m ? ifreq[ii] : INF;
                     const unsigned long long t = lf < nf ? lf : nf;
@@ -231,7 +239,18 @@ __device__ __forceinline__ void lc_codebook_body(const uint32_t *__restrict__ hi
     int *A = D + k;
     const int ni = k - 1;
     constexpr int NJ = 8;
-    if (ni <= NJ * LC_CB_THREADS) {
+    const int nbatch = s_nbatch;
+    if (nbatch <= LC_CB_MAXB && (ni > NJ * LC_CB_THREADS || nbatch < 32)) {
+        // reverse batch order: a batch's parents are all in later batches
+        if (tid == 0) D[ni - 1] = 0;
+        __syncthreads();
+        for (int bi = nbatch - 1; bi >= 0; --bi) {
+            const int b0 = s_bstart[bi], b1 = bi + 1 < nbatch ? s_bstart[bi + 1] : ni;
+            for (int m = b0 + tid; m < b1; m += LC_CB_THREADS)
+                if (m != ni - 1) D[m] = D[parent[k + m]] + 1;
+            __syncthreads();
+        }
+    } else if (ni <= NJ * LC_CB_THREADS) {
         for (int m = tid; m < ni; m += LC_CB_THREADS) {
             const bool root = m == ni - 1;
             D[m] = root ? 0 : 1;

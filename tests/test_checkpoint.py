@@ -130,8 +130,13 @@ def test_lossy_images_byte_identical(lc, ckg):
         want = ckg[name + "/image"].tobytes()
         for xin in (x, torch.from_numpy(x).cuda()):
             img, cost = ck.checkpoint_lossy(SimpleNamespace(x=xin, iteration=int(it)), _cfg(lc, mode, param),
-                                            ck.StorageTarget(), commit=False)
+                                            ck.StorageTarget(), commit=False, block_version=1)
             assert img.to_bytes() == want, name
+            # the repo's default image (v3 block) decodes to the same reconstruction
+            img3, _ = ck.checkpoint_lossy(SimpleNamespace(x=xin, iteration=int(it)), _cfg(lc, mode, param),
+                                          ck.StorageTarget(), commit=False)
+            assert lc.CompressedBlock.from_bytes(img3.payload).version == 3
+            assert np.array_equal(ck.decode_payload(img3).view(np.int64), ckg[name + "/recon"].view(np.int64))
             assert cost.t_compress > 0.0 and cost.payload_bytes == len(want)
 
 
@@ -166,4 +171,5 @@ def test_async_checkpointer_overlaps_and_matches(lc, ckg, tmp_path):
         sync, _ = ck.checkpoint_lossy(SimpleNamespace(x=xs, iteration=it), cfg, ck.StorageTarget(), commit=False)
         assert img.to_bytes() == sync.to_bytes()
     assert ck.CheckpointImage.from_bytes((tmp_path / "async.img").read_bytes()).iteration == 3
-    assert images[0].payload == ck.CheckpointImage.from_bytes(ckg["lossy_rel4/image"].tobytes()).payload
+    ref0 = ck.CheckpointImage.from_bytes(ckg["lossy_rel4/image"].tobytes()).payload
+    assert lc.CompressedBlock.from_bytes(images[0].payload).payload == lc.CompressedBlock.from_bytes(ref0).payload

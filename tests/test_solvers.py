@@ -320,6 +320,6 @@ def test_checkpoint_uses_producer_range(dev):
         ranged = compressor.compress(s.x, cfg, value_range=s.x_range).to_bytes()
         n1 = ctx.lib.lc_launch_count(ctx.h)
         assert ranged == plain
-        img, _ = ckpt.checkpoint_lossy(s, cfg, ckpt.StorageTarget())
+        img, _ = ckpt.checkpoint_lossy(s, cfg, ckpt.StorageTarget(), block_version=1)
         assert img.payload == plain
         assert n1 - n0 >= 1
