@@ -129,7 +129,12 @@ int lc_debug_check(lc_ctx *ctx, const char *what, const char *file, int line)
 {
     lc_trace_mark(ctx, what);
     cudaError_t e = cudaGetLastError();
-    if (e == cudaSuccess && ctx->debug_sync) e = cudaStreamSynchronize(ctx->stream);
+    if (e == cudaSuccess && ctx->debug_sync) {
+        const bool log = getenv("LC_DEBUG_LOG") != nullptr;       // LC_DEBUG_LOG=1: name every checked launch (stderr)
+        if (log) fprintf(stderr, "[lc] %s:%d %s ...", file, line, what);
+        e = cudaStreamSynchronize(ctx->stream);
+        if (log) fprintf(stderr, " %s\n", cudaGetErrorName(e));
+    }
     if (e != cudaSuccess) return lc_fail(ctx, e, what, file, line);
     return 0;
 }
@@ -175,6 +180,10 @@ int lc_ctx_create(lc_ctx **out, int device, void *stream)
             for (int &o : a2) o = o > 0 ? o : 1;
     }
     LC_CUDA_OK((cudaError_t)lc_decode_init_attrs());
+    LC_CUDA_OK(cudaFuncSetAttribute(lc_histw_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(LC_HW_BINS * sizeof(uint32_t))));
+    LC_CUDA_OK(cudaFuncSetAttribute(lc_histw_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(LC_HW_BINS * sizeof(uint32_t))));
     LC_CUDA_OK(cudaFuncSetAttribute(lc_codebook_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)lc_codebook_smem_bytes()));
     LC_CUDA_OK(cudaFuncSetAttribute(lc_encode_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -313,7 +322,7 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     const uint64_t m = n - 1;
     LC_CUDA_OK(lc_reserve(ctx->codes, m * sizeof(CodeT)));
     LC_CUDA_OK(lc_reserve(ctx->hist, nbins * sizeof(uint32_t)));
-    LC_CUDA_OK(lc_reserve(ctx->counters, 64));
+    LC_CUDA_OK(lc_reserve(ctx->counters, 128));
     LC_CUDA_OK(lc_reserve(ctx->bad_end, nchunks * sizeof(double)));
     if (record) {
         LC_CUDA_OK(lc_reserve(ctx->pe, m * sizeof(double)));
@@ -322,6 +331,7 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     unsigned int *tile_counter = (unsigned int *)ctx->counters.p;
     unsigned long long *first_bad = (unsigned long long *)((char *)ctx->counters.p + 16);
     unsigned long long *exact_count = (unsigned long long *)((char *)ctx->counters.p + 32);
+    unsigned long long *nbig = (unsigned long long *)((char *)ctx->counters.p + 64);
 
     LcQuantParams P;
     memset(&P, 0, sizeof P);
@@ -353,6 +363,7 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     P.pe_rec = record ? (double *)ctx->pe_rec.p : nullptr;
     P.verify = ctx->opt[LC_OPT_VERIFY] ? 1 : 0;
     P.exact_count = exact_count;
+    P.nbig = nbig;
     P.resume = 0;
     P.first_tile = 0;
     P.resume_chunk = -1;
@@ -369,6 +380,7 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
 
     LC_CUDA_OK(cudaMemsetAsync(P.hist, 0, nbins * sizeof(uint32_t), st));
     LC_CUDA_OK(cudaMemsetAsync(exact_count, 0, 8, st));
+    LC_CUDA_OK(cudaMemsetAsync(nbig, 0, 8, st));
 
     unsigned long long *hbad = (unsigned long long *)ctx->pinned;
     LcCodebookOut *hcb = (LcCodebookOut *)((char *)ctx->pinned + 64);
@@ -400,7 +412,9 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
         LC_CUDA_OK(cudaMemsetAsync(first_bad, 0xff, 8, st));
         if (P.use_anchors) {
             lc_anchor_tiles_kernel<<<(int)((P.ntiles + 7) / 8 < ga ? (P.ntiles + 7) / 8 : ga), LC_TPB, 0, st>>>(P);
+            { int _rc = lc_debug_check(ctx, "lc_anchor_tiles_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
             lc_anchor_scan_kernel<<<1, 1024, 0, st>>>(P.tile_last_esc, anc_in, P.ntiles, P.first_chunk * LC_L, dyn);
+            { int _rc = lc_debug_check(ctx, "lc_anchor_scan_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
             ctx->launches += 2;
         }
         const long long wcta = (P.ntiles + LC_QW_TPB / 32 - 1) / (LC_QW_TPB / 32);
@@ -410,6 +424,7 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
         { int _rc = lc_debug_check(ctx, "lc_quant_wa_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
         LC_CUDA_OK((cudaError_t)lc_launch_map_scan(P.tile_agg, P.tile_D, P.ntiles, ctx->mapscan_scratch,
                                                    ctx->sm_count, st));
+        { int _rc = lc_debug_check(ctx, "lc_map_scan_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
         if (P.pe) lc_quant_wfix_kernel<CodeT, true><<<(int)(wcta < gf ? wcta : gf), LC_QW_TPB, fsmem, st>>>(P, codes);
         else lc_quant_wfix_kernel<CodeT, false><<<(int)(wcta < gf ? wcta : gf), LC_QW_TPB, fsmem, st>>>(P, codes);
         { int _rc = lc_debug_check(ctx, "lc_quant_wfix_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
@@ -459,12 +474,22 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     E.sync = (unsigned long long *)ctx->sync.p;
     E.sync_esc = (unsigned long long *)ctx->sync.p + 2 * (ctx->nsync + 1);
     E.dyn = dyn;
+    E.pending = first_bad;
     const int egrid = (int)(etiles < (uint64_t)(4 * ctx->sm_count) ? etiles : 4 * ctx->sm_count);
+    auto histw_launch = [&]() -> int {                   // codes beyond pass A's shared-memory bins
+        if (nbins <= LC_HBINS_B) return 0;
+        lc_histw_kernel<CodeT><<<2 * ctx->sm_count, 512, LC_HW_BINS * sizeof(uint32_t), st>>>(
+            codes, m, P.hist, nbins, LC_HBINS_B, nbig, first_bad, dyn);
+        { int _rc = lc_debug_check(ctx, "lc_histw_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+        ctx->launches += 1;
+        return 0;
+    };
     auto codebook_launch = [&]() -> int {
         LC_CUDA_OK(cudaEventRecord(ctx->pev[2], st));
         lc_codebook_kernel<<<1, 1024, lc_codebook_smem_bytes(), st>>>(
             P.hist, nbins, (uint8_t *)ctx->lengths.p, (unsigned long long *)ctx->cw.p,
-            (unsigned long long *)ctx->gkeys.p, (unsigned long long *)ctx->ifreq.p, (int *)ctx->parent.p, cbo, dyn);
+            (unsigned long long *)ctx->gkeys.p, (unsigned long long *)ctx->ifreq.p, (int *)ctx->parent.p, cbo, dyn,
+            first_bad);
         { int _rc = lc_debug_check(ctx, "lc_codebook_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
         LC_CUDA_OK(cudaEventRecord(ctx->pev[3], st));
         ctx->launches += 1;
@@ -494,6 +519,7 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
 
     // common path: quantize, codebook and encode back to back, one sync
     { int _rc = quant_launch(); if (_rc) return _rc; }
+    { int _rc = histw_launch(); if (_rc) return _rc; }
     { int _rc = codebook_launch(); if (_rc) return _rc; }
     { int _rc = encode_launch(); if (_rc) return _rc; }
     { int _rc = readback(); if (_rc) return _rc; }
@@ -524,10 +550,12 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
                 if (P.pe) lc_quant_wfix_kernel<CodeT, true><<<1, 32, fsmem, st>>>(P, codes);
                 else lc_quant_wfix_kernel<CodeT, false><<<1, 32, fsmem, st>>>(P, codes);
                 ctx->launches += 1;
+                { int _rc = lc_debug_check(ctx, "lc_quant_wfix_kernel (resume 1)", __FILE__, __LINE__); if (_rc) return _rc; }
                 if (wf + 1 < P.ntiles) {
                     LC_CUDA_OK((cudaError_t)lc_launch_map_scan(P.tile_agg + wf + 1, P.tile_D + wf + 1,
                                                                P.ntiles - wf - 1, ctx->mapscan_scratch,
                                                                ctx->sm_count, st, P.resume_D0));
+                    { int _rc = lc_debug_check(ctx, "lc_map_scan_kernel (resume)", __FILE__, __LINE__); if (_rc) return _rc; }
                     P.resume = 2;
                     P.first_tile = wf + 1;
                     if (P.pe) lc_quant_wfix_kernel<CodeT, true><<<(int)(wcta < gf ? wcta : gf), LC_QW_TPB, fsmem, st>>>(P, codes);
@@ -567,6 +595,7 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
             P.inject_chunk = -1;
             if ((long long)relaunches > ctx->opt[LC_OPT_MAX_QUANT]) {   // pathological input: exact serial chain
                 ctx->quant_serial = 1;
+                LC_CUDA_OK(cudaMemsetAsync(first_bad, 0xff, 8, st));    // nothing pending after the exact chain
                 lc_quant_serial_kernel<CodeT><<<1, 32, 0, st>>>(P, codes);
                 { int _rc = lc_debug_check(ctx, "lc_quant_serial_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
                 ctx->launches += 1;
@@ -587,7 +616,9 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
             lc_hist_kernel<CodeT><<<4 * ctx->sm_count, 256, 0, st>>>(codes, m, P.hist, nbins);
         { int _rc = lc_debug_check(ctx, "lc_hist_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
         ctx->launches += 1;
+        LC_CUDA_OK(cudaMemsetAsync(nbig, 0, 8, st));     // the recount covered every bin
         }
+        { int _rc = histw_launch(); if (_rc) return _rc; }
         { int _rc = codebook_launch(); if (_rc) return _rc; }
         { int _rc = encode_launch(); if (_rc) return _rc; }
         { int _rc = readback(); if (_rc) return _rc; }
@@ -905,7 +936,7 @@ int lc_debug_codebook(lc_ctx *ctx, const uint32_t *hist, uint32_t nbins, uint8_t
     lc_codebook_kernel<<<1, 1024, lc_codebook_smem_bytes(), st>>>(
         (const uint32_t *)ctx->hist.p, nbins, (uint8_t *)ctx->lengths.p, (unsigned long long *)ctx->cw.p,
         (unsigned long long *)ctx->gkeys.p, (unsigned long long *)ctx->ifreq.p, (int *)ctx->parent.p,
-        (LcCodebookOut *)ctx->cbout.p, nullptr);
+        (LcCodebookOut *)ctx->cbout.p, nullptr, nullptr);
     ctx->launches += 1;
     { int _rc = lc_debug_check(ctx, "lc_codebook_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
     LcCodebookOut *h = (LcCodebookOut *)((char *)ctx->pinned + 1024);

@@ -235,24 +235,6 @@ __device__ __forceinline__ void lc_mbar_wait(unsigned long long *bar, unsigned p
     } while (!ok);
 }
 
-// Inclusive scan (in place) of nw <= 32 per-warp map aggregates by warp 0
-// (log2(nw) shuffle levels instead of a sequential loop); call from all
-// threads between two __syncthreads().
-__device__ __forceinline__ void lc_scan_warp_maps(OffMap *agg, int nw)
-{
-    if ((threadIdx.x >> 5) == 0) {
-        const int lane = threadIdx.x & 31;
-        OffMap v = lane < nw ? agg[lane] : lc_map_neutral();
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            if (o >= nw) break;
-            const OffMap up = lc_shfl_up_map(v, o);
-            if (lane >= o) v = lc_map_compose(v, up);
-        }
-        if (lane < nw) agg[lane] = v;
-    }
-}
-
 // ---- compacted replay of flagged chunks -------------------------------------
 // Chunks whose hot loop flagged possible map events are queued in shared memory
 // and replayed by consecutive threads (full warps) instead of by their owners
@@ -346,11 +328,33 @@ __device__ __forceinline__ void lc_prefetch_bytes(const void *p, size_t bytes)
     for (const char *q = c + 128 * threadIdx.x; q < e; q += 128 * blockDim.x) lc_prefetch_l2(q);
 }
 
-// Inclusive warp scan of chunk maps (lane 0 earliest), in place.  When every
-// lane holds a translation with a non-zero grid (the common case: chunks
-// without events), compose(H2, H1) = H1 with y = H1.y + H2.y, so the scan is a
-// prefix sum of y in the same tree order (same roundings) and every lane ends
-// with lane 0's grid fields; otherwise the general composition.
+__device__ __forceinline__ OffMap lc_shfl_idx_map(const OffMap &m, int src)
+{
+    OffMap r;
+    r.kind = __shfl_sync(0xffffffffu, m.kind, src);
+    r.v = __shfl_sync(0xffffffffu, m.v, src);
+    r.B = __shfl_sync(0xffffffffu, m.B, src);
+    r.t0 = __shfl_sync(0xffffffffu, m.t0, src);
+    r.t1 = __shfl_sync(0xffffffffu, m.t1, src);
+    r.y = __shfl_sync(0xffffffffu, m.y, src);
+    r.og = __shfl_sync(0xffffffffu, m.og, src);
+    return r;
+}
+
+// Inclusive warp scan of chunk maps (lane 0 earliest), in place.  Call from all
+// 32 lanes.  LANE-UNIFORM CONTROL FLOW ONLY: no lane ever runs a composition
+// the other lanes do not run.  (The earlier form -- `if (lane >= o) inc =
+// compose(inc, up)` per shuffle round -- left a lane split off from its warp
+// on sm_100a after a long composition on config 4's 256^3 GMRES vector: ptxas
+// had removed the warp barriers it believed redundant, the next shuffles read
+// inactive lanes, and pass A's tile loop never ended for the lone lane.)
+//   1. every lane a translation with a non-zero grid (chunks without events):
+//      prefix sum of y, lane 0's grid fields;
+//   2. translations and constants only (constants: chunks with an escape):
+//      the same shuffle rounds with the composition written as selects;
+//   3. otherwise (a periodic or invalid map somewhere): 32 sequential
+//      compositions on broadcast operands, identical in every lane.
+// Compositions are exact (power-of-two grids), so the order does not matter.
 __device__ __forceinline__ void lc_warp_scan_maps(OffMap &inc)
 {
     const int lane = threadIdx.x & 31;
@@ -359,7 +363,7 @@ __device__ __forceinline__ void lc_warp_scan_maps(OffMap &inc)
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const double up = __shfl_up_sync(0xffffffffu, y, o);
-            if (lane >= o) y = up + y;
+            y = lane >= o ? up + y : y;
         }
         inc.y = y;
         inc.v = __shfl_sync(0xffffffffu, inc.v, 0);
@@ -369,9 +373,51 @@ __device__ __forceinline__ void lc_warp_scan_maps(OffMap &inc)
         inc.og = __shfl_sync(0xffffffffu, inc.og, 0);
         return;
     }
+    if (__all_sync(0xffffffffu, inc.kind == LC_MAP_TRANS || inc.kind == LC_MAP_CONST)) {
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const OffMap up = lc_shfl_up_map(inc, o);
-        if (lane >= o) inc = lc_map_compose(inc, up);
+        for (int o = 1; o < 32; o <<= 1) {
+            const OffMap up = lc_shfl_up_map(inc, o);
+            // lc_map_compose(inc, up) for these kinds: a constant `inc` absorbs `up`; a
+            // constant `up` gives the constant up.y + inc.y; two translations add, the
+            // grid fields come from `up` unless it is the neutral map (v == 0)
+            const bool use = lane >= o && inc.kind != LC_MAP_CONST;
+            const bool upc = up.kind == LC_MAP_CONST;
+            const bool own = !upc && up.v == 0.0;
+            const double y = up.y + inc.y;
+            inc.kind = use ? (upc ? (int)LC_MAP_CONST : (int)LC_MAP_TRANS) : inc.kind;
+            inc.y = use ? y : inc.y;
+            inc.v = use ? (upc ? 0.0 : (own ? inc.v : up.v)) : inc.v;
+            inc.B = use ? (upc ? 0.0 : (own ? inc.B : up.B)) : inc.B;
+            inc.t1 = use ? (upc ? 0.0 : (own ? inc.t1 : up.t1)) : inc.t1;
+            inc.og = use ? (upc ? 0.0 : (own ? inc.og : up.og)) : inc.og;
+            inc.t0 = use ? (upc ? 0.0 : up.t0) : inc.t0;
+        }
+        return;
+    }
+    const OffMap mine = inc;
+    OffMap acc = lc_map_neutral();
+    for (int l = 0; l < 32; ++l) {
+        const OffMap m = lc_shfl_idx_map(mine, l);
+        acc = lc_map_compose(m, acc);                // the same operands in every lane
+        const bool me = lane == l;
+        inc.kind = me ? acc.kind : inc.kind;
+        inc.v = me ? acc.v : inc.v;
+        inc.B = me ? acc.B : inc.B;
+        inc.t0 = me ? acc.t0 : inc.t0;
+        inc.t1 = me ? acc.t1 : inc.t1;
+        inc.y = me ? acc.y : inc.y;
+        inc.og = me ? acc.og : inc.og;
+    }
+}
+
+// Inclusive scan (in place) of nw <= 32 per-warp map aggregates by warp 0; call
+// from all threads between two __syncthreads().
+__device__ __forceinline__ void lc_scan_warp_maps(OffMap *agg, int nw)
+{
+    if ((threadIdx.x >> 5) == 0) {
+        const int lane = threadIdx.x & 31;
+        OffMap v = lane < nw ? agg[lane] : lc_map_neutral();
+        lc_warp_scan_maps(v);
+        if (lane < nw) agg[lane] = v;
     }
 }

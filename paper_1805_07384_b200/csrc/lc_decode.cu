@@ -1612,9 +1612,11 @@ __global__ void __launch_bounds__(LC_TPB, 4) lc_rec_a_kernel(LcRecParams P, LcRe
         __syncthreads();
         lc_scan_warp_maps(warp_agg, LC_TPB / 32);
         __syncthreads();
-        if (wid > 0) inc_map = lc_map_compose(inc_map, warp_agg[wid - 1]);
+        // shuffle first (the warp is converged after the scan), compose per lane afterwards:
+        // no shuffle may follow a per-lane composition (see lc_warp_scan_maps)
         OffMap exc_map = lc_shfl_up_map(inc_map, 1);
-        if (lane == 0) exc_map = wid > 0 ? warp_agg[wid - 1] : lc_map_neutral();
+        if (lane == 0) exc_map = lc_map_neutral();
+        if (wid > 0) exc_map = lc_map_compose(exc_map, warp_agg[wid - 1]);
         if (len > 0) {
             S.pred.kind[c] = exc_map.kind;
             S.pred.B[c] = exc_map.B;

@@ -366,9 +366,12 @@ __device__ __forceinline__ void lc_codebook_body(const uint32_t *__restrict__ hi
 __global__ void __launch_bounds__(LC_CB_THREADS) lc_codebook_kernel(
     const uint32_t *__restrict__ hist, uint32_t nbins, uint8_t *__restrict__ lengths,
     unsigned long long *__restrict__ codes, unsigned long long *__restrict__ gkeys,
-    unsigned long long *__restrict__ ifreq_g, int *__restrict__ parent_g, LcCodebookOut *out, const LcQuantDyn *dyn)
+    unsigned long long *__restrict__ ifreq_g, int *__restrict__ parent_g, LcCodebookOut *out, const LcQuantDyn *dyn,
+    const unsigned long long *pending)
 {
-    if (dyn && dyn->skip) {                          // nothing was quantized (lc_compress_auto_f64)
+    // nothing was quantized (lc_compress_auto_f64), or a chunk prediction failed and the
+    // quantizer will be resumed first (the codebook and the encoder are launched again then)
+    if ((dyn && dyn->skip) || (pending && *pending != ~0ULL)) {
         if (threadIdx.x == 0) { out->total_bits = 0; out->n_esc = 0; out->max_len = 0; out->used = 0; out->status = 0; }
         return;
     }
@@ -457,6 +460,7 @@ template <typename CodeT>
 __global__ void __launch_bounds__(LC_ENC_NT, 4) lc_encode_kernel(LcEncParams P)
 {
     if (P.dyn && P.dyn->skip) return;
+    if (P.pending && *P.pending != ~0ULL) return;    // the quantizer is resumed first
     typedef cub::BlockScan<unsigned long long, LC_ENC_NT> ScanU;
     extern __shared__ __align__(16) unsigned char lc_dyn_smem[];
     uint32_t *tpk = reinterpret_cast<uint32_t *>(lc_dyn_smem);   // (len << 27) | code

@@ -79,6 +79,7 @@ struct LcQuantParams {
     unsigned long long *first_bad;
     double *bad_end;         // per chunk: exact end value when its successor failed
     double *pe, *pe_rec;     // optional traces
+    unsigned long long *nbig;      // codes >= the shared-memory histogram's range seen so far (lc_histw_kernel counts them)
     unsigned long long *timeline;  // optional: 8 globaltimer stamps per tile (profiling)
     // split-pass data
     int use_anchors;             // 0: no definite escape possible (range pass), anchor = launch anchor
@@ -151,6 +152,7 @@ struct LcEncParams {
     unsigned long long esc_cap;   // capacity of esc_idx / esc_val (host re-runs when short)
     unsigned long long *sync; // v2 sync table [ceil(m / LC_SYNC_K)] (bit offsets), may be null
     unsigned long long *sync_esc;   // v3: escape codes before every LC_SYNC_K-th symbol, may be null
+    const unsigned long long *pending;   // quantizer's first failed chunk (~0: none); set: nothing to encode yet
 };
 
 __global__ void lc_range_kernel(const double *__restrict__ x, uint64_t n, LcRangePart *__restrict__ parts,
@@ -184,7 +186,13 @@ __global__ void lc_hist16_kernel(const uint16_t *__restrict__ codes, uint64_t m,
 __global__ void lc_codebook_kernel(const uint32_t *__restrict__ hist, uint32_t nbins, uint8_t *__restrict__ lengths,
                                    unsigned long long *__restrict__ codes, unsigned long long *__restrict__ gkeys,
                                    unsigned long long *__restrict__ ifreq, int *__restrict__ parent, LcCodebookOut *out,
-                                   const LcQuantDyn *dyn);
+                                   const LcQuantDyn *dyn,
+                                   const unsigned long long *pending);
+#define LC_HW_BINS 16384            // shared-memory bins of the wide-alphabet histogram pass (64 KB)
+template <typename CodeT>
+__global__ void lc_histw_kernel(const CodeT *__restrict__ codes, uint64_t m, uint32_t *__restrict__ hist, uint32_t nbins,
+                                uint32_t lo, const unsigned long long *__restrict__ nbig,
+                                const unsigned long long *__restrict__ pending, const LcQuantDyn *dyn);
 __global__ void lc_zero_words_kernel(uint32_t *__restrict__ p, const LcCodebookOut *__restrict__ cb);
 template <typename CodeT> __global__ void lc_encode_kernel(LcEncParams P);
 size_t lc_codebook_smem_bytes();

@@ -278,16 +278,26 @@ __global__ void __launch_bounds__(1024) lc_map_scan_kernel(const OffMap *__restr
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, g = blockIdx.x;
     const long long b0 = min(ntiles, ((long long)g * 1024 + tid) * per), b1 = min(ntiles, b0 + per);
     OffMap run = lc_map_neutral();
-    for (long long t = b0; t < b1; ++t) run = lc_map_compose(agg[t], run);
+    if (per == 1) {                                  // the usual case: no per-thread composition at all
+        if (b0 < b1) run = agg[b0];
+    } else {
+        for (long long t = b0; t < b1; ++t) run = lc_map_compose(agg[t], run);
+        __syncwarp();
+    }
     OffMap inc = run;
     lc_warp_scan_maps(inc);                          // prefix sum when every map is a translation
     if (lane == 31) wsum[wid] = inc;
     __syncthreads();
     lc_scan_warp_maps(wsum, 32);
     __syncthreads();
-    if (wid > 0) inc = lc_map_compose(inc, wsum[wid - 1]);
+    // exclusive maps: shuffle first (the warp is converged after the scan), compose per lane
+    // afterwards -- no shuffle may follow a per-lane composition (see lc_warp_scan_maps)
     OffMap exc = lc_shfl_up_map(inc, 1);
-    if (lane == 0) exc = wid > 0 ? wsum[wid - 1] : lc_map_neutral();
+    if (lane == 0) exc = lc_map_neutral();
+    if (wid > 0) {
+        exc = lc_map_compose(exc, wsum[wid - 1]);
+        inc = lc_map_compose(inc, wsum[wid - 1]);
+    }
     if (wid == 0) {
         // publish this group's aggregate, then fold the aggregates of all earlier
         // groups 32 at a time (parallel acquire loads, shuffle-tree composition)
@@ -306,12 +316,9 @@ __global__ void __launch_bounds__(1024) lc_map_scan_kernel(const OffMap *__restr
                 v.kind = __ldcg(&q->kind); v.v = __ldcg(&q->v); v.B = __ldcg(&q->B); v.t0 = __ldcg(&q->t0);
                 v.t1 = __ldcg(&q->t1); v.y = __ldcg(&q->y); v.og = __ldcg(&q->og);
             }
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const OffMap other = lc_shfl_down_map(v, off);   // a later group
-                if (lane + off < 32) v = lc_map_compose(other, v);
-            }
-            acc = lc_map_compose(v, acc);
+            __syncwarp();
+            lc_warp_scan_maps(v);                    // lane-uniform; lane 31 holds the 32 groups' composition
+            acc = lc_map_compose(lc_shfl_idx_map(v, 31), acc);   // the same operands in every lane
         }
         if (lane == 0) s_D = lc_map_eval(acc, D0);
     }
@@ -390,6 +397,59 @@ __global__ void __launch_bounds__(256) lc_hist_kernel(const CodeT *__restrict__ 
     for (uint32_t i = threadIdx.x; i < lim; i += blockDim.x)
         if (hs[i]) atomicAdd(&hist[i], hs[i]);
 }
+
+// Wide alphabets (np.bincount, compressor.py:411, for codes >= lo): pass A counts codes
+// below `lo` (= its shared-memory histogram) itself and only counts how many were
+// larger (*nbig); this pass streams over the final codes and counts the codes in
+// [lo, lo + LC_HW_BINS) with shared-memory atomics (64 KB per CTA) and the rest with
+// global ones.  Without it every such code was a global atomic on a few thousand
+// addresses (config 5: 12k symbols, 134M codes, 3.4 ms).  Exits at once when no code
+// was large, or when a chunk prediction failed (the quantizer is resumed first).
+template <typename CodeT>
+__global__ void __launch_bounds__(512) lc_histw_kernel(const CodeT *__restrict__ codes, uint64_t m,
+                                                      uint32_t *__restrict__ hist, uint32_t nbins, uint32_t lo,
+                                                      const unsigned long long *__restrict__ nbig,
+                                                      const unsigned long long *__restrict__ pending,
+                                                      const LcQuantDyn *dyn)
+{
+    if (dyn && dyn->skip) return;
+    if (*nbig == 0 || (pending && *pending != ~0ULL)) return;
+    extern __shared__ __align__(16) unsigned char lc_dyn_smem[];
+    uint32_t *hs = reinterpret_cast<uint32_t *>(lc_dyn_smem);
+    for (uint32_t i = threadIdx.x; i < LC_HW_BINS; i += blockDim.x) hs[i] = 0;
+    __syncthreads();
+    constexpr int V = 16 / sizeof(CodeT);
+    const uint64_t nv = m / V;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint4 *c4 = reinterpret_cast<const uint4 *>(codes);
+    auto add = [&](uint32_t code) {
+        const uint32_t r = code - lo;
+        if (code >= lo) {
+            if (r < LC_HW_BINS) atomicAdd(&hs[r], 1u);
+            else atomicAdd(&hist[code], 1u);
+        }
+    };
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
+        const uint4 q = __ldcs(c4 + i);
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (sizeof(CodeT) == 2) { add(w[k] & 0xffffu); add(w[k] >> 16); }
+            else add(w[k]);
+        }
+    }
+    if (blockIdx.x == 0)
+        for (uint64_t i = nv * V + threadIdx.x; i < m; i += blockDim.x) add((uint32_t)codes[i]);
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < LC_HW_BINS; i += blockDim.x)
+        if (hs[i] && lo + i < nbins) atomicAdd(&hist[lo + i], hs[i]);
+}
+template __global__ void lc_histw_kernel<uint16_t>(const uint16_t *, uint64_t, uint32_t *, uint32_t, uint32_t,
+                                                   const unsigned long long *, const unsigned long long *,
+                                                   const LcQuantDyn *);
+template __global__ void lc_histw_kernel<uint32_t>(const uint32_t *, uint64_t, uint32_t *, uint32_t, uint32_t,
+                                                   const unsigned long long *, const unsigned long long *,
+                                                   const LcQuantDyn *);
 
 // Histogram of u16 codes (np.bincount, compressor.py:411) as its own streaming
 // pass: 16-byte loads, codes 1..16 (the small |m| of smooth data) in packed

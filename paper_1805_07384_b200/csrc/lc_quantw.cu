@@ -177,12 +177,15 @@ __device__ __forceinline__ void lc_qw_pass_a(const LcQuantParams &P, long long w
     double r = L.g0;
     double amax = 0.0;                                   // max |RN(pe * inv) - fq| (~ |frac(qq) - 1/2|)
     uint32_t h0 = 0, h1 = 0, h2 = 0, h3 = 0;             // byte counters of codes 1..16 (4 per word)
+    bool anybig = false;
+    uint16_t *crow = nullptr;
+    uint32_t *crow32 = nullptr;
     if (len > 0) {
         LcFlags F;
         lc_flags_init(F, L.g0);
         bool anyesc = false, anyf = false;
-        uint16_t *crow = cw + lane * LC_QW_CW;
-        uint32_t *crow32 = reinterpret_cast<uint32_t *>(cw) + lane * 33;
+        crow = cw + lane * LC_QW_CW;
+        crow32 = reinterpret_cast<uint32_t *>(cw) + lane * 33;
         auto body = [&](int j) {
             const double v = row[j];
             const double pe = LC_SUB(v, r);
@@ -202,7 +205,7 @@ __device__ __forceinline__ void lc_qw_pass_a(const LcQuantParams &P, long long w
                 const uint32_t idx = min(code - 1u, 16u);    // escape (0) and codes > 16 -> zero entry
                 const uint4 e = hinc[idx];           // shared memory: same code -> broadcast
                 h0 += e.x; h1 += e.y; h2 += e.z; h3 += e.w;
-                if (code - 1u >= 16u) lc_qw_hist_add(hs, P.hist, hb, code, 1u);   // escapes and codes > 16
+                anybig |= code - 1u >= 16u;          // escapes and codes > 16: counted after the chain
             }
             anyesc |= !keep;
             anyf |= lc_flag_test(F, r, inc, rn);
@@ -235,6 +238,30 @@ __device__ __forceinline__ void lc_qw_pass_a(const LcQuantParams &P, long long w
             for (int b = 0; b < 4; ++b)
                 if (lane == 4 * k + b) mine = (wsum[2 * k + (b & 1)] >> (16 * (b >> 1))) & 0xffffu;
         if (lane < 16 && mine) lc_qw_hist_add(hs, P.hist, hb, (uint32_t)lane + 1u, mine);
+        // the other codes (escapes, |m| > 8): a second walk over the lane's staged row, outside
+        // the dependent chain, so the (divergent) atomics pipeline instead of stalling it
+        if (__any_sync(0xffffffffu, anybig)) {
+            if (anybig) {
+                unsigned nbig = 0;                   // codes beyond the shared-memory bins: lc_histw_kernel's
+                if (sizeof(CodeT) == 2) {
+                    const uint32_t *c2 = reinterpret_cast<const uint32_t *>(crow);   // rows start word aligned
+#pragma unroll 4
+                    for (int j = 0; j < len; j += 2) {
+                        const uint32_t pr = c2[j >> 1];
+                        const uint32_t ca = pr & 0xffffu, cb = pr >> 16;
+                        if (ca - 1u >= 16u) { if (ca < hb) atomicAdd(&hs[ca], 1u); else ++nbig; }
+                        if (j + 1 < len && cb - 1u >= 16u) { if (cb < hb) atomicAdd(&hs[cb], 1u); else ++nbig; }
+                    }
+                } else {
+#pragma unroll 4
+                    for (int j = 0; j < len; ++j) {
+                        const uint32_t ca = crow32[j];
+                        if (ca - 1u >= 16u) { if (ca < hb) atomicAdd(&hs[ca], 1u); else ++nbig; }
+                    }
+                }
+                if (nbig) atomicAdd(&hs[LC_HBINS_B], nbig);   // the CTA's count, flushed with the histogram
+            }
+        }
     }
     // flagged lanes replay their chunk from its start, applying the exact step map
     // at every flagged step (a flagged non-event is a no-op)
@@ -300,7 +327,7 @@ __global__ void __launch_bounds__(LC_QW_TPB, 5) lc_quant_wa_kernel(LcQuantParams
                    + (LC_QW_TPB / 32) * CWW;
     const long long nel = (long long)P.n - 1;
     const uint32_t hb = P.nbins < LC_HBINS_B ? P.nbins : LC_HBINS_B;
-    for (uint32_t i = tid; i < LC_HBINS_B; i += LC_QW_TPB) hs[i] = 0;
+    for (uint32_t i = tid; i <= LC_HBINS_B; i += LC_QW_TPB) hs[i] = 0;      // [LC_HBINS_B]: codes beyond the bins
     __shared__ uint4 s_hinc[17];
     if (tid < 17) s_hinc[tid] = c_qw_hinc[tid];
     __syncthreads();
@@ -358,6 +385,7 @@ __global__ void __launch_bounds__(LC_QW_TPB, 5) lc_quant_wa_kernel(LcQuantParams
     __syncthreads();
     for (uint32_t i = tid; i < hb; i += LC_QW_TPB)
         if (hs[i]) atomicAdd(&P.hist[i], hs[i]);
+    if (tid == 0 && hs[LC_HBINS_B]) atomicAdd(P.nbig, (unsigned long long)hs[LC_HBINS_B]);
 }
 
 // Exact reference chain of one chunk from `start` (certified decisions, IEEE
@@ -385,9 +413,11 @@ __device__ __forceinline__ void lc_qw_exact_chunk(const LcQuantParams &P, CodeT 
         const double rn = ieee ? lc_step(P.Q, row[j], r2, &code, &esc, &inc, &pe)
                                : lc_step_nb(P.Q, row[j], r2, &code, &inc, &esc, &pe, ok2);
         const uint32_t old = (uint32_t)codes[q0 + j];
-        if (old != code) {
-            atomicAdd(&P.hist[old], 0xffffffffu);
-            atomicAdd(&P.hist[code], 1u);
+        if (old != code) {                              // bins >= LC_HBINS_B belong to lc_histw_kernel (final codes)
+            const uint32_t hb = P.nbins < LC_HBINS_B ? P.nbins : LC_HBINS_B;
+            if (old < hb) atomicAdd(&P.hist[old], 0xffffffffu);
+            if (code < hb) atomicAdd(&P.hist[code], 1u);
+            else atomicAdd(P.nbig, 1ull);
             codes[q0 + j] = (CodeT)code;
         }
         if (REC) { P.pe[q0 + j] = pe; P.pe_rec[q0 + j] = LC_SUB(rn, r2); }
@@ -496,7 +526,7 @@ size_t lc_quantw_smem_bytes(int code_bytes)
 {
     const size_t cww = code_bytes == 2 ? 32 * LC_QW_CW / 2 : 32 * 33;
     return sizeof(double) * LC_QW_TPB / 32 * LC_QW_ROWS + sizeof(uint32_t) * (LC_QW_TPB / 32) * cww +
-           sizeof(uint32_t) * LC_HBINS_B;
+           sizeof(uint32_t) * (LC_HBINS_B + 4);
 }
 size_t lc_quantw_fix_smem_bytes() { return sizeof(double) * LC_QW_TPB / 32 * LC_QW_ROWS; }
 

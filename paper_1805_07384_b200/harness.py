@@ -107,7 +107,7 @@ class TrialResult:
 
 def multi_failure_trial(method, a, m, b, solve_config: solvers.SolveConfig, comp_config: Optional[CompressorConfig],
                         failures, ckpt_intvl: Optional[int] = None, baseline_n: Optional[int] = None,
-                        comm=None) -> TrialResult:
+                        comm=None, block_version: Optional[int] = None) -> TrialResult:
     """One run with several injected failures (BASELINE.json config 3: failures
     at iterations 100 and 300).  A checkpoint is taken every k iterations
     (not again at the iteration just recovered to); when the solver first
@@ -115,7 +115,8 @@ def multi_failure_trial(method, a, m, b, solve_config: solvers.SolveConfig, comp
     image (from scratch if none).  N' = final - baseline iterations.  The
     same protocol as tests/golden/make_config_golden.py runs on the real
     reference (simulate.measure_n_prime, simulate.py:461-508, with more than
-    one failure per run)."""
+    one failure per run).  block_version: the image's block format (None: the
+    checkpoint layer's default, v3; 1: the reference's bytes and ratios)."""
     import time
     k = solve_config.ckpt_intvl if ckpt_intvl is None else ckpt_intvl
     if k < 1:
@@ -152,7 +153,7 @@ def multi_failure_trial(method, a, m, b, solve_config: solvers.SolveConfig, comp
             if comp_config is None:
                 last, cost = ckpt.checkpoint_traditional(solver, store)
             else:
-                last, cost = ckpt.checkpoint_lossy(solver, comp_config, store)
+                last, cost = ckpt.checkpoint_lossy(solver, comp_config, store, block_version=block_version)
                 ratios.append(solver.x.numel() * 8 / len(last.payload))
                 tc.append(cost.t_compress)
         nxt = [it - it % k + k]

@@ -1,7 +1,7 @@
 """Profiling driver: one warm-up + one measured compress/decompress of the config-2 vector
 (n = 2^26) at one bound through the public API.  Used under ncu:
 
-    python profiles/prof_codec.py [eb_rel] [log2n]
+    python profiles/prof_codec.py [eb_rel] [log2n] [block_version]
 Prints the quantizer's relaunches and exactly re-run chunks of the last compress.
 """
 import os
@@ -18,9 +18,10 @@ from bench import make_vector  # noqa: E402
 eb = float(sys.argv[1]) if len(sys.argv) > 1 else 1e-4
 n = 1 << (int(sys.argv[2]) if len(sys.argv) > 2 else 26)
 xd = torch.from_numpy(make_vector(n)).cuda()
+ver = int(sys.argv[3]) if len(sys.argv) > 3 else 1          # block version (3: one-pass decoder)
 cfg = lc.CompressorConfig.value_range_relative(eb)
 for _ in range(2):
-    blk = lc.compress(xd, cfg)
+    blk = lc.compress(xd, cfg, block_version=ver)
     rec = lc.decompress(blk, device="cuda")
 torch.cuda.synchronize()
 err = float((rec - xd).abs().max())
