@@ -421,7 +421,7 @@ def run_b200(args, rank, world, local_rank):
     # encoder / read by the decoder); codes are an internal intermediate.
     peak, peak_src = measured_peak()
     groups = {
-        "quantizer[lc_quant_wa+lc_map_scan+lc_quant_wfix]": lambda d: d["compress_phase_ms"]["quantize"],
+        "quantizer[lc_quant_wa+lc_map_scan+lc_quant_wfix+lc_histw]": lambda d: d["compress_phase_ms"]["quantize"],
         ("reconstruction[lc_dec_v3: Huffman walk + reference chain]" if fmt3 else
          "reconstruction[lc_rec_a+lc_map_scan+lc_rec_b]"):
             lambda d: d["decompress_phase_ms"]["reconstruct"],
@@ -440,7 +440,8 @@ def run_b200(args, rank, world, local_rank):
            "encoder": pay + 16 * esc}[dom.split("[")[0]]
     t_ms = shares[dom] / len(per)
     achieved = alg / (t_ms / 1e3) / 1e9
-    nc = ncu_traffic().get(dom.split("[")[0], {})
+    nkey = dom.split("[")[0]
+    nc = ncu_traffic().get("decode_v3" if (fmt3 and nkey == "reconstruction") else nkey, {})
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "peak_source": peak_src,
                 "traffic": nc.get("dram_bytes_per_launch"), "algorithmic_bytes": alg,

@@ -15,5 +15,6 @@ for r in csv.reader(io.StringIO(out)):
         rows.append((f,int(r[0]),r[1][:100],int(r[7] or 0),int(r[4] or 0)))
 ti=sum(x[3] for x in rows); ts=sum(x[4] for x in rows)
 print('total warp instr',ti,'samples',ts)
-for x in sorted(rows,key=lambda x:-x[4])[:int(sys.argv[3]) if len(sys.argv)>3 else 40]:
+bykey = 3 if len(sys.argv) > 4 and sys.argv[4] == "ins" else 4
+for x in sorted(rows,key=lambda x:-x[bykey])[:int(sys.argv[3]) if len(sys.argv)>3 else 40]:
     print(f"{x[4]/ts*100:5.1f}% smp {x[3]/ti*100:5.1f}% ins  {x[0]}:{x[1]}  {x[2]}")
