@@ -9,7 +9,7 @@
 #define LC_TILE (LC_TPB * LC_L)    // codes per tile (8192)
 #define LC_ROW (LC_L + 1)          // padded smem row (conflict-free column walk)
 #define LC_HBINS 4096              // histogram bins privatised in smem
-#define LC_HBINS_B 1024            // ... in the split pass B (keeps 3 CTAs per SM)
+#define LC_HBINS_B 512             // ... in pass A (44.6 KB per CTA: five 4-warp CTAs per SM); larger codes: lc_histw_kernel
 
 // Look-back descriptor of one tile (decoupled look-back, two channels:
 // anchor positions and offset maps).
