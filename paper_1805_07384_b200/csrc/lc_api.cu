@@ -949,12 +949,13 @@ int lc_debug_codebook(lc_ctx *ctx, const uint32_t *hist, uint32_t nbins, uint8_t
 }
 
 // Debug/test hook: copy an intermediate of the last compress to host.
-// what: 0 codes, 1 histogram (u32), 2 code lengths (u8), 3 codewords (u64)
+// what: 0 codes, 1 histogram (u32), 2 code lengths (u8), 3 codewords (u64), 5 codebook summary,
+// 6 warp-tile aggregates (OffMap[ntiles + 1], then offsets / slacks / guesses)
 int lc_debug_copy(lc_ctx *ctx, int what, void *host, uint64_t bytes)
 {
     LcDeviceGuard guard(ctx->device);
     const void *src = what == 0 ? ctx->codes.p : what == 1 ? ctx->hist.p : what == 2 ? ctx->lengths.p
-                    : what == 3 ? ctx->cw.p : what == 5 ? ctx->cbout.p : ctx->timeline.p;
+                    : what == 3 ? ctx->cw.p : what == 5 ? ctx->cbout.p : what == 6 ? ctx->tiles.p : ctx->timeline.p;
     LC_CUDA_OK(cudaMemcpyAsync(host, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
     LC_CUDA_OK(cudaStreamSynchronize(ctx->stream));
     return 0;
