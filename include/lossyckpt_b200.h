@@ -180,6 +180,11 @@ int lc_debug_codebook(lc_ctx *ctx, const uint32_t *hist, uint32_t nbins, uint8_t
                       uint64_t *codes_out, int *max_len_out);
 long long lc_ctx_get_stat(lc_ctx *ctx, int key);
 
+/* Diagnostics by environment (read at context creation): LC_DEBUG_SYNC=1
+ * synchronises and checks after every launch the library names (a CUDA
+ * fault is then reported at its kernel); with LC_DEBUG_LOG=1 as well every
+ * such launch is named on stderr before and after its synchronisation (a
+ * hang shows the kernel that never returned).                              */
 /* Launch timeline (diagnostics; contexts created with LC_TRACE=1 in the
  * environment): lc_trace_mark_api adds a named mark, every launch adds one
  * with the kernel name; lc_trace_read syncs the stream, writes one line
