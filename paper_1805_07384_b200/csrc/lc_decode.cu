@@ -1052,7 +1052,11 @@ __global__ void __launch_bounds__(LC_V3_TPB) lc_dec_v3_kernel(LcDecParams P, con
     const int tml = Tg->max_len;
     const unsigned long0 = tml > LC_LUT_BITS ? (unsigned)Tg->offset[LC_LUT_BITS + 1] : 0u;
     const unsigned nlong_all = tml > LC_LUT_BITS ? (unsigned)Tg->used - long0 : 0u;
-    const unsigned nlong = nlong_all <= LC_V3_LONG_SMEM ? nlong_all : 0u;
+    // blocks with codes of 13..32 bits: s_long holds the symbols of the 13..16-bit codes by
+    // 16-bit prefix instead (sym16, beside Ts.len16), so the straight-line walk resolves them
+    // with two independent loads; longer codes then read `sorted` from global memory
+    const bool cand16 = tml > LC_LUT_BITS && tml <= 32;
+    const unsigned nlong = cand16 ? 0u : (nlong_all <= LC_V3_LONG_SMEM ? nlong_all : 0u);
     for (unsigned i = threadIdx.x; i < nlong; i += blockDim.x) s_long[i] = __ldg(P.sorted + long0 + i);
     if (threadIdx.x == 0) { Ts.max_len = Tg->max_len; Ts.canon = Tg->canon; Ts.s16 = Tg->s16; }
     for (int i = threadIdx.x; i < 34; i += blockDim.x) Ts.lim[i] = Tg->lim[i];
@@ -1062,6 +1066,23 @@ __global__ void __launch_bounds__(LC_V3_TPB) lc_dec_v3_kernel(LcDecParams P, con
     for (int i = threadIdx.x; i < LC_L16 / 16; i += blockDim.x)
         reinterpret_cast<uint4 *>(Ts.len16)[i] = __ldg(reinterpret_cast<const uint4 *>(Tg->len16) + i);
     __syncthreads();
+    uint16_t *sym16 = reinterpret_cast<uint16_t *>(s_long);
+    bool m16 = cand16;
+    if (cand16) {
+        static_assert(LC_L16 * sizeof(uint16_t) <= LC_V3_LONG_SMEM * sizeof(uint32_t), "sym16 must fit s_long");
+        int big = 0;
+        for (int i = threadIdx.x; i < LC_L16; i += blockDim.x) {
+            const int l = Ts.len16[i];
+            uint32_t sy = 0;
+            if (l) {
+                const unsigned long long v = (unsigned long long)(Ts.s16 + (unsigned)i) >> (16 - l);
+                sy = __ldg(P.sorted + Ts.offset[l] + (v - Ts.first_code[l]));
+                big |= sy > 0xffffu;
+            }
+            sym16[i] = (uint16_t)sy;
+        }
+        m16 = __syncthreads_or(big) == 0;                // symbols beyond u16 (u32 codes): table unused
+    }
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     double *stg = v3_stage + (size_t)wid * 32 * 33;
     double *myrow = stg + lane * 33;
@@ -1140,16 +1161,22 @@ __global__ void __launch_bounds__(LC_V3_TPB) lc_dec_v3_kernel(LcDecParams P, con
                     if ((next & 3u) == 0) turn();
                 }
                 double *orow = out + j * LC_SYNC_K + 1 - lane * LC_SYNC_K;   // + rr * 1024 + lane below
+                uint32_t wnext = word(next);                               // the ring word the next refill takes
                 for (unsigned sb = 0; sb < LC_SYNC_K; sb += 32) {
-#pragma unroll 2
+#pragma unroll 4
                     for (unsigned t = 0; t < 32; ++t) {
                         const bool act = !tail || sb + t < todo;           // tail: the walk stops at the interval's end
                         const uint32_t e1 = Ts.lut[(unsigned)(buf >> (64 - LC_LUT_BITS))];
                         uint32_t sym = act ? e1 & 0xffffffu : 1u;          // 1: m = 0
                         int l = (int)(e1 >> 24);
                         if (act && l > LC_LUT_BITS) {                      // a code longer than the LUT (<= 32 bits here)
-                            const int l2 = lc_long_len_fast(Ts, buf);      // 13..16 bits by table, longer by the limits
-                            if (l2 > 0 && l2 <= 32) {
+                            const unsigned i16 = (unsigned)(buf >> 48) - Ts.s16;
+                            const int l16 = (m16 && i16 < (unsigned)LC_L16) ? (int)Ts.len16[i16] : 0;
+                            const int l2 = l16 ? l16 : lc_long_len_fast(Ts, buf);   // 13..16 bits by table, longer by the limits
+                            if (l16) {
+                                sym = sym16[i16];
+                                l = l16;
+                            } else if (l2 > 0 && l2 <= 32) {
                                 const unsigned long long v = (buf >> 32) >> (32 - l2);
                                 const unsigned long long idx = Ts.offset[l2] + (v - Ts.first_code[l2]);
                                 sym = idx - long0 < nlong ? s_long[idx - long0] : __ldg(P.sorted + idx);
@@ -1169,12 +1196,15 @@ __global__ void __launch_bounds__(LC_V3_TPB) lc_dec_v3_kernel(LcDecParams P, con
                         buf <<= lc;
                         nb -= lc;
                         pos += lc;
-                        if (nb <= 32) {                                    // refill from the ring
-                            buf |= (unsigned long long)word(next) << (32 - nb);
-                            nb += 32;
-                            ++next;
-                            if ((next & 3u) == 0) turn();
-                        }
+                        // refill without a branch: the next ring word is always at hand (loaded one step
+                        // ahead, so its shared-memory latency is off the dependent walk); only the ring
+                        // turn every fourth refill branches
+                        const bool rf = nb <= 32;
+                        buf |= rf ? (unsigned long long)wnext << ((32 - nb) & 63) : 0ull;
+                        nb += rf ? 32 : 0;
+                        next += rf ? 1u : 0u;
+                        if (rf && (next & 3u) == 0) turn();
+                        wnext = word(next);
                         z0 |= sym == 0;
                         const uint32_t zz = sym - 1u;                      // compressor.py:370-374
                         const int mm = (int)(zz >> 1) ^ -(int)(zz & 1u);
