@@ -22,6 +22,7 @@
 // Reconstruction runs the same chunked exact chain as the encoder
 // (lc_chain.cuh): guesses from the m-prefix since the last escape, offset
 // maps + look-back, exact re-run, end/start checks (host relaunch on failure).
+#include <type_traits>
 #include <cub/block/block_scan.cuh>
 #include "lc_kernels.cuh"
 #include "../../include/lossyckpt_b200.h"
@@ -1113,9 +1114,9 @@ __global__ void __launch_bounds__(LC_V3_TPB) lc_dec_v3_kernel(LcDecParams P, con
         double r = live ? starts[j] : 0.0;
         unsigned long long e = live ? sesc[j] : 0ull;
         int fl0 = 0, fl1 = 0;
-        // Fast path: a warp whose 32 intervals are all escape-free (per the escape table), in a
-        // block whose codes are at most 32 bits long, runs a straight-line walk: no escape or
-        // payload-end branches, codes longer than the LUT resolved out of line where they occur; refills come from a per-lane shared-memory ring
+        // Fast path: in a block whose codes are at most 32 bits long, a warp without a malformed
+        // table entry runs a straight-line walk: no payload-end branches, codes longer than the
+        // LUT and escapes resolved where they occur (rare branches); refills come from a per-lane shared-memory ring
         // kept two 16-byte groups ahead by asynchronous loads.  Invalid codewords, escape
         // codes or table disagreements are caught after the walk (status 1 / 6).
         {
@@ -1123,7 +1124,7 @@ __global__ void __launch_bounds__(LC_V3_TPB) lc_dec_v3_kernel(LcDecParams P, con
             // (tail): otherwise the last warp alone would run the slower general walk and set the
             // kernel's duration (measured: 350 instead of 175 us at 2^26, eb 1e-3)
             const bool lastiv = live && j + 1 == nsync;
-            const bool full = !live || (!bad && (lastiv ? e == n_esc : (todo == LC_SYNC_K && sesc[j + 1] == e)));
+            const bool full = !live || (!bad && (lastiv || todo == LC_SYNC_K));
             const bool tail = __any_sync(0xffffffffu, !live || lastiv);
             if (Ts.max_len <= 32 && __all_sync(0xffffffffu, full)) {
                 const unsigned f = (unsigned)(lane >> 2) & 7u;             // ring swizzle (bank spread)
@@ -1146,7 +1147,7 @@ __global__ void __launch_bounds__(LC_V3_TPB) lc_dec_v3_kernel(LcDecParams P, con
                 int nb = 64 - sh;
                 next += 2;
                 unsigned pos = p0;
-                bool inv = false, z0 = false;
+                bool inv = false;
                 auto turn = [&]() {                                        // entering group next >> 2
                     const unsigned gg = next >> 2, sl = ((gg + 1u) & 1u) * 4u;
                     ring[(sl + 0) ^ f] = pend.x; ring[(sl + 1) ^ f] = pend.y;
@@ -1161,6 +1162,11 @@ __global__ void __launch_bounds__(LC_V3_TPB) lc_dec_v3_kernel(LcDecParams P, con
                     if ((next & 3u) == 0) turn();
                 }
                 double *orow = out + j * LC_SYNC_K + 1 - lane * LC_SYNC_K;   // + rr * 1024 + lane below
+                // The walk is bound by the latency of one warp's dependent steps, where every branch in
+                // the loop costs a pipeline bubble even when it is never taken: the escape and
+                // long-code branches are compiled in only for warps / blocks that can need them.
+                auto walk = [&](auto esc_tag, auto long_tag) {
+                constexpr bool ESC = decltype(esc_tag)::value, LONG = decltype(long_tag)::value;
                 uint32_t wnext = word(next);                               // the ring word the next refill takes
                 for (unsigned sb = 0; sb < LC_SYNC_K; sb += 32) {
 #pragma unroll 4
@@ -1169,7 +1175,7 @@ __global__ void __launch_bounds__(LC_V3_TPB) lc_dec_v3_kernel(LcDecParams P, con
                         const uint32_t e1 = Ts.lut[(unsigned)(buf >> (64 - LC_LUT_BITS))];
                         uint32_t sym = act ? e1 & 0xffffffu : 1u;          // 1: m = 0
                         int l = (int)(e1 >> 24);
-                        if (act && l > LC_LUT_BITS) {                      // a code longer than the LUT (<= 32 bits here)
+                        if (LONG && act && l > LC_LUT_BITS) {              // a code longer than the LUT (<= 32 bits here)
                             const unsigned i16 = (unsigned)(buf >> 48) - Ts.s16;
                             const int l16 = (m16 && i16 < (unsigned)LC_L16) ? (int)Ts.len16[i16] : 0;
                             const int l2 = l16 ? l16 : lc_long_len_fast(Ts, buf);   // 13..16 bits by table, longer by the limits
@@ -1192,7 +1198,7 @@ __global__ void __launch_bounds__(LC_V3_TPB) lc_dec_v3_kernel(LcDecParams P, con
                             if (l == 0 || l > 32) { inv = true; l = 1; sym = 1u; }   // no codeword here: flagged, walk on
                             }
                         }
-                        const int lc = act ? l : 0;
+                        const int lc = act ? (LONG ? l : (l & 15)) : 0;
                         buf <<= lc;
                         nb -= lc;
                         pos += lc;
@@ -1205,7 +1211,18 @@ __global__ void __launch_bounds__(LC_V3_TPB) lc_dec_v3_kernel(LcDecParams P, con
                         next += rf ? 1u : 0u;
                         if (rf && (next & 3u) == 0) turn();
                         wnext = word(next);
-                        z0 |= sym == 0;
+                        if (ESC && act && sym == 0u) {                     // escape (compressor.py:365-369): rare
+                            const unsigned long long posn = o0 + sb + t + 1;   // element index
+                            if (e < n_esc) {
+                                r = __ldg(esc_val + e);
+                                fl1 |= __ldg(esc_idx + e) != posn;
+                            } else {
+                                fl0 = 1;
+                            }
+                            ++e;
+                        }
+                        if (!ESC) e += (act && sym == 0u) ? 1ull : 0ull;  // an escape the table does not know: the end check fails
+                        if (!LONG) inv |= act && l > LC_LUT_BITS;
                         const uint32_t zz = sym - 1u;                      // compressor.py:370-374
                         const int mm = (int)(zz >> 1) ^ -(int)(zz & 1u);
                         const double inc = LC_MUL((double)mm, delta);
@@ -1227,10 +1244,22 @@ __global__ void __launch_bounds__(LC_V3_TPB) lc_dec_v3_kernel(LcDecParams P, con
                     }
                     __syncwarp();
                 }
+                };
+                const bool has_esc = __any_sync(0xffffffffu, live && (lastiv ? e != n_esc : sesc[j + 1] != e));
+                const bool has_long = Ts.max_len > LC_LUT_BITS;
+                if (has_esc) {
+                    if (has_long) walk(std::true_type{}, std::true_type{});
+                    else walk(std::true_type{}, std::false_type{});
+                } else {
+                    if (has_long) walk(std::false_type{}, std::true_type{});
+                    else walk(std::false_type{}, std::false_type{});
+                }
                 if (live) {
                     if (inv) atomicExch(&fin->status, 1);
-                    else if (z0 || wbase + pos != s1 || (!lastiv && lc_bits(r) != lc_bits(starts[j + 1])))
+                    else if (wbase + pos != s1 || (!lastiv && (lc_bits(r) != lc_bits(starts[j + 1]) || e != sesc[j + 1])))
                         atomicExch(&fin->status, 6);
+                    if (fl0) atomicExch(&fin->esc_flags[0], 1);
+                    if (fl1) atomicExch(&fin->esc_flags[1], 1);
                     if (lastiv) fin->esc_total = (long long)e;
                 }
                 continue;
