@@ -216,3 +216,30 @@ def test_v3_corrupted_tables(lc):
             lc.decompress(dataclasses.replace(b3, **{field: t}))
     with pytest.raises(lc.IntegrityError):
         lc.decompress(dataclasses.replace(b3, escape_indices=b3.escape_indices + 1))
+
+
+@pytest.mark.gpu
+def test_v3_straight_line_walk_variants(lc):
+    """The v3 decoder's straight-line walk in its four specialisations and its fallbacks:
+    long codes (13..32 bits) with u16 symbols (16-bit prefix symbol table) and with u32 symbols
+    (bin budget 100000: the table is unusable), escapes in most intervals, escape-free tiny
+    alphabets, a short last interval, vectors shorter than one warp group -- all bit-identical
+    to the reference reconstruction and equal to the v1 decode."""
+    rng = np.random.default_rng(81)
+    walk = rng.normal(size=600_000).cumsum()
+    spiky = walk.copy()
+    spiky[rng.integers(0, spiky.size, 6000)] += 1e8                    # escapes in most intervals
+    cases = [(walk, dict(eb=1e-7), {}),                                  # long codes, u16 symbols
+             (walk, dict(eb=1e-7), dict(n_bins_half=100_000)),           # long codes, u32 symbols
+             (spiky, dict(eb=1e-9), {}),                                 # escapes + long codes
+             (_sine(300_000, 3) , dict(eb=1e-2), {}),                    # tiny alphabet, no escapes
+             (spiky[:40_000], dict(eb=1e-3), {}),                        # escapes, short codes
+             (walk[:1500], dict(eb=1e-5), {}), (walk[:33 * 1024 + 7], dict(eb=1e-5), {})]
+    for x, kw, ckw in cases:
+        cfg3 = lc.CompressorConfig.value_range_relative(kw["eb"], block_version=3, **ckw)
+        b3 = lc.compress(x, cfg3)
+        ref = orc.compress(x, "value_range_relative", kw["eb"], n_bins_half=ckw.get("n_bins_half", 32768))
+        r3 = lc.decompress(lc.CompressedBlock.from_bytes(b3.to_bytes()))
+        assert np.array_equal(r3.view(np.int64), ref["recon"].view(np.int64)), (x.size, kw, ckw)
+        b1 = lc.compress(x, lc.CompressorConfig.value_range_relative(kw["eb"], **ckw))
+        assert np.array_equal(lc.decompress(b1).view(np.int64), r3.view(np.int64))
