@@ -332,6 +332,7 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     unsigned long long *first_bad = (unsigned long long *)((char *)ctx->counters.p + 16);
     unsigned long long *exact_count = (unsigned long long *)((char *)ctx->counters.p + 32);
     unsigned long long *nbig = (unsigned long long *)((char *)ctx->counters.p + 64);
+    unsigned *maxcode = (unsigned *)((char *)ctx->counters.p + 72);
 
     LcQuantParams P;
     memset(&P, 0, sizeof P);
@@ -364,6 +365,7 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     P.verify = ctx->opt[LC_OPT_VERIFY] ? 1 : 0;
     P.exact_count = exact_count;
     P.nbig = nbig;
+    P.maxcode = maxcode;
     P.resume = 0;
     P.first_tile = 0;
     P.resume_chunk = -1;
@@ -380,7 +382,7 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
 
     LC_CUDA_OK(cudaMemsetAsync(P.hist, 0, nbins * sizeof(uint32_t), st));
     LC_CUDA_OK(cudaMemsetAsync(exact_count, 0, 8, st));
-    LC_CUDA_OK(cudaMemsetAsync(nbig, 0, 8, st));
+    LC_CUDA_OK(cudaMemsetAsync(nbig, 0, 16, st));            // nbig and maxcode
 
     unsigned long long *hbad = (unsigned long long *)ctx->pinned;
     LcCodebookOut *hcb = (LcCodebookOut *)((char *)ctx->pinned + 64);
@@ -489,7 +491,7 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
         lc_codebook_kernel<<<1, 1024, lc_codebook_smem_bytes(), st>>>(
             P.hist, nbins, (uint8_t *)ctx->lengths.p, (unsigned long long *)ctx->cw.p,
             (unsigned long long *)ctx->gkeys.p, (unsigned long long *)ctx->ifreq.p, (int *)ctx->parent.p, cbo, dyn,
-            first_bad);
+            first_bad, full ? nullptr : maxcode);
         { int _rc = lc_debug_check(ctx, "lc_codebook_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
         LC_CUDA_OK(cudaEventRecord(ctx->pev[3], st));
         ctx->launches += 1;
@@ -936,7 +938,7 @@ int lc_debug_codebook(lc_ctx *ctx, const uint32_t *hist, uint32_t nbins, uint8_t
     lc_codebook_kernel<<<1, 1024, lc_codebook_smem_bytes(), st>>>(
         (const uint32_t *)ctx->hist.p, nbins, (uint8_t *)ctx->lengths.p, (unsigned long long *)ctx->cw.p,
         (unsigned long long *)ctx->gkeys.p, (unsigned long long *)ctx->ifreq.p, (int *)ctx->parent.p,
-        (LcCodebookOut *)ctx->cbout.p, nullptr, nullptr);
+        (LcCodebookOut *)ctx->cbout.p, nullptr, nullptr, nullptr);
     ctx->launches += 1;
     { int _rc = lc_debug_check(ctx, "lc_codebook_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
     LcCodebookOut *h = (LcCodebookOut *)((char *)ctx->pinned + 1024);

@@ -80,6 +80,7 @@ struct LcQuantParams {
     double *bad_end;         // per chunk: exact end value when its successor failed
     double *pe, *pe_rec;     // optional traces
     unsigned long long *nbig;      // codes >= the shared-memory histogram's range seen so far (lc_histw_kernel counts them)
+    unsigned *maxcode;             // largest code produced so far (the codebook searches [0, maxcode] only)
     unsigned long long *timeline;  // optional: 8 globaltimer stamps per tile (profiling)
     // split-pass data
     int use_anchors;             // 0: no definite escape possible (range pass), anchor = launch anchor
@@ -187,7 +188,7 @@ __global__ void lc_codebook_kernel(const uint32_t *__restrict__ hist, uint32_t n
                                    unsigned long long *__restrict__ codes, unsigned long long *__restrict__ gkeys,
                                    unsigned long long *__restrict__ ifreq, int *__restrict__ parent, LcCodebookOut *out,
                                    const LcQuantDyn *dyn,
-                                   const unsigned long long *pending);
+                                   const unsigned long long *pending, const unsigned *maxcode);
 #define LC_HW_BINS 16384            // shared-memory bins of the wide-alphabet histogram pass (64 KB)
 template <typename CodeT>
 __global__ void lc_histw_kernel(const CodeT *__restrict__ codes, uint64_t m, uint32_t *__restrict__ hist, uint32_t nbins,

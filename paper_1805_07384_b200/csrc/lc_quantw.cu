@@ -178,6 +178,7 @@ __device__ __forceinline__ void lc_qw_pass_a(const LcQuantParams &P, long long w
     double amax = 0.0;                                   // max |RN(pe * inv) - fq| (~ |frac(qq) - 1/2|)
     uint32_t h0 = 0, h1 = 0, h2 = 0, h3 = 0;             // byte counters of codes 1..16 (4 per word)
     bool anybig = false;
+    uint32_t maxc = 0;                                   // largest code of the chunk
     uint16_t *crow = nullptr;
     uint32_t *crow32 = nullptr;
     if (len > 0) {
@@ -206,6 +207,7 @@ __device__ __forceinline__ void lc_qw_pass_a(const LcQuantParams &P, long long w
                 const uint4 e = hinc[idx];           // shared memory: same code -> broadcast
                 h0 += e.x; h1 += e.y; h2 += e.z; h3 += e.w;
                 anybig |= code - 1u >= 16u;          // escapes and codes > 16: counted after the chain
+                maxc = code > maxc ? code : maxc;
             }
             anyesc |= !keep;
             anyf |= lc_flag_test(F, r, inc, rn);
@@ -238,6 +240,10 @@ __device__ __forceinline__ void lc_qw_pass_a(const LcQuantParams &P, long long w
             for (int b = 0; b < 4; ++b)
                 if (lane == 4 * k + b) mine = (wsum[2 * k + (b & 1)] >> (16 * (b >> 1))) & 0xffffu;
         if (lane < 16 && mine) lc_qw_hist_add(hs, P.hist, hb, (uint32_t)lane + 1u, mine);
+        {
+            const uint32_t wm = __reduce_max_sync(0xffffffffu, maxc);
+            if (lane == 0 && wm > hs[LC_HBINS_B + 1]) atomicMax(&hs[LC_HBINS_B + 1], wm);
+        }
         // the other codes (escapes, |m| > 8): a second walk over the lane's staged row, outside
         // the dependent chain, so the (divergent) atomics pipeline instead of stalling it
         if (__any_sync(0xffffffffu, anybig)) {
@@ -327,7 +333,7 @@ __global__ void __launch_bounds__(LC_QW_TPB, 5) lc_quant_wa_kernel(LcQuantParams
                    + (LC_QW_TPB / 32) * CWW;
     const long long nel = (long long)P.n - 1;
     const uint32_t hb = P.nbins < LC_HBINS_B ? P.nbins : LC_HBINS_B;
-    for (uint32_t i = tid; i <= LC_HBINS_B; i += LC_QW_TPB) hs[i] = 0;      // [LC_HBINS_B]: codes beyond the bins
+    for (uint32_t i = tid; i <= LC_HBINS_B + 1; i += LC_QW_TPB) hs[i] = 0;  // [LC_HBINS_B]: codes beyond the bins, [+1]: max code
     __shared__ uint4 s_hinc[17];
     if (tid < 17) s_hinc[tid] = c_qw_hinc[tid];
     __syncthreads();
@@ -386,6 +392,7 @@ __global__ void __launch_bounds__(LC_QW_TPB, 5) lc_quant_wa_kernel(LcQuantParams
     for (uint32_t i = tid; i < hb; i += LC_QW_TPB)
         if (hs[i]) atomicAdd(&P.hist[i], hs[i]);
     if (tid == 0 && hs[LC_HBINS_B]) atomicAdd(P.nbig, (unsigned long long)hs[LC_HBINS_B]);
+    if (tid == 0 && hs[LC_HBINS_B + 1]) atomicMax(P.maxcode, hs[LC_HBINS_B + 1]);
 }
 
 // Exact reference chain of one chunk from `start` (certified decisions, IEEE
@@ -418,6 +425,7 @@ __device__ __forceinline__ void lc_qw_exact_chunk(const LcQuantParams &P, CodeT 
             if (old < hb) atomicAdd(&P.hist[old], 0xffffffffu);
             if (code < hb) atomicAdd(&P.hist[code], 1u);
             else atomicAdd(P.nbig, 1ull);
+            atomicMax(P.maxcode, code);
             codes[q0 + j] = (CodeT)code;
         }
         if (REC) { P.pe[q0 + j] = pe; P.pe_rec[q0 + j] = LC_SUB(rn, r2); }
