@@ -92,6 +92,8 @@ __global__ void __launch_bounds__(1024) lc_dec_tables_kernel(const uint8_t *__re
     __shared__ int s_max;
     __shared__ unsigned long long s_first[66], s_off[66];
     __shared__ unsigned int s_lut[1 << LC_LUT_BITS];
+    __shared__ unsigned long long s_lim[34];         // T->lim, kept on chip for the length table below
+    __shared__ unsigned s_s16;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
     if (tid < 66) s_cnt[tid] = 0;
     if (tid == 0) s_max = 0;
@@ -138,25 +140,28 @@ __global__ void __launch_bounds__(1024) lc_dec_tables_kernel(const uint8_t *__re
             else if (canon && l == ml)
                 v = (s_first[l] + (unsigned long long)s_cnt[l]) << (32 - l);
             T->lim[l] = v;
+            s_lim[l] = v;
         }
         T->canon = canon;
         // long canonical codes occupy the 12-bit prefixes from lim[12] upwards
-        T->s16 = (canon && ml > LC_LUT_BITS) ? (unsigned)(T->lim[LC_LUT_BITS] >> 16) : 0x10000u;
+        s_s16 = (canon && ml > LC_LUT_BITS) ? (unsigned)(s_lim[LC_LUT_BITS] >> 16) : 0x10000u;
+        T->s16 = s_s16;
     }
     __syncthreads();
     {
         // lengths 13..16 depend on the top 16 bits only (lim[l] is a multiple
-        // of 2^16 for l <= 16); same rule as lc_long_len
-        const unsigned s16 = T->s16;
+        // of 2^16 for l <= 16); same rule as lc_long_len.  (Limits read from shared memory:
+        // reading T->lim back from global memory put ~10 dependent L2 round trips here.)
+        const unsigned s16 = s_s16;
         const int ml = s_max;
         for (int i = tid; i < LC_L16; i += blockDim.x) {
             const unsigned w16 = s16 + (unsigned)i;
             int len = 0;
             if (w16 < 0x10000u) {
                 const unsigned long long w = (unsigned long long)w16 << 16;
-                if (w < T->lim[ml <= 32 ? ml : 32])
+                if (w < s_lim[ml <= 32 ? ml : 32])
                     for (int l = LC_LUT_BITS + 1; l <= 16 && l <= ml; ++l)
-                        if (w < T->lim[l]) { len = l; break; }
+                        if (w < s_lim[l]) { len = l; break; }
             }
             T->len16[i] = (unsigned char)len;
         }
