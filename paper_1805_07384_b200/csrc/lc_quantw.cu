@@ -337,7 +337,13 @@ __global__ void __launch_bounds__(LC_QW_TPB, 5) lc_quant_wa_kernel(LcQuantParams
     __shared__ uint4 s_hinc[17];
     if (tid < 17) s_hinc[tid] = c_qw_hinc[tid];
     __syncthreads();
-    const bool force = P.verify || P.pe != nullptr || !(P.rmax < INFINITY) || P.inject_chunk >= 0;
+    // vectors whose whole range lies below 2^-960 have subnormal ulps: the offset-map arithmetic
+    // is not exact there, so nothing is certified (every chunk is re-run exactly and end-checked)
+    // small bin budgets (n_bins_half < 1024): the chain cannot follow x, so it can sit far from the
+    // guess lattice and the offsets stop being exactly representable (g + D off by an ulp: found by a
+    // randomized run as wrong v3 sync starts at n_bins_half = 1 and 7): nothing is certified either
+    const bool force = P.verify || P.pe != nullptr || !(P.rmax < INFINITY) || P.rmax < 0x1p-960 || P.nbins < 2048u ||
+                       P.inject_chunk >= 0;
     // warp tiles are claimed by ticket (balanced tail); the next ticket is taken
     // one tile ahead so its x can be prefetched into L2 while this one runs
     long long w = 0, wnext = 0;
@@ -457,7 +463,7 @@ __global__ void __launch_bounds__(LC_QW_TPB, 5) lc_quant_wfix_kernel(LcQuantPara
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     double *xw = reinterpret_cast<double *>(lc_dyn_smem) + wid * LC_QW_ROWS;
     unsigned long long exact_chunks = 0;
-    const bool force = P.verify || REC || !(P.rmax < INFINITY) || P.inject_chunk >= 0;
+    const bool force = P.verify || REC || !(P.rmax < INFINITY) || P.rmax < 0x1p-960 || P.nbins < 2048u || P.inject_chunk >= 0;
     if (P.resume == 1) {
         if (wid != 0) return;
         const long long rel = P.resume_chunk - P.first_chunk;

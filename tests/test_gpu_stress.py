@@ -173,3 +173,51 @@ def test_edge_corpus_relaunches_reported(lc, ctx):
     blk = lc.compress(torch.from_numpy(x).cuda(), lc.CompressorConfig.absolute(1e-3))
     assert ctx.lib.lc_ctx_get_stat(ctx.h, STAT_QUANT_RELAUNCHES) >= 1
     assert ctx.lib.lc_ctx_get_stat(ctx.h, 4) >= 1                          # chunks re-run exactly
+
+
+def test_subnormal_ulp_vectors(lc, ctx):
+    """Vectors whose values are so small that their ulps are subnormal (|x| < 2^-960): the
+    offset-map arithmetic is not exact there, so the quantizer certifies nothing and falls back
+    to exact re-runs / the sequential chain.  Bytes equal the oracle's, v3 tables and both
+    reconstructions are exact (found by a randomized run: v3 sync starts were off by an ulp)."""
+    r = np.random.default_rng(5)
+    for n, sc, eb in ((4098, 1e-300, 1e-2), (50_000, 1e-300, 1e-4), (300_000, 1e-305, 1e-3), (300_000, 1e-290, 1e-5)):
+        x = r.normal(0, sc, n).cumsum()
+        ref = orc.compress(x, "value_range_relative", eb)
+        b1 = lc.compress(x, lc.CompressorConfig.value_range_relative(eb))
+        assert b1.to_bytes() == orc.to_bytes(ref), (n, sc, eb)
+        b3 = lc.compress(x, lc.CompressorConfig.value_range_relative(eb, block_version=3))
+        st, es = orc.sync_v3(ref["codes"], ref["recon"])
+        assert np.array_equal(b3.sync_starts.view(np.int64), st.view(np.int64)), (n, sc, eb)
+        for b in (b1, b3):
+            assert np.array_equal(lc.decompress(b).view(np.int64), ref["recon"].view(np.int64)), (n, sc, eb, b.version)
+    n = 400_000                                                # decays into the subnormal range and back
+    env = np.concatenate([np.logspace(0, -320, n // 2), np.logspace(-320, 0, n // 2)])
+    x = env * (1 + 0.1 * np.sin(np.arange(n) / 50.0))
+    ref = orc.compress(x, "absolute", 1e-293)
+    for v in (1, 3):
+        b = lc.compress(x, lc.CompressorConfig.absolute(1e-293, block_version=v))
+        assert np.array_equal(lc.decompress(b).view(np.int64), ref["recon"].view(np.int64)), v
+    assert lc.compress(x, lc.CompressorConfig.absolute(1e-293)).to_bytes() == orc.to_bytes(ref)
+
+
+def test_small_bin_budgets_v3_tables(lc, ctx):
+    """n_bins_half = 1 / 7 with an error bound comparable to the data: the chain cannot follow x and
+    sits far from the guess lattice, so the offsets are not exactly representable (a randomized run
+    found v3 sync starts off by an ulp).  Such budgets are never certified: tables, bytes and
+    both reconstructions are exact."""
+    r = np.random.default_rng(3)
+    n = 300_000
+    t = np.arange(n) / n
+    mixed = np.sin(40 * t) * (1 + 1e3 * (r.random(n) < 1e-4)) + r.normal(0, 1e-4, n)
+    steps = np.repeat(r.normal(0, 1, 10_000), 100)[:999_999].copy()
+    for x, frac, nbh in ((mixed, 0.011, 1), (mixed, 0.011, 7), (steps, 0.0088, 1), (r.normal(0, 1, 49_999), 0.019, 1)):
+        eb = frac * float(np.ptp(x))
+        ref = orc.compress(x, "absolute", eb, n_bins_half=nbh)
+        b1 = lc.compress(x, lc.CompressorConfig.absolute(eb, n_bins_half=nbh))
+        assert b1.to_bytes() == orc.to_bytes(ref), (x.size, nbh)
+        b3 = lc.compress(x, lc.CompressorConfig.absolute(eb, n_bins_half=nbh, block_version=3))
+        st, es = orc.sync_v3(ref["codes"], ref["recon"])
+        assert np.array_equal(b3.sync_starts.view(np.int64), st.view(np.int64)), (x.size, nbh)
+        for b in (b1, b3):
+            assert np.array_equal(lc.decompress(b).view(np.int64), ref["recon"].view(np.int64)), (x.size, nbh, b.version)
