@@ -526,6 +526,21 @@ static int lc_compress_t(lc_ctx *ctx, const double *dx, uint64_t n, double eb_ab
     { int _rc = encode_launch(); if (_rc) return _rc; }
     { int _rc = readback(); if (_rc) return _rc; }
     if (dyn && hdyn->status) return hdyn->status;        // non-finite / constant / bad bound: no results
+    if (dyn && hdyn->rmax < 0x1p-960) {
+        // every value below 2^-960: ulps are subnormal and the offset-map arithmetic is not exact
+        // (predicted chunk and tile starts can be an ulp off), so the sequential exact chain does
+        // the whole vector; it also writes the v3 sync starts itself
+        P.first_chunk = 0;
+        P.inject_chunk = -1;
+        ctx->quant_serial = 1;
+        LC_CUDA_OK(cudaMemsetAsync(first_bad, 0xff, 8, st));
+        lc_quant_serial_kernel<CodeT><<<1, 32, 0, st>>>(P, codes);
+        { int _rc = lc_debug_check(ctx, "lc_quant_serial_kernel", __FILE__, __LINE__); if (_rc) return _rc; }
+        ctx->launches += 1;
+        relaunches = 1;
+        full = true;
+        *hbad = ~0ULL;
+    }
     if (*hbad != ~0ULL) {
         // a chunk prediction failed.  Resume (default): pass A's results stand, the
         // chunks from the first bad one to the end of its warp tile are re-run from

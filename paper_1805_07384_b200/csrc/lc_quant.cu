@@ -355,7 +355,7 @@ __global__ void lc_quant_serial_kernel(LcQuantParams P, CodeT *__restrict__ code
 {
     if (!lc_quant_dyn(P)) return;
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    double r = P.anchor_val;
+    double r = P.first_chunk == 0 ? P.x[0] : P.anchor_val;   // a launch from the start is anchored at x[0]
     for (uint64_t i = (uint64_t)P.first_chunk * LC_L + 1; i < P.n; ++i) {
         uint32_t code; int esc; double inc, pe;
         if (P.sync_start && ((i - 1) & (LC_SYNC_K - 1)) == 0) P.sync_start[(i - 1) / LC_SYNC_K] = r;
