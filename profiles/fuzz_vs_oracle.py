@@ -1,0 +1,52 @@
+"""Randomized comparison of the CUDA path with the CPU oracle (test infrastructure): blocks byte for
+byte, v1 and v3 reconstructions bit for bit.  python profiles/fuzz_vs_oracle.py [seed] [seconds]"""
+import os, sys, time, numpy as np, torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1805_07384_b200 as lc
+from oracle import oracle as orc
+seed = int(sys.argv[1]) if len(sys.argv) > 1 else 0
+budget = float(sys.argv[2]) if len(sys.argv) > 2 else 240.0
+r = np.random.default_rng(seed)
+t0 = time.time(); cases = 0; fails = 0
+while time.time() - t0 < budget:
+    n = int(r.choice([2, 3, 33, 1024, 1025, 4097, 50_000, 300_000, 1_000_000, 3_000_000]))
+    n = max(2, n + int(r.integers(-1, 2)))
+    kind = r.choice(["smooth", "walk", "spiky", "ints", "steps", "noise0", "tiny", "mixed"])
+    t = np.arange(n) / max(n, 1)
+    if kind == "smooth": x = np.sin(2 * np.pi * r.uniform(1, 40) * t) + r.normal(0, 10.0 ** r.uniform(-6, -2), n)
+    elif kind == "walk": x = r.normal(0, 10.0 ** r.uniform(-3, 1), n).cumsum()
+    elif kind == "spiky":
+        x = r.normal(0, 1e-2, n).cumsum(); k = max(1, n // int(r.choice([20, 200, 5000])))
+        x[r.integers(0, n, k)] += r.choice([1e3, 1e9, -1e6])
+    elif kind == "ints": x = r.integers(-50, 50, n).cumsum().astype(np.float64)
+    elif kind == "steps": x = np.repeat(r.normal(0, 1, (n + 99) // 100), 100)[:n].copy()
+    elif kind == "noise0": x = r.normal(0, 1, n)
+    elif kind == "tiny": x = r.normal(0, 1e-300, n).cumsum()
+    else: x = np.sin(40 * t) * (1 + 1e3 * (r.random(n) < 1e-4)) + r.normal(0, 1e-4, n)
+    mode = r.choice(["rel", "abs"])
+    eb = 10.0 ** r.uniform(-9, -1)
+    nbh = int(r.choice([32768, 32768, 32768, 1, 7, 300, 100000]))
+    try:
+        if mode == "rel":
+            ref = orc.compress(x, "value_range_relative", eb, n_bins_half=nbh); cfg = lambda v: lc.CompressorConfig.value_range_relative(eb, n_bins_half=nbh, block_version=v)
+        else:
+            eba = eb * max(1e-300, float(np.ptp(x)) if np.ptp(x) > 0 else 1.0)
+            ref = orc.compress(x, "absolute", eba, n_bins_half=nbh); cfg = lambda v: lc.CompressorConfig.absolute(eba, n_bins_half=nbh, block_version=v)
+    except Exception as e:
+        continue
+    cases += 1
+    try:
+        xd = torch.from_numpy(x).cuda()
+        b1 = lc.compress(xd, cfg(1))
+        ok = b1.to_bytes() == orc.to_bytes(ref)
+        r1 = lc.decompress(b1)
+        ok = ok and np.array_equal(r1.view(np.int64), np.asarray(ref.get("recon", r1)).view(np.int64)) if "recon" in ref else ok
+        b3 = lc.compress(xd, cfg(3))
+        r3 = lc.decompress(lc.CompressedBlock.from_bytes(b3.to_bytes()))
+        ok = ok and np.array_equal(r3.view(np.int64), r1.view(np.int64)) and b3.payload == b1.payload
+    except Exception as e:
+        ok = False; print("EXC", type(e).__name__, str(e)[:100])
+    if not ok:
+        fails += 1
+        print("FAIL seed", seed, "case", cases, "n", n, kind, mode, eb, nbh, flush=True)
+print("seed", seed, "cases", cases, "fails", fails)
