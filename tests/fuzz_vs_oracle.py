@@ -1,5 +1,5 @@
 """Randomized comparison of the CUDA path with the CPU oracle (test infrastructure): blocks byte for
-byte, v1 and v3 reconstructions bit for bit.  python profiles/fuzz_vs_oracle.py [seed] [seconds]"""
+byte, v1 and v3 reconstructions bit for bit.  python tests/fuzz_vs_oracle.py [seed] [seconds]"""
 import os, sys, time, numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1805_07384_b200 as lc
